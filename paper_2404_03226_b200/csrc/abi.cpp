@@ -1,0 +1,991 @@
+// abi.cpp -- implementation of include/tbsim_b200.h.
+//
+// Host orchestration only: argument checks, CSR ingestion into HBM, kernel
+// launches, result download and the mapping of per-graph device status codes
+// onto the reference's exception types and texts.  All compute runs in the
+// CUDA kernels (attributes.cu, simulate.cu); there is no host fallback.
+#include "tbsim_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "attributes.cuh"
+#include "common.cuh"
+#include "hostbatch.hpp"
+#include "simulate.cuh"
+
+using namespace tbsim_dev;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Error {
+    tbsim_status code;
+    std::string msg;
+};
+
+[[noreturn]] void raise(tbsim_status code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) raise(TBSIM_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+tbsim_status guarded(F&& f) {
+    try {
+        f();
+        return TBSIM_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return TBSIM_E_INVALID_ARGUMENT;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return TBSIM_E_OUT_OF_RANGE;
+    } catch (const std::logic_error& e) {
+        g_err = e.what();
+        return TBSIM_E_LOGIC;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return TBSIM_E_RUNTIME;
+    }
+}
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* get(size_t need) {
+        need = std::max<size_t>(need, 16);
+        if (need > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            bytes = 0;
+            cuda_check(cudaMalloc(&p, need), "cudaMalloc");
+            bytes = need;
+        }
+        return p;
+    }
+    template <typename T>
+    T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+
+}  // namespace
+
+struct tbsim_ctx {
+    int device = 0;
+    cudaStream_t own = nullptr;
+    cudaStream_t stream = nullptr;
+    int n_sms = 0;
+    size_t smem_optin = 0;
+    int64_t launches = 0;
+    bool timing = false;
+    std::map<std::string, double> last_ms;
+    std::map<std::string, std::pair<cudaEvent_t, cudaEvent_t>> events;
+    std::map<std::string, DevBuf> bufs;
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+
+    DevBuf& buf(const std::string& name) { return bufs[name]; }
+    void* host_stage(size_t bytes) {
+        if (bytes > pinned_bytes) {
+            if (pinned) cudaFreeHost(pinned);
+            pinned = nullptr;
+            cuda_check(cudaHostAlloc(&pinned, bytes, cudaHostAllocDefault), "cudaHostAlloc");
+            pinned_bytes = bytes;
+        }
+        return pinned;
+    }
+    void begin(const char* k) {
+        ++launches;
+        if (!timing) return;
+        auto& ev = events[k];
+        if (!ev.first) {
+            cudaEventCreate(&ev.first);
+            cudaEventCreate(&ev.second);
+        }
+        cudaEventRecord(ev.first, stream);
+    }
+    void end(const char* k) {
+        cuda_check(cudaGetLastError(), k);
+        if (!timing) return;
+        cudaEventRecord(events[k].second, stream);
+    }
+    void collect_timing() {
+        if (!timing) return;
+        for (auto& [k, ev] : events) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) last_ms[k] = ms;
+        }
+    }
+    void sync() { cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+};
+
+struct tbsim_batch {
+    DevBatch d{};
+    void* mem = nullptr;
+    int64_t h2d_bytes = 0;
+    std::vector<int64_t> task_base;    // host copy
+    std::vector<int64_t> task_id;      // host copy (messages)
+    std::vector<std::string> type_names;
+    int32_t max_workers_seen = 0;
+};
+
+namespace {
+
+std::string type_name(const tbsim_batch* b, int32_t ty) {
+    if (ty >= 0 && ty < static_cast<int32_t>(b->type_names.size())) return b->type_names[ty];
+    return "type" + std::to_string(ty);
+}
+
+int64_t task_ident(const tbsim_batch* b, int64_t g, int64_t pos) {
+    const int64_t t = b->task_base[g] + pos;
+    return b->task_id.empty() ? pos : b->task_id[t];
+}
+
+DevCosts to_dev_costs(const tbsim_costs& c, int32_t n_types_batch) {
+    if (c.n_types > kMaxTypes || n_types_batch > kMaxTypes)
+        raise(TBSIM_E_INVALID_ARGUMENT, "more than " + std::to_string(kMaxTypes) + " task types");
+    DevCosts d{};
+    d.n_types = std::max(c.n_types, 0);
+    for (int i = 0; i < c.n_types; ++i) {
+        d.cpu[i] = c.cpu_ms && c.cpu_ms[i] > 0.0 ? c.cpu_ms[i] : 0.0;
+        d.gpu[i] = c.gpu_ms && c.gpu_ms[i] > 0.0 ? c.gpu_ms[i] : 0.0;
+    }
+    return d;
+}
+
+DevPlatform to_dev_platform(const tbsim_platform_desc& p, int32_t n_types_batch) {
+    if (p.n_workers < 1) raise(TBSIM_E_RUNTIME, "platform has no workers");
+    if (p.n_workers > kMaxWorkers)
+        raise(TBSIM_E_INVALID_ARGUMENT, "device simulator supports at most " + std::to_string(kMaxWorkers) + " workers");
+    if (p.n_nodes < 1 || p.n_nodes > kMaxNodes)
+        raise(TBSIM_E_INVALID_ARGUMENT, "device simulator supports 1.." + std::to_string(kMaxNodes) + " memory nodes");
+    DevPlatform d{};
+    d.n_workers = p.n_workers;
+    d.n_nodes = p.n_nodes;
+    d.latency_ms = p.latency_ms;
+    for (int w = 0; w < p.n_workers; ++w) {
+        d.kind[w] = p.kind[w] ? 1 : 0;
+        d.node[w] = p.memory_node[w];
+        if (d.node[w] < 0 || d.node[w] >= p.n_nodes)
+            raise(TBSIM_E_RUNTIME, "worker " + std::to_string(w) + " references unknown memory node");
+    }
+    for (int a = 0; a < p.n_nodes; ++a)
+        for (int b = 0; b < p.n_nodes; ++b) d.bw[a * kMaxNodes + b] = p.bandwidth[a * p.n_nodes + b];
+    d.costs = to_dev_costs(p.costs, n_types_batch);
+    return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tbsim_last_error(void) { return g_err.c_str(); }
+int tbsim_abi_version(void) { return TBSIM_ABI_VERSION; }
+
+tbsim_status tbsim_ctx_create(int device, tbsim_ctx** out) {
+    return guarded([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            raise(TBSIM_E_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+        }
+        if (device < 0 || device >= n) raise(TBSIM_E_INVALID_ARGUMENT, "bad device index");
+        auto c = std::make_unique<tbsim_ctx>();
+        c->device = device;
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major < 10)
+            raise(TBSIM_E_CUDA, std::string("device ") + prop.name + " is not sm_100 (built for sm_100a)");
+        c->n_sms = prop.multiProcessorCount;
+        c->smem_optin = prop.sharedMemPerBlockOptin;
+        cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
+        c->stream = c->own;
+        *out = c.release();
+    });
+}
+
+tbsim_status tbsim_ctx_destroy(tbsim_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        for (auto& [k, b] : ctx->bufs) b.release();
+        for (auto& [k, ev] : ctx->events) {
+            cudaEventDestroy(ev.first);
+            cudaEventDestroy(ev.second);
+        }
+        if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        if (ctx->own) cudaStreamDestroy(ctx->own);
+        delete ctx;
+    });
+}
+
+tbsim_status tbsim_ctx_set_stream(tbsim_ctx* ctx, void* s) {
+    return guarded([&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
+}
+
+tbsim_status tbsim_ctx_synchronize(tbsim_ctx* ctx) {
+    return guarded([&] { ctx->sync(); });
+}
+
+int64_t tbsim_ctx_launch_count(const tbsim_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+tbsim_status tbsim_ctx_set_timing(tbsim_ctx* ctx, int enable) {
+    return guarded([&] { ctx->timing = enable != 0; });
+}
+
+tbsim_status tbsim_ctx_last_kernel_ms(const tbsim_ctx* ctx, const char* kernel, double* ms) {
+    return guarded([&] {
+        auto it = ctx->last_ms.find(kernel);
+        *ms = it == ctx->last_ms.end() ? 0.0 : it->second;
+    });
+}
+
+// ------------------------------------------------------------------ upload
+
+tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim_batch** out) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int64_t G = h->n_graphs;
+        if (G < 0) raise(TBSIM_E_INVALID_ARGUMENT, "negative graph count");
+        auto b = std::make_unique<tbsim_batch>();
+        const int64_t T = h->task_base[G], E = h->edge_base[G], H = h->handle_base[G];
+        const int64_t I = h->in_base[G], O = h->out_base[G];
+        if (h->n_type_names > kMaxTypes) raise(TBSIM_E_INVALID_ARGUMENT, "more than 64 task types");
+        // per-graph maxima (device scratch sizing) and cheap sanity checks
+        int32_t max_n = 0, max_e = 0, max_h = 0;
+        for (int64_t g = 0; g < G; ++g) {
+            const int64_t n = h->task_base[g + 1] - h->task_base[g];
+            const int64_t e = h->edge_base[g + 1] - h->edge_base[g];
+            const int64_t nh = h->handle_base[g + 1] - h->handle_base[g];
+            if (n < 0 || e < 0 || nh < 0) raise(TBSIM_E_INVALID_ARGUMENT, "batch bases must be non-decreasing");
+            if (n >= (1 << 24)) raise(TBSIM_E_INVALID_ARGUMENT, "graph exceeds 2^24 tasks");
+            if (e > INT32_MAX || nh > INT32_MAX) raise(TBSIM_E_INVALID_ARGUMENT, "graph exceeds 2^31 entries");
+            max_n = std::max<int32_t>(max_n, static_cast<int32_t>(n));
+            max_e = std::max<int32_t>(max_e, static_cast<int32_t>(e));
+            max_h = std::max<int32_t>(max_h, static_cast<int32_t>(nh));
+        }
+        struct Sec { const void* src; size_t bytes; void** dst; };
+        DevBatch& d = b->d;
+        std::vector<Sec> secs = {
+            {h->task_base, static_cast<size_t>(G + 1) * 8, (void**)&d.task_base}, {h->edge_base, static_cast<size_t>(G + 1) * 8, (void**)&d.edge_base},
+            {h->handle_base, static_cast<size_t>(G + 1) * 8, (void**)&d.handle_base}, {h->in_base, static_cast<size_t>(G + 1) * 8, (void**)&d.in_base},
+            {h->out_base, static_cast<size_t>(G + 1) * 8, (void**)&d.out_base}, {h->dep_off, static_cast<size_t>(T + G) * 4, (void**)&d.dep_off},
+            {h->dep, static_cast<size_t>(E) * 4, (void**)&d.dep}, {h->in_off, static_cast<size_t>(T + G) * 4, (void**)&d.in_off},
+            {h->in, static_cast<size_t>(I) * 4, (void**)&d.in}, {h->out_off, static_cast<size_t>(T + G) * 4, (void**)&d.out_off},
+            {h->out, static_cast<size_t>(O) * 4, (void**)&d.out}, {h->type, static_cast<size_t>(T) * 4, (void**)&d.type},
+            {h->handle_bytes, static_cast<size_t>(H) * 8, (void**)&d.handle_bytes}};
+        size_t total = 0;
+        for (const auto& s : secs) total += al16(s.bytes);
+        const size_t derived = al16((T + G) * 4) + al16(E * 4);
+        cuda_check(cudaMalloc(&b->mem, total + derived + 16), "cudaMalloc(batch)");
+        char* p = static_cast<char*>(b->mem);
+        int64_t moved = 0;
+        for (const auto& s : secs) {
+            *s.dst = p;
+            if (s.bytes) {
+                cuda_check(cudaMemcpyAsync(p, s.src, s.bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D batch");
+                moved += static_cast<int64_t>(s.bytes);
+            }
+            p += al16(s.bytes);
+        }
+        d.succ_off = reinterpret_cast<int32_t*>(p);
+        d.succ = reinterpret_cast<int32_t*>(p + al16((T + G) * 4));
+        d.G = G; d.T = T; d.E = E; d.H = H; d.I = I; d.O = O;
+        d.max_n = max_n; d.max_e = max_e; d.max_h = max_h;
+        // type ids index the cost table; without a name table, scan them
+        int32_t n_types = h->n_type_names;
+        if (n_types <= 0) {
+            for (int64_t t = 0; t < T; ++t) n_types = std::max(n_types, h->type[t] + 1);
+            if (n_types > kMaxTypes) raise(TBSIM_E_INVALID_ARGUMENT, "more than 64 task types");
+        }
+        d.n_types = std::max(n_types, 1);
+        b->h2d_bytes = moved;
+        b->task_base.assign(h->task_base, h->task_base + G + 1);
+        if (h->task_id) b->task_id.assign(h->task_id, h->task_id + T);
+        for (int i = 0; i < h->n_type_names; ++i)
+            b->type_names.push_back(h->type_names && h->type_names[i] ? h->type_names[i] : "type" + std::to_string(i));
+        // derived successor CSR (sorted, multi-edges kept)
+        if (G > 0) {
+            int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(T + G);
+            const int grid = static_cast<int>(std::min<int64_t>(G, 8LL * ctx->n_sms));
+            ctx->begin("k_ingest");
+            k_ingest<<<grid, 256, 0, ctx->stream>>>(d, cursor);
+            ctx->end("k_ingest");
+        }
+        *out = b.release();
+    });
+}
+
+tbsim_status tbsim_batch_free(tbsim_ctx* ctx, tbsim_batch* b) {
+    return guarded([&] {
+        if (!b) return;
+        if (ctx) cudaStreamSynchronize(ctx->stream);
+        if (b->mem) cudaFree(b->mem);
+        delete b;
+    });
+}
+
+int64_t tbsim_batch_h2d_bytes(const tbsim_batch* b) { return b ? b->h2d_bytes : 0; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- attributes
+
+namespace {
+
+struct AttrRun {
+    AttrScratch s{};
+    std::vector<GraphInfo> info;  // host copy after sync
+};
+
+AttrScratch alloc_attr_scratch(tbsim_ctx* ctx, const DevBatch& d) {
+    AttrScratch s{};
+    const int64_t T = d.T, G = d.G, E = d.E, NT = d.n_types;
+    s.tmp = ctx->buf("a_tmp").as<int32_t>(T + G);
+    s.tmp2 = ctx->buf("a_tmp2").as<int32_t>(T + G);
+    s.order = ctx->buf("a_order").as<int32_t>(T);
+    s.level = ctx->buf("a_level").as<int32_t>(T);
+    s.lstart = ctx->buf("a_lstart").as<int32_t>(T + G);
+    s.height = ctx->buf("a_height").as<int32_t>(T);
+    s.lastuse = ctx->buf("a_lastuse").as<int32_t>(T);
+    s.slot = ctx->buf("a_slot").as<int32_t>(T);
+    s.rel_order = ctx->buf("a_rel").as<int32_t>(T);
+    s.fstack = ctx->buf("a_fstack").as<int32_t>(T);
+    s.cls = ctx->buf("a_cls").as<int32_t>(T);
+    s.cls_mark = ctx->buf("a_clsmark").as<int32_t>(T * NT);
+    s.pslot = ctx->buf("a_pslot").as<int32_t>(E);
+    s.rank = ctx->buf("a_rank").as<double>(T);
+    s.hist = ctx->buf("a_hist").as<uint64_t>(4 * T);
+    s.info = ctx->buf("a_info").as<GraphInfo>(G);
+    s.median = ctx->buf("a_median").as<double>(G);
+    s.tile_base = ctx->buf("a_tilebase").as<int64_t>(G + 1);
+    s.tile_s = ctx->buf("a_tiles").as<int32_t>(G);
+    return s;
+}
+
+constexpr int kSweepThreads = 512;
+
+int64_t sweep_smem_bytes(tbsim_ctx* ctx) {
+    // leave room for the kernel's static shared memory (costs + histogram)
+    int64_t opt = static_cast<int64_t>(ctx->smem_optin);
+    return std::max<int64_t>(0, opt - 8 * 1024);
+}
+
+// Launch the whole attribute pipeline on a device batch.  Returns with the
+// per-graph GraphInfo copied to the host (one sync).
+void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_costs, const int32_t* d_cost_idx,
+                    int32_t sweep_mode, const double* d_unit_time, bool want_rank, bool do_sweep,
+                    AttrOutDev o, int32_t prio_kind, bool want_prio, AttrRun& run) {
+    const DevBatch& d = b->d;
+    const int64_t G = d.G;
+    run.s = alloc_attr_scratch(ctx, d);
+    if (G == 0) return;
+    const int grid_g = static_cast<int>(std::min<int64_t>(G, 4LL * ctx->n_sms));
+    ctx->begin("k_structure");
+    k_structure<<<grid_g, 512, 0, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, want_rank ? 1 : 0);
+    ctx->end("k_structure");
+    if (do_sweep) {
+        const int64_t smem = sweep_smem_bytes(ctx);
+        ctx->begin("k_tile_plan");
+        k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, run.s, smem, 0);
+        ctx->end("k_tile_plan");
+        // graphs whose distance window exceeds shared memory use a global
+        // window; size it from the worst case (every node live)
+        int64_t gwin_stride = 0;
+        double* gwin = nullptr;
+        const int sweep_grid = ctx->n_sms;  // one 512-thread CTA per SM (smem bound)
+        if (static_cast<int64_t>(d.max_n) * 8 * 8 > smem) {
+            gwin_stride = static_cast<int64_t>(d.max_n) * 32;
+            gwin = ctx->buf("a_gwin").as<double>(gwin_stride * sweep_grid);
+        }
+        unsigned long long* counter = ctx->buf("a_counter").as<unsigned long long>(1);
+        cuda_check(cudaMemsetAsync(counter, 0, 8, ctx->stream), "memset");
+        const int64_t total_tiles = -1;  // read on the device from tile_base[G]
+        static bool attr_set = false;
+        if (!attr_set) {
+            cuda_check(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+                       "cudaFuncSetAttribute(k_sweep)");
+            attr_set = true;
+        }
+        ctx->begin("k_sweep");
+        k_sweep<<<sweep_grid, kSweepThreads, smem, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, sweep_mode, d_unit_time,
+                                                                  total_tiles, counter, smem, gwin, gwin_stride);
+        ctx->end("k_sweep");
+        const int64_t cls_stride = static_cast<int64_t>(d.max_n) * (kWindows + 1) + 16;
+        int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride * grid_g);
+        ctx->begin("k_finalize");
+        k_finalize<<<grid_g, 256, 0, ctx->stream>>>(d, run.s, sweep_mode, d_unit_time, o, cls_scratch, cls_stride);
+        ctx->end("k_finalize");
+    }
+    if (o.layer || o.depth || (want_prio && o.static_priority)) {
+        const int grid = static_cast<int>(std::min<int64_t>((d.T + 255) / 256, 16LL * ctx->n_sms));
+        if (grid > 0) {
+            ctx->begin("k_structure_out");
+            k_structure_out<<<grid, 256, 0, ctx->stream>>>(d, run.s, o, prio_kind, want_prio ? 1 : 0);
+            ctx->end("k_structure_out");
+        }
+    }
+    run.info.resize(G);
+    cuda_check(cudaMemcpyAsync(run.info.data(), run.s.info, G * sizeof(GraphInfo), cudaMemcpyDeviceToHost, ctx->stream),
+               "D2H info");
+}
+
+// Compose the reference's exception for the first failing graph, in the
+// order each reference function checks its preconditions.
+void attr_errors(const tbsim_batch* b, const std::vector<GraphInfo>& info, int32_t request, const double* unit_time) {
+    for (int64_t g = 0; g < static_cast<int64_t>(info.size()); ++g) {
+        const GraphInfo& gi = info[g];
+        const int64_t n = b->task_base[g + 1] - b->task_base[g];
+        const bool cyc = gi.processed != n;
+        auto ty_of = [&](int32_t pos) -> std::string {
+            // type id is on the device; fetch lazily
+            int32_t ty = 0;
+            cudaMemcpy(&ty, b->d.type + b->task_base[g] + pos, 4, cudaMemcpyDeviceToHost);
+            return type_name(b, ty);
+        };
+        if (request & (TBSIM_ATTR_ALL | TBSIM_ATTR_CALIBRATE)) {
+            // calibrate_unit_time: topological_layers, then median_gpu_time_ms
+            if (cyc) raise(TBSIM_E_RUNTIME, "graph has a dependency cycle");
+            if (n == 0) raise(TBSIM_E_RUNTIME, "empty graph has no median time");
+            if (gi.miss_gpu >= 0) raise(TBSIM_E_RUNTIME, "no gpu cost entry for task type " + ty_of(gi.miss_gpu));
+        }
+        if (request & TBSIM_ATTR_EFFICIENCY) {
+            // efficiency_impl: window check, gpu times, then topological_order
+            const double w = unit_time ? unit_time[g] : 0.0;
+            if (!(w >= 0.0)) raise(TBSIM_E_INVALID_ARGUMENT, "unit time must be non-negative");
+            if (n > 0 && gi.miss_gpu >= 0) raise(TBSIM_E_RUNTIME, "no gpu cost entry for task type " + ty_of(gi.miss_gpu));
+            if (cyc) raise(TBSIM_E_RUNTIME, "graph has a dependency cycle");
+        }
+        if (request & TBSIM_ATTR_RANK) {
+            if (gi.miss_any >= 0) raise(TBSIM_E_RUNTIME, "no cost entry for task type " + ty_of(gi.miss_any));
+            if (cyc) raise(TBSIM_E_RUNTIME, "graph has a dependency cycle");
+        }
+        if (request & (TBSIM_ATTR_DEPTH | TBSIM_ATTR_LAYERS))
+            if (cyc) raise(TBSIM_E_RUNTIME, "graph has a dependency cycle");
+    }
+}
+
+// Device output staging for host-pointer outputs.
+struct OutStage {
+    AttrOutDev dev{};
+    std::vector<std::pair<void*, std::pair<const void*, size_t>>> copies;  // host dst, (dev src, bytes)
+};
+
+template <typename T>
+T* stage_out(tbsim_ctx* ctx, OutStage& st, const char* name, T* host, size_t count, bool on_device) {
+    if (!host) return nullptr;
+    if (on_device) return host;
+    T* dev = ctx->buf(name).as<T>(count);
+    st.copies.push_back({host, {dev, count * sizeof(T)}});
+    return dev;
+}
+
+}  // namespace
+
+extern "C" tbsim_status tbsim_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const tbsim_costs* costs,
+                                         int32_t request, int32_t priority_kind, tbsim_attr_out* out) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const DevBatch& d = b->d;
+        const int64_t T = d.T, G = d.G;
+        const bool dev = out->on_device != 0;
+        // efficiency-only: window validation happens before any device work
+        if ((request & TBSIM_ATTR_EFFICIENCY) && !(request & (TBSIM_ATTR_ALL | TBSIM_ATTR_CALIBRATE))) {
+            if (!out->unit_time_ms) raise(TBSIM_E_INVALID_ARGUMENT, "efficiency needs unit_time_ms");
+            if (!dev)
+                for (int64_t g = 0; g < G; ++g)
+                    if (!(out->unit_time_ms[g] >= 0.0)) raise(TBSIM_E_INVALID_ARGUMENT, "unit time must be non-negative");
+        }
+        DevCosts hc = to_dev_costs(*costs, d.n_types);
+        DevCosts* d_costs = ctx->buf("costs").as<DevCosts>(1);
+        cuda_check(cudaMemcpyAsync(d_costs, &hc, sizeof hc, cudaMemcpyHostToDevice, ctx->stream), "H2D costs");
+
+        OutStage st;
+        AttrOutDev o{};
+        const bool all = request & TBSIM_ATTR_ALL;
+        const bool calib = all || (request & TBSIM_ATTR_CALIBRATE);
+        const bool eff_only = (request & TBSIM_ATTR_EFFICIENCY) && !calib;
+        o.ability = stage_out(ctx, st, "o_ability", out->ability, T, dev);
+        if (!(all || (request & TBSIM_ATTR_ABILITY))) o.ability = nullptr;
+        o.efficiency = stage_out(ctx, st, "o_eff", out->efficiency, T, dev);
+        if (!(all || (request & (TBSIM_ATTR_EFFICIENCY | TBSIM_ATTR_CALIBRATE)))) o.efficiency = nullptr;
+        o.static_priority = stage_out(ctx, st, "o_prio", out->static_priority, T, dev);
+        o.depth = (request & TBSIM_ATTR_DEPTH) ? stage_out(ctx, st, "o_depth", out->depth, T, dev) : nullptr;
+        o.layer = (request & TBSIM_ATTR_LAYERS) ? stage_out(ctx, st, "o_layer", out->layer, T, dev) : nullptr;
+        o.w0_ms = calib ? stage_out(ctx, st, "o_w0", out->w0_ms, G, dev) : nullptr;
+        o.best_score = calib ? stage_out(ctx, st, "o_best", out->best_score, G, dev) : nullptr;
+        o.w0_score = calib ? stage_out(ctx, st, "o_w0s", out->w0_score, G, dev) : nullptr;
+        o.evaluations = calib ? stage_out(ctx, st, "o_evals", out->evaluations, G, dev) : nullptr;
+        double* d_unit = nullptr;
+        if (out->unit_time_ms) {
+            if (dev) {
+                d_unit = out->unit_time_ms;
+            } else {
+                d_unit = ctx->buf("o_unit").as<double>(G);
+                if (eff_only)
+                    cuda_check(cudaMemcpyAsync(d_unit, out->unit_time_ms, G * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D unit");
+                if (calib) st.copies.push_back({out->unit_time_ms, {d_unit, static_cast<size_t>(G) * 8}});
+            }
+        }
+        o.unit_time_ms = calib ? d_unit : nullptr;
+        // static priority: ALL selects by kind; RANK alone -> rank
+        bool want_prio = false;
+        int32_t pk = priority_kind;
+        if (all) want_prio = true;
+        if (request & TBSIM_ATTR_RANK) { want_prio = true; pk = TBSIM_PRIO_UPWARD_RANK; }
+        if (!want_prio) o.static_priority = nullptr;
+        const bool want_rank = want_prio && pk == TBSIM_PRIO_UPWARD_RANK;
+        const bool do_sweep = all || (request & (TBSIM_ATTR_ABILITY | TBSIM_ATTR_EFFICIENCY | TBSIM_ATTR_CALIBRATE));
+        const int32_t mode = calib ? SWEEP_CALIBRATE : eff_only ? SWEEP_SINGLE : SWEEP_ABILITY;
+        AttrRun run;
+        run_attributes(ctx, b, d_costs, nullptr, mode, d_unit, want_rank, do_sweep, o, pk, want_prio, run);
+        for (const auto& c : st.copies)
+            cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H out");
+        ctx->sync();
+        ctx->collect_timing();
+        std::vector<double> unit_host;
+        if (eff_only && dev) {
+            unit_host.resize(G);
+            cudaMemcpy(unit_host.data(), d_unit, G * 8, cudaMemcpyDeviceToHost);
+        }
+        attr_errors(b, run.info, request, eff_only ? (dev ? unit_host.data() : out->unit_time_ms) : nullptr);
+    });
+}
+
+// ---------------------------------------------------------------- simulate
+
+namespace {
+
+struct SimRun {
+    std::vector<int32_t> status, aux;
+};
+
+void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_items) {
+    const int kThreads = 256, kWarps = kThreads / 32;
+    const DevBatch& d = p.b;
+    const int64_t qcap_full = std::max<int32_t>(d.max_n, 1);
+    // shared-memory state when it fits a useful number of warps per CTA
+    const int64_t budget = static_cast<int64_t>(ctx->smem_optin) - 1024;
+    int64_t qcap = qcap_full;
+    int64_t bytes = sim_state_bytes(d.max_n, d.max_h, max_workers, qcap);
+    p.use_smem = 0;
+    if (bytes * kWarps > budget) {
+        // try a bounded queue capacity in shared memory (overflow -> rerun)
+        const int64_t fixed = sim_state_bytes(d.max_n, d.max_h, max_workers, 0);
+        const int64_t room = budget / kWarps - fixed;
+        const int64_t cap = room / (4 * max_workers);
+        if (cap >= 64) {
+            qcap = std::min<int64_t>(cap & ~int64_t(3), qcap_full);
+            bytes = sim_state_bytes(d.max_n, d.max_h, max_workers, qcap);
+            p.use_smem = 1;
+        }
+    } else {
+        p.use_smem = 1;
+    }
+    if (p.qcap > 0) {  // forced (rerun) configuration: global state, full capacity
+        qcap = p.qcap;
+        bytes = sim_state_bytes(d.max_n, d.max_h, max_workers, qcap);
+        p.use_smem = 0;
+    }
+    p.qcap = static_cast<int32_t>(qcap);
+    p.state_bytes = bytes;
+    p.max_workers = max_workers;
+    p.n_items = n_items;
+    const int blocks_per_sm = 2;
+    int grid = static_cast<int>(std::min<int64_t>((n_items + kWarps - 1) / kWarps, static_cast<int64_t>(blocks_per_sm) * ctx->n_sms));
+    grid = std::max(grid, 1);
+    const size_t smem = p.use_smem ? static_cast<size_t>(bytes * kWarps) : 0;
+    if (!p.use_smem) p.gstate = static_cast<char*>(ctx->buf("s_gstate").get(static_cast<size_t>(bytes) * kWarps * grid));
+    unsigned long long* counter = ctx->buf("s_counter").as<unsigned long long>(1);
+    cuda_check(cudaMemsetAsync(counter, 0, 8, ctx->stream), "memset");
+    p.work_counter = counter;
+    const bool w2 = max_workers > 32;
+    auto kern = w2 ? k_simulate_w2 : k_simulate_w1;
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+               "cudaFuncSetAttribute(k_simulate)");
+    ctx->begin("k_simulate");
+    kern<<<grid, kThreads, smem, ctx->stream>>>(p);
+    ctx->end("k_simulate");
+}
+
+// Runs the simulator over every graph, reruns queue overflows with full
+// capacity in HBM, and raises the first graph's error.
+void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t max_workers) {
+    const int64_t G = b->d.G;
+    if (G == 0) return;
+    p.graph_list = nullptr;
+    p.qcap = 0;
+    launch_sim(ctx, p, max_workers, G);
+    std::vector<int32_t> status(G), aux(G);
+    cuda_check(cudaMemcpyAsync(status.data(), p.status, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
+    cuda_check(cudaMemcpyAsync(aux.data(), p.status_aux, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H aux");
+    ctx->sync();
+    std::vector<int32_t> rerun;
+    for (int64_t g = 0; g < G; ++g)
+        if (status[g] == GS_QUEUE_OVERFLOW) rerun.push_back(static_cast<int32_t>(g));
+    if (!rerun.empty()) {
+        int32_t* d_list = ctx->buf("s_rerun").as<int32_t>(rerun.size());
+        cuda_check(cudaMemcpyAsync(d_list, rerun.data(), rerun.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D rerun");
+        // reset the reruns' regulator state is not needed: a graph that
+        // overflowed never wrote its state back (status checked first)
+        SimParams q = p;
+        q.graph_list = d_list;
+        q.qcap = std::max<int32_t>(b->d.max_n, 1);
+        launch_sim(ctx, q, max_workers, static_cast<int64_t>(rerun.size()));
+        cuda_check(cudaMemcpyAsync(status.data(), p.status, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
+        cuda_check(cudaMemcpyAsync(aux.data(), p.status_aux, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H aux");
+        ctx->sync();
+    }
+    for (int64_t g = 0; g < G; ++g) {
+        if (status[g] == GS_OK) continue;
+        const int64_t t0 = b->task_base[g], n = b->task_base[g + 1] - t0;
+        auto ty_at = [&](int32_t pos) {
+            int32_t ty = 0;
+            cudaMemcpy(&ty, b->d.type + t0 + pos, 4, cudaMemcpyDeviceToHost);
+            return type_name(b, ty);
+        };
+        switch (status[g]) {
+            case GS_NO_WORKER: raise(TBSIM_E_RUNTIME, "no worker can run task type " + ty_at(aux[g]));
+            case GS_DEGENERATE_TIME:
+                raise(TBSIM_E_RUNTIME, "event of task " + std::to_string(task_ident(b, g, aux[g])) +
+                                           " would fire at the current time (transfer/exec below FP64 resolution)");
+            case GS_STUCK: {
+                std::vector<int32_t> w(n);
+                int64_t done = 0;
+                cudaMemcpy(&done, p.completed + g, 8, cudaMemcpyDeviceToHost);
+                if (n) cudaMemcpy(w.data(), p.worker + t0, n * 4, cudaMemcpyDeviceToHost);
+                std::string msg = "simulation stuck with " + std::to_string(n - done) + " tasks unfinished:";
+                int64_t listed = 0;
+                for (int64_t i = 0; i < n && listed < 20; ++i)
+                    if (w[i] < 0) { msg += " " + std::to_string(task_ident(b, g, i)); ++listed; }
+                if (listed < n - done) msg += " ...";
+                raise(TBSIM_E_RUNTIME, msg);
+            }
+            default: raise(TBSIM_E_RUNTIME, "device simulator failed with status " + std::to_string(status[g]));
+        }
+    }
+}
+
+struct SimStage {
+    std::vector<std::pair<void*, std::pair<const void*, size_t>>> copies;
+};
+
+template <typename T>
+T* sim_out_ptr(tbsim_ctx* ctx, SimStage& st, const char* name, T* host, size_t count, bool on_device, bool upload = false) {
+    if (!host) return nullptr;
+    if (on_device) return host;
+    T* dev = ctx->buf(name).as<T>(count);
+    if (upload) cuda_check(cudaMemcpyAsync(dev, host, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    st.copies.push_back({host, {dev, count * sizeof(T)}});
+    return dev;
+}
+
+template <typename T>
+T* scratch_if_null(tbsim_ctx* ctx, const char* name, T* p, size_t count) {
+    return p ? p : ctx->buf(name).as<T>(count);
+}
+
+int32_t upload_platforms(tbsim_ctx* ctx, const tbsim_batch* b, const tbsim_platform_desc* platforms, int32_t n_platforms,
+                         DevPlatform** d_out, std::vector<DevPlatform>& host) {
+    if (n_platforms < 1) raise(TBSIM_E_INVALID_ARGUMENT, "need at least one platform");
+    int32_t maxw = 0;
+    host.clear();
+    for (int i = 0; i < n_platforms; ++i) {
+        host.push_back(to_dev_platform(platforms[i], b->d.n_types));
+        maxw = std::max(maxw, platforms[i].n_workers);
+    }
+    *d_out = ctx->buf("platforms").as<DevPlatform>(n_platforms);
+    cuda_check(cudaMemcpyAsync(*d_out, host.data(), host.size() * sizeof(DevPlatform), cudaMemcpyHostToDevice, ctx->stream),
+               "H2D platforms");
+    return maxw;
+}
+
+void check_reg(const tbsim_regulator_cfg& r) {
+    if (r.slope_samples < 0 || r.slope_samples > TBSIM_MAX_SLOPE_SAMPLES)
+        raise(TBSIM_E_INVALID_ARGUMENT, "slope_samples must be in [0, " + std::to_string(TBSIM_MAX_SLOPE_SAMPLES) +
+                                             "] on the device");
+}
+
+}  // namespace
+
+extern "C" tbsim_status tbsim_simulate(tbsim_ctx* ctx, const tbsim_batch* b, const tbsim_platform_desc* platforms,
+                                       int32_t n_platforms, const int32_t* platform_of, int32_t policy,
+                                       const tbsim_regulator_cfg* reg, const tbsim_attr_in* attrs, tbsim_sim_out* out) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (policy < 0 || policy > TBSIM_POLICY_INSPIRIT) raise(TBSIM_E_RUNTIME, "unknown policy id");
+        const DevBatch& d = b->d;
+        const int64_t T = d.T, G = d.G;
+        if (!reg) raise(TBSIM_E_INVALID_ARGUMENT, "tbsim_simulate needs a regulator config per graph");
+        for (int64_t g = 0; g < G; ++g) check_reg(reg[g]);
+        std::vector<DevPlatform> hp;
+        DevPlatform* d_pf = nullptr;
+        const int32_t maxw = upload_platforms(ctx, b, platforms, n_platforms, &d_pf, hp);
+        SimStage st;
+        const bool dev = out->on_device != 0;
+        SimParams p{};
+        p.b = d;
+        p.platforms = d_pf;
+        if (platform_of) {
+            for (int64_t g = 0; g < G && !dev; ++g)
+                if (platform_of[g] < 0 || platform_of[g] >= n_platforms) raise(TBSIM_E_INVALID_ARGUMENT, "platform index out of range");
+            int32_t* dpo = ctx->buf("s_pof").as<int32_t>(G);
+            cuda_check(cudaMemcpyAsync(dpo, platform_of, G * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D pof");
+            p.platform_of = dpo;
+        }
+        p.policy = policy;
+        tbsim_regulator_cfg* d_reg = ctx->buf("s_reg").as<tbsim_regulator_cfg>(G);
+        cuda_check(cudaMemcpyAsync(d_reg, reg, G * sizeof(tbsim_regulator_cfg), cudaMemcpyHostToDevice, ctx->stream), "H2D reg");
+        p.reg = d_reg;
+        p.median_stride = 1;
+        auto up_attr = [&](const int64_t* a, const char* name) -> const int64_t* {
+            if (!a) return nullptr;
+            if (attrs->on_device) return a;
+            int64_t* dv = ctx->buf(name).as<int64_t>(T);
+            cuda_check(cudaMemcpyAsync(dv, a, T * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D attrs");
+            return dv;
+        };
+        if (attrs) {
+            p.ability = up_attr(attrs->ability, "s_ab");
+            p.efficiency = up_attr(attrs->efficiency, "s_ef");
+            p.prio = up_attr(attrs->static_priority, "s_pr");
+        }
+        p.worker = scratch_if_null(ctx, "s_worker", sim_out_ptr(ctx, st, "s_worker", out->worker, T, dev), T);
+        p.start_ms = scratch_if_null(ctx, "s_start", sim_out_ptr(ctx, st, "s_start", out->start_ms, T, dev), T);
+        p.end_ms = scratch_if_null(ctx, "s_end", sim_out_ptr(ctx, st, "s_end", out->end_ms, T, dev), T);
+        p.makespan = scratch_if_null(ctx, "s_mk", sim_out_ptr(ctx, st, "s_mk", out->makespan_ms, G, dev), G);
+        p.completed = scratch_if_null(ctx, "s_done", sim_out_ptr(ctx, st, "s_done", out->completed, G, dev), G);
+        p.pop_counts = sim_out_ptr(ctx, st, "s_pops", out->pop_mode_counts, 3 * G, dev);
+        p.reg_state = sim_out_ptr(ctx, st, "s_rstate", out->reg_state, G, dev, /*upload=*/true);
+        p.push_time = sim_out_ptr(ctx, st, "s_pusht", out->push_time, T, dev);
+        p.push_task = sim_out_ptr(ctx, st, "s_pushk", out->push_task, T, dev);
+        p.pop_time = sim_out_ptr(ctx, st, "s_popt", out->pop_time, T, dev);
+        p.pop_task = sim_out_ptr(ctx, st, "s_popk", out->pop_task, T, dev);
+        p.pop_worker = sim_out_ptr(ctx, st, "s_popw", out->pop_worker, T, dev);
+        p.sample_time = sim_out_ptr(ctx, st, "s_samt", out->sample_time, 2 * T, dev);
+        p.sample_nready = sim_out_ptr(ctx, st, "s_samn", out->sample_nready, 2 * T, dev);
+        if (!(p.push_time && p.push_task && p.pop_time && p.pop_task && p.pop_worker && p.sample_time && p.sample_nready)) {
+            p.push_time = nullptr; p.push_task = nullptr; p.pop_time = nullptr; p.pop_task = nullptr;
+            p.pop_worker = nullptr; p.sample_time = nullptr; p.sample_nready = nullptr;
+        }
+        p.status = ctx->buf("s_status").as<int32_t>(G);
+        p.status_aux = ctx->buf("s_aux").as<int32_t>(G);
+        run_simulation(ctx, b, p, maxw);
+        for (const auto& c : st.copies)
+            cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ctx->sync();
+        ctx->collect_timing();
+    });
+}
+
+extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, const tbsim_platform_desc* platforms,
+                                       int32_t n_platforms, const int32_t* platform_of, int32_t policy,
+                                       int32_t priority_kind, tbsim_attr_out* attr_out, tbsim_sim_out* out) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (policy < 0 || policy > TBSIM_POLICY_INSPIRIT) raise(TBSIM_E_RUNTIME, "unknown policy id");
+        const DevBatch& d = b->d;
+        const int64_t T = d.T, G = d.G;
+        std::vector<DevPlatform> hp;
+        DevPlatform* d_pf = nullptr;
+        const int32_t maxw = upload_platforms(ctx, b, platforms, n_platforms, &d_pf, hp);
+        // cost tables of the platforms, one per platform (compute_attributes
+        // runs on platform.costs, src/bench.cpp:104)
+        std::vector<DevCosts> hc;
+        for (const auto& p : hp) hc.push_back(p.costs);
+        DevCosts* d_costs = ctx->buf("costs_pf").as<DevCosts>(hc.size());
+        cuda_check(cudaMemcpyAsync(d_costs, hc.data(), hc.size() * sizeof(DevCosts), cudaMemcpyHostToDevice, ctx->stream),
+                   "H2D costs");
+        int32_t* d_pof = nullptr;
+        if (platform_of) {
+            d_pof = ctx->buf("s_pof").as<int32_t>(G);
+            cuda_check(cudaMemcpyAsync(d_pof, platform_of, G * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D pof");
+        }
+        // ---- attributes (compute_attributes on every graph)
+        tbsim_attr_out dummy{};
+        tbsim_attr_out* ao = attr_out ? attr_out : &dummy;
+        const bool adev = ao->on_device != 0;
+        OutStage ast;
+        AttrOutDev o{};
+        o.ability = scratch_if_null(ctx, "f_ab", stage_out(ctx, ast, "f_ab", ao->ability, T, adev), T);
+        o.efficiency = scratch_if_null(ctx, "f_ef", stage_out(ctx, ast, "f_ef", ao->efficiency, T, adev), T);
+        o.static_priority = scratch_if_null(ctx, "f_pr", stage_out(ctx, ast, "f_pr", ao->static_priority, T, adev), T);
+        o.unit_time_ms = scratch_if_null(ctx, "f_ut", stage_out(ctx, ast, "f_ut", ao->unit_time_ms, G, adev), G);
+        o.w0_ms = stage_out(ctx, ast, "f_w0", ao->w0_ms, G, adev);
+        o.best_score = stage_out(ctx, ast, "f_bs", ao->best_score, G, adev);
+        o.w0_score = stage_out(ctx, ast, "f_ws", ao->w0_score, G, adev);
+        o.evaluations = stage_out(ctx, ast, "f_ev", ao->evaluations, G, adev);
+        AttrRun run;
+        run_attributes(ctx, b, d_costs, d_pof, SWEEP_CALIBRATE, nullptr, priority_kind == TBSIM_PRIO_UPWARD_RANK, true,
+                       o, priority_kind, true, run);
+        ctx->sync();
+        attr_errors(b, run.info, TBSIM_ATTR_ALL, nullptr);
+        // ---- default_regulator_config + simulate
+        SimStage st;
+        const bool dev = out->on_device != 0;
+        SimParams p{};
+        p.b = d;
+        p.platforms = d_pf;
+        p.platform_of = d_pof;
+        p.policy = policy;
+        p.reg = nullptr;
+        p.median = run.s.median;
+        p.median_stride = 1;
+        p.ability = o.ability;
+        p.efficiency = o.efficiency;
+        p.prio = o.static_priority;
+        p.worker = scratch_if_null(ctx, "s_worker", sim_out_ptr(ctx, st, "s_worker", out->worker, T, dev), T);
+        p.start_ms = scratch_if_null(ctx, "s_start", sim_out_ptr(ctx, st, "s_start", out->start_ms, T, dev), T);
+        p.end_ms = scratch_if_null(ctx, "s_end", sim_out_ptr(ctx, st, "s_end", out->end_ms, T, dev), T);
+        p.makespan = scratch_if_null(ctx, "s_mk", sim_out_ptr(ctx, st, "s_mk", out->makespan_ms, G, dev), G);
+        p.completed = scratch_if_null(ctx, "s_done", sim_out_ptr(ctx, st, "s_done", out->completed, G, dev), G);
+        p.pop_counts = sim_out_ptr(ctx, st, "s_pops", out->pop_mode_counts, 3 * G, dev);
+        p.reg_state = sim_out_ptr(ctx, st, "s_rstate", out->reg_state, G, dev, true);
+        p.status = ctx->buf("s_status").as<int32_t>(G);
+        p.status_aux = ctx->buf("s_aux").as<int32_t>(G);
+        run_simulation(ctx, b, p, maxw);
+        for (const auto& c : ast.copies)
+            cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        for (const auto& c : st.copies)
+            cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        ctx->sync();
+        ctx->collect_timing();
+    });
+}
+
+extern "C" tbsim_status tbsim_default_regulator_config(int32_t n_workers, double median, tbsim_regulator_cfg* out) {
+    return guarded([&] {
+        // default_regulator_config, src/policies.cpp:139-151
+        const int64_t n = n_workers;
+        const int64_t tw = std::max<int64_t>(2, (n + 3) / 4);
+        *out = tbsim_regulator_cfg{};
+        out->task_window = tw;
+        out->s_inc = n;
+        out->k_inc = static_cast<double>(n) / median;
+        out->s_dec = tw;
+        out->c = (tw + 1) / 2;
+        out->dec_step = tw;
+        out->slope_samples = 8;
+    });
+}
+
+// --------------------------------------------------------------- generators
+
+struct tbsim_hostbatch {
+    tbsim_host::HostBatch hb;
+};
+
+extern "C" {
+
+tbsim_status tbsim_hostbatch_new(tbsim_hostbatch** out) {
+    return guarded([&] { *out = new tbsim_hostbatch(); });
+}
+tbsim_status tbsim_hostbatch_free(tbsim_hostbatch* hb) {
+    return guarded([&] { delete hb; });
+}
+
+tbsim_status tbsim_hostbatch_add_layered(tbsim_hostbatch* hb, int32_t n_tasks, int32_t n_layers, double p,
+                                         const uint64_t* seeds, int64_t n_seeds, int32_t n_threads) {
+    return guarded([&] {
+        std::vector<tbsim_host::GraphCSR> gs(n_seeds);
+        int nt = n_threads > 0 ? n_threads : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+        nt = static_cast<int>(std::min<int64_t>(nt, std::max<int64_t>(n_seeds, 1)));
+        std::vector<std::thread> pool;
+        std::exception_ptr err;
+        std::mutex mu;
+        for (int t = 0; t < nt; ++t)
+            pool.emplace_back([&, t] {
+                try {
+                    for (int64_t i = t; i < n_seeds; i += nt) gs[i] = tbsim_host::gen_layered(n_tasks, n_layers, p, seeds[i]);
+                } catch (...) {
+                    std::lock_guard<std::mutex> lk(mu);
+                    err = std::current_exception();
+                }
+            });
+        for (auto& th : pool) th.join();
+        if (err) std::rethrow_exception(err);
+        hb->hb.append_many(std::move(gs));
+    });
+}
+
+tbsim_status tbsim_hostbatch_add_cholesky(tbsim_hostbatch* hb, int32_t nb, int64_t bytes) {
+    return guarded([&] { hb->hb.append(tbsim_host::gen_cholesky(nb, bytes)); });
+}
+tbsim_status tbsim_hostbatch_add_lu(tbsim_hostbatch* hb, int32_t nb, int64_t bytes) {
+    return guarded([&] { hb->hb.append(tbsim_host::gen_lu(nb, bytes)); });
+}
+tbsim_status tbsim_hostbatch_add_qr(tbsim_hostbatch* hb, int32_t nb, int64_t bytes) {
+    return guarded([&] { hb->hb.append(tbsim_host::gen_qr(nb, bytes)); });
+}
+
+tbsim_status tbsim_hostbatch_add_csr(tbsim_hostbatch* hb, int32_t n, const int32_t* dep_off, const int32_t* dep,
+                                     const int32_t* in_off, const int32_t* in, const int32_t* out_off,
+                                     const int32_t* out, const int32_t* type, int32_t n_handles,
+                                     const int64_t* handle_bytes, const int64_t* task_id) {
+    return guarded([&] {
+        tbsim_host::GraphCSR g;
+        g.dep_off.assign(dep_off, dep_off + n + 1);
+        g.dep.assign(dep, dep + dep_off[n]);
+        g.in_off.assign(in_off, in_off + n + 1);
+        g.in.assign(in, in + in_off[n]);
+        g.out_off.assign(out_off, out_off + n + 1);
+        g.out.assign(out, out + out_off[n]);
+        g.type.assign(type, type + n);
+        g.handle_bytes.assign(handle_bytes, handle_bytes + n_handles);
+        hb->hb.append(g, task_id);
+    });
+}
+
+tbsim_status tbsim_hostbatch_desc(const tbsim_hostbatch* hb, tbsim_batch_desc* out) {
+    return guarded([&] { *out = const_cast<tbsim_hostbatch*>(hb)->hb.desc(); });
+}
+
+int32_t tbsim_type_count(void) { return tbsim_host::T_COUNT; }
+const char* tbsim_type_name(int32_t id) {
+    return id >= 0 && id < tbsim_host::T_COUNT ? tbsim_host::kTypeNames[id] : nullptr;
+}
+
+tbsim_status tbsim_default_costs(double* cpu, double* gpu) {
+    return guarded([&] {
+        // default_cost_table, src/platform.cpp:93-98 (GPU ms, CPU/GPU ratio);
+        // QR rows are builder-chosen (no reference counterpart)
+        struct Row { int32_t id; double gpu, ratio; };
+        static const Row rows[] = {
+            {tbsim_host::T_GEMM, 0.4, 10.0}, {tbsim_host::T_SYRK, 1.0, 10.0}, {tbsim_host::T_TRSM, 1.2, 10.0},
+            {tbsim_host::T_POTRF, 2.0, 3.0}, {tbsim_host::T_GETRF, 2.0, 3.0}, {tbsim_host::T_STENCIL, 0.8, 5.0},
+            {tbsim_host::T_LAYERK0, 0.5, 5.0}, {tbsim_host::T_LAYERK1, 1.0, 8.0}, {tbsim_host::T_LAYERK2, 2.0, 3.0},
+            {tbsim_host::T_LAYERK3, 4.0, 6.0}, {tbsim_host::T_UNIT, 1.0, 1.0}, {tbsim_host::T_GEQRT, 2.0, 3.0},
+            {tbsim_host::T_UNMQR, 0.8, 10.0}, {tbsim_host::T_TSQRT, 2.4, 3.0}, {tbsim_host::T_TSMQR, 0.8, 10.0}};
+        for (int i = 0; i < tbsim_host::T_COUNT; ++i) cpu[i] = gpu[i] = 0.0;
+        for (const Row& r : rows) {
+            gpu[r.id] = r.gpu;
+            cpu[r.id] = r.gpu * r.ratio;
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,628 @@
+// attributes.cu -- CSR ingestion and the attribute kernels of the INSPIRIT
+// hot path (reference: src/taskgraph.cpp, src/attributes.cpp).
+//
+//   k_ingest     successor CSR from the dependency CSR (build_index,
+//                taskgraph.cpp:11-43): counting sort + per-list sort, so every
+//                succ list is ascending with multi-edges kept.
+//   k_structure  one CTA per graph: level-synchronous Kahn frontiers
+//                (topological_layers, taskgraph.cpp:197-219) producing a
+//                level order; reverse level sweep for height (= depth_priority,
+//                attributes.cpp:255-265) and HEFT upward rank
+//                (attributes.cpp:234-253); lower-median GPU time
+//                (platform.cpp:233-240); (layer,type) calibration classes
+//                (attributes.cpp:193-201); and a live-range slot assignment
+//                for the source sweep.
+//   k_sweep      the efficiency kernel.  One CTA per (graph, tile of S
+//                sources): a forward max-plus sweep over the level order with
+//                the sources' distance columns resident in shared memory.
+//                dist(s,v) = gpu[v] + max_{u in pred(v)} dist(s,u) reproduces
+//                efficiency_of (attributes.cpp:110-137) bit-for-bit because FP64
+//                rounding is monotone, so max(a+g, b+g) == max(a,b)+g.  One pass
+//                bins every reachable descendant by the first calibration window
+//                it fits (k = -4..6, attributes.cpp:221-230), which yields all
+//                11 calibration evaluations, the final efficiency and the
+//                inspiring ability (reachable count, attributes.cpp:57-92) at once.
+//   k_finalize   per graph: per-class sums for each window, distinct reduced
+//                fractions (attributes.cpp:205-217), the strict-> winner, and the
+//                per-task efficiency / ability.
+#include <cfloat>
+#include <cstdint>
+
+#include "attributes.cuh"
+#include "blockscan.cuh"
+#include "common.cuh"
+
+namespace tbsim_dev {
+
+// ------------------------------------------------------------------ ingest
+
+__device__ void sort_small(int32_t* a, int32_t len) {
+    if (len <= 48) {
+        for (int32_t i = 1; i < len; ++i) {
+            int32_t x = a[i], j = i - 1;
+            while (j >= 0 && a[j] > x) { a[j + 1] = a[j]; --j; }
+            a[j + 1] = x;
+        }
+        return;
+    }
+    // heapsort for long lists
+    auto sift = [&](int32_t root, int32_t end) {
+        while (2 * root + 1 < end) {
+            int32_t c = 2 * root + 1;
+            if (c + 1 < end && a[c] < a[c + 1]) ++c;
+            if (a[root] >= a[c]) return;
+            int32_t t = a[root]; a[root] = a[c]; a[c] = t;
+            root = c;
+        }
+    };
+    for (int32_t i = len / 2 - 1; i >= 0; --i) sift(i, len);
+    for (int32_t end = len - 1; end > 0; --end) {
+        int32_t t = a[0]; a[0] = a[end]; a[end] = t;
+        sift(0, end);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_ingest(DevBatch b, int32_t* cursor_scratch) {
+    __shared__ int32_t warp_tot[32];
+    for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) {
+        const int64_t t0 = b.task_base[g];
+        const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
+        const int32_t* doff = b.dep_off + t0 + g;
+        const int32_t* dep = b.dep + b.edge_base[g];
+        int32_t* soff = b.succ_off + t0 + g;
+        int32_t* succ = b.succ + b.edge_base[g];
+        int32_t* cur = cursor_scratch + t0 + g;
+        for (int32_t i = threadIdx.x; i <= n; i += blockDim.x) soff[i] = 0;
+        __syncthreads();
+        for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
+            for (int32_t k = doff[v]; k < doff[v + 1]; ++k) atomicAdd(&soff[dep[k]], 1);
+        __syncthreads();
+        block_exclusive_scan_inplace(soff, n + 1, warp_tot);
+        for (int32_t i = threadIdx.x; i <= n; i += blockDim.x) cur[i] = soff[i];
+        __syncthreads();
+        for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
+            for (int32_t k = doff[v]; k < doff[v + 1]; ++k) succ[atomicAdd(&cur[dep[k]], 1)] = v;
+        __syncthreads();
+        for (int32_t u = threadIdx.x; u < n; u += blockDim.x) sort_small(succ + soff[u], soff[u + 1] - soff[u]);
+        __syncthreads();
+    }
+}
+
+// --------------------------------------------------------------- structure
+
+__global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* costs_g,
+                                                  const int32_t* cost_idx, AttrScratch s,
+                                                  int32_t want_rank) {
+    __shared__ DevCosts sc;
+    __shared__ double s_mean[kMaxTypes];
+    __shared__ int32_t s_tcount[kMaxTypes];
+    __shared__ int32_t warp_tot[32];
+    __shared__ int32_t s_tail, s_end, s_miss_gpu, s_miss_any;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    int32_t loaded = -1;
+    for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) {
+        const int64_t t0 = b.task_base[g];
+        const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
+        const int32_t* doff = b.dep_off + t0 + g;
+        const int32_t* dep = b.dep + b.edge_base[g];
+        const int32_t* soff = b.succ_off + t0 + g;
+        const int32_t* succ = b.succ + b.edge_base[g];
+        const int32_t* type = b.type + t0;
+        int32_t* indeg = s.tmp + t0 + g;
+        int32_t* order = s.order + t0;
+        int32_t* level = s.level + t0;
+        int32_t* lstart = s.lstart + t0 + g;
+        int32_t* height = s.height + t0;
+        int32_t* lastuse = s.lastuse + t0;
+        int32_t* slot = s.slot + t0;
+        double* rank = s.rank + t0;
+
+        // cost table of this graph (per-platform tables in a schedule batch)
+        const int32_t ci = cost_idx ? cost_idx[g] : 0;
+        if (ci != loaded) {
+            __syncthreads();
+            for (int i = tid; i < static_cast<int>(sizeof(DevCosts) / 8); i += nthr)
+                reinterpret_cast<double*>(&sc)[i] = reinterpret_cast<const double*>(costs_g + ci)[i];
+            __syncthreads();
+            if (tid < kMaxTypes) {
+                // mean_ms (platform.cpp:39-50): ((0 + cpu) + gpu) / count
+                double sum = 0.0;
+                int cnt = 0;
+                if (tid < sc.n_types && sc.cpu[tid] > 0.0) { sum += sc.cpu[tid]; ++cnt; }
+                if (tid < sc.n_types && sc.gpu[tid] > 0.0) { sum += sc.gpu[tid]; ++cnt; }
+                s_mean[tid] = cnt ? sum / cnt : 0.0;
+            }
+            loaded = ci;
+        }
+        const int32_t NT = b.n_types;
+        if (tid == 0) { s_tail = 0; s_miss_gpu = INT32_MAX; s_miss_any = INT32_MAX; }
+        if (tid < kMaxTypes) s_tcount[tid] = 0;
+        __syncthreads();
+        // ---- entries, cost diagnostics, type histogram
+        for (int32_t v = tid; v < n; v += nthr) {
+            indeg[v] = doff[v + 1] - doff[v];
+            level[v] = 0;
+            const int32_t ty = type[v];
+            const bool has_gpu = ty < NT && sc.gpu[ty] > 0.0;
+            const bool has_cpu = ty < NT && sc.cpu[ty] > 0.0;
+            if (!has_gpu) atomicMin(&s_miss_gpu, v);
+            if (!has_gpu && !has_cpu) atomicMin(&s_miss_any, v);
+            if (has_gpu) atomicAdd(&s_tcount[ty], 1);
+            if (indeg[v] == 0) order[atomicAdd(&s_tail, 1)] = v;
+        }
+        // ---- level-synchronous Kahn (topological_layers)
+        int32_t head = 0, L = 0;
+        if (tid == 0) lstart[0] = 0;
+        for (;;) {
+            __syncthreads();
+            if (tid == 0) s_end = s_tail;
+            __syncthreads();
+            const int32_t end = s_end;
+            if (end == head) break;
+            if (tid == 0) lstart[L + 1] = end;
+            for (int32_t i = head + tid; i < end; i += nthr) {
+                const int32_t u = order[i];
+                for (int32_t k = soff[u]; k < soff[u + 1]; ++k) {
+                    const int32_t v = succ[k];
+                    if (atomicSub(&indeg[v], 1) == 1) {
+                        level[v] = L + 1;
+                        order[atomicAdd(&s_tail, 1)] = v;
+                    }
+                }
+            }
+            head = end;
+            ++L;
+        }
+        const int32_t processed = head;
+        // ---- reverse level sweep: height (depth), upward rank, last use
+        for (int32_t lv = L - 1; lv >= 0; --lv) {
+            for (int32_t i = lstart[lv] + tid; i < lstart[lv + 1]; i += nthr) {
+                const int32_t u = order[i];
+                int32_t h = 0, lu = lv;
+                double best = 0.0;
+                for (int32_t k = soff[u]; k < soff[u + 1]; ++k) {
+                    const int32_t v = succ[k];
+                    h = max(h, height[v] + 1);
+                    best = fmax(best, rank[v]);
+                    lu = max(lu, level[v]);
+                }
+                height[u] = h;
+                lastuse[u] = lu;
+                if (want_rank) rank[u] = s_mean[type[u] < kMaxTypes ? type[u] : 0] + best;
+            }
+            __syncthreads();
+        }
+        // ---- slot assignment: group nodes by last-use level (counting sort)
+        int32_t* cnt = indeg;                // reuse [n+1]
+        int32_t* rel_order = s.rel_order + t0;
+        int32_t* cur = s.tmp2 + t0 + g;      // [n+1]
+        int32_t* fstack = s.fstack + t0;
+        for (int32_t i = tid; i <= L; i += nthr) cnt[i] = 0;
+        __syncthreads();
+        for (int32_t i = tid; i < processed; i += nthr) atomicAdd(&cnt[lastuse[order[i]]], 1);
+        __syncthreads();
+        block_exclusive_scan_inplace(cnt, L + 1, warp_tot);
+        for (int32_t i = tid; i <= L; i += nthr) cur[i] = cnt[i];
+        __syncthreads();
+        for (int32_t i = tid; i < processed; i += nthr) {
+            const int32_t v = order[i];
+            rel_order[atomicAdd(&cur[lastuse[v]], 1)] = v;
+        }
+        __syncthreads();
+        int32_t fs = 0, P = 0;
+        for (int32_t lv = 0; lv < L; ++lv) {
+            const int32_t a0 = lstart[lv], a = lstart[lv + 1] - a0;
+            for (int32_t i = tid; i < a; i += nthr)
+                slot[order[a0 + i]] = i < fs ? fstack[fs - 1 - i] : P + (i - fs);
+            __syncthreads();
+            const int32_t nfs = max(fs - a, 0);
+            P += max(a - fs, 0);
+            const int32_t r0 = cnt[lv], r = cnt[lv + 1] - r0;
+            for (int32_t j = tid; j < r; j += nthr) fstack[nfs + j] = slot[rel_order[r0 + j]];
+            __syncthreads();
+            fs = nfs + r;
+        }
+        // ---- predecessor slots (edge-major) and static priority
+        int32_t* pslot = s.pslot + b.edge_base[g];
+        for (int32_t v = tid; v < n; v += nthr)
+            for (int32_t k = doff[v]; k < doff[v + 1]; ++k) pslot[k] = slot[dep[k]];
+        // ---- calibration classes: dense ids of present (layer, type) pairs
+        int32_t* mark = s.cls_mark + t0 * NT;   // [L * NT] <= n * NT
+        const int64_t nkeys = static_cast<int64_t>(L) * NT;
+        for (int64_t i = tid; i < nkeys; i += nthr) mark[i] = 0;
+        __syncthreads();
+        for (int32_t v = tid; v < n; v += nthr) {
+            const int32_t ty = type[v];
+            if (ty < NT) mark[static_cast<int64_t>(level[v]) * NT + ty] = 1;
+        }
+        __syncthreads();
+        int32_t n_cls = 0;
+        {
+            // exclusive scan over nkeys (int64 length, int32 values)
+            int32_t carry = 0;
+            for (int64_t base = 0; base < nkeys; base += nthr) {
+                const int64_t i = base + tid;
+                int32_t x = i < nkeys ? mark[i] : 0;
+                int32_t tot;
+                int32_t inc = block_inclusive_scan(x, warp_tot, &tot);
+                if (i < nkeys) mark[i] = carry + inc - x;
+                carry += tot;
+            }
+            n_cls = carry;
+        }
+        __syncthreads();
+        for (int32_t v = tid; v < n; v += nthr) {
+            const int32_t ty = type[v];
+            s.cls[t0 + v] = ty < NT ? mark[static_cast<int64_t>(level[v]) * NT + ty] : 0;
+        }
+        // ---- per-graph scalars: lower median of GPU times
+        if (tid == 0) {
+            GraphInfo gi;
+            gi.n_levels = L;
+            gi.processed = processed;
+            gi.peak_slots = P;
+            gi.n_classes = n_cls;
+            gi.miss_gpu = s_miss_gpu == INT32_MAX ? -1 : s_miss_gpu;
+            gi.miss_any = s_miss_any == INT32_MAX ? -1 : s_miss_any;
+            gi.median = 0.0;
+            if (n > 0 && gi.miss_gpu < 0) {
+                // sort present types by GPU time; walk counts to rank (n-1)/2
+                int32_t ids[kMaxTypes];
+                int32_t m = 0;
+                for (int32_t t = 0; t < NT && t < kMaxTypes; ++t)
+                    if (s_tcount[t] > 0) {
+                        int32_t j = m++;
+                        while (j > 0 && sc.gpu[ids[j - 1]] > sc.gpu[t]) { ids[j] = ids[j - 1]; --j; }
+                        ids[j] = t;
+                    }
+                const int32_t want = (n - 1) / 2;
+                int32_t acc = 0;
+                for (int32_t j = 0; j < m; ++j) {
+                    acc += s_tcount[ids[j]];
+                    if (acc > want) { gi.median = sc.gpu[ids[j]]; break; }
+                }
+            }
+            s.info[g] = gi;
+            s.median[g] = gi.median;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------- sweep
+
+// Window bin of a reachable distance d (attributes.cpp:124): the first k with
+// d <= W_k, kBins-1 when beyond every window.  Fast path compares exponent
+// and mantissa bits at once: W_k = W_0 * 2^k exactly (ldexp), so for normal
+// thresholds bits(W_k) = bits(W_0) + k<<52 and non-negative doubles order
+// like their bit patterns.
+struct Thresholds {
+    int32_t mode;       // 0: calibration grid fast path, 1: ladder, 2: ability only
+    int64_t w0bits;     // bits(W_0)
+    double w[kWindows];
+};
+
+__device__ __forceinline__ int bin_of(double d, const Thresholds& th) {
+    if (th.mode == 0) {
+        const int64_t delta = __double_as_longlong(d) - th.w0bits;
+        if (delta <= 0) return 0;
+        const int64_t k = ((delta - 1) >> 52) + 1;
+        return k > kWindows ? kWindows : static_cast<int>(k);
+    }
+    if (th.mode == 2) return kWindows;
+    int k = 0;
+#pragma unroll
+    for (int j = 0; j < kWindows; ++j) k += d > th.w[j];
+    return k;
+}
+
+__device__ __forceinline__ void bump(uint64_t (&h)[4], int bin) {
+    // 12 counters of 21 bits, three per word
+    const int w = bin / 3;
+    const uint64_t inc = 1ull << (21 * (bin - 3 * w));
+    h[0] += w == 0 ? inc : 0ull;
+    h[1] += w == 1 ? inc : 0ull;
+    h[2] += w == 2 ? inc : 0ull;
+    h[3] += w == 3 ? inc : 0ull;
+}
+
+__device__ Thresholds make_thresholds(int32_t mode_req, double w0_or_unit) {
+    Thresholds th;
+    if (mode_req == SWEEP_ABILITY) {
+        th.mode = 2;
+        th.w0bits = 0;
+        for (int j = 0; j < kWindows; ++j) th.w[j] = 0.0;
+        return th;
+    }
+    if (mode_req == SWEEP_SINGLE) {
+        th.mode = 1;
+        th.w0bits = 0;
+        for (int j = 0; j < kWindows; ++j) th.w[j] = w0_or_unit;
+        return th;
+    }
+    for (int j = 0; j < kWindows; ++j) th.w[j] = ldexp(w0_or_unit, j - 4);
+    th.w0bits = __double_as_longlong(th.w[0]);
+    const bool normal = th.w[0] >= DBL_MIN && th.w[kWindows - 1] <= DBL_MAX;
+    th.mode = normal ? 0 : 1;
+    return th;
+}
+
+// Group of GL lanes handles one node for S sources (S/GL per lane).
+template <int S>
+__device__ void sweep_tile(const DevBatch& b, const AttrScratch& s, const DevCosts& sc, int64_t g,
+                           int32_t tile, double* win, int32_t P, const Thresholds& th,
+                           unsigned long long* s_hist) {
+    constexpr int GL = S < 32 ? S : 32;   // lanes per node group
+    constexpr int SPL = S / GL;           // sources per lane
+    constexpr int GPW = 32 / GL;          // groups per warp
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int gl = lane % GL, grp = lane / GL;
+    const unsigned gmask = GL == 32 ? 0xffffffffu : (((1u << GL) - 1u) << (grp * GL));
+
+    const int64_t t0 = b.task_base[g];
+    const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
+    const int32_t* doff = b.dep_off + t0 + g;
+    const int32_t* type = b.type + t0;
+    const int32_t* order = s.order + t0;
+    const int32_t* level = s.level + t0;
+    const int32_t* lstart = s.lstart + t0 + g;
+    const int32_t* slot = s.slot + t0;
+    const int32_t* pslot = s.pslot + b.edge_base[g];
+    const GraphInfo gi = s.info[g];
+    const int32_t first = tile * S;
+    const int32_t nsrc = min(S, gi.processed - first);
+
+    for (int64_t i = threadIdx.x; i < static_cast<int64_t>(P) * S; i += blockDim.x) win[i] = -1.0;
+    for (int i = threadIdx.x; i < S * 4; i += blockDim.x) s_hist[i] = 0ull;
+    int32_t src[SPL];
+    uint64_t hist[SPL][4];
+#pragma unroll
+    for (int q = 0; q < SPL; ++q) {
+        const int si = gl * SPL + q;
+        src[q] = si < nsrc ? order[first + si] : -1;
+        hist[q][0] = hist[q][1] = hist[q][2] = hist[q][3] = 0;
+    }
+    const int32_t La = level[order[first]];
+    __syncthreads();
+
+    for (int32_t lv = La; lv < gi.n_levels; ++lv) {
+        const int32_t a0 = lstart[lv], a1 = lstart[lv + 1];
+        // groups are independent: every lane of a group sees the same node
+        for (int32_t i = a0 + warp * GPW + grp; i < a1; i += nwarps * GPW) {
+            const int32_t v = order[i];
+            const int32_t p0 = doff[v];
+            const int32_t deg = doff[v + 1] - p0;
+            const double gv = th.mode == 2 ? 1.0 : cost_of(sc, type[v], 1);
+            double m[SPL];
+#pragma unroll
+            for (int q = 0; q < SPL; ++q) m[q] = -1.0;
+            for (int32_t c = 0; c < deg; c += GL) {
+                const int32_t myps = (c + gl < deg) ? pslot[p0 + c + gl] : 0;
+                const int32_t lim = min(GL, deg - c);
+                for (int32_t j = 0; j < lim; ++j) {
+                    const int32_t ps = __shfl_sync(gmask, myps, grp * GL + j);
+                    const double* row = win + static_cast<int64_t>(ps) * S + gl * SPL;
+                    if constexpr (SPL == 2) {
+                        const double2 x = *reinterpret_cast<const double2*>(row);
+                        m[0] = fmax(m[0], x.x);
+                        m[1] = fmax(m[1], x.y);
+                    } else {
+                        m[0] = fmax(m[0], row[0]);
+                    }
+                }
+            }
+            double* out = win + static_cast<int64_t>(slot[v]) * S + gl * SPL;
+#pragma unroll
+            for (int q = 0; q < SPL; ++q) {
+                double d;
+                if (v == src[q]) {
+                    d = 0.0;
+                } else {
+                    d = m[q] < 0.0 ? -1.0 : m[q] + gv;
+                    if (d >= 0.0 && src[q] >= 0) bump(hist[q], bin_of(d, th));
+                }
+                out[q] = d;
+            }
+        }
+        __syncthreads();
+    }
+    // every group saw a different subset of nodes: reduce the packed
+    // partial histograms (fields never carry: totals stay < 2^21)
+#pragma unroll
+    for (int q = 0; q < SPL; ++q)
+        if (src[q] >= 0)
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+                if (hist[q][w]) atomicAdd(&s_hist[(gl * SPL + q) * 4 + w], static_cast<unsigned long long>(hist[q][w]));
+    __syncthreads();
+    for (int i = threadIdx.x; i < nsrc * 4; i += blockDim.x)
+        s.hist[(t0 + order[first + i / 4]) * 4 + (i & 3)] = s_hist[i];
+}
+
+__global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs_g,
+                                              const int32_t* cost_idx, AttrScratch s,
+                                              int32_t sweep_mode, const double* unit_time,
+                                              int64_t total_tiles, unsigned long long* work_counter,
+                                              int64_t smem_bytes, double* gwin, int64_t gwin_stride) {
+    extern __shared__ double win_smem[];
+    __shared__ DevCosts sc;
+    __shared__ int64_t s_item;
+    __shared__ unsigned long long s_hist[64 * 4];
+    int32_t loaded = -1;
+    if (total_tiles < 0) total_tiles = s.tile_base[b.G];
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(work_counter, 1ull);
+        __syncthreads();
+        const int64_t item = s_item;
+        __syncthreads();
+        if (item >= total_tiles) break;
+        // locate graph: tile_base is [G+1] prefix of tiles per graph
+        int64_t lo = 0, hi = b.G;
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (s.tile_base[mid] <= item) lo = mid; else hi = mid;
+        }
+        const int64_t g = lo;
+        const int32_t tile = static_cast<int32_t>(item - s.tile_base[g]);
+        const int32_t ci = cost_idx ? cost_idx[g] : 0;
+        if (ci != loaded) {  // uniform: every thread read the same item
+            for (int i = threadIdx.x; i < static_cast<int>(sizeof(DevCosts) / 8); i += blockDim.x)
+                reinterpret_cast<double*>(&sc)[i] = reinterpret_cast<const double*>(costs_g + ci)[i];
+            __syncthreads();
+            loaded = ci;
+        }
+        const GraphInfo gi = s.info[g];
+        if (gi.processed != static_cast<int32_t>(b.task_base[g + 1] - b.task_base[g])) continue;  // cyclic
+        const int32_t P = max(gi.peak_slots, 1);
+        Thresholds th;
+        if (sweep_mode == SWEEP_SINGLE) th = make_thresholds(SWEEP_SINGLE, unit_time[g]);
+        else th = make_thresholds(sweep_mode, 2.0 * gi.median);
+        const int32_t S = s.tile_s[g];
+        double* win = win_smem;
+        if (static_cast<int64_t>(P) * S * 8 > smem_bytes) win = gwin + blockIdx.x * gwin_stride;
+        switch (S) {
+            case 64: sweep_tile<64>(b, s, sc, g, tile, win, P, th, s_hist); break;
+            case 32: sweep_tile<32>(b, s, sc, g, tile, win, P, th, s_hist); break;
+            case 16: sweep_tile<16>(b, s, sc, g, tile, win, P, th, s_hist); break;
+            default: sweep_tile<8>(b, s, sc, g, tile, win, P, th, s_hist); break;
+        }
+        __syncthreads();
+    }
+}
+
+// Tiles per graph and their prefix (single CTA; G can be large).
+__global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s) {
+    __shared__ int32_t warp_tot[32];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < b.G; base += blockDim.x) {
+        const int64_t g = base + threadIdx.x;
+        int32_t tiles = 0;
+        if (g < b.G) {
+            const GraphInfo gi = s.info[g];
+            const int32_t P = max(gi.peak_slots, 1);
+            int32_t S = 8;
+            if (force_s) S = force_s;
+            else if (static_cast<int64_t>(P) * 64 * 8 <= smem_bytes) S = 64;
+            else if (static_cast<int64_t>(P) * 32 * 8 <= smem_bytes) S = 32;
+            else if (static_cast<int64_t>(P) * 16 * 8 <= smem_bytes) S = 16;
+            else if (static_cast<int64_t>(P) * 8 * 8 <= smem_bytes) S = 8;
+            else S = 32;  // global-memory window
+            s.tile_s[g] = S;
+            tiles = (gi.processed + S - 1) / S;
+        }
+        int32_t tot;
+        const int32_t inc = block_inclusive_scan(tiles, warp_tot, &tot);
+        if (g < b.G) s.tile_base[g] = carry + inc - tiles;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) s.tile_base[b.G] = carry;
+}
+
+// ---------------------------------------------------------------- finalize
+
+__device__ __forceinline__ int64_t field(const uint64_t* h, int bin) {
+    return static_cast<int64_t>((h[bin / 3] >> (21 * (bin % 3))) & ((1ull << 21) - 1));
+}
+
+__device__ int64_t gcd64(int64_t a, int64_t b) {
+    a = a < 0 ? -a : a;
+    b = b < 0 ? -b : b;
+    while (b) { const int64_t t = a % b; a = b; b = t; }
+    return a;
+}
+
+__global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int32_t sweep_mode,
+                                                 const double* unit_time_in, AttrOutDev o,
+                                                 int64_t* cls_scratch, int64_t cls_stride) {
+    __shared__ int32_t s_score[kWindows];
+    int64_t* sums = cls_scratch + blockIdx.x * cls_stride;  // [C][kWindows] then cnt[C]
+    for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) {
+        const int64_t t0 = b.task_base[g];
+        const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
+        const GraphInfo gi = s.info[g];
+        if (gi.processed != n) continue;
+        const uint64_t* hist = s.hist + t0 * 4;
+        int best = 0;
+        if (sweep_mode == SWEEP_CALIBRATE) {
+            const int32_t C = gi.n_classes;
+            int64_t* cnt = sums + static_cast<int64_t>(C) * kWindows;
+            for (int64_t i = threadIdx.x; i < static_cast<int64_t>(C) * (kWindows + 1); i += blockDim.x) sums[i] = 0;
+            if (threadIdx.x < kWindows) s_score[threadIdx.x] = 0;
+            __syncthreads();
+            for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+                const int32_t c = s.cls[t0 + v];
+                const uint64_t* h = hist + static_cast<int64_t>(v) * 4;
+                int64_t acc = 0;
+                for (int k = 0; k < kWindows; ++k) {
+                    acc += field(h, k);
+                    if (acc) atomicAdd(reinterpret_cast<unsigned long long*>(&sums[static_cast<int64_t>(c) * kWindows + k]),
+                                       static_cast<unsigned long long>(acc));
+                }
+                atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[c]), 1ull);
+            }
+            __syncthreads();
+            // distinct reduced fractions per window (attributes.cpp:205-217)
+            for (int64_t item = threadIdx.x; item < static_cast<int64_t>(C) * kWindows; item += blockDim.x) {
+                const int32_t c = static_cast<int32_t>(item / kWindows);
+                const int k = static_cast<int>(item % kWindows);
+                const int64_t sc_ = sums[static_cast<int64_t>(c) * kWindows + k], cc = cnt[c];
+                const int64_t d = gcd64(sc_ == 0 ? cc : sc_, cc);
+                const int64_t a = sc_ / d, q = cc / d;
+                bool first = true;
+                for (int32_t c2 = 0; c2 < c && first; ++c2) {
+                    const int64_t s2 = sums[static_cast<int64_t>(c2) * kWindows + k], c2c = cnt[c2];
+                    const int64_t d2 = gcd64(s2 == 0 ? c2c : s2, c2c);
+                    if (s2 / d2 == a && c2c / d2 == q) first = false;
+                }
+                if (first) atomicAdd(&s_score[k], 1);
+            }
+            __syncthreads();
+            int64_t best_score = -1;
+            for (int k = 0; k < kWindows; ++k)
+                if (s_score[k] > best_score) { best_score = s_score[k]; best = k; }
+            if (threadIdx.x == 0) {
+                const double w0 = 2.0 * gi.median;
+                if (o.unit_time_ms) o.unit_time_ms[g] = ldexp(w0, best - 4);
+                if (o.w0_ms) o.w0_ms[g] = w0;
+                if (o.best_score) o.best_score[g] = best_score;
+                if (o.w0_score) o.w0_score[g] = s_score[4];
+                if (o.evaluations) o.evaluations[g] = kWindows;
+            }
+        }
+        for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+            const uint64_t* h = hist + static_cast<int64_t>(v) * 4;
+            int64_t eff = 0, abil = 0;
+            for (int k = 0; k < kBins; ++k) {
+                const int64_t f = field(h, k);
+                if (k <= best) eff += f;
+                abil += f;
+            }
+            if (o.efficiency && sweep_mode != SWEEP_ABILITY) o.efficiency[t0 + v] = eff;
+            if (o.ability) o.ability[t0 + v] = abil;
+        }
+        __syncthreads();
+    }
+}
+
+// Per-task outputs of the structure pass (layers, depth, static priority).
+__global__ void k_structure_out(DevBatch b, AttrScratch s, AttrOutDev o, int32_t prio_kind, int32_t want_prio) {
+    const int64_t T = b.T;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < T;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (o.layer) o.layer[i] = s.level[i];
+        if (o.depth) o.depth[i] = s.height[i];
+        if (want_prio && o.static_priority) {
+            int64_t p = 0;
+            if (prio_kind == TBSIM_PRIO_UPWARD_RANK) p = static_cast<int64_t>(s.rank[i] * 1000.0);
+            else if (prio_kind == TBSIM_PRIO_DEPTH) p = s.height[i];
+            o.static_priority[i] = p;
+        }
+    }
+}
+
+}  // namespace tbsim_dev

@@ -1,0 +1,76 @@
+// attributes.cuh -- scratch layout and launch interface of the attribute kernels.
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace tbsim_dev {
+
+enum SweepMode : int32_t {
+    SWEEP_CALIBRATE = 0,  // 11-window calibration grid (also final efficiency + ability)
+    SWEEP_SINGLE = 1,     // efficiency at a caller-given window (unit_time_ms[g])
+    SWEEP_ABILITY = 2,    // reachable counts only
+};
+
+struct GraphInfo {
+    int32_t n_levels;    // topological layers (0 for an empty graph)
+    int32_t processed;   // tasks released by Kahn (< n means a cycle)
+    int32_t peak_slots;  // distance-column slots the sweep needs
+    int32_t n_classes;   // distinct (layer, type) calibration classes
+    int32_t miss_gpu;    // first task position without a GPU cost, -1 if none
+    int32_t miss_any;    // first task position without any cost, -1 if none
+    double median;       // lower-median GPU time (valid when miss_gpu < 0 and n > 0)
+};
+
+// Device scratch of one attribute pass over a batch (T tasks, E edges,
+// G graphs, NT types).
+struct AttrScratch {
+    int32_t* tmp;        // [T+G]
+    int32_t* tmp2;       // [T+G]
+    int32_t* order;      // [T]  level order (local positions)
+    int32_t* level;      // [T]
+    int32_t* lstart;     // [T+G] per graph n_levels+1 offsets into order
+    int32_t* height;     // [T]
+    int32_t* lastuse;    // [T]
+    int32_t* slot;       // [T]
+    int32_t* rel_order;  // [T]
+    int32_t* fstack;     // [T]
+    int32_t* cls;        // [T]
+    int32_t* cls_mark;   // [T*NT]
+    int32_t* pslot;      // [E]
+    double* rank;        // [T]
+    uint64_t* hist;      // [4T] packed 12 x 21-bit window bins per source
+    GraphInfo* info;     // [G]
+    double* median;      // [G] lower-median GPU time (regulator defaults)
+    int64_t* tile_base;  // [G+1]
+    int32_t* tile_s;     // [G]
+};
+
+struct AttrOutDev {
+    int64_t* ability;
+    int64_t* efficiency;
+    int64_t* static_priority;
+    int64_t* depth;
+    int32_t* layer;
+    double* unit_time_ms;
+    double* w0_ms;
+    int64_t* best_score;
+    int64_t* w0_score;
+    int32_t* evaluations;
+};
+
+__global__ void k_ingest(DevBatch b, int32_t* cursor_scratch);
+__global__ void k_structure(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
+                            int32_t want_rank);
+__global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s);
+__global__ void k_sweep(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
+                        int32_t sweep_mode,
+                        const double* unit_time, int64_t total_tiles, unsigned long long* work_counter,
+                        int64_t smem_bytes, double* gwin, int64_t gwin_stride);
+__global__ void k_finalize(DevBatch b, AttrScratch s, int32_t sweep_mode, const double* unit_time_in,
+                           AttrOutDev o, int64_t* cls_scratch, int64_t cls_stride);
+__global__ void k_structure_out(DevBatch b, AttrScratch s, AttrOutDev o, int32_t prio_kind,
+                                int32_t want_prio);
+
+}  // namespace tbsim_dev

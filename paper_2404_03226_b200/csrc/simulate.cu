@@ -1,0 +1,613 @@
+// simulate.cu -- batched, bit-exact replay of the reference's discrete-event
+// list scheduler (src/engine.cpp) with its push/pop rules and the INSPIRIT
+// Nready regulator (src/policies.cpp).  One warp simulates one DAG; lane w owns
+// worker w (and w+32 when the platform has more than 32 workers).
+//
+// Event order without a heap.  The reference orders events by (time, seq)
+// with seq a global enqueue counter (engine.cpp:16-31).  TaskReady/PushDone
+// are always enqueued at `now` (engine.cpp:121,183), while TransferDone and
+// TaskDone are enqueued strictly in the future (transfer > 0, exec > 0,
+// engine.cpp:164-165; checked below, GS_DEGENERATE_TIME otherwise).  Hence at
+// each time T the reference processes (1) every worker event stamped T in
+// enqueue order, then (2) the TaskReady events those created, in creation
+// order, then (3) the matching PushDones in the same order.  Each worker holds
+// at most one pending TransferDone and one TaskDone, so the heap collapses to
+// two slots per lane plus a ready list, and "next event" is a warp-wide
+// (time, seq) min done with REDUX on 32-bit halves.
+//
+// worker_free_at (engine.cpp:53-59) is cached per lane and extended with
+// `+= exec` on every push (the same left-to-right sum the reference forms);
+// after a dispatch it is recomputed from busy_until in queue order.
+#include <climits>
+#include <cstdint>
+
+#include "common.cuh"
+#include "simulate.cuh"
+
+namespace tbsim_dev {
+
+namespace {
+
+constexpr uint32_t kNone = 0xffffffffu;
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ uint64_t ord_f64(double x) {
+    const uint64_t u = dbits(x);
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ uint64_t ord_i64(int64_t x) {
+    return static_cast<uint64_t>(x) ^ 0x8000000000000000ull;
+}
+
+template <int WPL>
+struct Sim {
+    // ---- graph
+    int64_t g, t0;
+    int32_t n, nh;
+    const int32_t *doff, *soff, *succ, *ioff, *in, *ooff, *out, *type;
+    const int64_t* hbytes;
+    const DevPlatform* pf;
+    int32_t W, nn;
+    double lat;
+    int32_t policy;
+    const int64_t *ability, *efficiency, *prio;
+    // ---- per-warp state memory
+    int32_t* unmet;
+    uint32_t* resid;
+    int32_t* ready;
+    int32_t* queue;
+    double* samp_t;
+    int64_t* samp_n;
+    int32_t qcap;
+    // ---- lane-owned workers
+    int32_t kind[WPL], node[WPL], qlen[WPL];
+    bool busy[WPL], fdirty[WPL];
+    double busy_until[WPL], fsum[WPL];
+    double xt[WPL], dt[WPL];
+    uint32_t xs[WPL], ds[WPL];
+    int32_t xtask[WPL], dtask[WPL];
+    // ---- warp-uniform scalars
+    int lane;
+    double now, makespan;
+    int64_t nready;
+    int32_t completed, rcount;
+    uint32_t seq;
+    int64_t n_push, n_pop, n_samp;
+    int64_t pop0, pop1, pop2;
+    int32_t status, aux;
+    // regulator (RegulatorState, policies.hpp:89-98) + ring of samples
+    int32_t mode, phase;
+    int64_t peak, prev_nready, last_trigger, s_dec_count;
+    double cur_k;
+    int32_t r_head, r_count;
+    tbsim_regulator_cfg cfg;
+    const SimParams* P;
+
+    __device__ __forceinline__ double cost(int32_t ty, int32_t k) const {
+        return k ? __ldg(&pf->costs.gpu[ty]) : __ldg(&pf->costs.cpu[ty]);
+    }
+
+    // transfer_one_ms (engine.cpp:86-103): fastest resident copy, ties to the
+    // lowest node; Platform::transfer_time_ms (platform.cpp:56-63).
+    __device__ __forceinline__ double transfer_one(int32_t h, int32_t to) const {
+        const uint32_t m = resid[h];
+        if ((m >> to) & 1u) return 0.0;
+        int32_t best = 0;
+        double bbw = -1.0;
+        for (uint32_t mm = m; mm; mm &= mm - 1) {
+            const int32_t nd = __ffs(mm) - 1;
+            const double bw = __ldg(&pf->bw[nd * kMaxNodes + to]);
+            if (bw > bbw) { bbw = bw; best = nd; }
+        }
+        return lat + static_cast<double>(__ldg(&hbytes[h])) / __ldg(&pf->bw[best * kMaxNodes + to]);
+    }
+    // transfer_total_ms (engine.cpp:105-110): inputs in order
+    __device__ __forceinline__ double transfer_total(int32_t task, int32_t to) const {
+        double total = 0.0;
+        for (int32_t k = __ldg(&ioff[task]); k < __ldg(&ioff[task + 1]); ++k) total += transfer_one(__ldg(&in[k]), to);
+        return total;
+    }
+    // resident_fraction (engine.cpp:63-74)
+    __device__ __forceinline__ double resident_fraction(int32_t task, int32_t nd) const {
+        const int32_t k0 = __ldg(&ioff[task]), k1 = __ldg(&ioff[task + 1]);
+        if (k0 == k1) return 1.0;
+        int64_t total = 0, local = 0;
+        for (int32_t k = k0; k < k1; ++k) {
+            const int32_t h = __ldg(&in[k]);
+            const int64_t by = __ldg(&hbytes[h]);
+            total += by;
+            if ((resid[h] >> nd) & 1u) local += by;
+        }
+        return static_cast<double>(local) / static_cast<double>(total);
+    }
+
+    // ---------------------------------------------------------- regulator
+    __device__ __forceinline__ double calculate_k() const {  // policies.cpp:153-169
+        if (r_count < 2) return 0.0;
+        double sx = 0.0, sy = 0.0;
+        for (int i = 0; i < r_count; ++i) {
+            const int idx = (r_head + i) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+            sx += samp_t[idx];
+            sy += static_cast<double>(samp_n[idx]);
+        }
+        const double dn = static_cast<double>(r_count);
+        const double mx = sx / dn, my = sy / dn;
+        double sxx = 0.0, sxy = 0.0;
+        for (int i = 0; i < r_count; ++i) {
+            const int idx = (r_head + i) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+            const double dx = samp_t[idx] - mx;
+            sxx += dx * dx;
+            sxy += dx * (static_cast<double>(samp_n[idx]) - my);
+        }
+        if (sxx == 0.0) return 0.0;
+        return sxy / sxx;
+    }
+
+    __device__ __forceinline__ void regulator_step(int64_t cur) {  // policies.cpp:171-203
+        __syncwarp();
+        const int idx = (r_head + r_count) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+        if (lane == 0) { samp_t[idx] = now; samp_n[idx] = cur; }
+        __syncwarp();
+        if (r_count < TBSIM_MAX_SLOPE_SAMPLES) ++r_count;
+        else r_head = (r_head + 1) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+        while (r_count > cfg.slope_samples) {
+            r_head = (r_head + 1) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+            --r_count;
+        }
+        const int64_t d = cur - last_trigger;
+        if ((d < 0 ? -d : d) < cfg.task_window) return;
+        last_trigger = cur;
+        peak = cur > peak ? cur : peak;
+        phase = cur >= peak - cfg.dec_step ? TBSIM_PHASE_INC : TBSIM_PHASE_DEC;
+        if (phase == TBSIM_PHASE_INC) {
+            if (cur - prev_nready >= cfg.s_inc) {
+                cur_k = calculate_k();
+                if (cur_k < cfg.k_inc) mode = TBSIM_MODE_EFFICIENCY;
+                else if (cur_k > cfg.k_inc) mode = TBSIM_MODE_ABILITY;
+            }
+        } else {
+            if (cur > peak - cfg.s_dec * s_dec_count) {
+                mode = TBSIM_MODE_ABILITY;
+            } else if (cur <= peak - cfg.s_dec * (s_dec_count + 1) + cfg.c) {
+                mode = TBSIM_MODE_LOCALITY;
+                if (cur <= peak - cfg.s_dec * (s_dec_count + 1)) s_dec_count += 1;
+            }
+        }
+        prev_nready = cur;
+    }
+
+    __device__ __forceinline__ void queue_event() {
+        if (P->sample_time && lane == 0) {
+            P->sample_time[2 * t0 + n_samp] = now;
+            P->sample_nready[2 * t0 + n_samp] = nready;
+        }
+        ++n_samp;
+        if (policy == TBSIM_POLICY_INSPIRIT) regulator_step(nready);
+    }
+
+    // ---------------------------------------------------------- push rules
+    __device__ __forceinline__ void refresh_free() {
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+            const int32_t w = lane + 32 * j;
+            if (w < W && busy[j] && fdirty[j]) {
+                double t = busy_until[j];
+                const int32_t* q = queue + static_cast<int64_t>(w) * qcap;
+                for (int32_t i = 0; i < qlen[j]; ++i) t += cost(static_cast<uint32_t>(q[i]) >> 24, kind[j]);
+                fsum[j] = t;
+                fdirty[j] = false;
+            }
+        }
+    }
+
+    // push_fifo / push_dm / push_dmda (policies.cpp:37-72): argmin over
+    // capable workers, strict < so ties keep the lowest id.
+    __device__ __forceinline__ int32_t select_worker(int32_t task, int32_t ty) {
+        if (policy != TBSIM_POLICY_FIFO) refresh_free();
+        uint64_t bk = ~0ull;
+        int32_t bw = INT_MAX;
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+            const int32_t w = lane + 32 * j;
+            if (w >= W) continue;
+            const double ce = cost(ty, kind[j]);
+            if (!(ce > 0.0)) continue;
+            double key;
+            if (policy == TBSIM_POLICY_FIFO) {
+                key = static_cast<double>(qlen[j]) + (busy[j] ? 1.0 : 0.0);
+            } else {
+                const double fa = busy[j] ? fsum[j] : now;
+                const double st = now < fa ? fa : now;  // std::max(now, free_at)
+                if (policy == TBSIM_POLICY_DM) key = st + ce;
+                else key = (st + transfer_total(task, node[j])) + ce;
+            }
+            const uint64_t kb = ord_f64(key);
+            if (kb < bk) { bk = kb; bw = w; }
+        }
+        const uint64_t mk = warp_min_u64(bk);
+        const int32_t w = __reduce_min_sync(kFull, bk == mk ? bw : INT_MAX);
+        return mk == ~0ull ? -1 : w;
+    }
+
+    // ----------------------------------------------------------- pop rules
+    // pop_fifo / pop_priority / pop_adaptive (policies.cpp:74-137) as one
+    // lexicographic argmax over (k0, k1, static priority, -seq); queue
+    // position is insertion (= seq) order.
+    __device__ __forceinline__ int32_t select_entry(int32_t w, int32_t ql, int32_t nd) {
+        if (policy <= TBSIM_POLICY_DMDA) return 0;
+        int32_t m = TBSIM_MODE_EFFICIENCY;
+        if (policy == TBSIM_POLICY_INSPIRIT) {
+            m = mode;
+            pop0 += m == 0;
+            pop1 += m == 1;
+            pop2 += m == 2;
+        }
+        const int32_t* q = queue + static_cast<int64_t>(w) * qcap;
+        uint64_t b0 = 0, b1 = 0, b2 = 0;
+        int32_t bpos = INT_MAX;
+        for (int32_t i = lane; i < ql; i += 32) {
+            const int32_t t = q[i] & 0xffffff;
+            uint64_t k0, k1;
+            if (policy == TBSIM_POLICY_DMDAP) {
+                k0 = k1 = 1;
+            } else if (m == TBSIM_MODE_ABILITY) {
+                k0 = ord_f64(ability ? static_cast<double>(__ldg(&ability[t0 + t])) : 0.0);
+                k1 = ord_f64(0.0);
+            } else if (m == TBSIM_MODE_EFFICIENCY) {
+                k0 = ord_f64(efficiency ? static_cast<double>(__ldg(&efficiency[t0 + t])) : 0.0);
+                k1 = ord_f64(0.0);
+            } else {
+                k0 = ord_f64(resident_fraction(t, nd));
+                k1 = ord_f64(efficiency ? static_cast<double>(__ldg(&efficiency[t0 + t])) : 0.0);
+            }
+            const uint64_t k2 = ord_i64(prio ? __ldg(&prio[t0 + t]) : 0);
+            const bool better = bpos == INT_MAX || k0 > b0 ||
+                                (k0 == b0 && (k1 > b1 || (k1 == b1 && k2 > b2)));
+            if (better) { b0 = k0; b1 = k1; b2 = k2; bpos = i; }
+        }
+        const bool has = bpos != INT_MAX;
+        const uint64_t m0 = warp_max_u64(has ? b0 : 0);
+        const bool c0 = has && b0 == m0;
+        const uint64_t m1 = warp_max_u64(c0 ? b1 : 0);
+        const bool c1 = c0 && b1 == m1;
+        const uint64_t m2 = warp_max_u64(c1 ? b2 : 0);
+        const bool c2 = c1 && b2 == m2;
+        return __reduce_min_sync(kFull, c2 ? bpos : INT_MAX);
+    }
+
+    // ------------------------------------------------------------- engine
+    __device__ __forceinline__ void maybe_dispatch(int32_t w) {  // engine.cpp:143-166
+        const int j = w >> 5, owner = w & 31;
+        int32_t ql = 0, bz = 0, kd = 0, nd = 0;
+#pragma unroll
+        for (int jj = 0; jj < WPL; ++jj)
+            if (jj == j) { ql = qlen[jj]; bz = busy[jj]; kd = kind[jj]; nd = node[jj]; }
+        ql = __shfl_sync(kFull, ql, owner);
+        bz = __shfl_sync(kFull, bz, owner);
+        kd = __shfl_sync(kFull, kd, owner);
+        nd = __shfl_sync(kFull, nd, owner);
+        if (bz || ql == 0) return;
+        const int32_t pick = select_entry(w, ql, nd);
+        int32_t* q = queue + static_cast<int64_t>(w) * qcap;
+        const uint32_t e = static_cast<uint32_t>(q[pick]);
+        __syncwarp();
+        for (int32_t base = pick; base < ql - 1; base += 32) {
+            const int32_t i = base + lane;
+            const int32_t val = i < ql - 1 ? q[i + 1] : 0;
+            __syncwarp();
+            if (i < ql - 1) q[i] = val;
+            __syncwarp();
+        }
+        const int32_t task = static_cast<int32_t>(e & 0xffffffu);
+        const int32_t ty = static_cast<int32_t>(e >> 24);
+        nready -= 1;
+        if (P->pop_time && lane == 0) {
+            P->pop_time[t0 + n_pop] = now;
+            P->pop_task[t0 + n_pop] = task;
+            P->pop_worker[t0 + n_pop] = w;
+        }
+        ++n_pop;
+        queue_event();
+        const double xfer = transfer_total(task, nd);
+        const double exec = cost(ty, kd);
+        const double start = now + xfer;
+        const double end = start + exec;
+        if ((xfer > 0.0 && !(start > now)) || !(end > now)) {
+            status = GS_DEGENERATE_TIME;
+            aux = task;
+            return;
+        }
+        if (lane == 0) {
+            P->worker[t0 + task] = w;
+            P->start_ms[t0 + task] = start;
+            P->end_ms[t0 + task] = end;
+        }
+        const uint32_t sx = seq;
+        if (xfer > 0.0) ++seq;
+        const uint32_t sd = seq++;
+#pragma unroll
+        for (int jj = 0; jj < WPL; ++jj)
+            if (jj == j && lane == owner) {
+                qlen[jj] -= 1;
+                busy[jj] = true;
+                busy_until[jj] = end;
+                fdirty[jj] = true;
+                if (xfer > 0.0) { xt[jj] = start; xs[jj] = sx; xtask[jj] = task; }
+                dt[jj] = end; ds[jj] = sd; dtask[jj] = task;
+            }
+    }
+
+    __device__ __forceinline__ void on_push(int32_t task) {  // engine.cpp:124-141
+        const int32_t ty = __ldg(&type[task]);
+        const int32_t w = select_worker(task, ty);
+        if (w < 0) { status = GS_NO_WORKER; aux = task; return; }
+        const int j = w >> 5, owner = w & 31;
+        int32_t ovf = 0;
+#pragma unroll
+        for (int jj = 0; jj < WPL; ++jj)
+            if (jj == j && lane == owner) {
+                if (qlen[jj] >= qcap) {
+                    ovf = 1;
+                } else {
+                    queue[static_cast<int64_t>(w) * qcap + qlen[jj]] = (ty << 24) | task;
+                    qlen[jj] += 1;
+                    if (busy[jj] && !fdirty[jj]) fsum[jj] += cost(ty, kind[jj]);
+                }
+            }
+        if (__shfl_sync(kFull, ovf, owner)) { status = GS_QUEUE_OVERFLOW; aux = task; return; }
+        __syncwarp();
+        nready += 1;
+        if (P->push_time && lane == 0) {
+            P->push_time[t0 + n_push] = now;
+            P->push_task[t0 + n_push] = task;
+        }
+        ++n_push;
+        queue_event();
+        maybe_dispatch(w);
+    }
+
+    __device__ __forceinline__ void run() {  // Simulation::run, engine.cpp:207-248
+        // roots in position order (engine.cpp:218-221)
+        rcount = 0;
+        for (int32_t base = 0; base < n; base += 32) {
+            const int32_t v = base + lane;
+            bool root = false;
+            if (v < n) {
+                const int32_t deg = __ldg(&doff[v + 1]) - __ldg(&doff[v]);
+                unmet[v] = deg;
+                root = deg == 0;
+            }
+            const unsigned bal = __ballot_sync(kFull, root);
+            if (root) ready[rcount + __popc(bal & ((1u << lane) - 1u))] = v;
+            rcount += __popc(bal);
+        }
+        for (int32_t h = lane; h < nh; h += 32) resid[h] = 1u;  // engine.cpp:215-216
+        __syncwarp();
+        for (;;) {
+            // (2)+(3): pushes of the tasks made ready at `now`, creation order
+            for (int32_t r = 0; r < rcount && status == GS_OK; ++r) on_push(ready[r]);
+            rcount = 0;
+            if (status != GS_OK) return;
+            // next worker-event time
+            uint64_t lt = ~0ull;
+#pragma unroll
+            for (int j = 0; j < WPL; ++j) {
+                if (xs[j] != kNone) lt = min(lt, dbits(xt[j]));
+                if (ds[j] != kNone) lt = min(lt, dbits(dt[j]));
+            }
+            const uint64_t mt = warp_min_u64(lt);
+            if (mt == ~0ull) break;
+            now = __longlong_as_double(static_cast<long long>(mt));
+            // (1): every worker event at `now`, enqueue order
+            for (;;) {
+                uint32_t ls = kNone;
+#pragma unroll
+                for (int j = 0; j < WPL; ++j) {
+                    if (xs[j] != kNone && dbits(xt[j]) == mt) ls = min(ls, xs[j]);
+                    if (ds[j] != kNone && dbits(dt[j]) == mt) ls = min(ls, ds[j]);
+                }
+                const uint32_t ms = __reduce_min_sync(kFull, ls);
+                if (ms == kNone) break;
+                const int owner = __ffs(__ballot_sync(kFull, ls == ms)) - 1;
+                int32_t info = 0;
+                if (lane == owner) {
+#pragma unroll
+                    for (int j = 0; j < WPL; ++j) {
+                        if (xs[j] == ms) { info = (j << 30) | xtask[j]; xs[j] = kNone; }
+                        if (ds[j] == ms) { info = (1 << 29) | (j << 30) | dtask[j]; ds[j] = kNone; }
+                    }
+                }
+                info = __shfl_sync(kFull, info, owner);
+                const int32_t task = info & 0xffffff;
+                const int32_t w = owner + 32 * (static_cast<uint32_t>(info) >> 30);
+                const bool is_done = (info >> 29) & 1;
+                int32_t nd = 0;
+#pragma unroll
+                for (int j = 0; j < WPL; ++j)
+                    if (j == (w >> 5)) nd = node[j];
+                nd = __shfl_sync(kFull, nd, owner);
+                const uint32_t bit = 1u << nd;
+                if (!is_done) {  // TransferDone: inputs resident (engine.cpp:168-172)
+                    for (int32_t k = __ldg(&ioff[task]) + lane; k < __ldg(&ioff[task + 1]); k += 32) {
+                        const int32_t h = __ldg(&in[k]);
+                        resid[h] |= bit;
+                    }
+                    __syncwarp();
+                    continue;
+                }
+                // TaskDone (engine.cpp:174-185)
+                for (int32_t k = __ldg(&ooff[task]) + lane; k < __ldg(&ooff[task + 1]); k += 32) {
+                    const int32_t h = __ldg(&out[k]);
+                    resid[h] |= bit;
+                }
+#pragma unroll
+                for (int j = 0; j < WPL; ++j)
+                    if (j == (w >> 5) && lane == owner) busy[j] = false;
+                completed += 1;
+                makespan = now > makespan ? now : makespan;
+                const int32_t s0 = __ldg(&soff[task]), s1 = __ldg(&soff[task + 1]);
+                for (int32_t base = s0; base < s1; base += 32) {
+                    const int32_t k = base + lane;
+                    bool rdy = false;
+                    int32_t sv = 0;
+                    if (k < s1) {
+                        sv = __ldg(&succ[k]);
+                        rdy = atomicSub(&unmet[sv], 1) == 1;
+                    }
+                    const unsigned bal = __ballot_sync(kFull, rdy);
+                    if (rdy) ready[rcount + __popc(bal & ((1u << lane) - 1u))] = sv;
+                    rcount += __popc(bal);
+                }
+                __syncwarp();
+                maybe_dispatch(w);
+                if (status != GS_OK) return;
+            }
+        }
+    }
+};
+
+template <int WPL>
+__device__ void simulate_impl(const SimParams& p) {
+    extern __shared__ __align__(16) char smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp_in_block = threadIdx.x >> 5;
+    const int warps_per_block = blockDim.x >> 5;
+    char* base = p.use_smem ? smem + static_cast<int64_t>(warp_in_block) * p.state_bytes
+                            : p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
+    const DevBatch& b = p.b;
+    const int64_t max_n = b.max_n, max_h = b.max_h;
+    auto al = [](int64_t x) { return (x + 15) & ~int64_t(15); };
+    Sim<WPL> s;
+    s.P = &p;
+    s.lane = lane;
+    s.unmet = reinterpret_cast<int32_t*>(base);
+    s.resid = reinterpret_cast<uint32_t*>(base + al(4 * max_n));
+    s.ready = reinterpret_cast<int32_t*>(base + al(4 * max_n) + al(4 * max_h));
+    s.queue = reinterpret_cast<int32_t*>(base + 2 * al(4 * max_n) + al(4 * max_h));
+    char* ring = base + 2 * al(4 * max_n) + al(4 * max_h) + al(4LL * p.max_workers * p.qcap);
+    s.samp_t = reinterpret_cast<double*>(ring);
+    s.samp_n = reinterpret_cast<int64_t*>(ring + 8 * TBSIM_MAX_SLOPE_SAMPLES);
+    s.qcap = p.qcap;
+    s.policy = p.policy;
+
+    for (;;) {
+        unsigned long long item = 0;
+        if (lane == 0) item = atomicAdd(p.work_counter, 1ull);
+        item = __shfl_sync(kFull, item, 0);
+        if (item >= static_cast<unsigned long long>(p.n_items)) break;
+        const int64_t g = p.graph_list ? p.graph_list[item] : static_cast<int64_t>(item);
+        s.g = g;
+        s.t0 = b.task_base[g];
+        s.n = static_cast<int32_t>(b.task_base[g + 1] - s.t0);
+        s.nh = static_cast<int32_t>(b.handle_base[g + 1] - b.handle_base[g]);
+        s.doff = b.dep_off + s.t0 + g;
+        s.soff = b.succ_off + s.t0 + g;
+        s.succ = b.succ + b.edge_base[g];
+        s.ioff = b.in_off + s.t0 + g;
+        s.in = b.in + b.in_base[g];
+        s.ooff = b.out_off + s.t0 + g;
+        s.out = b.out + b.out_base[g];
+        s.type = b.type + s.t0;
+        s.hbytes = b.handle_bytes + b.handle_base[g];
+        s.pf = p.platforms + (p.platform_of ? p.platform_of[g] : 0);
+        s.W = s.pf->n_workers;
+        s.nn = s.pf->n_nodes;
+        s.lat = s.pf->latency_ms;
+        s.ability = p.ability;
+        s.efficiency = p.efficiency;
+        s.prio = p.prio;
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) {
+            const int32_t w = lane + 32 * j;
+            s.kind[j] = w < s.W ? s.pf->kind[w] : 0;
+            s.node[j] = w < s.W ? s.pf->node[w] : 0;
+            s.qlen[j] = 0;
+            s.busy[j] = false;
+            s.fdirty[j] = false;
+            s.busy_until[j] = 0.0;
+            s.fsum[j] = 0.0;
+            s.xt[j] = s.dt[j] = 0.0;
+            s.xs[j] = s.ds[j] = kNone;
+            s.xtask[j] = s.dtask[j] = 0;
+        }
+        s.now = 0.0;
+        s.makespan = 0.0;
+        s.nready = 0;
+        s.completed = 0;
+        s.seq = 0;
+        s.n_push = s.n_pop = s.n_samp = 0;
+        s.pop0 = s.pop1 = s.pop2 = 0;
+        s.status = GS_OK;
+        s.aux = -1;
+        // regulator config: explicit, or default_regulator_config
+        // (policies.cpp:139-151) from the worker count and the median
+        if (p.reg) {
+            s.cfg = p.reg[g];
+        } else {
+            const int64_t nw = s.W;
+            const int64_t tw = (nw + 3) / 4 > 2 ? (nw + 3) / 4 : 2;
+            s.cfg.task_window = tw;
+            s.cfg.s_inc = nw;
+            s.cfg.k_inc = static_cast<double>(nw) / p.median[g * p.median_stride];
+            s.cfg.s_dec = tw;
+            s.cfg.c = (tw + 1) / 2;
+            s.cfg.dec_step = tw;
+            s.cfg.slope_samples = 8;
+        }
+        // regulator state: caller-provided (in/out) or RegulatorState{}
+        if (p.reg_state) {
+            const tbsim_regulator_state& rs = p.reg_state[g];
+            s.mode = rs.mode; s.phase = rs.phase; s.peak = rs.peak; s.prev_nready = rs.prev_nready;
+            s.last_trigger = rs.last_trigger_nready; s.s_dec_count = rs.s_dec_count; s.cur_k = rs.cur_k;
+            s.r_head = 0;
+            s.r_count = rs.n_samples;
+            for (int i = lane; i < rs.n_samples; i += 32) { s.samp_t[i] = rs.sample_time[i]; s.samp_n[i] = rs.sample_nready[i]; }
+        } else {
+            s.mode = TBSIM_MODE_EFFICIENCY; s.phase = TBSIM_PHASE_INC; s.peak = 0; s.prev_nready = 0;
+            s.last_trigger = 0; s.s_dec_count = 1; s.cur_k = 0.0; s.r_head = 0; s.r_count = 0;
+        }
+        for (int32_t v = lane; v < s.n; v += 32) {
+            p.worker[s.t0 + v] = -1;
+            p.start_ms[s.t0 + v] = 0.0;
+            p.end_ms[s.t0 + v] = 0.0;
+        }
+        __syncwarp();
+        s.run();
+        if (lane == 0) {
+            int32_t st = s.status;
+            if (st == GS_OK && s.completed != s.n) st = GS_STUCK;
+            p.status[g] = st;
+            p.status_aux[g] = s.aux;
+            p.makespan[g] = s.makespan;
+            p.completed[g] = s.completed;
+            if (p.pop_counts) {
+                p.pop_counts[3 * g + 0] = s.pop0;
+                p.pop_counts[3 * g + 1] = s.pop1;
+                p.pop_counts[3 * g + 2] = s.pop2;
+            }
+            if (p.reg_state && p.policy == TBSIM_POLICY_INSPIRIT) {
+                tbsim_regulator_state& rs = p.reg_state[g];
+                rs.mode = s.mode; rs.phase = s.phase; rs.peak = s.peak; rs.prev_nready = s.prev_nready;
+                rs.last_trigger_nready = s.last_trigger; rs.s_dec_count = s.s_dec_count; rs.cur_k = s.cur_k;
+                rs.n_samples = s.r_count;
+            }
+        }
+        if (p.reg_state && p.policy == TBSIM_POLICY_INSPIRIT) {
+            __syncwarp();
+            tbsim_regulator_state& rs = p.reg_state[g];
+            for (int i = lane; i < s.r_count; i += 32) {
+                const int idx = (s.r_head + i) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+                rs.sample_time[i] = s.samp_t[idx];
+                rs.sample_nready[i] = s.samp_n[idx];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256, 2) k_simulate_w1(const __grid_constant__ SimParams p) { simulate_impl<1>(p); }
+__global__ void __launch_bounds__(256, 2) k_simulate_w2(const __grid_constant__ SimParams p) { simulate_impl<2>(p); }
+
+}  // namespace tbsim_dev

@@ -1,0 +1,58 @@
+// simulate.cuh -- launch interface of the batched event simulator.
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace tbsim_dev {
+
+struct SimParams {
+    DevBatch b;
+    const DevPlatform* platforms;
+    const int32_t* platform_of;       // [G] or null
+    int32_t policy;
+    const tbsim_regulator_cfg* reg;   // [G] or null -> default from median
+    const double* median;             // [G] lower-median GPU time (default cfg)
+    int32_t median_stride;            // elements between consecutive graphs' medians
+    const int64_t* ability;           // [T] or null
+    const int64_t* efficiency;        // [T] or null
+    const int64_t* prio;              // [T] or null
+    // outputs
+    int32_t* worker;
+    double* start_ms;
+    double* end_ms;
+    double* makespan;                 // [G]
+    int64_t* completed;               // [G]
+    int64_t* pop_counts;              // [3G] or null
+    tbsim_regulator_state* reg_state; // [G] in/out or null
+    double* push_time;  int32_t* push_task;
+    double* pop_time;   int32_t* pop_task;  int32_t* pop_worker;
+    double* sample_time; int64_t* sample_nready;
+    int32_t* status;                  // [G]
+    int32_t* status_aux;              // [G]
+    // per-warp state
+    char* gstate;                     // global fallback region base
+    int64_t state_bytes;              // bytes per warp state
+    int32_t qcap;                     // queue capacity per worker
+    int32_t use_smem;
+    int32_t max_workers;
+    const int32_t* graph_list;        // subset of graphs (rerun) or null
+    int64_t n_items;                  // graphs to process (list length or G)
+    unsigned long long* work_counter;
+};
+
+__global__ void k_simulate_w1(const __grid_constant__ SimParams p);  // <= 32 workers
+__global__ void k_simulate_w2(const __grid_constant__ SimParams p);  // <= 64 workers
+
+// bytes of per-warp state for a batch
+__host__ __device__ inline int64_t sim_state_bytes(int64_t max_n, int64_t max_h, int64_t max_workers, int64_t qcap) {
+    auto al = [](int64_t x) { return (x + 15) & ~int64_t(15); };
+    return al(4 * max_n)                       // unmet
+         + al(4 * max_h)                       // residency masks
+         + al(4 * max_n)                       // ready list
+         + al(4 * max_workers * qcap)          // queues
+         + al(16 * TBSIM_MAX_SLOPE_SAMPLES);   // regulator sample ring
+}
+
+}  // namespace tbsim_dev
