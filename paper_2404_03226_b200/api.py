@@ -226,6 +226,21 @@ class Context:
         out.update({"attr_" + k: v for k, v in aout.items()})
         return out
 
+    def schedule_device(self, db: DeviceBatch, platforms: Sequence[Platform], policy: str,
+                        ptrs: dict, platform_of=None, prio: int = abi.PRIO_UPWARD_RANK):
+        """tbsim_schedule writing straight into device buffers (e.g. torch
+        tensors' data_ptr()): keys worker/start_ms/end_ms [T], makespan_ms [G]."""
+        parr = platform_array(platforms, db.type_names)
+        pof = None if platform_of is None else np.ascontiguousarray(platform_of, np.int32)
+        o = abi.SimOut()
+        o.on_device = 1
+        for k, ct in (("worker", C.c_int32), ("start_ms", C.c_double), ("end_ms", C.c_double),
+                      ("makespan_ms", C.c_double)):
+            if ptrs.get(k):
+                setattr(o, k, C.cast(C.c_void_p(ptrs[k]), C.POINTER(ct)))
+        _check(load().tbsim_schedule(self.h, db.h, parr, len(platforms), _p(pof, C.c_int32),
+                                     abi.POLICY_ID[policy], prio, None, C.byref(o)))
+
     def __del__(self):
         try:
             self.close()

@@ -1,0 +1,216 @@
+"""GPU: the CUDA path (through the C-ABI) against the reference's golden
+fixtures and the oracle -- bit-exact for every integer attribute, every
+assignment/start/end double, the push/pop/nready ledger and the regulator
+state.  Run with `pytest -m gpu` on a B200."""
+import numpy as np
+import pytest
+
+from golden_util import SIM_KEYS, Fixture, names, reg_rows
+from oracle import pyoracle as po
+from paper_2404_03226_b200 import abi, api
+from paper_2404_03226_b200 import platform as P
+from paper_2404_03226_b200.batch import GraphBatch, TaskGraph, TaskNode
+
+pytestmark = pytest.mark.gpu
+FIXTURES = names()
+MIXED = ["LAYERK0", "LAYERK1", "LAYERK2", "LAYERK3", "UNIT"]
+
+
+def eq(a, b, msg):
+    np.testing.assert_array_equal(np.asarray(a), np.asarray(b), err_msg=msg)
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_attributes_match_reference_fixture(ctx, name):
+    f = Fixture(name)
+    db = ctx.upload(f.batch)
+    a = ctx.attributes(db, f.costs, abi.ATTR_ALL, f.prio)
+    for k in ("ability", "efficiency", "static_priority", "unit_time_ms"):
+        eq(a[k], f.z["attr_" + k], k)
+    c = ctx.attributes(db, f.costs, abi.ATTR_CALIBRATE)
+    for k in ("w0_ms", "best_score", "w0_score", "evaluations"):
+        eq(c[k], f.z["calib_" + k], k)
+    eq(ctx.attributes(db, f.costs, abi.ATTR_DEPTH)["depth"], f.z["depth"], "depth")
+    eq(ctx.attributes(db, f.costs, abi.ATTR_LAYERS)["layer"], f.z["layer"], "layer")
+    eq(ctx.attributes(db, f.costs, abi.ATTR_RANK)["static_priority"], f.z["rank"], "rank")
+    eq(ctx.attributes(db, f.costs, abi.ATTR_ABILITY)["ability"], f.z["attr_ability"], "ability only")
+    for w in (0.5, 1.0, 4.0, 16.0):
+        e = ctx.attributes(db, f.costs, abi.ATTR_EFFICIENCY, unit_time=np.full(f.batch.n_graphs, w))
+        eq(e["efficiency"], f.z[f"eff_w{w}"], f"eff@{w}")
+
+
+@pytest.mark.parametrize("name", FIXTURES)
+def test_simulation_matches_reference_fixture(ctx, name):
+    f = Fixture(name)
+    db = ctx.upload(f.batch)
+    for pname in f.platform_names:
+        pl = f.platform(pname)
+        reg = f.reg_cfgs(pname, po)
+        for pol in abi.POLICIES:
+            r = ctx.simulate(db, [pl], pol, reg, attrs=f.attrs(), record=True)
+            want = f.sim(pname, pol)
+            for k in SIM_KEYS:
+                eq(r[k], want[k], f"{pname}/{pol}/{k}")
+            if pol == "inspirit":
+                eq(reg_rows(r["reg_state"], f.batch.n_graphs), want["reg"], "regulator state")
+                eq([s.cur_k for s in r["reg_state"][:f.batch.n_graphs]], want["reg_cur_k"], "cur_k")
+
+
+def random_graphs(seed, count, with_handles=True):
+    """Random DAGs with non-contiguous ids, multi-edges, ids out of order and
+    inputs that are not dependencies (a construction unlike both generators)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for gi in range(count):
+        n = int(rng.integers(1, 120))
+        ids = rng.permutation(np.arange(n) * 7 + 1000)
+        tasks = []
+        handles = [(5000 + 3 * h, int(rng.integers(1, 5)) * 100_000) for h in range(n)]
+        for i in range(n):
+            deps = [int(ids[j]) for j in range(i) if rng.random() < 0.08]
+            if deps and rng.random() < 0.2:
+                deps.append(deps[0])  # multi-edge
+            inputs = [5000 + 3 * int(rng.integers(0, n)) for _ in range(int(rng.integers(0, 4)))] if with_handles else []
+            outputs = [5000 + 3 * i] if with_handles else []
+            tasks.append(TaskNode(int(ids[i]), MIXED[int(rng.integers(0, 5))], deps, inputs, outputs))
+        out.append(TaskGraph(f"r{gi}", tasks, handles if with_handles else []))
+    return GraphBatch.from_taskgraphs(out, P.TYPE_NAMES)
+
+
+def test_random_graphs_all_policies_platform_mix(ctx):
+    b = random_graphs(7, 40)
+    costs = P.default_cost_table()
+    pls = [P.make_preset("26cpu_2gpu"), P.make_preset("2gpu"), P.make_preset("homog2"),
+           P.assemble("32c4g", 32, 4), P.assemble("4c1g", 4, 1)]
+    pof = np.arange(b.n_graphs) % len(pls)
+    db = ctx.upload(b)
+    ga = ctx.attributes(db, costs, abi.ATTR_ALL)
+    oa = po.attributes(b, costs, abi.ATTR_ALL)
+    for k in ("ability", "efficiency", "static_priority", "unit_time_ms"):
+        eq(ga[k], oa[k], k)
+    reg = [po.default_regulator_config(b, g, pls[pof[g]]) for g in range(b.n_graphs)]
+    for pol in abi.POLICIES:
+        g = ctx.simulate(db, pls, pol, reg, platform_of=pof, attrs=oa, record=True)
+        o = po.simulate(b, pls, pol, platform_of=pof, reg=reg, attrs=oa, record=True)
+        for k in SIM_KEYS:
+            eq(g[k], o[k], f"{pol}/{k}")
+
+
+def test_schedule_pipeline_matches_oracle(ctx):
+    hb = api.HostBatch().add_cholesky(10, 960 * 960 * 4).add_layered(1000, 10, 0.05, [3, 4, 5])
+    hb.add_lu(12, 160 * 160 * 4).add_qr(10, 160 * 160 * 4)
+    b = hb.view()
+    pls = [P.assemble("4c1g", 4, 1, True), P.assemble("8c2g", 8, 2, True), P.assemble("32c4g", 32, 4, True)]
+    pof = np.array([0, 1, 1, 1, 2, 2], np.int32)
+    db = ctx.upload(hb)
+    for prio in (abi.PRIO_UPWARD_RANK, abi.PRIO_DEPTH, abi.PRIO_ZERO):
+        r = ctx.schedule(db, pls, "inspirit", platform_of=pof, prio=prio)
+        oa = po.attributes(b, pls[0].costs, abi.ATTR_ALL, prio)
+        for k in ("ability", "efficiency", "static_priority", "unit_time_ms"):
+            eq(r["attr_" + k], oa[k], f"prio{prio}/{k}")
+        reg = [po.default_regulator_config(b, g, pls[pof[g]]) for g in range(b.n_graphs)]
+        o = po.simulate(b, pls, "inspirit", platform_of=pof, reg=reg, attrs=oa, record=False)
+        for k in ("worker", "start_ms", "end_ms", "makespan_ms", "pop_mode_counts"):
+            eq(r[k], o[k], f"prio{prio}/{k}")
+
+
+def test_c2_batch_sample_and_properties(ctx):
+    seeds = np.arange(4096)
+    hb = api.HostBatch().add_layered(1000, 10, 0.05, seeds)
+    b = hb.view()
+    pl = [P.assemble("8c2g", 8, 2)]
+    db = ctx.upload(hb)
+    r = ctx.schedule(db, pl, "inspirit")
+    # size-independent properties over the whole batch
+    assert np.all(r["attr_efficiency"] <= r["attr_ability"])
+    assert np.all(r["worker"] >= 0) and np.all(r["worker"] < 10)
+    assert np.all(r["end_ms"] > r["start_ms"])
+    for g in range(0, 4096, 97):
+        t0, t1 = b.task_base[g], b.task_base[g + 1]
+        assert r["makespan_ms"][g] == r["end_ms"][t0:t1].max()
+        off, dep = b.graph_deps(g)
+        st, en = r["start_ms"][t0:t1], r["end_ms"][t0:t1]
+        for v in range(t1 - t0):  # precedence (trace_checks.hpp:64-73)
+            preds = dep[off[v]:off[v + 1]]
+            if len(preds):
+                assert st[v] >= en[preds].max()
+    # exact parity on a sample
+    idx = list(range(0, 4096, 256))
+    sub = b.slice(idx)
+    costs = P.default_cost_table()
+    oa = po.attributes(sub, costs, abi.ATTR_ALL)
+    reg = [po.default_regulator_config(sub, i, pl[0]) for i in range(sub.n_graphs)]
+    o = po.simulate(sub, pl, "inspirit", reg=reg, attrs=oa, record=False)
+    eq(r["makespan_ms"][idx], o["makespan_ms"], "makespan sample")
+    rows = np.concatenate([np.arange(b.task_base[g], b.task_base[g + 1]) for g in idx])
+    eq(r["worker"][rows], o["worker"], "assignment sample")
+    eq(r["attr_efficiency"][rows], oa["efficiency"], "efficiency sample")
+
+
+def test_regulator_state_carries_across_runs(ctx):
+    # a policy object reused for a second simulate() continues from its state
+    f = Fixture("cholesky")
+    pl = f.platform("26cpu_2gpu")
+    reg = f.reg_cfgs("26cpu_2gpu", po)
+    db = ctx.upload(f.batch)
+    g1 = ctx.simulate(db, [pl], "inspirit", reg, attrs=f.attrs())
+    g2 = ctx.simulate(db, [pl], "inspirit", reg, attrs=f.attrs(), states=g1["reg_state"])
+    o1 = po.simulate(f.batch, [pl], "inspirit", reg=reg, attrs=f.attrs())
+    o2 = po.simulate(f.batch, [pl], "inspirit", reg=reg, attrs=f.attrs(), states=o1["reg_state"])
+    for k in SIM_KEYS:
+        eq(g2[k], o2[k], k)
+    eq(reg_rows(g2["reg_state"], f.batch.n_graphs), reg_rows(o2["reg_state"], f.batch.n_graphs), "state")
+
+
+def _tg(tasks):
+    return GraphBatch.from_taskgraphs([TaskGraph("t", tasks)], P.TYPE_NAMES)
+
+
+def test_errors_carry_reference_type_and_text(ctx):
+    costs = P.default_cost_table()
+    cyc = _tg([TaskNode(0, "UNIT", [1]), TaskNode(1, "UNIT", [0])])
+    db = ctx.upload(cyc)
+    with pytest.raises(api.TbsimRuntimeError, match="graph has a dependency cycle"):
+        ctx.attributes(db, costs, abi.ATTR_ALL)
+    with pytest.raises(api.TbsimRuntimeError, match="graph has a dependency cycle"):
+        ctx.attributes(db, costs, abi.ATTR_LAYERS)
+    reg = [api.default_regulator_config(2, 1.0)]
+    with pytest.raises(api.TbsimRuntimeError, match=r"simulation stuck with 2 tasks unfinished: 0 1$"):
+        ctx.simulate(db, [P.make_preset("homog2")], "fifo", reg)
+    gonly = GraphBatch.from_taskgraphs([TaskGraph("g", [TaskNode(0, "GONLY_TYPE")])])
+    pl = P.make_preset("homog2")
+    pl.costs = P.CostTable()
+    pl.costs.set("GONLY_TYPE", P.GPU, 1.0)
+    with pytest.raises(api.TbsimRuntimeError, match="no worker can run task type GONLY_TYPE"):
+        ctx.simulate(ctx.upload(gonly), [pl], "dmda", reg)
+    unit = P.CostTable()
+    unit.set("UNIT", P.GPU, 1.0)
+    chain = ctx.upload(_tg([TaskNode(0, "UNIT"), TaskNode(1, "UNIT", [0])]))
+    with pytest.raises(api.TbsimInvalidArgument, match="unit time must be non-negative"):
+        ctx.attributes(chain, unit, abi.ATTR_EFFICIENCY, unit_time=[-1.0])
+    nogpu = P.CostTable()
+    nogpu.set("UNIT", P.CPU, 1.0)
+    with pytest.raises(api.TbsimRuntimeError, match="no gpu cost entry for task type UNIT"):
+        ctx.attributes(chain, nogpu, abi.ATTR_ALL)
+    empty = ctx.upload(GraphBatch.from_taskgraphs([TaskGraph("e", [])], P.TYPE_NAMES))
+    with pytest.raises(api.TbsimRuntimeError, match="empty graph has no median time"):
+        ctx.attributes(empty, costs, abi.ATTR_ALL)
+    assert ctx.attributes(empty, costs, abi.ATTR_ABILITY)["ability"].size == 0
+
+
+def test_c3_lu_and_qr_on_32c4g(ctx):
+    # BASELINE configs[2]: 40x40 tiles, 36 workers (two workers per lane)
+    hb = api.HostBatch().add_lu(40, 160 * 160 * 4).add_qr(40, 160 * 160 * 4)
+    b = hb.view()
+    pl = [P.assemble("32c4g", 32, 4, True)]
+    db = ctx.upload(hb)
+    r = ctx.schedule(db, pl, "inspirit")
+    oa = po.attributes(b, pl[0].costs, abi.ATTR_ALL)
+    for k in ("ability", "efficiency", "static_priority", "unit_time_ms"):
+        eq(r["attr_" + k], oa[k], k)
+    reg = [po.default_regulator_config(b, g, pl[0]) for g in range(2)]
+    for pol in ("dmda", "inspirit"):
+        g = ctx.simulate(db, pl, pol, reg, attrs=oa, record=True)
+        o = po.simulate(b, pl, pol, reg=reg, attrs=oa, record=True)
+        for k in SIM_KEYS:
+            eq(g[k], o[k], f"{pol}/{k}")
