@@ -297,6 +297,11 @@ def main():
             traffic = None
 
     # ---------------- e2e: host buffers through the public API
+    pinned = {"worker": torch.empty(T, dtype=torch.int32, pin_memory=True).numpy(),
+              "start_ms": torch.empty(T, dtype=torch.float64, pin_memory=True).numpy(),
+              "end_ms": torch.empty(T, dtype=torch.float64, pin_memory=True).numpy(),
+              "makespan_ms": torch.empty(G, dtype=torch.float64, pin_memory=True).numpy(),
+              "completed": torch.empty(G, dtype=torch.int64, pin_memory=True).numpy()}
     e2e_times = []
     h2d = d2h = 0
     for k in range(args.steps + 1):
@@ -304,7 +309,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         db2 = ctx.upload(hb)
-        res = ctx.schedule(db2, platforms, w["policy"], want_attrs=False)
+        res = ctx.schedule(db2, platforms, w["policy"], want_attrs=False, out_arrays=pinned, want_states=False)
         if dist is not None:
             ms_t = torch.from_numpy(res["makespan_ms"]).to(dev)
             dist.all_gather_into_tensor(gathered_ms, ms_t)

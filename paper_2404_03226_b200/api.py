@@ -213,13 +213,15 @@ class Context:
     # ------------------------------------------------------------ schedule
     def schedule(self, db: DeviceBatch, platforms: Sequence[Platform], policy: str = "inspirit",
                  platform_of=None, prio: int = abi.PRIO_UPWARD_RANK, want_attrs=True,
-                 record=False) -> dict:
-        """compute_attributes + default_regulator_config + simulate per graph."""
+                 record=False, out_arrays=None, want_states=True) -> dict:
+        """compute_attributes + default_regulator_config + simulate per graph.
+        out_arrays: preallocated (pinned) host arrays worker/start_ms/end_ms/
+        makespan_ms/completed/pop_mode_counts to receive the results."""
         G = db.n_graphs
         parr = platform_array(platforms, db.type_names)
         pof = None if platform_of is None else np.ascontiguousarray(platform_of, np.int32)
         aout, ao = outbuf.attr_out(db.n_tasks, G) if want_attrs else ({}, None)
-        out, o = outbuf.sim_out(db.n_tasks, G, False)
+        out, o = outbuf.sim_out(db.n_tasks, G, False, want_states=want_states, arrays=out_arrays)
         _check(load().tbsim_schedule(self.h, db.h, parr, len(platforms), _p(pof, C.c_int32),
                                      abi.POLICY_ID[policy], prio,
                                      None if ao is None else C.byref(ao), C.byref(o)))

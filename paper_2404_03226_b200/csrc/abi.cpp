@@ -105,8 +105,25 @@ struct tbsim_ctx {
     std::map<std::string, DevBuf> bufs;
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
+    std::vector<std::pair<void*, size_t>> batch_pool;  // freed batch allocations for reuse
 
     DevBuf& buf(const std::string& name) { return bufs[name]; }
+    void* batch_alloc(size_t bytes, size_t* got) {
+        size_t best = batch_pool.size();
+        for (size_t i = 0; i < batch_pool.size(); ++i)
+            if (batch_pool[i].second >= bytes && (best == batch_pool.size() || batch_pool[i].second < batch_pool[best].second))
+                best = i;
+        if (best < batch_pool.size()) {
+            void* p = batch_pool[best].first;
+            *got = batch_pool[best].second;
+            batch_pool.erase(batch_pool.begin() + static_cast<std::ptrdiff_t>(best));
+            return p;
+        }
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(batch)");
+        *got = bytes;
+        return p;
+    }
     void* host_stage(size_t bytes) {
         if (bytes > pinned_bytes) {
             if (pinned) cudaFreeHost(pinned);
@@ -144,6 +161,7 @@ struct tbsim_ctx {
 struct tbsim_batch {
     DevBatch d{};
     void* mem = nullptr;
+    size_t mem_bytes = 0;
     int64_t h2d_bytes = 0;
     std::vector<int64_t> task_base;    // host copy
     std::vector<int64_t> task_id;      // host copy (messages)
@@ -233,6 +251,7 @@ tbsim_status tbsim_ctx_destroy(tbsim_ctx* ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         for (auto& [k, b] : ctx->bufs) b.release();
+        for (auto& pb : ctx->batch_pool) cudaFree(pb.first);
         for (auto& [k, ev] : ctx->events) {
             cudaEventDestroy(ev.first);
             cudaEventDestroy(ev.second);
@@ -301,7 +320,7 @@ tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim
         size_t total = 0;
         for (const auto& s : secs) total += al16(s.bytes);
         const size_t derived = al16((T + G) * 4) + al16(E * 4);
-        cuda_check(cudaMalloc(&b->mem, total + derived + 16), "cudaMalloc(batch)");
+        b->mem = ctx->batch_alloc(total + derived + 16, &b->mem_bytes);
         char* p = static_cast<char*>(b->mem);
         int64_t moved = 0;
         for (const auto& s : secs) {
@@ -343,8 +362,13 @@ tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim
 tbsim_status tbsim_batch_free(tbsim_ctx* ctx, tbsim_batch* b) {
     return guarded([&] {
         if (!b) return;
-        if (ctx) cudaStreamSynchronize(ctx->stream);
-        if (b->mem) cudaFree(b->mem);
+        if (ctx) {
+            // stream-ordered reuse: later uploads on this stream run after
+            // every kernel that reads this batch
+            if (b->mem) ctx->batch_pool.push_back({b->mem, b->mem_bytes});
+        } else if (b->mem) {
+            cudaFree(b->mem);
+        }
         delete b;
     });
 }
@@ -584,47 +608,59 @@ struct SimRun {
     std::vector<int32_t> status, aux;
 };
 
+int32_t pow2_at_least(int32_t x) {
+    int32_t r = 1;
+    while (r < x) r <<= 1;
+    return r;
+}
+
+// Picks the per-warp state placement: shared memory (compact types when the
+// batch allows) with 16 then 8 warps per SM, else HBM with full queues.
 void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_items) {
     const int kThreads = 256, kWarps = kThreads / 32;
     const DevBatch& d = p.b;
     const int64_t qcap_full = std::max<int32_t>(d.max_n, 1);
-    // shared-memory state when it fits a useful number of warps per CTA
-    const int64_t budget = static_cast<int64_t>(ctx->smem_optin) - 1024;
+    const bool compact = d.max_n < 32768 && p.max_nodes <= 8;
+    auto layout = [&](int64_t qcap) {
+        return sim_layout(d.max_n, d.max_h, max_workers, qcap, p.ring, p.n_types, p.max_nodes, compact);
+    };
+    const bool forced = p.qcap > 0;  // rerun of queue overflows: HBM state, full capacity
     int64_t qcap = qcap_full;
-    int64_t bytes = sim_state_bytes(d.max_n, d.max_h, max_workers, qcap);
+    int ctas_per_sm = 2;
     p.use_smem = 0;
-    if (bytes * kWarps > budget) {
-        // try a bounded queue capacity in shared memory (overflow -> rerun)
-        const int64_t fixed = sim_state_bytes(d.max_n, d.max_h, max_workers, 0);
-        const int64_t room = budget / kWarps - fixed;
-        const int64_t cap = room / (4 * max_workers);
-        if (cap >= 64) {
-            qcap = std::min<int64_t>(cap & ~int64_t(3), qcap_full);
-            bytes = sim_state_bytes(d.max_n, d.max_h, max_workers, qcap);
-            p.use_smem = 1;
+    if (!forced) {
+        const int64_t per_sm = static_cast<int64_t>(ctx->smem_optin) + 1024;  // 228 KB per SM
+        for (int c : {2, 1}) {
+            const int64_t per_warp = (per_sm / c - 1024) / kWarps;
+            if (layout(qcap_full).total <= per_warp) {
+                qcap = qcap_full;
+                ctas_per_sm = c;
+                p.use_smem = 1;
+                break;
+            }
+            const int64_t cap = (per_warp - layout(0).total - 64) / (4 * max_workers);
+            if (cap >= 64) {
+                qcap = std::min<int64_t>(cap & ~int64_t(3), qcap_full);
+                ctas_per_sm = c;
+                p.use_smem = 1;
+                break;
+            }
         }
-    } else {
-        p.use_smem = 1;
-    }
-    if (p.qcap > 0) {  // forced (rerun) configuration: global state, full capacity
-        qcap = p.qcap;
-        bytes = sim_state_bytes(d.max_n, d.max_h, max_workers, qcap);
-        p.use_smem = 0;
     }
     p.qcap = static_cast<int32_t>(qcap);
-    p.state_bytes = bytes;
+    p.state_bytes = layout(qcap).total;
     p.max_workers = max_workers;
     p.n_items = n_items;
-    const int blocks_per_sm = 2;
-    int grid = static_cast<int>(std::min<int64_t>((n_items + kWarps - 1) / kWarps, static_cast<int64_t>(blocks_per_sm) * ctx->n_sms));
+    int grid = static_cast<int>(std::min<int64_t>((n_items + kWarps - 1) / kWarps,
+                                                  static_cast<int64_t>(ctas_per_sm) * ctx->n_sms));
     grid = std::max(grid, 1);
-    const size_t smem = p.use_smem ? static_cast<size_t>(bytes * kWarps) : 0;
-    if (!p.use_smem) p.gstate = static_cast<char*>(ctx->buf("s_gstate").get(static_cast<size_t>(bytes) * kWarps * grid));
+    const size_t smem = p.use_smem ? static_cast<size_t>(p.state_bytes * kWarps) : 0;
+    if (!p.use_smem) p.gstate = static_cast<char*>(ctx->buf("s_gstate").get(static_cast<size_t>(p.state_bytes) * kWarps * grid));
     unsigned long long* counter = ctx->buf("s_counter").as<unsigned long long>(1);
     cuda_check(cudaMemsetAsync(counter, 0, 8, ctx->stream), "memset");
     p.work_counter = counter;
     const bool w2 = max_workers > 32;
-    auto kern = w2 ? k_simulate_w2 : k_simulate_w1;
+    auto kern = compact ? (w2 ? k_simulate_w2c : k_simulate_w1c) : (w2 ? k_simulate_w2 : k_simulate_w1);
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "cudaFuncSetAttribute(k_simulate)");
     ctx->begin("k_simulate");
@@ -710,13 +746,15 @@ T* scratch_if_null(tbsim_ctx* ctx, const char* name, T* p, size_t count) {
 }
 
 int32_t upload_platforms(tbsim_ctx* ctx, const tbsim_batch* b, const tbsim_platform_desc* platforms, int32_t n_platforms,
-                         DevPlatform** d_out, std::vector<DevPlatform>& host) {
+                         DevPlatform** d_out, std::vector<DevPlatform>& host, int32_t* max_nodes) {
     if (n_platforms < 1) raise(TBSIM_E_INVALID_ARGUMENT, "need at least one platform");
     int32_t maxw = 0;
+    *max_nodes = 1;
     host.clear();
     for (int i = 0; i < n_platforms; ++i) {
         host.push_back(to_dev_platform(platforms[i], b->d.n_types));
         maxw = std::max(maxw, platforms[i].n_workers);
+        *max_nodes = std::max(*max_nodes, platforms[i].n_nodes);
     }
     *d_out = ctx->buf("platforms").as<DevPlatform>(n_platforms);
     cuda_check(cudaMemcpyAsync(*d_out, host.data(), host.size() * sizeof(DevPlatform), cudaMemcpyHostToDevice, ctx->stream),
@@ -744,12 +782,25 @@ extern "C" tbsim_status tbsim_simulate(tbsim_ctx* ctx, const tbsim_batch* b, con
         for (int64_t g = 0; g < G; ++g) check_reg(reg[g]);
         std::vector<DevPlatform> hp;
         DevPlatform* d_pf = nullptr;
-        const int32_t maxw = upload_platforms(ctx, b, platforms, n_platforms, &d_pf, hp);
+        int32_t max_nodes = 1;
+        const int32_t maxw = upload_platforms(ctx, b, platforms, n_platforms, &d_pf, hp, &max_nodes);
         SimStage st;
         const bool dev = out->on_device != 0;
         SimParams p{};
         p.b = d;
         p.platforms = d_pf;
+        p.max_nodes = max_nodes;
+        p.n_types = d.n_types;
+        int32_t ring = 1;
+        for (int64_t g = 0; g < G; ++g) ring = std::max(ring, reg[g].slope_samples);
+        if (out->reg_state && !dev)
+            for (int64_t g = 0; g < G; ++g) {
+                if (out->reg_state[g].n_samples < 0 || out->reg_state[g].n_samples > TBSIM_MAX_SLOPE_SAMPLES)
+                    raise(TBSIM_E_INVALID_ARGUMENT, "regulator state holds too many samples");
+                ring = std::max(ring, out->reg_state[g].n_samples);
+            }
+        if (out->reg_state && dev) ring = TBSIM_MAX_SLOPE_SAMPLES;
+        p.ring = pow2_at_least(ring);
         if (platform_of) {
             for (int64_t g = 0; g < G && !dev; ++g)
                 if (platform_of[g] < 0 || platform_of[g] >= n_platforms) raise(TBSIM_E_INVALID_ARGUMENT, "platform index out of range");
@@ -812,7 +863,8 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         const int64_t T = d.T, G = d.G;
         std::vector<DevPlatform> hp;
         DevPlatform* d_pf = nullptr;
-        const int32_t maxw = upload_platforms(ctx, b, platforms, n_platforms, &d_pf, hp);
+        int32_t max_nodes = 1;
+        const int32_t maxw = upload_platforms(ctx, b, platforms, n_platforms, &d_pf, hp, &max_nodes);
         // cost tables of the platforms, one per platform (compute_attributes
         // runs on platform.costs, src/bench.cpp:104)
         std::vector<DevCosts> hc;
@@ -851,6 +903,14 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         p.b = d;
         p.platforms = d_pf;
         p.platform_of = d_pof;
+        p.max_nodes = max_nodes;
+        p.n_types = d.n_types;
+        p.ring = 8;  // default_regulator_config: slope_samples = 8
+        if (out->reg_state) {
+            if (out->on_device) p.ring = TBSIM_MAX_SLOPE_SAMPLES;
+            else
+                for (int64_t g = 0; g < G; ++g) p.ring = std::max(p.ring, pow2_at_least(out->reg_state[g].n_samples));
+        }
         p.policy = policy;
         p.reg = nullptr;
         p.median = run.s.median;

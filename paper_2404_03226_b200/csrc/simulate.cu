@@ -18,8 +18,12 @@
 // worker_free_at (engine.cpp:53-59) is cached per lane and extended with
 // `+= exec` on every push (the same left-to-right sum the reference forms);
 // after a dispatch it is recomputed from busy_until in queue order.
+// Transfer estimates (engine.cpp:105-110) are computed lanes-over-inputs and
+// summed in input order with shuffles, so a push costs one round of loads
+// instead of one dependent chain per input.
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "common.cuh"
 #include "simulate.cuh"
@@ -39,26 +43,30 @@ __device__ __forceinline__ uint64_t ord_i64(int64_t x) {
     return static_cast<uint64_t>(x) ^ 0x8000000000000000ull;
 }
 
-template <int WPL>
+template <int WPL, bool COMPACT>
 struct Sim {
+    using UnmetT = typename std::conditional<COMPACT, int16_t, int32_t>::type;
+    using ResidT = typename std::conditional<COMPACT, uint8_t, uint32_t>::type;
+    using ReadyT = UnmetT;
     // ---- graph
     int64_t g, t0;
     int32_t n, nh;
     const int32_t *doff, *soff, *succ, *ioff, *in, *ooff, *out, *type;
     const int64_t* hbytes;
-    const DevPlatform* pf;
     int32_t W, nn;
     double lat;
     int32_t policy;
     const int64_t *ability, *efficiency, *prio;
-    // ---- per-warp state memory
-    int32_t* unmet;
-    uint32_t* resid;
-    int32_t* ready;
+    // ---- per-warp state memory (shared memory when it fits)
+    UnmetT* unmet;
+    ResidT* resid;
+    ReadyT* ready;
     int32_t* queue;
     double* samp_t;
     int64_t* samp_n;
-    int32_t qcap;
+    double* costs;   // [2*NT]: cpu, gpu per type
+    double* bw;      // [nn*nn]
+    int32_t qcap, ring_mask;
     // ---- lane-owned workers
     int32_t kind[WPL], node[WPL], qlen[WPL];
     bool busy[WPL], fdirty[WPL];
@@ -83,30 +91,65 @@ struct Sim {
     tbsim_regulator_cfg cfg;
     const SimParams* P;
 
-    __device__ __forceinline__ double cost(int32_t ty, int32_t k) const {
-        return k ? __ldg(&pf->costs.gpu[ty]) : __ldg(&pf->costs.cpu[ty]);
-    }
+    __device__ __forceinline__ double cost(int32_t ty, int32_t k) const { return costs[2 * ty + k]; }
 
     // transfer_one_ms (engine.cpp:86-103): fastest resident copy, ties to the
     // lowest node; Platform::transfer_time_ms (platform.cpp:56-63).
-    __device__ __forceinline__ double transfer_one(int32_t h, int32_t to) const {
-        const uint32_t m = resid[h];
+    __device__ __forceinline__ double transfer_one(uint32_t m, int64_t bytes, int32_t to) const {
         if ((m >> to) & 1u) return 0.0;
         int32_t best = 0;
         double bbw = -1.0;
         for (uint32_t mm = m; mm; mm &= mm - 1) {
             const int32_t nd = __ffs(mm) - 1;
-            const double bw = __ldg(&pf->bw[nd * kMaxNodes + to]);
-            if (bw > bbw) { bbw = bw; best = nd; }
+            const double b = bw[nd * nn + to];
+            if (b > bbw) { bbw = b; best = nd; }
         }
-        return lat + static_cast<double>(__ldg(&hbytes[h])) / __ldg(&pf->bw[best * kMaxNodes + to]);
+        return lat + static_cast<double>(bytes) / bw[best * nn + to];
     }
-    // transfer_total_ms (engine.cpp:105-110): inputs in order
-    __device__ __forceinline__ double transfer_total(int32_t task, int32_t to) const {
-        double total = 0.0;
-        for (int32_t k = __ldg(&ioff[task]); k < __ldg(&ioff[task + 1]); ++k) total += transfer_one(__ldg(&in[k]), to);
-        return total;
+
+    // transfer_total_ms (engine.cpp:105-110) for node `want` (may differ per
+    // lane): lanes hold the inputs, the per-input times are summed in input
+    // order by shuffles, for every node that any lane asks for.
+    __device__ __forceinline__ double transfer_total_lanes(int32_t task, int32_t want) const {
+        const int32_t k0 = __ldg(&ioff[task]), k1 = __ldg(&ioff[task + 1]);
+        const int32_t nin = k1 - k0;
+        double mine = 0.0;
+        if (nin == 0) return 0.0;
+        const unsigned want_nodes = __reduce_or_sync(kFull, 1u << want);
+        if (nin <= 32) {
+            uint32_t m = 0;
+            int64_t by = 0;
+            if (lane < nin) {
+                const int32_t h = __ldg(&in[k0 + lane]);
+                m = resid[h];
+                by = __ldg(&hbytes[h]);
+            }
+            for (unsigned wn = want_nodes; wn; wn &= wn - 1) {
+                const int32_t to = __ffs(wn) - 1;
+                const double t = lane < nin ? transfer_one(m, by, to) : 0.0;
+                double acc = 0.0;
+                for (int32_t j = 0; j < nin; ++j) acc += __shfl_sync(kFull, t, j);
+                if (want == to) mine = acc;
+            }
+            return mine;
+        }
+        for (unsigned wn = want_nodes; wn; wn &= wn - 1) {
+            const int32_t to = __ffs(wn) - 1;
+            double acc = 0.0;
+            for (int32_t base = 0; base < nin; base += 32) {
+                const int32_t cnt = min(32, nin - base);
+                double t = 0.0;
+                if (lane < cnt) {
+                    const int32_t h = __ldg(&in[k0 + base + lane]);
+                    t = transfer_one(resid[h], __ldg(&hbytes[h]), to);
+                }
+                for (int32_t j = 0; j < cnt; ++j) acc += __shfl_sync(kFull, t, j);
+            }
+            if (want == to) mine = acc;
+        }
+        return mine;
     }
+
     // resident_fraction (engine.cpp:63-74)
     __device__ __forceinline__ double resident_fraction(int32_t task, int32_t nd) const {
         const int32_t k0 = __ldg(&ioff[task]), k1 = __ldg(&ioff[task + 1]);
@@ -116,7 +159,7 @@ struct Sim {
             const int32_t h = __ldg(&in[k]);
             const int64_t by = __ldg(&hbytes[h]);
             total += by;
-            if ((resid[h] >> nd) & 1u) local += by;
+            if ((static_cast<uint32_t>(resid[h]) >> nd) & 1u) local += by;
         }
         return static_cast<double>(local) / static_cast<double>(total);
     }
@@ -126,7 +169,7 @@ struct Sim {
         if (r_count < 2) return 0.0;
         double sx = 0.0, sy = 0.0;
         for (int i = 0; i < r_count; ++i) {
-            const int idx = (r_head + i) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+            const int idx = (r_head + i) & ring_mask;
             sx += samp_t[idx];
             sy += static_cast<double>(samp_n[idx]);
         }
@@ -134,7 +177,7 @@ struct Sim {
         const double mx = sx / dn, my = sy / dn;
         double sxx = 0.0, sxy = 0.0;
         for (int i = 0; i < r_count; ++i) {
-            const int idx = (r_head + i) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+            const int idx = (r_head + i) & ring_mask;
             const double dx = samp_t[idx] - mx;
             sxx += dx * dx;
             sxy += dx * (static_cast<double>(samp_n[idx]) - my);
@@ -145,13 +188,13 @@ struct Sim {
 
     __device__ __forceinline__ void regulator_step(int64_t cur) {  // policies.cpp:171-203
         __syncwarp();
-        const int idx = (r_head + r_count) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+        const int idx = (r_head + r_count) & ring_mask;
         if (lane == 0) { samp_t[idx] = now; samp_n[idx] = cur; }
         __syncwarp();
-        if (r_count < TBSIM_MAX_SLOPE_SAMPLES) ++r_count;
-        else r_head = (r_head + 1) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+        if (r_count <= ring_mask) ++r_count;
+        else r_head = (r_head + 1) & ring_mask;
         while (r_count > cfg.slope_samples) {
-            r_head = (r_head + 1) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+            r_head = (r_head + 1) & ring_mask;
             --r_count;
         }
         const int64_t d = cur - last_trigger;
@@ -204,8 +247,15 @@ struct Sim {
     // capable workers, strict < so ties keep the lowest id.
     __device__ __forceinline__ int32_t select_worker(int32_t task, int32_t ty) {
         if (policy != TBSIM_POLICY_FIFO) refresh_free();
+        double xfer[WPL];
+#pragma unroll
+        for (int j = 0; j < WPL; ++j) xfer[j] = 0.0;
+        if (policy >= TBSIM_POLICY_DMDA) {
+#pragma unroll
+            for (int j = 0; j < WPL; ++j) xfer[j] = transfer_total_lanes(task, node[j]);
+        }
         uint64_t bk = ~0ull;
-        int32_t bw = INT_MAX;
+        int32_t bwk = INT_MAX;
 #pragma unroll
         for (int j = 0; j < WPL; ++j) {
             const int32_t w = lane + 32 * j;
@@ -219,13 +269,13 @@ struct Sim {
                 const double fa = busy[j] ? fsum[j] : now;
                 const double st = now < fa ? fa : now;  // std::max(now, free_at)
                 if (policy == TBSIM_POLICY_DM) key = st + ce;
-                else key = (st + transfer_total(task, node[j])) + ce;
+                else key = (st + xfer[j]) + ce;
             }
             const uint64_t kb = ord_f64(key);
-            if (kb < bk) { bk = kb; bw = w; }
+            if (kb < bk) { bk = kb; bwk = w; }
         }
         const uint64_t mk = warp_min_u64(bk);
-        const int32_t w = __reduce_min_sync(kFull, bk == mk ? bw : INT_MAX);
+        const int32_t w = __reduce_min_sync(kFull, bk == mk ? bwk : INT_MAX);
         return mk == ~0ull ? -1 : w;
     }
 
@@ -308,7 +358,7 @@ struct Sim {
         }
         ++n_pop;
         queue_event();
-        const double xfer = transfer_total(task, nd);
+        const double xfer = transfer_total_lanes(task, nd);
         const double exec = cost(ty, kd);
         const double start = now + xfer;
         const double end = start + exec;
@@ -374,11 +424,11 @@ struct Sim {
             bool root = false;
             if (v < n) {
                 const int32_t deg = __ldg(&doff[v + 1]) - __ldg(&doff[v]);
-                unmet[v] = deg;
+                unmet[v] = static_cast<UnmetT>(deg);
                 root = deg == 0;
             }
             const unsigned bal = __ballot_sync(kFull, root);
-            if (root) ready[rcount + __popc(bal & ((1u << lane) - 1u))] = v;
+            if (root) ready[rcount + __popc(bal & ((1u << lane) - 1u))] = static_cast<ReadyT>(v);
             rcount += __popc(bal);
         }
         for (int32_t h = lane; h < nh; h += 32) resid[h] = 1u;  // engine.cpp:215-216
@@ -430,7 +480,7 @@ struct Sim {
                 if (!is_done) {  // TransferDone: inputs resident (engine.cpp:168-172)
                     for (int32_t k = __ldg(&ioff[task]) + lane; k < __ldg(&ioff[task + 1]); k += 32) {
                         const int32_t h = __ldg(&in[k]);
-                        resid[h] |= bit;
+                        resid[h] = static_cast<ResidT>(resid[h] | bit);
                     }
                     __syncwarp();
                     continue;
@@ -438,25 +488,31 @@ struct Sim {
                 // TaskDone (engine.cpp:174-185)
                 for (int32_t k = __ldg(&ooff[task]) + lane; k < __ldg(&ooff[task + 1]); k += 32) {
                     const int32_t h = __ldg(&out[k]);
-                    resid[h] |= bit;
+                    resid[h] = static_cast<ResidT>(resid[h] | bit);
                 }
 #pragma unroll
                 for (int j = 0; j < WPL; ++j)
                     if (j == (w >> 5) && lane == owner) busy[j] = false;
                 completed += 1;
                 makespan = now > makespan ? now : makespan;
+                // successors: sorted, multi-edges adjacent; the lowest lane of
+                // each run of equal ids decrements by the run length
                 const int32_t s0 = __ldg(&soff[task]), s1 = __ldg(&soff[task + 1]);
                 for (int32_t base = s0; base < s1; base += 32) {
                     const int32_t k = base + lane;
+                    const bool valid = k < s1;
+                    const int32_t sv = valid ? __ldg(&succ[k]) : -1 - lane;
+                    const unsigned peers = __match_any_sync(kFull, sv);
                     bool rdy = false;
-                    int32_t sv = 0;
-                    if (k < s1) {
-                        sv = __ldg(&succ[k]);
-                        rdy = atomicSub(&unmet[sv], 1) == 1;
+                    if (valid && (__ffs(peers) - 1) == lane) {
+                        const int32_t left = static_cast<int32_t>(unmet[sv]) - __popc(peers);
+                        unmet[sv] = static_cast<UnmetT>(left);
+                        rdy = left == 0;
                     }
                     const unsigned bal = __ballot_sync(kFull, rdy);
-                    if (rdy) ready[rcount + __popc(bal & ((1u << lane) - 1u))] = sv;
+                    if (rdy) ready[rcount + __popc(bal & ((1u << lane) - 1u))] = static_cast<ReadyT>(sv);
                     rcount += __popc(bal);
+                    __syncwarp();
                 }
                 __syncwarp();
                 maybe_dispatch(w);
@@ -466,7 +522,7 @@ struct Sim {
     }
 };
 
-template <int WPL>
+template <int WPL, bool COMPACT>
 __device__ void simulate_impl(const SimParams& p) {
     extern __shared__ __align__(16) char smem[];
     const int lane = threadIdx.x & 31;
@@ -475,20 +531,23 @@ __device__ void simulate_impl(const SimParams& p) {
     char* base = p.use_smem ? smem + static_cast<int64_t>(warp_in_block) * p.state_bytes
                             : p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
     const DevBatch& b = p.b;
-    const int64_t max_n = b.max_n, max_h = b.max_h;
-    auto al = [](int64_t x) { return (x + 15) & ~int64_t(15); };
-    Sim<WPL> s;
+    const SimLayout L = sim_layout(b.max_n, b.max_h, p.max_workers, p.qcap, p.ring, p.n_types, p.max_nodes, COMPACT);
+    using S = Sim<WPL, COMPACT>;
+    S s;
     s.P = &p;
     s.lane = lane;
-    s.unmet = reinterpret_cast<int32_t*>(base);
-    s.resid = reinterpret_cast<uint32_t*>(base + al(4 * max_n));
-    s.ready = reinterpret_cast<int32_t*>(base + al(4 * max_n) + al(4 * max_h));
-    s.queue = reinterpret_cast<int32_t*>(base + 2 * al(4 * max_n) + al(4 * max_h));
-    char* ring = base + 2 * al(4 * max_n) + al(4 * max_h) + al(4LL * p.max_workers * p.qcap);
-    s.samp_t = reinterpret_cast<double*>(ring);
-    s.samp_n = reinterpret_cast<int64_t*>(ring + 8 * TBSIM_MAX_SLOPE_SAMPLES);
+    s.unmet = reinterpret_cast<typename S::UnmetT*>(base + L.unmet);
+    s.resid = reinterpret_cast<typename S::ResidT*>(base + L.resid);
+    s.ready = reinterpret_cast<typename S::ReadyT*>(base + L.ready);
+    s.queue = reinterpret_cast<int32_t*>(base + L.queue);
+    s.samp_t = reinterpret_cast<double*>(base + L.ring);
+    s.samp_n = reinterpret_cast<int64_t*>(base + L.ring + 8 * p.ring);
+    s.costs = reinterpret_cast<double*>(base + L.costs);
+    s.bw = reinterpret_cast<double*>(base + L.bw);
     s.qcap = p.qcap;
+    s.ring_mask = p.ring - 1;
     s.policy = p.policy;
+    int32_t loaded_pf = -1;
 
     for (;;) {
         unsigned long long item = 0;
@@ -509,18 +568,29 @@ __device__ void simulate_impl(const SimParams& p) {
         s.out = b.out + b.out_base[g];
         s.type = b.type + s.t0;
         s.hbytes = b.handle_bytes + b.handle_base[g];
-        s.pf = p.platforms + (p.platform_of ? p.platform_of[g] : 0);
-        s.W = s.pf->n_workers;
-        s.nn = s.pf->n_nodes;
-        s.lat = s.pf->latency_ms;
+        const int32_t pfi = p.platform_of ? p.platform_of[g] : 0;
+        const DevPlatform* pf = p.platforms + pfi;
+        s.W = pf->n_workers;
+        s.nn = pf->n_nodes;
+        s.lat = pf->latency_ms;
+        if (pfi != loaded_pf) {  // platform tables into this warp's state
+            __syncwarp();
+            for (int i = lane; i < p.n_types; i += 32) {
+                s.costs[2 * i] = pf->costs.cpu[i];
+                s.costs[2 * i + 1] = pf->costs.gpu[i];
+            }
+            for (int i = lane; i < s.nn * s.nn; i += 32) s.bw[i] = pf->bw[(i / s.nn) * kMaxNodes + i % s.nn];
+            __syncwarp();
+            loaded_pf = pfi;
+        }
         s.ability = p.ability;
         s.efficiency = p.efficiency;
         s.prio = p.prio;
 #pragma unroll
         for (int j = 0; j < WPL; ++j) {
             const int32_t w = lane + 32 * j;
-            s.kind[j] = w < s.W ? s.pf->kind[w] : 0;
-            s.node[j] = w < s.W ? s.pf->node[w] : 0;
+            s.kind[j] = w < s.W ? pf->kind[w] : 0;
+            s.node[j] = w < s.W ? pf->node[w] : 0;
             s.qlen[j] = 0;
             s.busy[j] = false;
             s.fdirty[j] = false;
@@ -585,18 +655,18 @@ __device__ void simulate_impl(const SimParams& p) {
                 p.pop_counts[3 * g + 1] = s.pop1;
                 p.pop_counts[3 * g + 2] = s.pop2;
             }
-            if (p.reg_state && p.policy == TBSIM_POLICY_INSPIRIT) {
+            if (p.reg_state && p.policy == TBSIM_POLICY_INSPIRIT && s.status == GS_OK) {
                 tbsim_regulator_state& rs = p.reg_state[g];
                 rs.mode = s.mode; rs.phase = s.phase; rs.peak = s.peak; rs.prev_nready = s.prev_nready;
                 rs.last_trigger_nready = s.last_trigger; rs.s_dec_count = s.s_dec_count; rs.cur_k = s.cur_k;
                 rs.n_samples = s.r_count;
             }
         }
-        if (p.reg_state && p.policy == TBSIM_POLICY_INSPIRIT) {
+        if (p.reg_state && p.policy == TBSIM_POLICY_INSPIRIT && s.status == GS_OK) {
             __syncwarp();
             tbsim_regulator_state& rs = p.reg_state[g];
             for (int i = lane; i < s.r_count; i += 32) {
-                const int idx = (s.r_head + i) & (TBSIM_MAX_SLOPE_SAMPLES - 1);
+                const int idx = (s.r_head + i) & s.ring_mask;
                 rs.sample_time[i] = s.samp_t[idx];
                 rs.sample_nready[i] = s.samp_n[idx];
             }
@@ -607,7 +677,9 @@ __device__ void simulate_impl(const SimParams& p) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(256, 2) k_simulate_w1(const __grid_constant__ SimParams p) { simulate_impl<1>(p); }
-__global__ void __launch_bounds__(256, 2) k_simulate_w2(const __grid_constant__ SimParams p) { simulate_impl<2>(p); }
+__global__ void __launch_bounds__(256, 2) k_simulate_w1c(const __grid_constant__ SimParams p) { simulate_impl<1, true>(p); }
+__global__ void __launch_bounds__(256, 2) k_simulate_w2c(const __grid_constant__ SimParams p) { simulate_impl<2, true>(p); }
+__global__ void __launch_bounds__(256, 2) k_simulate_w1(const __grid_constant__ SimParams p) { simulate_impl<1, false>(p); }
+__global__ void __launch_bounds__(256, 2) k_simulate_w2(const __grid_constant__ SimParams p) { simulate_impl<2, false>(p); }
 
 }  // namespace tbsim_dev

@@ -37,22 +37,40 @@ struct SimParams {
     int32_t qcap;                     // queue capacity per worker
     int32_t use_smem;
     int32_t max_workers;
+    int32_t max_nodes;                // platform copy: nodes x nodes bandwidth
+    int32_t n_types;                  // platform copy: cost rows
+    int32_t ring;                     // regulator sample ring capacity (power of 2)
     const int32_t* graph_list;        // subset of graphs (rerun) or null
     int64_t n_items;                  // graphs to process (list length or G)
     unsigned long long* work_counter;
 };
 
-__global__ void k_simulate_w1(const __grid_constant__ SimParams p);  // <= 32 workers
-__global__ void k_simulate_w2(const __grid_constant__ SimParams p);  // <= 64 workers
+__global__ void k_simulate_w1c(const __grid_constant__ SimParams p);  // <= 32 workers, compact state
+__global__ void k_simulate_w2c(const __grid_constant__ SimParams p);  // <= 64 workers, compact state
+__global__ void k_simulate_w1(const __grid_constant__ SimParams p);   // <= 32 workers, wide state
+__global__ void k_simulate_w2(const __grid_constant__ SimParams p);   // <= 64 workers, wide state
 
-// bytes of per-warp state for a batch
-__host__ __device__ inline int64_t sim_state_bytes(int64_t max_n, int64_t max_h, int64_t max_workers, int64_t qcap) {
+// Per-warp state layout (bytes, 16-aligned sections).  Compact state
+// (n < 32768, <= 8 memory nodes) stores unmet counts and the ready list as
+// int16 and residency masks as uint8.
+struct SimLayout {
+    int64_t unmet, resid, ready, queue, ring, costs, bw, total;
+};
+
+__host__ __device__ inline SimLayout sim_layout(int64_t max_n, int64_t max_h, int64_t max_workers, int64_t qcap,
+                                                int64_t ring, int64_t n_types, int64_t max_nodes, bool compact) {
     auto al = [](int64_t x) { return (x + 15) & ~int64_t(15); };
-    return al(4 * max_n)                       // unmet
-         + al(4 * max_h)                       // residency masks
-         + al(4 * max_n)                       // ready list
-         + al(4 * max_workers * qcap)          // queues
-         + al(16 * TBSIM_MAX_SLOPE_SAMPLES);   // regulator sample ring
+    SimLayout L;
+    int64_t off = 0;
+    L.unmet = off; off += al((compact ? 2 : 4) * max_n);
+    L.resid = off; off += al((compact ? 1 : 4) * max_h);
+    L.ready = off; off += al((compact ? 2 : 4) * max_n);
+    L.queue = off; off += al(4 * max_workers * qcap);
+    L.ring = off; off += al(16 * ring);
+    L.costs = off; off += al(16 * n_types);
+    L.bw = off; off += al(8 * max_nodes * max_nodes);
+    L.total = off;
+    return L;
 }
 
 }  // namespace tbsim_dev

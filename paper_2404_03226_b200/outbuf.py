@@ -30,21 +30,26 @@ def attr_out(T: int, G: int, unit_time=None):
     return out, o
 
 
-def sim_out(T: int, G: int, record: bool, states=None):
-    out = {"worker": np.zeros(T, np.int32), "start_ms": np.zeros(T), "end_ms": np.zeros(T),
-           "makespan_ms": np.zeros(G), "completed": np.zeros(G, np.int64),
-           "pop_mode_counts": np.zeros(3 * G, np.int64)}
-    if states is None:
+def sim_out(T: int, G: int, record: bool, states=None, want_states=True, arrays=None):
+    """arrays: optional dict of preallocated (ideally pinned) numpy outputs."""
+    if arrays is not None:
+        out = dict(arrays)
+    else:
+        out = {"worker": np.zeros(T, np.int32), "start_ms": np.zeros(T), "end_ms": np.zeros(T),
+               "makespan_ms": np.zeros(G), "completed": np.zeros(G, np.int64),
+               "pop_mode_counts": np.zeros(3 * G, np.int64)}
+    if states is None and want_states:
         states = (abi.RegulatorState * max(G, 1))()
+        fresh = abi.fresh_regulator_state()
         for i in range(G):
-            states[i] = abi.fresh_regulator_state()
+            states[i] = fresh
     o = abi.SimOut()
     o.worker = _p(out["worker"], C.c_int32)
     o.start_ms = _p(out["start_ms"], C.c_double)
     o.end_ms = _p(out["end_ms"], C.c_double)
     o.makespan_ms = _p(out["makespan_ms"], C.c_double)
     o.completed = _p(out["completed"], C.c_int64)
-    o.pop_mode_counts = _p(out["pop_mode_counts"], C.c_int64)
+    o.pop_mode_counts = _p(out.get("pop_mode_counts"), C.c_int64)
     o.reg_state = states
     if record:
         out.update(push_time=np.zeros(T), push_task=np.zeros(T, np.int32),
