@@ -401,7 +401,10 @@ AttrScratch alloc_attr_scratch(tbsim_ctx* ctx, const DevBatch& d) {
     s.fstack = ctx->buf("a_fstack").as<int32_t>(T);
     s.cls = ctx->buf("a_cls").as<int32_t>(T);
     s.cls_mark = ctx->buf("a_clsmark").as<int32_t>(T * NT);
-    s.pslot = ctx->buf("a_pslot").as<int32_t>(E);
+    s.om_slot = ctx->buf("a_omslot").as<int32_t>(T);
+    s.om_gpu = ctx->buf("a_omgpu").as<double>(T);
+    s.om_poff = ctx->buf("a_ompoff").as<int32_t>(T + G);
+    s.om_pslot = ctx->buf("a_ompslot").as<int32_t>(E);
     s.rank = ctx->buf("a_rank").as<double>(T);
     s.hist = ctx->buf("a_hist").as<uint64_t>(4 * T);
     s.info = ctx->buf("a_info").as<GraphInfo>(G);

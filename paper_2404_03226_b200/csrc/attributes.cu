@@ -222,10 +222,27 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
             __syncthreads();
             fs = nfs + r;
         }
-        // ---- predecessor slots (edge-major) and static priority
-        int32_t* pslot = s.pslot + b.edge_base[g];
-        for (int32_t v = tid; v < n; v += nthr)
-            for (int32_t k = doff[v]; k < doff[v + 1]; ++k) pslot[k] = slot[dep[k]];
+        // ---- order-major node records for the sweep: slot, GPU time and
+        //      the predecessors' slots, contiguous in level order
+        int32_t* om_slot = s.om_slot + t0;
+        double* om_gpu = s.om_gpu + t0;
+        int32_t* om_poff = s.om_poff + t0 + g;
+        int32_t* om_ps = s.om_pslot + b.edge_base[g];
+        for (int32_t i = tid; i < processed; i += nthr) {
+            const int32_t v = order[i];
+            om_slot[i] = slot[v];
+            const int32_t ty = type[v];
+            om_gpu[i] = ty < NT ? sc.gpu[ty] : 0.0;
+            om_poff[i] = doff[v + 1] - doff[v];
+        }
+        if (tid == 0) om_poff[processed] = 0;
+        __syncthreads();
+        block_exclusive_scan_inplace(om_poff, processed + 1, warp_tot);
+        for (int32_t i = tid; i < processed; i += nthr) {
+            const int32_t v = order[i];
+            const int32_t o = om_poff[i] - doff[v];
+            for (int32_t k = doff[v]; k < doff[v + 1]; ++k) om_ps[o + k] = slot[dep[k]];
+        }
         // ---- calibration classes: dense ids of present (layer, type) pairs
         int32_t* mark = s.cls_mark + t0 * NT;   // [L * NT] <= n * NT
         const int64_t nkeys = static_cast<int64_t>(L) * NT;
@@ -347,11 +364,12 @@ __device__ Thresholds make_thresholds(int32_t mode_req, double w0_or_unit) {
     return th;
 }
 
-// Group of GL lanes handles one node for S sources (S/GL per lane).
+// Group of GL lanes handles one node for S sources (S/GL per lane).  Node
+// records are read in level order (order-major arrays), the sources' distance
+// columns live in shared memory: win[slot][S].
 template <int S>
-__device__ void sweep_tile(const DevBatch& b, const AttrScratch& s, const DevCosts& sc, int64_t g,
-                           int32_t tile, double* win, int32_t P, const Thresholds& th,
-                           unsigned long long* s_hist) {
+__device__ void sweep_tile(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile, double* win,
+                           int32_t P, const Thresholds& th, unsigned long long* s_hist) {
     constexpr int GL = S < 32 ? S : 32;   // lanes per node group
     constexpr int SPL = S / GL;           // sources per lane
     constexpr int GPW = 32 / GL;          // groups per warp
@@ -361,68 +379,66 @@ __device__ void sweep_tile(const DevBatch& b, const AttrScratch& s, const DevCos
     const unsigned gmask = GL == 32 ? 0xffffffffu : (((1u << GL) - 1u) << (grp * GL));
 
     const int64_t t0 = b.task_base[g];
-    const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
-    const int32_t* doff = b.dep_off + t0 + g;
-    const int32_t* type = b.type + t0;
-    const int32_t* order = s.order + t0;
-    const int32_t* level = s.level + t0;
     const int32_t* lstart = s.lstart + t0 + g;
-    const int32_t* slot = s.slot + t0;
-    const int32_t* pslot = s.pslot + b.edge_base[g];
+    const int32_t* om_slot = s.om_slot + t0;
+    const double* om_gpu = s.om_gpu + t0;
+    const int32_t* om_poff = s.om_poff + t0 + g;
+    const int32_t* om_ps = s.om_pslot + b.edge_base[g];
     const GraphInfo gi = s.info[g];
     const int32_t first = tile * S;
     const int32_t nsrc = min(S, gi.processed - first);
 
     for (int64_t i = threadIdx.x; i < static_cast<int64_t>(P) * S; i += blockDim.x) win[i] = -1.0;
     for (int i = threadIdx.x; i < S * 4; i += blockDim.x) s_hist[i] = 0ull;
-    int32_t src[SPL];
     uint64_t hist[SPL][4];
 #pragma unroll
-    for (int q = 0; q < SPL; ++q) {
-        const int si = gl * SPL + q;
-        src[q] = si < nsrc ? order[first + si] : -1;
-        hist[q][0] = hist[q][1] = hist[q][2] = hist[q][3] = 0;
-    }
-    const int32_t La = level[order[first]];
+    for (int q = 0; q < SPL; ++q) hist[q][0] = hist[q][1] = hist[q][2] = hist[q][3] = 0;
+    const int32_t La = s.level[t0 + s.order[t0 + first]];
+    const int32_t my_first = first + gl * SPL;  // order position of this lane's first source
     __syncthreads();
 
     for (int32_t lv = La; lv < gi.n_levels; ++lv) {
-        const int32_t a0 = lstart[lv], a1 = lstart[lv + 1];
+        const int32_t a1 = lstart[lv + 1];
         // groups are independent: every lane of a group sees the same node
-        for (int32_t i = a0 + warp * GPW + grp; i < a1; i += nwarps * GPW) {
-            const int32_t v = order[i];
-            const int32_t p0 = doff[v];
-            const int32_t deg = doff[v + 1] - p0;
-            const double gv = th.mode == 2 ? 1.0 : cost_of(sc, type[v], 1);
+        for (int32_t i = lstart[lv] + warp * GPW + grp; i < a1; i += nwarps * GPW) {
+            const int32_t p0 = om_poff[i];
+            const int32_t deg = om_poff[i + 1] - p0;
+            const double gv = th.mode == 2 ? 1.0 : om_gpu[i];
+            const int32_t sl = om_slot[i];
             double m[SPL];
 #pragma unroll
             for (int q = 0; q < SPL; ++q) m[q] = -1.0;
             for (int32_t c = 0; c < deg; c += GL) {
-                const int32_t myps = (c + gl < deg) ? pslot[p0 + c + gl] : 0;
+                const int32_t myps = (c + gl < deg) ? om_ps[p0 + c + gl] : 0;
                 const int32_t lim = min(GL, deg - c);
                 for (int32_t j = 0; j < lim; ++j) {
                     const int32_t ps = __shfl_sync(gmask, myps, grp * GL + j);
                     const double* row = win + static_cast<int64_t>(ps) * S + gl * SPL;
-                    if constexpr (SPL == 2) {
-                        const double2 x = *reinterpret_cast<const double2*>(row);
-                        m[0] = fmax(m[0], x.x);
-                        m[1] = fmax(m[1], x.y);
+                    if constexpr (SPL >= 2) {
+#pragma unroll
+                        for (int q = 0; q < SPL; q += 2) {
+                            const double2 x = *reinterpret_cast<const double2*>(row + q);
+                            m[q] = fmax(m[q], x.x);
+                            m[q + 1] = fmax(m[q + 1], x.y);
+                        }
                     } else {
                         m[0] = fmax(m[0], row[0]);
                     }
                 }
             }
-            double* out = win + static_cast<int64_t>(slot[v]) * S + gl * SPL;
+            double d[SPL];
 #pragma unroll
             for (int q = 0; q < SPL; ++q) {
-                double d;
-                if (v == src[q]) {
-                    d = 0.0;
-                } else {
-                    d = m[q] < 0.0 ? -1.0 : m[q] + gv;
-                    if (d >= 0.0 && src[q] >= 0) bump(hist[q], bin_of(d, th));
-                }
-                out[q] = d;
+                const bool is_src = i == my_first + q;
+                d[q] = is_src ? 0.0 : (m[q] < 0.0 ? -1.0 : m[q] + gv);
+                if (!is_src && d[q] >= 0.0) bump(hist[q], bin_of(d[q], th));
+            }
+            double* outp = win + static_cast<int64_t>(sl) * S + gl * SPL;
+            if constexpr (SPL >= 2) {
+#pragma unroll
+                for (int q = 0; q < SPL; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(d[q], d[q + 1]);
+            } else {
+                outp[0] = d[0];
             }
         }
         __syncthreads();
@@ -431,11 +447,12 @@ __device__ void sweep_tile(const DevBatch& b, const AttrScratch& s, const DevCos
     // partial histograms (fields never carry: totals stay < 2^21)
 #pragma unroll
     for (int q = 0; q < SPL; ++q)
-        if (src[q] >= 0)
+        if (gl * SPL + q < nsrc)
 #pragma unroll
             for (int w = 0; w < 4; ++w)
                 if (hist[q][w]) atomicAdd(&s_hist[(gl * SPL + q) * 4 + w], static_cast<unsigned long long>(hist[q][w]));
     __syncthreads();
+    const int32_t* order = s.order + t0;
     for (int i = threadIdx.x; i < nsrc * 4; i += blockDim.x)
         s.hist[(t0 + order[first + i / 4]) * 4 + (i & 3)] = s_hist[i];
 }
@@ -446,10 +463,10 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
                                               int64_t total_tiles, unsigned long long* work_counter,
                                               int64_t smem_bytes, double* gwin, int64_t gwin_stride) {
     extern __shared__ double win_smem[];
-    __shared__ DevCosts sc;
     __shared__ int64_t s_item;
-    __shared__ unsigned long long s_hist[64 * 4];
-    int32_t loaded = -1;
+    __shared__ unsigned long long s_hist[128 * 4];
+    (void)costs_g;
+    (void)cost_idx;
     if (total_tiles < 0) total_tiles = s.tile_base[b.G];
     for (;;) {
         if (threadIdx.x == 0) s_item = atomicAdd(work_counter, 1ull);
@@ -465,13 +482,6 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
         }
         const int64_t g = lo;
         const int32_t tile = static_cast<int32_t>(item - s.tile_base[g]);
-        const int32_t ci = cost_idx ? cost_idx[g] : 0;
-        if (ci != loaded) {  // uniform: every thread read the same item
-            for (int i = threadIdx.x; i < static_cast<int>(sizeof(DevCosts) / 8); i += blockDim.x)
-                reinterpret_cast<double*>(&sc)[i] = reinterpret_cast<const double*>(costs_g + ci)[i];
-            __syncthreads();
-            loaded = ci;
-        }
         const GraphInfo gi = s.info[g];
         if (gi.processed != static_cast<int32_t>(b.task_base[g + 1] - b.task_base[g])) continue;  // cyclic
         const int32_t P = max(gi.peak_slots, 1);
@@ -482,10 +492,11 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
         double* win = win_smem;
         if (static_cast<int64_t>(P) * S * 8 > smem_bytes) win = gwin + blockIdx.x * gwin_stride;
         switch (S) {
-            case 64: sweep_tile<64>(b, s, sc, g, tile, win, P, th, s_hist); break;
-            case 32: sweep_tile<32>(b, s, sc, g, tile, win, P, th, s_hist); break;
-            case 16: sweep_tile<16>(b, s, sc, g, tile, win, P, th, s_hist); break;
-            default: sweep_tile<8>(b, s, sc, g, tile, win, P, th, s_hist); break;
+            case 128: sweep_tile<128>(b, s, g, tile, win, P, th, s_hist); break;
+            case 64: sweep_tile<64>(b, s, g, tile, win, P, th, s_hist); break;
+            case 32: sweep_tile<32>(b, s, g, tile, win, P, th, s_hist); break;
+            case 16: sweep_tile<16>(b, s, g, tile, win, P, th, s_hist); break;
+            default: sweep_tile<8>(b, s, g, tile, win, P, th, s_hist); break;
         }
         __syncthreads();
     }
@@ -505,6 +516,7 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
             const int32_t P = max(gi.peak_slots, 1);
             int32_t S = 8;
             if (force_s) S = force_s;
+            else if (static_cast<int64_t>(P) * 128 * 8 <= smem_bytes) S = 128;
             else if (static_cast<int64_t>(P) * 64 * 8 <= smem_bytes) S = 64;
             else if (static_cast<int64_t>(P) * 32 * 8 <= smem_bytes) S = 32;
             else if (static_cast<int64_t>(P) * 16 * 8 <= smem_bytes) S = 16;

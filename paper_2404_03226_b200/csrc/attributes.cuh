@@ -38,7 +38,10 @@ struct AttrScratch {
     int32_t* fstack;     // [T]
     int32_t* cls;        // [T]
     int32_t* cls_mark;   // [T*NT]
-    int32_t* pslot;      // [E]
+    int32_t* om_slot;    // [T]   order-major: slot of the node at level-order position i
+    double* om_gpu;      // [T]   order-major: GPU time of that node
+    int32_t* om_poff;    // [T+G] order-major CSR offsets of predecessor slots
+    int32_t* om_pslot;   // [E]   order-major predecessor slots
     double* rank;        // [T]
     uint64_t* hist;      // [4T] packed 12 x 21-bit window bins per source
     GraphInfo* info;     // [G]
