@@ -343,6 +343,15 @@ __device__ __forceinline__ void bump(uint64_t (&h)[4], int bin) {
     h[3] += w == 3 ? inc : 0ull;
 }
 
+// 12 counters of 16 bits, four per word (per-tile counts < 2^16: n < 65536)
+__device__ __forceinline__ void bump16(uint64_t (&h)[3], int bin) {
+    const int w = bin >> 2;
+    const uint64_t inc = 1ull << (16 * (bin & 3));
+    h[0] += w == 0 ? inc : 0ull;
+    h[1] += w == 1 ? inc : 0ull;
+    h[2] += w == 2 ? inc : 0ull;
+}
+
 __device__ Thresholds make_thresholds(int32_t mode_req, double w0_or_unit) {
     Thresholds th;
     if (mode_req == SWEEP_ABILITY) {
@@ -367,9 +376,48 @@ __device__ Thresholds make_thresholds(int32_t mode_req, double w0_or_unit) {
 // Group of GL lanes handles one node for S sources (S/GL per lane).  Node
 // records are read in level order (order-major arrays), the sources' distance
 // columns live in shared memory: win[slot][S].
-template <int S>
-__device__ void sweep_tile(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile, double* win,
-                           int32_t P, const Thresholds& th, unsigned long long* s_hist) {
+// Window bin with the threshold mode known at compile time.
+template <int TMODE>
+__device__ __forceinline__ int bin_t(double d, const Thresholds& th) {
+    if constexpr (TMODE == 0) {
+        const int64_t delta = __double_as_longlong(d) - th.w0bits;
+        if (delta <= 0) return 0;
+        const int k = static_cast<int>(static_cast<uint64_t>(delta - 1) >> 52) + 1;
+        return k > kWindows ? kWindows : k;
+    } else if constexpr (TMODE == 2) {
+        return kWindows;
+    } else {
+        int k = 0;
+#pragma unroll
+        for (int j = 0; j < kWindows; ++j) k += d > th.w[j];
+        return k;
+    }
+}
+
+// Flush 8-bit per-lane bin counters into the CTA's 21-bit accumulators.
+__device__ __forceinline__ void flush8(uint32_t (&h)[3], unsigned long long* dst) {
+    uint64_t h21[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int bn = 0; bn < kBins; ++bn) {
+        const uint64_t c = (h[bn >> 2] >> (8 * (bn & 3))) & 0xffu;
+        h21[bn / 3] += c << (21 * (bn % 3));
+    }
+#pragma unroll
+    for (int w = 0; w < 4; ++w)
+        if (h21[w]) atomicAdd(&dst[w], static_cast<unsigned long long>(h21[w]));
+    h[0] = h[1] = h[2] = 0;
+}
+
+// Group of GL lanes handles one node for S sources (S/GL per lane).  Node
+// records are read in level order (order-major arrays); the sources' distance
+// columns live in shared memory, win[slot][S].  Window bins are counted in
+// 8-bit fields (three u32 per source) and flushed every 255 node visits.
+template <int S, bool SMEM, int TMODE>
+__device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
+                                           double* gwin, int32_t P, const Thresholds& th,
+                                           unsigned long long* s_hist) {
+    extern __shared__ double win_smem[];
+    double* win = SMEM ? win_smem : gwin;
     constexpr int GL = S < 32 ? S : 32;   // lanes per node group
     constexpr int SPL = S / GL;           // sources per lane
     constexpr int GPW = 32 / GL;          // groups per warp
@@ -390,9 +438,10 @@ __device__ void sweep_tile(const DevBatch& b, const AttrScratch& s, int64_t g, i
 
     for (int64_t i = threadIdx.x; i < static_cast<int64_t>(P) * S; i += blockDim.x) win[i] = -1.0;
     for (int i = threadIdx.x; i < S * 4; i += blockDim.x) s_hist[i] = 0ull;
-    uint64_t hist[SPL][4];
+    uint32_t hist[SPL][3];
 #pragma unroll
-    for (int q = 0; q < SPL; ++q) hist[q][0] = hist[q][1] = hist[q][2] = hist[q][3] = 0;
+    for (int q = 0; q < SPL; ++q) hist[q][0] = hist[q][1] = hist[q][2] = 0;
+    int32_t visits = 0;  // node visits since the last flush (uniform per group)
     const int32_t La = s.level[t0 + s.order[t0 + first]];
     const int32_t my_first = first + gl * SPL;  // order position of this lane's first source
     __syncthreads();
@@ -401,28 +450,30 @@ __device__ void sweep_tile(const DevBatch& b, const AttrScratch& s, int64_t g, i
         const int32_t a1 = lstart[lv + 1];
         // groups are independent: every lane of a group sees the same node
         for (int32_t i = lstart[lv] + warp * GPW + grp; i < a1; i += nwarps * GPW) {
-            const int32_t p0 = om_poff[i];
-            const int32_t deg = om_poff[i + 1] - p0;
-            const double gv = th.mode == 2 ? 1.0 : om_gpu[i];
-            const int32_t sl = om_slot[i];
+            const int32_t p0 = __ldg(&om_poff[i]);
+            const int32_t deg = __ldg(&om_poff[i + 1]) - p0;
+            const double gv = TMODE == 2 ? 1.0 : __ldg(&om_gpu[i]);
+            const int32_t sl = __ldg(&om_slot[i]);
             double m[SPL];
 #pragma unroll
             for (int q = 0; q < SPL; ++q) m[q] = -1.0;
             for (int32_t c = 0; c < deg; c += GL) {
-                const int32_t myps = (c + gl < deg) ? om_ps[p0 + c + gl] : 0;
+                const int32_t myps = (c + gl < deg) ? __ldg(&om_ps[p0 + c + gl]) : 0;
                 const int32_t lim = min(GL, deg - c);
                 for (int32_t j = 0; j < lim; ++j) {
                     const int32_t ps = __shfl_sync(gmask, myps, grp * GL + j);
-                    const double* row = win + static_cast<int64_t>(ps) * S + gl * SPL;
+                    const double* row = win + ps * S + gl * SPL;
+                    // plain compare-select: operands are -1 or non-negative, never NaN
                     if constexpr (SPL >= 2) {
 #pragma unroll
                         for (int q = 0; q < SPL; q += 2) {
                             const double2 x = *reinterpret_cast<const double2*>(row + q);
-                            m[q] = fmax(m[q], x.x);
-                            m[q + 1] = fmax(m[q + 1], x.y);
+                            m[q] = x.x > m[q] ? x.x : m[q];
+                            m[q + 1] = x.y > m[q + 1] ? x.y : m[q + 1];
                         }
                     } else {
-                        m[0] = fmax(m[0], row[0]);
+                        const double x = row[0];
+                        m[0] = x > m[0] ? x : m[0];
                     }
                 }
             }
@@ -430,31 +481,48 @@ __device__ void sweep_tile(const DevBatch& b, const AttrScratch& s, int64_t g, i
 #pragma unroll
             for (int q = 0; q < SPL; ++q) {
                 const bool is_src = i == my_first + q;
-                d[q] = is_src ? 0.0 : (m[q] < 0.0 ? -1.0 : m[q] + gv);
-                if (!is_src && d[q] >= 0.0) bump(hist[q], bin_of(d[q], th));
+                const double reach = m[q] + gv;
+                const bool counted = !is_src && m[q] >= 0.0;
+                d[q] = is_src ? 0.0 : (m[q] < 0.0 ? -1.0 : reach);
+                const int bn = bin_t<TMODE>(reach, th);
+                const uint32_t inc = counted ? 1u << (8 * (bn & 3)) : 0u;
+                const int w = bn >> 2;
+                hist[q][0] += w == 0 ? inc : 0u;
+                hist[q][1] += w == 1 ? inc : 0u;
+                hist[q][2] += w == 2 ? inc : 0u;
             }
-            double* outp = win + static_cast<int64_t>(sl) * S + gl * SPL;
+            double* outp = win + sl * S + gl * SPL;
             if constexpr (SPL >= 2) {
 #pragma unroll
                 for (int q = 0; q < SPL; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(d[q], d[q + 1]);
             } else {
                 outp[0] = d[0];
             }
+            if (++visits == 255) {
+#pragma unroll
+                for (int q = 0; q < SPL; ++q)
+                    if (gl * SPL + q < nsrc) flush8(hist[q], s_hist + (gl * SPL + q) * 4);
+                visits = 0;
+            }
         }
         __syncthreads();
     }
-    // every group saw a different subset of nodes: reduce the packed
-    // partial histograms (fields never carry: totals stay < 2^21)
 #pragma unroll
     for (int q = 0; q < SPL; ++q)
-        if (gl * SPL + q < nsrc)
-#pragma unroll
-            for (int w = 0; w < 4; ++w)
-                if (hist[q][w]) atomicAdd(&s_hist[(gl * SPL + q) * 4 + w], static_cast<unsigned long long>(hist[q][w]));
+        if (gl * SPL + q < nsrc) flush8(hist[q], s_hist + (gl * SPL + q) * 4);
     __syncthreads();
     const int32_t* order = s.order + t0;
     for (int i = threadIdx.x; i < nsrc * 4; i += blockDim.x)
         s.hist[(t0 + order[first + i / 4]) * 4 + (i & 3)] = s_hist[i];
+}
+
+template <int S, bool SMEM>
+__device__ __forceinline__ void sweep_tile_mode(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
+                                                double* gwin, int32_t P, const Thresholds& th,
+                                                unsigned long long* s_hist) {
+    if (th.mode == 0) sweep_tile<S, SMEM, 0>(b, s, g, tile, gwin, P, th, s_hist);
+    else if (th.mode == 2) sweep_tile<S, SMEM, 2>(b, s, g, tile, gwin, P, th, s_hist);
+    else sweep_tile<S, SMEM, 1>(b, s, g, tile, gwin, P, th, s_hist);
 }
 
 __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs_g,
@@ -462,7 +530,6 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
                                               int32_t sweep_mode, const double* unit_time,
                                               int64_t total_tiles, unsigned long long* work_counter,
                                               int64_t smem_bytes, double* gwin, int64_t gwin_stride) {
-    extern __shared__ double win_smem[];
     __shared__ int64_t s_item;
     __shared__ unsigned long long s_hist[128 * 4];
     (void)costs_g;
@@ -489,14 +556,17 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
         if (sweep_mode == SWEEP_SINGLE) th = make_thresholds(SWEEP_SINGLE, unit_time[g]);
         else th = make_thresholds(sweep_mode, 2.0 * gi.median);
         const int32_t S = s.tile_s[g];
-        double* win = win_smem;
-        if (static_cast<int64_t>(P) * S * 8 > smem_bytes) win = gwin + blockIdx.x * gwin_stride;
-        switch (S) {
-            case 128: sweep_tile<128>(b, s, g, tile, win, P, th, s_hist); break;
-            case 64: sweep_tile<64>(b, s, g, tile, win, P, th, s_hist); break;
-            case 32: sweep_tile<32>(b, s, g, tile, win, P, th, s_hist); break;
-            case 16: sweep_tile<16>(b, s, g, tile, win, P, th, s_hist); break;
-            default: sweep_tile<8>(b, s, g, tile, win, P, th, s_hist); break;
+        double* gw = gwin + blockIdx.x * gwin_stride;
+        if (static_cast<int64_t>(P) * S * 8 > smem_bytes) {
+            sweep_tile_mode<32, false>(b, s, g, tile, gw, P, th, s_hist);
+        } else {
+            switch (S) {
+                case 128: sweep_tile_mode<128, true>(b, s, g, tile, gw, P, th, s_hist); break;
+                case 64: sweep_tile_mode<64, true>(b, s, g, tile, gw, P, th, s_hist); break;
+                case 32: sweep_tile_mode<32, true>(b, s, g, tile, gw, P, th, s_hist); break;
+                case 16: sweep_tile_mode<16, true>(b, s, g, tile, gw, P, th, s_hist); break;
+                default: sweep_tile_mode<8, true>(b, s, g, tile, gw, P, th, s_hist); break;
+            }
         }
         __syncthreads();
     }
