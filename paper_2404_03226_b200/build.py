@@ -27,6 +27,10 @@ CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off",
 
 CU_SRCS = ["attributes.cu", "simulate.cu", "abi.cpp"]  # abi.cpp launches kernels: nvcc -x cu
 CXX_SRCS = ["hostbatch.cpp"]
+# the drop-in C++ API (namespace tbsim, include/tbsim/*.hpp) over the C-ABI
+API_SRCS = ["api/taskgraph.cpp", "api/platform.cpp", "api/device.cpp", "api/attributes.cpp",
+            "api/policies.cpp", "api/engine.cpp", "api/bench.cpp", "api/text.cpp"]
+API_OUT = os.path.join(HERE, "libtbsim_cpp.so")
 
 
 def _host_cxx():
@@ -69,6 +73,26 @@ def build(verbose: bool = False) -> str:
         objs.append(o)
     if _stale(OUT, objs):
         cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", OUT] + objs + ["-lpthread"]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.check_call(cmd)
+    api_objs = []
+    api_hdrs = headers + [os.path.join(ROOT, "include", "tbsim", f) for f in os.listdir(os.path.join(ROOT, "include", "tbsim"))]
+    api_hdrs += [os.path.join(CSRC, "api", f) for f in os.listdir(os.path.join(CSRC, "api")) if f.endswith(".hpp")]
+    for src in API_SRCS:
+        s = os.path.join(CSRC, src)
+        o = os.path.join(BUILD, src.replace("/", "_") + ".o")
+        if _stale(o, [s] + api_hdrs):
+            cmd = [cxx, "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-I" + os.path.join(ROOT, "include"),
+                   "-I" + CSRC, "-c", s, "-o", o]
+            if verbose:
+                print(" ".join(cmd))
+            subprocess.check_call(cmd)
+        api_objs.append(o)
+    if _stale(API_OUT, api_objs + [OUT]):
+        # generators (tbsim_host::gen_*) and the C-ABI come from libtbsim_b200.so
+        cmd = [cxx, "-shared", "-o", API_OUT] + api_objs + ["-L" + HERE, "-ltbsim_b200", "-Wl,-rpath,$ORIGIN",
+                                                            "-lpthread"]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)
