@@ -190,6 +190,79 @@ def algorithmic_bytes(gb, dominant):
     return 4 * T + 4 * (T + G) + 4 * T + 4 * E + 32 * T
 
 
+def run_c4(args):
+    """BASELINE configs[3]: one 1M-task layered DAG, attributes only
+    (compute_attributes UpwardRank).  Reports attribute passes per second and
+    the HBM roofline of the bitset closure (ability)."""
+    import torch
+    from paper_2404_03226_b200 import abi, api
+    from paper_2404_03226_b200 import platform as P
+    n, layers, p = 1 << 20, 1024, 1.0 / 256
+    ctx = api.Context(0)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    t = time.perf_counter()
+    hb = api.HostBatch().add_layered(n, layers, p, [1])
+    gen_s = time.perf_counter() - t
+    gb = hb.view()
+    db = ctx.upload(hb)
+    costs = P.default_cost_table()
+    for _ in range(max(args.warmup, 1)):
+        res = ctx.attributes(db, costs, abi.ATTR_ALL)
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    times, kms = [], []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = ctx.attributes(db, costs, abi.ATTR_ALL)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        kms.append({k: ctx.last_kernel_ms(k) for k in ("k_ingest", "k_structure", "k_closure", "k_tile_plan",
+                                                       "k_sweep", "k_finalize", "k_structure_out")})
+    ctx.set_timing(False)
+    # algorithmic bytes of the closure: every successor's set read from its
+    # lower word bound, every node's set written from its own bound (8 B/word)
+    order_level = None
+    lvl = ctx.attributes(db, costs, abi.ATTR_LAYERS)["layer"]
+    counts = np.bincount(lvl, minlength=layers)
+    lstart = np.concatenate([[0], np.cumsum(counts)])
+    nw = (n + 63) // 64
+    lo_of_level = lstart[1:] // 64
+    off, dep = gb.graph_deps(0)
+    deg_out = np.bincount(dep, minlength=n)
+    words_written = (nw - lo_of_level[lvl]).astype(np.int64)
+    words_read = (deg_out * 0).astype(np.int64)
+    # each edge u->v reads set(v) from lo(v)
+    v_of_edge = np.repeat(np.arange(n), np.diff(off))
+    words_read = int((nw - lo_of_level[lvl[v_of_edge]]).sum())
+    alg_bytes = 8 * (int(words_written.sum()) + words_read)
+    closure_ms = statistics.median(k["k_closure"] for k in kms)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = alg_bytes / (closure_ms / 1e3) / 1e9
+    ab, ef = res["ability"], res["efficiency"]
+    props = {"efficiency_le_ability": bool(np.all(ef <= ab)),
+             "ability_monotone": bool(np.all(ab[dep] >= ab[v_of_edge] + 1))}
+    total_ms = statistics.median(times)
+    line = {"metric": "attribute passes/sec (1M-task DAG)", "value": 1e3 / total_ms, "unit": "DAGs/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": total_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic generate_layered_dag(1048576, 1024, 1/256, seed 1)",
+            "config": {"workload": "C4: single 1M-task DAG, compute_attributes(UpwardRank)", "n_tasks": n,
+                       "n_edges": gb.n_edges, "host_generation_s": gen_s},
+            "kernel_ms": {k: statistics.median(x[k] for x in kms) for k in kms[0]},
+            "roofline": {"bound": "hbm", "kernel": "k_closure", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "algorithmic_bytes": alg_bytes, "kernel_ms": closure_ms,
+                         "note": "trimmed descendant sets (level-ordered bit space); L2 reuse of the level cut can "
+                                 "push algorithmic GB/s above the DRAM copy peak"},
+            "properties": props, "unit_time_ms": float(res["unit_time_ms"][0])}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -198,9 +271,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n-dags", type=int, default=WORKLOAD["n_dags"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c4"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.workload == "c4":
+        return run_c4(args)
 
     import torch
     rank, world, local = env_rank()

@@ -119,6 +119,10 @@ tbsim_status tbsim_ctx_destroy(tbsim_ctx* ctx);
  * restores the context's own stream. */
 tbsim_status tbsim_ctx_set_stream(tbsim_ctx* ctx, void* cuda_stream);
 tbsim_status tbsim_ctx_synchronize(tbsim_ctx* ctx);
+/* Single graphs with at least this many tasks (default 65536) take the
+ * large-graph attribute path: ability by the HBM bitset closure, the
+ * efficiency sweep pruned at the largest window. */
+tbsim_status tbsim_ctx_set_large_graph_threshold(tbsim_ctx* ctx, int64_t n_tasks);
 /* Number of kernels this context launched since creation (bench evidence). */
 int64_t tbsim_ctx_launch_count(const tbsim_ctx* ctx);
 /* Name/duration of the most recent launch of the dominant kernel, in ms,

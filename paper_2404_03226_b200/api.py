@@ -170,6 +170,9 @@ class Context:
     def launch_count(self) -> int:
         return load().tbsim_ctx_launch_count(self.h)
 
+    def set_large_graph_threshold(self, n_tasks: int):
+        _check(load().tbsim_ctx_set_large_graph_threshold(self.h, n_tasks))
+
     def set_timing(self, on: bool):
         _check(load().tbsim_ctx_set_timing(self.h, int(on)))
 

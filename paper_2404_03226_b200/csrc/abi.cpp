@@ -106,6 +106,7 @@ struct tbsim_ctx {
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
     std::vector<std::pair<void*, size_t>> batch_pool;  // freed batch allocations for reuse
+    int64_t large_threshold = 65536;  // single graphs at least this large take the closure path
 
     DevBuf& buf(const std::string& name) { return bufs[name]; }
     void* batch_alloc(size_t bytes, size_t* got) {
@@ -272,6 +273,10 @@ tbsim_status tbsim_ctx_synchronize(tbsim_ctx* ctx) {
 
 int64_t tbsim_ctx_launch_count(const tbsim_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+tbsim_status tbsim_ctx_set_large_graph_threshold(tbsim_ctx* ctx, int64_t n_tasks) {
+    return guarded([&] { ctx->large_threshold = n_tasks; });
+}
+
 tbsim_status tbsim_ctx_set_timing(tbsim_ctx* ctx, int enable) {
     return guarded([&] { ctx->timing = enable != 0; });
 }
@@ -411,6 +416,9 @@ AttrScratch alloc_attr_scratch(tbsim_ctx* ctx, const DevBatch& d) {
     s.median = ctx->buf("a_median").as<double>(G);
     s.tile_base = ctx->buf("a_tilebase").as<int64_t>(G + 1);
     s.tile_s = ctx->buf("a_tiles").as<int32_t>(G);
+    s.opos = ctx->buf("a_opos").as<int32_t>(T);
+    s.firstuse = ctx->buf("a_firstuse").as<int32_t>(T);
+    s.rslot = ctx->buf("a_rslot").as<int32_t>(T);
     return s;
 }
 
@@ -431,11 +439,39 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
     const int64_t G = d.G;
     run.s = alloc_attr_scratch(ctx, d);
     if (G == 0) return;
+    // One huge graph (C4-like): ability by the HBM bitset closure, the sweep
+    // pruned at the largest window.  Batches: ability inside the sweep.
+    const bool large = G == 1 && d.max_n >= ctx->large_threshold && do_sweep;
     const int grid_g = static_cast<int>(std::min<int64_t>(G, 4LL * ctx->n_sms));
     ctx->begin("k_structure");
-    k_structure<<<grid_g, 512, 0, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, want_rank ? 1 : 0);
+    k_structure<<<grid_g, 512, 0, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, want_rank ? 1 : 0, large ? 1 : 0);
     ctx->end("k_structure");
-    if (do_sweep) {
+    bool ability_done = false;
+    if (large && o.ability) {
+        GraphInfo gi;
+        cuda_check(cudaMemcpyAsync(&gi, run.s.info, sizeof gi, cudaMemcpyDeviceToHost, ctx->stream), "D2H info");
+        ctx->sync();
+        if (gi.processed == d.max_n) {  // acyclic: otherwise the error path reports it
+            const int64_t nw = (static_cast<int64_t>(d.max_n) + 63) / 64;
+            uint64_t* sets = ctx->buf("a_sets").as<uint64_t>(static_cast<size_t>(std::max(gi.peak_rslots, 1)) * nw);
+            cuda_check(cudaMemsetAsync(o.ability, 0, static_cast<size_t>(d.T) * 8, ctx->stream), "memset ability");
+            int per_sm = 0;
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_closure<4>, 256, 0), "occupancy");
+            const int grid = std::max(1, per_sm) * ctx->n_sms;
+            int64_t g0 = 0;
+            int64_t nw_arg = nw;
+            DevBatch dv = d;
+            AttrScratch sv = run.s;
+            unsigned long long* ab = reinterpret_cast<unsigned long long*>(o.ability);
+            void* args[] = {&dv, &sv, &g0, &sets, &nw_arg, &ab};
+            ctx->begin("k_closure");
+            cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_closure<4>), grid, 256, args, 0, ctx->stream),
+                       "cudaLaunchCooperativeKernel(k_closure)");
+            ctx->end("k_closure");
+            ability_done = true;
+        }
+    }
+    if (do_sweep && !(large && sweep_mode == SWEEP_ABILITY)) {
         const int64_t smem = sweep_smem_bytes(ctx);
         ctx->begin("k_tile_plan");
         k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, run.s, smem, 0);
@@ -460,12 +496,14 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         }
         ctx->begin("k_sweep");
         k_sweep<<<sweep_grid, kSweepThreads, smem, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, sweep_mode, d_unit_time,
-                                                                  total_tiles, counter, smem, gwin, gwin_stride);
+                                                                  total_tiles, counter, smem, gwin, gwin_stride,
+                                                                  large ? 1 : 0);
         ctx->end("k_sweep");
-        const int64_t cls_stride = static_cast<int64_t>(d.max_n) * (kWindows + 1) + 16;
+        const int64_t cls_stride = static_cast<int64_t>(d.max_n) * (3 * kWindows + 1) + 16;
         int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride * grid_g);
         ctx->begin("k_finalize");
-        k_finalize<<<grid_g, 256, 0, ctx->stream>>>(d, run.s, sweep_mode, d_unit_time, o, cls_scratch, cls_stride);
+        k_finalize<<<grid_g, 256, 0, ctx->stream>>>(d, run.s, sweep_mode, d_unit_time, o, cls_scratch, cls_stride,
+                                                    (large || ability_done) ? 0 : 1);
         ctx->end("k_finalize");
     }
     if (o.layer || o.depth || (want_prio && o.static_priority)) {

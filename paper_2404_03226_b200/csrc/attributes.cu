@@ -25,6 +25,8 @@
 //   k_finalize   per graph: per-class sums for each window, distinct reduced
 //                fractions (attributes.cpp:205-217), the strict-> winner, and the
 //                per-task efficiency / ability.
+#include <cooperative_groups.h>
+
 #include <cfloat>
 #include <cstdint>
 
@@ -90,14 +92,50 @@ __global__ void __launch_bounds__(256) k_ingest(DevBatch b, int32_t* cursor_scra
 
 // --------------------------------------------------------------- structure
 
+// Live-range slot assignment over the level order.  Nodes of a level take
+// free slots (stack) or fresh ones; a node's slot is released after level
+// key[v] has been processed.  reverse = walk levels from the last to the
+// first.  Returns the number of slots used (peak live set).
+__device__ int32_t assign_slots(const int32_t* order, const int32_t* lstart, int32_t L, int32_t processed,
+                                const int32_t* key, bool reverse, int32_t* slot, int32_t* cnt, int32_t* cur,
+                                int32_t* rel_order, int32_t* fstack, int32_t* warp_tot) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    for (int32_t i = tid; i <= L; i += nthr) cnt[i] = 0;
+    __syncthreads();
+    for (int32_t i = tid; i < processed; i += nthr) atomicAdd(&cnt[key[order[i]]], 1);
+    __syncthreads();
+    block_exclusive_scan_inplace(cnt, L + 1, warp_tot);
+    for (int32_t i = tid; i <= L; i += nthr) cur[i] = cnt[i];
+    __syncthreads();
+    for (int32_t i = tid; i < processed; i += nthr) {
+        const int32_t v = order[i];
+        rel_order[atomicAdd(&cur[key[v]], 1)] = v;
+    }
+    __syncthreads();
+    int32_t fs = 0, P = 0;
+    for (int32_t step = 0; step < L; ++step) {
+        const int32_t lv = reverse ? L - 1 - step : step;
+        const int32_t a0 = lstart[lv], a = lstart[lv + 1] - a0;
+        for (int32_t i = tid; i < a; i += nthr) slot[order[a0 + i]] = i < fs ? fstack[fs - 1 - i] : P + (i - fs);
+        __syncthreads();
+        const int32_t nfs = max(fs - a, 0);
+        P += max(a - fs, 0);
+        const int32_t r0 = cnt[lv], r = cnt[lv + 1] - r0;
+        for (int32_t j = tid; j < r; j += nthr) fstack[nfs + j] = slot[rel_order[r0 + j]];
+        __syncthreads();
+        fs = nfs + r;
+    }
+    return P;
+}
+
 __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* costs_g,
                                                   const int32_t* cost_idx, AttrScratch s,
-                                                  int32_t want_rank) {
+                                                  int32_t want_rank, int32_t want_large) {
     __shared__ DevCosts sc;
     __shared__ double s_mean[kMaxTypes];
     __shared__ int32_t s_tcount[kMaxTypes];
     __shared__ int32_t warp_tot[32];
-    __shared__ int32_t s_tail, s_end, s_miss_gpu, s_miss_any;
+    __shared__ int32_t s_tail, s_end, s_miss_gpu, s_miss_any, s_span;
     const int tid = threadIdx.x, nthr = blockDim.x;
     int32_t loaded = -1;
     for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) {
@@ -192,35 +230,31 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
             }
             __syncthreads();
         }
-        // ---- slot assignment: group nodes by last-use level (counting sort)
-        int32_t* cnt = indeg;                // reuse [n+1]
-        int32_t* rel_order = s.rel_order + t0;
-        int32_t* cur = s.tmp2 + t0 + g;      // [n+1]
-        int32_t* fstack = s.fstack + t0;
-        for (int32_t i = tid; i <= L; i += nthr) cnt[i] = 0;
-        __syncthreads();
-        for (int32_t i = tid; i < processed; i += nthr) atomicAdd(&cnt[lastuse[order[i]]], 1);
-        __syncthreads();
-        block_exclusive_scan_inplace(cnt, L + 1, warp_tot);
-        for (int32_t i = tid; i <= L; i += nthr) cur[i] = cnt[i];
-        __syncthreads();
-        for (int32_t i = tid; i < processed; i += nthr) {
-            const int32_t v = order[i];
-            rel_order[atomicAdd(&cur[lastuse[v]], 1)] = v;
-        }
-        __syncthreads();
-        int32_t fs = 0, P = 0;
-        for (int32_t lv = 0; lv < L; ++lv) {
-            const int32_t a0 = lstart[lv], a = lstart[lv + 1] - a0;
-            for (int32_t i = tid; i < a; i += nthr)
-                slot[order[a0 + i]] = i < fs ? fstack[fs - 1 - i] : P + (i - fs);
+        // ---- live-range slots for the forward sweep (released after the
+        //      node's last consumer level)
+        const int32_t P = assign_slots(order, lstart, L, processed, lastuse, false, slot, indeg, s.tmp2 + t0 + g,
+                                       s.rel_order + t0, s.fstack + t0, warp_tot);
+        // ---- large graphs: inverse order, edge level span, reverse slots for
+        //      the bitset closure (released after the node's first consumer)
+        int32_t Pr = 0;
+        if (want_large) {
+            int32_t* opos = s.opos + t0;
+            int32_t* firstuse = s.firstuse + t0;
+            if (tid == 0) s_span = 1;
             __syncthreads();
-            const int32_t nfs = max(fs - a, 0);
-            P += max(a - fs, 0);
-            const int32_t r0 = cnt[lv], r = cnt[lv + 1] - r0;
-            for (int32_t j = tid; j < r; j += nthr) fstack[nfs + j] = slot[rel_order[r0 + j]];
+            for (int32_t i = tid; i < processed; i += nthr) opos[order[i]] = i;
+            for (int32_t v = tid; v < n; v += nthr) {
+                int32_t fu = level[v];
+                for (int32_t k = doff[v]; k < doff[v + 1]; ++k) {
+                    const int32_t lu = level[dep[k]];
+                    fu = min(fu, lu);
+                    if (level[v] - lu > 1) atomicMax(&s_span, level[v] - lu);
+                }
+                firstuse[v] = fu;
+            }
             __syncthreads();
-            fs = nfs + r;
+            Pr = assign_slots(order, lstart, L, processed, firstuse, true, s.rslot + t0, indeg, s.tmp2 + t0 + g,
+                              s.rel_order + t0, s.fstack + t0, warp_tot);
         }
         // ---- order-major node records for the sweep: slot, GPU time and
         //      the predecessors' slots, contiguous in level order
@@ -278,6 +312,8 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
             gi.n_levels = L;
             gi.processed = processed;
             gi.peak_slots = P;
+            gi.peak_rslots = Pr;
+            gi.max_span = want_large ? s_span : 0;
             gi.n_classes = n_cls;
             gi.miss_gpu = s_miss_gpu == INT32_MAX ? -1 : s_miss_gpu;
             gi.miss_any = s_miss_any == INT32_MAX ? -1 : s_miss_any;
@@ -415,7 +451,7 @@ __device__ __forceinline__ void flush8(uint32_t (&h)[3], unsigned long long* dst
 template <int S, bool SMEM, int TMODE>
 __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                            double* gwin, int32_t P, const Thresholds& th,
-                                           unsigned long long* s_hist) {
+                                           unsigned long long* s_hist, int32_t prune_span) {
     extern __shared__ double win_smem[];
     double* win = SMEM ? win_smem : gwin;
     constexpr int GL = S < 32 ? S : 32;   // lanes per node group
@@ -444,9 +480,17 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     int32_t visits = 0;  // node visits since the last flush (uniform per group)
     const int32_t La = s.level[t0 + s.order[t0 + first]];
     const int32_t my_first = first + gl * SPL;  // order position of this lane's first source
+    // Pruning (large graphs, ability computed elsewhere): distances only grow
+    // along paths, so once no distance within the largest window was written
+    // in the last `prune_span` levels (the longest edge span), no later node
+    // can fall inside any window and the tile is done.
+    const double wmax = th.w[kWindows - 1];
+    const uint64_t span_mask = prune_span >= 64 ? ~0ull : ((1ull << prune_span) - 1ull);
+    uint64_t recent = 0;
     __syncthreads();
 
     for (int32_t lv = La; lv < gi.n_levels; ++lv) {
+        int small = 0;
         const int32_t a1 = lstart[lv + 1];
         // groups are independent: every lane of a group sees the same node
         for (int32_t i = lstart[lv] + warp * GPW + grp; i < a1; i += nwarps * GPW) {
@@ -490,6 +534,7 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
                 hist[q][0] += w == 0 ? inc : 0u;
                 hist[q][1] += w == 1 ? inc : 0u;
                 hist[q][2] += w == 2 ? inc : 0u;
+                small |= d[q] >= 0.0 && d[q] <= wmax;
             }
             double* outp = win + sl * S + gl * SPL;
             if constexpr (SPL >= 2) {
@@ -505,7 +550,12 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
                 visits = 0;
             }
         }
-        __syncthreads();
+        if (prune_span > 0) {
+            recent = (recent << 1) | static_cast<uint64_t>(__syncthreads_or(small) != 0);
+            if (lv - La + 1 >= prune_span && (recent & span_mask) == 0) break;
+        } else {
+            __syncthreads();
+        }
     }
 #pragma unroll
     for (int q = 0; q < SPL; ++q)
@@ -519,17 +569,18 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
 template <int S, bool SMEM>
 __device__ __forceinline__ void sweep_tile_mode(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                                 double* gwin, int32_t P, const Thresholds& th,
-                                                unsigned long long* s_hist) {
-    if (th.mode == 0) sweep_tile<S, SMEM, 0>(b, s, g, tile, gwin, P, th, s_hist);
-    else if (th.mode == 2) sweep_tile<S, SMEM, 2>(b, s, g, tile, gwin, P, th, s_hist);
-    else sweep_tile<S, SMEM, 1>(b, s, g, tile, gwin, P, th, s_hist);
+                                                unsigned long long* s_hist, int32_t prune_span) {
+    if (th.mode == 0) sweep_tile<S, SMEM, 0>(b, s, g, tile, gwin, P, th, s_hist, prune_span);
+    else if (th.mode == 2) sweep_tile<S, SMEM, 2>(b, s, g, tile, gwin, P, th, s_hist, 0);
+    else sweep_tile<S, SMEM, 1>(b, s, g, tile, gwin, P, th, s_hist, prune_span);
 }
 
 __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs_g,
                                               const int32_t* cost_idx, AttrScratch s,
                                               int32_t sweep_mode, const double* unit_time,
                                               int64_t total_tiles, unsigned long long* work_counter,
-                                              int64_t smem_bytes, double* gwin, int64_t gwin_stride) {
+                                              int64_t smem_bytes, double* gwin, int64_t gwin_stride,
+                                              int32_t prune) {
     __shared__ int64_t s_item;
     __shared__ unsigned long long s_hist[128 * 4];
     (void)costs_g;
@@ -557,15 +608,17 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
         else th = make_thresholds(sweep_mode, 2.0 * gi.median);
         const int32_t S = s.tile_s[g];
         double* gw = gwin + blockIdx.x * gwin_stride;
+        // prune only when the edge span fits the 64-level history
+        const int32_t prune_span = (prune && gi.max_span > 0 && gi.max_span < 64) ? gi.max_span : 0;
         if (static_cast<int64_t>(P) * S * 8 > smem_bytes) {
-            sweep_tile_mode<32, false>(b, s, g, tile, gw, P, th, s_hist);
+            sweep_tile_mode<32, false>(b, s, g, tile, gw, P, th, s_hist, prune_span);
         } else {
             switch (S) {
-                case 128: sweep_tile_mode<128, true>(b, s, g, tile, gw, P, th, s_hist); break;
-                case 64: sweep_tile_mode<64, true>(b, s, g, tile, gw, P, th, s_hist); break;
-                case 32: sweep_tile_mode<32, true>(b, s, g, tile, gw, P, th, s_hist); break;
-                case 16: sweep_tile_mode<16, true>(b, s, g, tile, gw, P, th, s_hist); break;
-                default: sweep_tile_mode<8, true>(b, s, g, tile, gw, P, th, s_hist); break;
+                case 128: sweep_tile_mode<128, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+                case 64: sweep_tile_mode<64, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+                case 32: sweep_tile_mode<32, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+                case 16: sweep_tile_mode<16, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+                default: sweep_tile_mode<8, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
             }
         }
         __syncthreads();
@@ -620,7 +673,7 @@ __device__ int64_t gcd64(int64_t a, int64_t b) {
 
 __global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int32_t sweep_mode,
                                                  const double* unit_time_in, AttrOutDev o,
-                                                 int64_t* cls_scratch, int64_t cls_stride) {
+                                                 int64_t* cls_scratch, int64_t cls_stride, int32_t write_ability) {
     __shared__ int32_t s_score[kWindows];
     int64_t* sums = cls_scratch + blockIdx.x * cls_stride;  // [C][kWindows] then cnt[C]
     for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) {
@@ -648,19 +701,26 @@ __global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int
                 atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[c]), 1ull);
             }
             __syncthreads();
-            // distinct reduced fractions per window (attributes.cpp:205-217)
+            // distinct reduced fractions per window (attributes.cpp:205-217):
+            // reduce every (class, window) once, then count first occurrences
+            int64_t* fa = cnt + C;
+            int64_t* fq = fa + static_cast<int64_t>(C) * kWindows;
+            for (int64_t item = threadIdx.x; item < static_cast<int64_t>(C) * kWindows; item += blockDim.x) {
+                const int32_t c = static_cast<int32_t>(item / kWindows);
+                const int64_t sc_ = sums[item], cc = cnt[c];
+                const int64_t d = gcd64(sc_ == 0 ? cc : sc_, cc);
+                fa[item] = sc_ / d;
+                fq[item] = cc / d;
+            }
+            __syncthreads();
             for (int64_t item = threadIdx.x; item < static_cast<int64_t>(C) * kWindows; item += blockDim.x) {
                 const int32_t c = static_cast<int32_t>(item / kWindows);
                 const int k = static_cast<int>(item % kWindows);
-                const int64_t sc_ = sums[static_cast<int64_t>(c) * kWindows + k], cc = cnt[c];
-                const int64_t d = gcd64(sc_ == 0 ? cc : sc_, cc);
-                const int64_t a = sc_ / d, q = cc / d;
+                const int64_t a = fa[item], q = fq[item];
                 bool first = true;
-                for (int32_t c2 = 0; c2 < c && first; ++c2) {
-                    const int64_t s2 = sums[static_cast<int64_t>(c2) * kWindows + k], c2c = cnt[c2];
-                    const int64_t d2 = gcd64(s2 == 0 ? c2c : s2, c2c);
-                    if (s2 / d2 == a && c2c / d2 == q) first = false;
-                }
+                for (int32_t c2 = 0; c2 < c && first; ++c2)
+                    if (fa[static_cast<int64_t>(c2) * kWindows + k] == a && fq[static_cast<int64_t>(c2) * kWindows + k] == q)
+                        first = false;
                 if (first) atomicAdd(&s_score[k], 1);
             }
             __syncthreads();
@@ -685,11 +745,83 @@ __global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int
                 abil += f;
             }
             if (o.efficiency && sweep_mode != SWEEP_ABILITY) o.efficiency[t0 + v] = eff;
-            if (o.ability) o.ability[t0 + v] = abil;
+            if (o.ability && write_ability) o.ability[t0 + v] = abil;
         }
         __syncthreads();
     }
 }
+
+// ---------------------------------------------------------------- closure
+
+// Inspiring ability of one large graph as a descendant-bitset closure
+// (ability_impl, attributes.cpp:57-92) streaming through HBM.  Bits index the
+// level order, so the descendants of a node at level L occupy only words
+// >= lstart[L+1]/64: each set is written from that word on and read from its
+// own lower bound (lower words are zero by construction).  Levels are
+// processed from the last to the first with a grid-wide barrier in between;
+// sets live in reverse live-range slots (firstuse) so only the level cut is
+// resident.  A warp owns (node, 32*CH-word chunk): coalesced loads of every
+// successor's chunk, OR, store, popcount.
+template <int CH>
+__global__ void __launch_bounds__(256) k_closure(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets, int64_t nw,
+                                               unsigned long long* ability) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int64_t t0 = b.task_base[g];
+    const GraphInfo gi = s.info[g];
+    const int32_t* lstart = s.lstart + t0 + g;
+    const int32_t* order = s.order + t0;
+    const int32_t* opos = s.opos + t0;
+    const int32_t* rslot = s.rslot + t0;
+    const int32_t* level = s.level + t0;
+    const int32_t* soff = b.succ_off + t0 + g;
+    const int32_t* succ = b.succ + b.edge_base[g];
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    constexpr int64_t kChunk = 32 * CH;
+    for (int32_t lv = gi.n_levels - 1; lv >= 0; --lv) {
+        const int32_t a0 = lstart[lv], cnt = lstart[lv + 1] - a0;
+        const int64_t lo = lstart[lv + 1] >> 6;
+        const int64_t chunks = (nw - lo + kChunk - 1) / kChunk;
+        const int64_t items = static_cast<int64_t>(cnt) * chunks;
+        for (int64_t item = gwarp; item < items; item += nwarps) {
+            const int32_t i = a0 + static_cast<int32_t>(item / chunks);
+            const int64_t w0 = lo + (item % chunks) * kChunk;
+            const int32_t u = order[i];
+            uint64_t acc[CH];
+#pragma unroll
+            for (int j = 0; j < CH; ++j) acc[j] = 0;
+            for (int32_t k = __ldg(&soff[u]); k < __ldg(&soff[u + 1]); ++k) {
+                const int32_t v = __ldg(&succ[k]);
+                const int32_t ov = opos[v];
+                const int64_t lov = lstart[level[v] + 1] >> 6;
+                const uint64_t* sv = sets + static_cast<int64_t>(rslot[v]) * nw;
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int64_t w = w0 + lane + 32 * j;
+                    if (w >= lov && w < nw) acc[j] |= __ldcg(&sv[w]);
+                    if (w == (ov >> 6)) acc[j] |= 1ull << (ov & 63);
+                }
+            }
+            uint64_t* su = sets + static_cast<int64_t>(rslot[u]) * nw;
+            int pc = 0;
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+                const int64_t w = w0 + lane + 32 * j;
+                if (w < nw) {
+                    __stcg(&su[w], acc[j]);
+                    pc += __popcll(acc[j]);
+                }
+            }
+            pc = __reduce_add_sync(0xffffffffu, pc);
+            if (lane == 0 && pc) atomicAdd(&ability[t0 + u], static_cast<unsigned long long>(pc));
+        }
+        grid.sync();
+    }
+}
+
+template __global__ void k_closure<4>(DevBatch, AttrScratch, int64_t, uint64_t*, int64_t, unsigned long long*);
 
 // Per-task outputs of the structure pass (layers, depth, static priority).
 __global__ void k_structure_out(DevBatch b, AttrScratch s, AttrOutDev o, int32_t prio_kind, int32_t want_prio) {

@@ -18,6 +18,8 @@ struct GraphInfo {
     int32_t processed;   // tasks released by Kahn (< n means a cycle)
     int32_t peak_slots;  // distance-column slots the sweep needs
     int32_t n_classes;   // distinct (layer, type) calibration classes
+    int32_t peak_rslots; // bitset slots of the reverse closure (large-graph path)
+    int32_t max_span;    // max level(v) - level(u) over edges (large-graph path)
     int32_t miss_gpu;    // first task position without a GPU cost, -1 if none
     int32_t miss_any;    // first task position without any cost, -1 if none
     double median;       // lower-median GPU time (valid when miss_gpu < 0 and n > 0)
@@ -38,6 +40,9 @@ struct AttrScratch {
     int32_t* fstack;     // [T]
     int32_t* cls;        // [T]
     int32_t* cls_mark;   // [T*NT]
+    int32_t* opos;       // [T] order position of each node (large-graph path)
+    int32_t* firstuse;   // [T] lowest level of a predecessor (large-graph path)
+    int32_t* rslot;      // [T] reverse-closure slot (large-graph path)
     int32_t* om_slot;    // [T]   order-major: slot of the node at level-order position i
     double* om_gpu;      // [T]   order-major: GPU time of that node
     int32_t* om_poff;    // [T+G] order-major CSR offsets of predecessor slots
@@ -65,14 +70,17 @@ struct AttrOutDev {
 
 __global__ void k_ingest(DevBatch b, int32_t* cursor_scratch);
 __global__ void k_structure(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
-                            int32_t want_rank);
+                            int32_t want_rank, int32_t want_large);
 __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s);
 __global__ void k_sweep(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                         int32_t sweep_mode,
                         const double* unit_time, int64_t total_tiles, unsigned long long* work_counter,
-                        int64_t smem_bytes, double* gwin, int64_t gwin_stride);
+                        int64_t smem_bytes, double* gwin, int64_t gwin_stride, int32_t prune);
 __global__ void k_finalize(DevBatch b, AttrScratch s, int32_t sweep_mode, const double* unit_time_in,
-                           AttrOutDev o, int64_t* cls_scratch, int64_t cls_stride);
+                           AttrOutDev o, int64_t* cls_scratch, int64_t cls_stride, int32_t write_ability);
+template <int CH>
+__global__ void k_closure(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets, int64_t nw,
+                          unsigned long long* ability);
 __global__ void k_structure_out(DevBatch b, AttrScratch s, AttrOutDev o, int32_t prio_kind,
                                 int32_t want_prio);
 

@@ -19,6 +19,7 @@ EXPORTS = [
     "tbsim_last_error", "tbsim_abi_version",
     "tbsim_ctx_create", "tbsim_ctx_destroy", "tbsim_ctx_set_stream", "tbsim_ctx_synchronize",
     "tbsim_ctx_launch_count", "tbsim_ctx_set_timing", "tbsim_ctx_last_kernel_ms",
+    "tbsim_ctx_set_large_graph_threshold",
     "tbsim_batch_upload", "tbsim_batch_free", "tbsim_batch_h2d_bytes",
     "tbsim_attributes", "tbsim_simulate", "tbsim_schedule", "tbsim_default_regulator_config",
     "tbsim_hostbatch_new", "tbsim_hostbatch_free", "tbsim_hostbatch_add_layered",
@@ -53,6 +54,7 @@ def load():
     L.tbsim_ctx_launch_count.argtypes = [vp]
     L.tbsim_ctx_launch_count.restype = i64
     L.tbsim_ctx_set_timing.argtypes = [vp, C.c_int]
+    L.tbsim_ctx_set_large_graph_threshold.argtypes = [vp, i64]
     L.tbsim_ctx_last_kernel_ms.argtypes = [vp, C.c_char_p, P(dbl)]
     L.tbsim_batch_upload.argtypes = [vp, P(abi.BatchDesc), P(vp)]
     L.tbsim_batch_free.argtypes = [vp, vp]

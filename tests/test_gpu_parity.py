@@ -214,3 +214,50 @@ def test_c3_lu_and_qr_on_32c4g(ctx):
         o = po.simulate(b, pl, pol, reg=reg, attrs=oa, record=True)
         for k in SIM_KEYS:
             eq(g[k], o[k], f"{pol}/{k}")
+
+
+def _long_edge_graph(seed, n, levels, p_long):
+    """Layered DAG plus random long edges (edge spans > 1 exercise the
+    pruning history and the reverse live ranges)."""
+    rng = np.random.default_rng(seed)
+    tasks = []
+    per = n // levels
+    for i in range(n):
+        lv = i // per
+        deps = []
+        if lv > 0:
+            prev = list(range((lv - 1) * per, lv * per))
+            deps = [int(x) for x in rng.choice(prev, size=min(3, per), replace=False)]
+            if lv > 2 and rng.random() < p_long:
+                deps.append(int(rng.integers(0, (lv - 2) * per)))
+        tasks.append(TaskNode(i, MIXED[int(rng.integers(0, 4))], deps))
+    return GraphBatch.from_taskgraphs([TaskGraph("long", tasks)], P.TYPE_NAMES)
+
+
+@pytest.mark.parametrize("kind", ["layered", "long_edges", "span_beyond_64"])
+def test_large_graph_path_matches_batched_path_and_oracle(ctx, kind):
+    costs = P.default_cost_table()
+    if kind == "layered":
+        b = api.HostBatch().add_layered(12288, 96, 1.0 / 32, [5]).view()
+    elif kind == "long_edges":
+        b = _long_edge_graph(3, 6000, 60, 0.3)
+    else:
+        b = _long_edge_graph(4, 4000, 200, 0.05)
+    db = ctx.upload(b)
+    ctx.set_large_graph_threshold(1 << 30)
+    small = ctx.attributes(db, costs, abi.ATTR_ALL)
+    ctx.set_large_graph_threshold(1000)
+    try:
+        large = ctx.attributes(db, costs, abi.ATTR_ALL)
+        ab_only = ctx.attributes(db, costs, abi.ATTR_ABILITY)
+        eff3 = ctx.attributes(db, costs, abi.ATTR_EFFICIENCY, unit_time=[3.0])
+    finally:
+        ctx.set_large_graph_threshold(65536)
+    for k in ("ability", "efficiency", "static_priority", "unit_time_ms"):
+        eq(large[k], small[k], f"large vs batched {k}")
+    eq(ab_only["ability"], small["ability"], "closure ability")
+    o = po.attributes(b, costs, abi.ATTR_ALL)
+    for k in ("ability", "efficiency", "static_priority", "unit_time_ms"):
+        eq(large[k], o[k], f"large vs oracle {k}")
+    o3 = po.attributes(b, costs, abi.ATTR_EFFICIENCY, unit_time=[3.0])
+    eq(eff3["efficiency"], o3["efficiency"], "pruned single window")
