@@ -190,6 +190,184 @@ def algorithmic_bytes(gb, dominant):
     return 4 * T + 4 * (T + G) + 4 * T + 4 * E + 32 * T
 
 
+def run_tiled(args):
+    """BASELINE configs[0] (C1: tiled Cholesky 10x10 on 4 CPU + 1 GPU) and
+    configs[2] (C3: tiled LU and QR 40x40 on 32 CPU + 4 GPU): the bench-cell
+    pipeline per DAG, device-timed and end to end, next to the reference
+    (oracle/_ref) on the same graphs."""
+    import torch
+    from oracle import pyref
+    from paper_2404_03226_b200 import abi, api
+    from paper_2404_03226_b200 import platform as P
+    from paper_2404_03226_b200.batch import GraphBatch
+    ctx = api.Context(0)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    if args.workload == "c1":
+        hb = api.HostBatch().add_cholesky(10, 960 * 960 * 4)
+        pl = P.assemble("4c1g", 4, 1)
+        name = "C1: tiled Cholesky 10x10 (220 tasks) on 4 CPU + 1 GPU"
+        policies = list(abi.POLICIES)
+    else:
+        hb = api.HostBatch().add_lu(40, 160 * 160 * 4).add_qr(40, 160 * 160 * 4)
+        pl = P.assemble("32c4g", 32, 4, with_qr=True)
+        name = "C3: tiled LU 40x40 + tiled QR 40x40 (22,140 tasks each) on 32 CPU + 4 GPU"
+        policies = ["inspirit", "dmda"]
+    gb = hb.view()
+    G, T = gb.n_graphs, gb.n_tasks
+    db = ctx.upload(hb)
+    out = {}
+    for pol in policies:
+        for _ in range(max(args.warmup, 1)):
+            ctx.schedule(db, [pl], pol, want_attrs=False, want_states=False)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = ctx.schedule(db, [pl], pol, want_attrs=False, want_states=False)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = statistics.median(times)
+        ctx.set_timing(True)
+        ctx.schedule(db, [pl], pol, want_attrs=False, want_states=False)
+        kms = {k: ctx.last_kernel_ms(k) for k in ("k_structure", "k_sweep", "k_finalize", "k_simulate")}
+        ctx.set_timing(False)
+        e2e = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            d2 = ctx.upload(hb)
+            r2 = ctx.schedule(d2, [pl], pol, want_attrs=False, want_states=False)
+            d2.free()
+            e2e.append(time.perf_counter() - t)
+        out[pol] = {"device_ms": ms, "dags_per_s": G / (ms / 1e3), "e2e_dags_per_s": G / statistics.median(e2e),
+                    "makespan_ms": r["makespan_ms"].tolist(), "kernel_ms": kms}
+    cpu = None
+    if pyref.available():
+        costs = pl.costs
+        threads = host_cores()
+        ref = {}
+        for pol in policies:
+            t = time.perf_counter()
+            a = pyref.attributes(gb, costs, abi.ATTR_ALL, threads=threads)
+            rr = pyref.simulate(gb, [pl], pol, attrs=a, record=False, threads=threads)
+            secs = time.perf_counter() - t
+            ref[pol] = {"seconds": secs, "dags_per_s": G / secs, "makespan_ms": rr["makespan_ms"].tolist(),
+                        "makespans_match_gpu": rr["makespan_ms"].tolist() == out[pol]["makespan_ms"]}
+        cpu = {"kind": "reference", "cores": threads, "cpu": cpu_model(), "per_policy": ref}
+    line = {"metric": "DAGs scheduled/sec", "value": out["inspirit"]["dags_per_s"], "unit": "DAGs/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": out["inspirit"]["device_ms"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generators; QR is this repo's own)",
+            "config": {"workload": name, "n_dags": G, "tasks": T},
+            "e2e": {"value": out["inspirit"]["e2e_dags_per_s"], "unit": "DAGs/s"},
+            "per_policy": out, "cpu_baseline": cpu}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+C5_MIXES = [(4, 1), (8, 2), (16, 2), (32, 4)]  # worker mix of seed s: C5_MIXES[s % 4]
+
+
+def run_c5(args):
+    """BASELINE configs[4]: 65,536 layered DAGs x 4096 tasks across worker
+    mixes (seed mod 4), sharded over the GPUs: this rank schedules its
+    contiguous shard of `--n-dags` (default 8192 = 65,536 / 8).  DAGs are
+    generated on the device from their seeds (bit-identical to the host
+    generator), so only seeds cross PCIe; the result is all-gathered."""
+    import torch
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2404_03226_b200 import api
+    from paper_2404_03226_b200 import platform as P
+    G = args.n_dags if args.n_dags != WORKLOAD["n_dags"] else 8192
+    n, L, p = 4096, 10, 0.05
+    ctx = api.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    seeds = np.arange(rank * G, (rank + 1) * G, dtype=np.uint64)
+    platforms = [P.assemble(f"{c}c{g}g", c, g) for c, g in C5_MIXES]
+    pof = (seeds % 4).astype(np.int32)
+    dev = torch.device("cuda", local)
+    gathered = torch.empty(world * G, dtype=torch.float64, device=dev)
+
+    def step(db=None):
+        own = db is None
+        if own:
+            db = ctx.generate_layered(n, L, p, seeds)
+        r = ctx.schedule(db, platforms, "inspirit", platform_of=pof, want_attrs=False, want_states=False)
+        if dist is not None:
+            dist.all_gather_into_tensor(gathered, torch.from_numpy(r["makespan_ms"]).to(dev))
+        if own:
+            db.free()
+        return r
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    resident = ctx.generate_layered(n, L, p, seeds)
+    ctx.set_timing(True)
+    times, e2e = [], []
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = step(resident)
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    kms = {k: ctx.last_kernel_ms(k) for k in ("k_ingest", "k_structure", "k_sweep", "k_finalize", "k_simulate")}
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = step()
+        e1.record(stream)
+        e1.synchronize()
+        e2e.append(e0.elapsed_time(e1))
+    ctx.set_timing(True)
+    step()
+    gen_ms = ctx.last_kernel_ms("k_gen_layered_count") + ctx.last_kernel_ms("k_gen_layered_fill")
+    ctx.set_timing(False)
+    tot = torch.tensor([sum(times), sum(e2e)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    value = G * world * args.steps / (float(tot[0]) / 1e3)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import pyref
+        if pyref.available():
+            threads = host_cores()
+            k = max(threads, 8)
+            idx = np.arange(0, G, max(1, G // k))[:k]  # every (G/k)-th DAG of the shard
+            bs = pyref.BenchSet(len(idx), n, L, p, seeds[idx], [C5_MIXES[int(x) % 4][0] for x in seeds[idx]],
+                                [C5_MIXES[int(x) % 4][1] for x in seeds[idx]], threads)
+            secs, ms = bs.run("inspirit", threads)
+            cpu = {"value": len(idx) / secs, "unit": "DAGs/s", "cores": threads, "kind": "reference",
+                   "sample": f"{len(idx)} DAGs (every {max(1, G // k)}th of the shard), {secs:.1f} s; extrapolated rate",
+                   "makespans_match_gpu": bool(np.array_equal(ms, r["makespan_ms"][idx]))}
+    if rank == 0:
+        line = {"metric": "DAGs scheduled/sec", "value": value, "unit": "DAGs/s", "n_gpus": world,
+                "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": float(tot[0]) / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic generate_layered_dag(4096, 10, 0.05, seed), generated on the device",
+                "config": {"workload": "C5 shard: 4096-task layered DAGs, worker mix by seed mod 4 "
+                                       "(4c1g, 8c2g, 16c2g, 32c4g), inspirit", "n_dags_per_gpu": G,
+                           "tasks_per_dag": n},
+                "decisions_per_sec": value * 2 * n, "kernel_ms": kms, "generation_ms": gen_ms,
+                "e2e": {"value": G * world * args.steps / (float(tot[1]) / 1e3), "unit": "DAGs/s",
+                        "h2d_bytes_per_step": int(G * 8), "d2h_bytes_per_step": int(G * 8 + G * n * 20)},
+                "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
 def run_c4(args):
     """BASELINE configs[3]: one 1M-task layered DAG, attributes only
     (compute_attributes UpwardRank).  Reports attribute passes per second and
@@ -271,12 +449,16 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n-dags", type=int, default=WORKLOAD["n_dags"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c2", choices=["c2", "c4"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.workload == "c4":
         return run_c4(args)
+    if args.workload in ("c1", "c3"):
+        return run_tiled(args)
+    if args.workload == "c5":
+        return run_c5(args)
 
     import torch
     rank, world, local = env_rank()

@@ -142,6 +142,17 @@ tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* host,
 tbsim_status tbsim_batch_free(tbsim_ctx* ctx, tbsim_batch* b);
 /* Bytes moved host->device by the last upload of this batch. */
 int64_t tbsim_batch_h2d_bytes(const tbsim_batch* b);
+/* generate_layered_dag (taskgraph.hpp:99-100) for every seed, generated on
+ * the device (bit-identical to the host generator): only the seeds cross
+ * PCIe.  Type ids follow tbsim_type_name(). */
+tbsim_status tbsim_batch_generate_layered(tbsim_ctx* ctx, int32_t n_tasks, int32_t n_layers,
+                                          double edge_prob, const uint64_t* seeds,
+                                          int64_t n_seeds, tbsim_batch** out);
+/* Totals of a device batch: [G, T, E, H, I, O]. */
+tbsim_status tbsim_batch_sizes(const tbsim_batch* b, int64_t* sizes6);
+/* Copy a device batch back into caller buffers laid out like
+ * tbsim_batch_desc; sizes from tbsim_batch_sizes, task_id/type_names unused. */
+tbsim_status tbsim_batch_download(tbsim_ctx* ctx, const tbsim_batch* b, tbsim_batch_desc* host);
 
 /* ------------------------------------------------------------------------
  * Attribute kernels (reference: include/tbsim/attributes.hpp).

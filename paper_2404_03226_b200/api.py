@@ -136,6 +136,18 @@ class DeviceBatch:
     def h2d_bytes(self) -> int:
         return load().tbsim_batch_h2d_bytes(self.h)
 
+    def download(self) -> GraphBatch:
+        """Copy the device CSR back to host numpy arrays (tests, debugging)."""
+        sz = (C.c_int64 * 6)()
+        _check(load().tbsim_batch_sizes(self.h, sz))
+        G, T, E, H, I, O = list(sz)
+        z = lambda k, dt: np.zeros(k, dt)
+        gb = GraphBatch(z(G + 1, np.int64), z(G + 1, np.int64), z(G + 1, np.int64), z(G + 1, np.int64),
+                        z(G + 1, np.int64), z(T + G, np.int32), z(E, np.int32), z(T + G, np.int32), z(I, np.int32),
+                        z(T + G, np.int32), z(O, np.int32), z(T, np.int32), z(H, np.int64), self.type_names)
+        _check(load().tbsim_batch_download(self.ctx.h, self.h, C.byref(gb.desc())))
+        return gb
+
     def free(self):
         if self.h:
             _check(load().tbsim_batch_free(self.ctx.h, self.h))
@@ -190,6 +202,14 @@ class Context:
         _check(load().tbsim_batch_upload(self.h, C.byref(desc), C.byref(h)))
         T = int(desc.task_base[desc.n_graphs])
         return DeviceBatch(self, h, T, int(desc.n_graphs), names)
+
+    def generate_layered(self, n_tasks, n_layers, edge_prob, seeds) -> DeviceBatch:
+        """generate_layered_dag for every seed, built directly in HBM."""
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        h = C.c_void_p()
+        _check(load().tbsim_batch_generate_layered(self.h, n_tasks, n_layers, edge_prob,
+                                                   _p(seeds, C.c_uint64), len(seeds), C.byref(h)))
+        return DeviceBatch(self, h, n_tasks * len(seeds), len(seeds), TYPE_NAMES)
 
     # ---------------------------------------------------------- attributes
     def attributes(self, db: DeviceBatch, costs: CostTable, request: int,

@@ -20,12 +20,12 @@ BUILD = os.path.join(ROOT, "build", "obj")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC",
+CU_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC", "-static-global-template-stub=false",
             "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
 CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off",
              "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I/usr/local/cuda/include"]
 
-CU_SRCS = ["attributes.cu", "simulate.cu", "abi.cpp"]  # abi.cpp launches kernels: nvcc -x cu
+CU_SRCS = ["attributes.cu", "simulate.cu", "generate.cu", "abi.cpp"]  # abi.cpp launches kernels: nvcc -x cu
 CXX_SRCS = ["hostbatch.cpp"]
 # the drop-in C++ API (namespace tbsim, include/tbsim/*.hpp) over the C-ABI
 API_SRCS = ["api/taskgraph.cpp", "api/platform.cpp", "api/device.cpp", "api/attributes.cpp",

@@ -21,6 +21,7 @@
 
 #include "attributes.cuh"
 #include "common.cuh"
+#include "generate.cuh"
 #include "hostbatch.hpp"
 #include "simulate.cuh"
 
@@ -163,6 +164,8 @@ struct tbsim_batch {
     DevBatch d{};
     void* mem = nullptr;
     size_t mem_bytes = 0;
+    void* mem2 = nullptr;  // edge-sized sections of a device-generated batch
+    size_t mem2_bytes = 0;
     int64_t h2d_bytes = 0;
     std::vector<int64_t> task_base;    // host copy
     std::vector<int64_t> task_id;      // host copy (messages)
@@ -371,14 +374,147 @@ tbsim_status tbsim_batch_free(tbsim_ctx* ctx, tbsim_batch* b) {
             // stream-ordered reuse: later uploads on this stream run after
             // every kernel that reads this batch
             if (b->mem) ctx->batch_pool.push_back({b->mem, b->mem_bytes});
-        } else if (b->mem) {
-            cudaFree(b->mem);
+            if (b->mem2) ctx->batch_pool.push_back({b->mem2, b->mem2_bytes});
+        } else {
+            if (b->mem) cudaFree(b->mem);
+            if (b->mem2) cudaFree(b->mem2);
         }
         delete b;
     });
 }
 
 int64_t tbsim_batch_h2d_bytes(const tbsim_batch* b) { return b ? b->h2d_bytes : 0; }
+
+tbsim_status tbsim_batch_sizes(const tbsim_batch* b, int64_t* s) {
+    return guarded([&] {
+        s[0] = b->d.G; s[1] = b->d.T; s[2] = b->d.E; s[3] = b->d.H; s[4] = b->d.I; s[5] = b->d.O;
+    });
+}
+
+tbsim_status tbsim_batch_download(tbsim_ctx* ctx, const tbsim_batch* b, tbsim_batch_desc* h) {
+    return guarded([&] {
+        const DevBatch& d = b->d;
+        const int64_t G = d.G, T = d.T;
+        auto cp = [&](const void* dst, const void* src, size_t bytes) {
+            if (dst && bytes)
+                cuda_check(cudaMemcpyAsync(const_cast<void*>(dst), src, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H batch");
+        };
+        cp(h->task_base, d.task_base, (G + 1) * 8);
+        cp(h->edge_base, d.edge_base, (G + 1) * 8);
+        cp(h->handle_base, d.handle_base, (G + 1) * 8);
+        cp(h->in_base, d.in_base, (G + 1) * 8);
+        cp(h->out_base, d.out_base, (G + 1) * 8);
+        cp(h->dep_off, d.dep_off, (T + G) * 4);
+        cp(h->dep, d.dep, d.E * 4);
+        cp(h->in_off, d.in_off, (T + G) * 4);
+        cp(h->in, d.in, d.I * 4);
+        cp(h->out_off, d.out_off, (T + G) * 4);
+        cp(h->out, d.out, d.O * 4);
+        cp(h->type, d.type, T * 4);
+        cp(h->handle_bytes, d.handle_bytes, d.H * 8);
+        ctx->sync();
+    });
+}
+
+tbsim_status tbsim_batch_generate_layered(tbsim_ctx* ctx, int32_t n, int32_t L, double p, const uint64_t* seeds,
+                                          int64_t n_seeds, tbsim_batch** out) {
+    return guarded([&] {
+        // generate_layered_dag's argument checks (src/generators.cpp:186-191)
+        if (L < 1) raise(TBSIM_E_INVALID_ARGUMENT, "autogen: n_layers must be >= 1");
+        if (n < L) raise(TBSIM_E_INVALID_ARGUMENT, "autogen: n_tasks must be >= n_layers");
+        if (!(p >= 0.0 && p <= 1.0)) raise(TBSIM_E_INVALID_ARGUMENT, "autogen: edge_prob must be in [0,1]");
+        if (n >= (1 << 24)) raise(TBSIM_E_INVALID_ARGUMENT, "graph exceeds 2^24 tasks");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int64_t G = n_seeds, T = G * n;
+        auto b = std::make_unique<tbsim_batch>();
+        GenParams q{};
+        q.G = G;
+        q.n = n;
+        q.L = L;
+        q.p = p;
+        uint64_t* d_seeds = ctx->buf("g_seeds").as<uint64_t>(G);
+        cuda_check(cudaMemcpyAsync(d_seeds, seeds, G * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D seeds");
+        b->h2d_bytes = G * 8;
+        q.seeds = d_seeds;
+        q.ndep = ctx->buf("g_ndep").as<int32_t>(T);
+        q.degree = ctx->buf("g_degree").as<int32_t>(T);
+        q.max_degree = 2 * ((n + L - 1) / L) + 2;
+        q.hist = ctx->buf("g_hist").as<int32_t>(G * (q.max_degree + 1));
+        q.edges = ctx->buf("g_edges").as<int64_t>(G);
+        q.type_base = tbsim_host::T_LAYERK0;
+        // fixed-size sections: bases, offsets, out, type, handle_bytes
+        DevBatch& d = b->d;
+        const size_t fixed = 5 * al16((G + 1) * 8) + 3 * al16((T + G) * 4) + al16(T * 4) + al16(T * 4) + al16(T * 8);
+        b->mem = ctx->batch_alloc(fixed + 16, &b->mem_bytes);
+        char* c = static_cast<char*>(b->mem);
+        auto take = [&](size_t bytes) { char* r = c; c += al16(bytes); return r; };
+        int64_t* task_base = reinterpret_cast<int64_t*>(take((G + 1) * 8));
+        int64_t* edge_base = reinterpret_cast<int64_t*>(take((G + 1) * 8));
+        int64_t* handle_base = reinterpret_cast<int64_t*>(take((G + 1) * 8));
+        int64_t* in_base = reinterpret_cast<int64_t*>(take((G + 1) * 8));
+        int64_t* out_base = reinterpret_cast<int64_t*>(take((G + 1) * 8));
+        d.dep_off = reinterpret_cast<int32_t*>(take((T + G) * 4));
+        d.in_off = reinterpret_cast<int32_t*>(take((T + G) * 4));
+        d.out_off = reinterpret_cast<int32_t*>(take((T + G) * 4));
+        d.out = reinterpret_cast<int32_t*>(take(T * 4));
+        int32_t* type = reinterpret_cast<int32_t*>(take(T * 4));
+        int64_t* hbytes = reinterpret_cast<int64_t*>(take(T * 8));
+        q.type = type;
+        q.handle_bytes = hbytes;
+        d.type = type;
+        d.handle_bytes = hbytes;
+        d.task_base = task_base;
+        d.edge_base = edge_base;
+        d.handle_base = handle_base;
+        d.in_base = in_base;
+        d.out_base = out_base;
+        if (G > 0) {
+            ctx->begin("k_gen_layered_count");
+            k_gen_layered_count<<<static_cast<unsigned>((G + 3) / 4), 128, 0, ctx->stream>>>(q);
+            ctx->end("k_gen_layered_count");
+        }
+        std::vector<int64_t> edges(G), ebase(G + 1, 0), tbase(G + 1, 0);
+        if (G > 0) cuda_check(cudaMemcpyAsync(edges.data(), q.edges, G * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H edges");
+        ctx->sync();
+        for (int64_t g = 0; g < G; ++g) {
+            ebase[g + 1] = ebase[g] + edges[g];
+            tbase[g + 1] = tbase[g] + n;
+        }
+        const int64_t E = ebase[G];
+        if (E > INT32_MAX * int64_t(G > 0 ? G : 1)) raise(TBSIM_E_INVALID_ARGUMENT, "batch too large");
+        for (int64_t* dst : {task_base, handle_base, out_base})
+            cuda_check(cudaMemcpyAsync(dst, tbase.data(), (G + 1) * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D bases");
+        for (int64_t* dst : {edge_base, in_base})
+            cuda_check(cudaMemcpyAsync(dst, ebase.data(), (G + 1) * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D bases");
+        b->h2d_bytes += 5 * (G + 1) * 8;
+        const size_t edge_sec = 2 * al16(E * 4) + al16((T + G) * 4) + al16(E * 4);
+        b->mem2 = ctx->batch_alloc(edge_sec + 16, &b->mem2_bytes);
+        c = static_cast<char*>(b->mem2);
+        d.dep = reinterpret_cast<int32_t*>(take(E * 4));
+        d.in = reinterpret_cast<int32_t*>(take(E * 4));
+        d.succ_off = reinterpret_cast<int32_t*>(take((T + G) * 4));
+        d.succ = reinterpret_cast<int32_t*>(take(E * 4));
+        d.G = G; d.T = T; d.E = E; d.H = T; d.I = E; d.O = T;
+        d.max_n = n;
+        d.max_h = n;
+        d.max_e = 0;
+        for (int64_t g = 0; g < G; ++g) d.max_e = std::max<int32_t>(d.max_e, static_cast<int32_t>(edges[g]));
+        d.n_types = tbsim_host::T_COUNT;
+        if (G > 0) {
+            ctx->begin("k_gen_layered_fill");
+            k_gen_layered_fill<<<static_cast<unsigned>((G + 3) / 4), 128, 0, ctx->stream>>>(q, d);
+            ctx->end("k_gen_layered_fill");
+            int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(T + G);
+            const int grid = static_cast<int>(std::min<int64_t>(G, 8LL * ctx->n_sms));
+            ctx->begin("k_ingest");
+            k_ingest<<<grid, 256, 0, ctx->stream>>>(d, cursor);
+            ctx->end("k_ingest");
+        }
+        b->task_base = tbase;
+        for (int i = 0; i < tbsim_host::T_COUNT; ++i) b->type_names.push_back(tbsim_host::kTypeNames[i]);
+        *out = b.release();
+    });
+}
 
 }  // extern "C"
 

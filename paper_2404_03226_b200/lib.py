@@ -20,7 +20,8 @@ EXPORTS = [
     "tbsim_ctx_create", "tbsim_ctx_destroy", "tbsim_ctx_set_stream", "tbsim_ctx_synchronize",
     "tbsim_ctx_launch_count", "tbsim_ctx_set_timing", "tbsim_ctx_last_kernel_ms",
     "tbsim_ctx_set_large_graph_threshold",
-    "tbsim_batch_upload", "tbsim_batch_free", "tbsim_batch_h2d_bytes",
+    "tbsim_batch_upload", "tbsim_batch_free", "tbsim_batch_h2d_bytes", "tbsim_batch_generate_layered",
+    "tbsim_batch_sizes", "tbsim_batch_download",
     "tbsim_attributes", "tbsim_simulate", "tbsim_schedule", "tbsim_default_regulator_config",
     "tbsim_hostbatch_new", "tbsim_hostbatch_free", "tbsim_hostbatch_add_layered",
     "tbsim_hostbatch_add_cholesky", "tbsim_hostbatch_add_lu", "tbsim_hostbatch_add_qr",
@@ -60,6 +61,9 @@ def load():
     L.tbsim_batch_free.argtypes = [vp, vp]
     L.tbsim_batch_h2d_bytes.argtypes = [vp]
     L.tbsim_batch_h2d_bytes.restype = i64
+    L.tbsim_batch_generate_layered.argtypes = [vp, i32, i32, dbl, P(C.c_uint64), i64, P(vp)]
+    L.tbsim_batch_sizes.argtypes = [vp, P(i64)]
+    L.tbsim_batch_download.argtypes = [vp, vp, P(abi.BatchDesc)]
     L.tbsim_attributes.argtypes = [vp, vp, P(abi.Costs), i32, i32, P(abi.AttrOut)]
     L.tbsim_simulate.argtypes = [vp, vp, P(abi.PlatformDesc), i32, P(i32), i32,
                                  P(abi.RegulatorCfg), P(abi.AttrIn), P(abi.SimOut)]

@@ -261,3 +261,23 @@ def test_large_graph_path_matches_batched_path_and_oracle(ctx, kind):
         eq(large[k], o[k], f"large vs oracle {k}")
     o3 = po.attributes(b, costs, abi.ATTR_EFFICIENCY, unit_time=[3.0])
     eq(eff3["efficiency"], o3["efficiency"], "pruned single window")
+
+
+@pytest.mark.parametrize("shape", [(1000, 10, 0.05), (4096, 10, 0.05), (300, 7, 0.2), (64, 64, 0.5), (50, 1, 0.1)])
+def test_device_generator_is_bit_identical_to_host(ctx, shape):
+    n, L, p = shape
+    seeds = np.array([0, 1, 2, 17, 123456789, 2**63 + 5], np.uint64)
+    dev = ctx.generate_layered(n, L, p, seeds).download()
+    host = api.HostBatch().add_layered(n, L, p, seeds).view()
+    for k in ("task_base", "edge_base", "handle_base", "in_base", "out_base", "dep_off", "dep", "in_off", "in_",
+              "out_off", "out", "type", "handle_bytes"):
+        eq(getattr(dev, k), getattr(host, k), k)
+
+
+def test_device_generated_batch_schedules_like_host_batch(ctx):
+    seeds = np.arange(300, 556)
+    pl = [P.assemble("8c2g", 8, 2)]
+    a = ctx.schedule(ctx.generate_layered(1000, 10, 0.05, seeds), pl, "inspirit")
+    b = ctx.schedule(ctx.upload(api.HostBatch().add_layered(1000, 10, 0.05, seeds)), pl, "inspirit")
+    for k in ("worker", "start_ms", "end_ms", "makespan_ms", "attr_efficiency", "attr_ability"):
+        eq(a[k], b[k], k)
