@@ -794,12 +794,16 @@ int32_t pow2_at_least(int32_t x) {
 // Picks the per-warp state placement: shared memory (compact types when the
 // batch allows) with 16 then 8 warps per SM, else HBM with full queues.
 void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_items) {
-    const int kThreads = 256, kWarps = kThreads / 32;
+    // Few DAGs (e.g. two 22k-task tiled factorizations): fewer warps per CTA
+    // so each warp gets more shared memory; many DAGs: 8 warps per CTA.
+    int kWarps = 8;
+    while (kWarps > 1 && n_items < static_cast<int64_t>(kWarps) * ctx->n_sms) kWarps >>= 1;
+    const int kThreads = 32 * kWarps;
     const DevBatch& d = p.b;
     const int64_t qcap_full = std::max<int32_t>(d.max_n, 1);
     const bool compact = d.max_n < 32768 && p.max_nodes <= 8;
     auto layout = [&](int64_t qcap) {
-        return sim_layout(d.max_n, d.max_h, max_workers, qcap, p.ring, p.n_types, p.max_nodes, compact);
+        return sim_layout(d.max_n, d.max_h, max_workers, qcap, p.ring, p.n_types, p.max_nodes, compact, p.policy);
     };
     const bool forced = p.qcap > 0;  // rerun of queue overflows: HBM state, full capacity
     int64_t qcap = qcap_full;
@@ -815,8 +819,10 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
                 p.use_smem = 1;
                 break;
             }
-            const int64_t cap = (per_warp - layout(0).total - 64) / (4 * max_workers);
-            if (cap >= 64) {
+            const int64_t cap = (per_warp - layout(0).total - 64) / ((4 + key_bytes(p.policy)) * max_workers);
+            // short queues are the common case (C2: <= 27 entries); a graph
+            // that overflows is re-run exactly with HBM state
+            if (cap >= (c == 2 ? 32 : 64)) {
                 qcap = std::min<int64_t>(cap & ~int64_t(3), qcap_full);
                 ctas_per_sm = c;
                 p.use_smem = 1;
@@ -883,6 +889,9 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
         };
         switch (status[g]) {
             case GS_NO_WORKER: raise(TBSIM_E_RUNTIME, "no worker can run task type " + ty_at(aux[g]));
+            case GS_TOO_LARGE:
+                raise(TBSIM_E_INVALID_ARGUMENT, "ability/efficiency of task " + std::to_string(task_ident(b, g, aux[g])) +
+                                                    " exceeds the device's int32 queue keys");
             case GS_DEGENERATE_TIME:
                 raise(TBSIM_E_RUNTIME, "event of task " + std::to_string(task_ident(b, g, aux[g])) +
                                            " would fire at the current time (transfer/exec below FP64 resolution)");

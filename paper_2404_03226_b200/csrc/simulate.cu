@@ -62,6 +62,9 @@ struct Sim {
     ResidT* resid;
     ReadyT* ready;
     int32_t* queue;
+    int32_t* qab;    // cached pop keys per queue entry (inspirit)
+    int32_t* qef;
+    int64_t* qprio;  // (dmdap, inspirit)
     double* samp_t;
     int64_t* samp_n;
     double* costs;   // [2*NT]: cpu, gpu per type
@@ -108,31 +111,32 @@ struct Sim {
     }
 
     // transfer_total_ms (engine.cpp:105-110) for node `want` (may differ per
-    // lane): lanes hold the inputs, the per-input times are summed in input
-    // order by shuffles, for every node that any lane asks for.
+    // lane).  Lanes hold (node, input) pairs, so every per-input transfer is
+    // computed once and in parallel; each node's total is then summed in
+    // input order by one shuffle chain shared by all nodes.
     __device__ __forceinline__ double transfer_total_lanes(int32_t task, int32_t want) const {
         const int32_t k0 = __ldg(&ioff[task]), k1 = __ldg(&ioff[task + 1]);
         const int32_t nin = k1 - k0;
-        double mine = 0.0;
         if (nin == 0) return 0.0;
         const unsigned want_nodes = __reduce_or_sync(kFull, 1u << want);
-        if (nin <= 32) {
-            uint32_t m = 0;
-            int64_t by = 0;
-            if (lane < nin) {
-                const int32_t h = __ldg(&in[k0 + lane]);
-                m = resid[h];
-                by = __ldg(&hbytes[h]);
-            }
-            for (unsigned wn = want_nodes; wn; wn &= wn - 1) {
+        const int32_t nw = __popc(want_nodes);
+        if (nin * nw <= 32) {
+            const int32_t r = lane / nin, k = lane - r * nin;
+            double t = 0.0;
+            if (r < nw) {
+                unsigned wn = want_nodes;
+                for (int32_t i = 0; i < r; ++i) wn &= wn - 1;
                 const int32_t to = __ffs(wn) - 1;
-                const double t = lane < nin ? transfer_one(m, by, to) : 0.0;
-                double acc = 0.0;
-                for (int32_t j = 0; j < nin; ++j) acc += __shfl_sync(kFull, t, j);
-                if (want == to) mine = acc;
+                const int32_t h = __ldg(&in[k0 + k]);
+                t = transfer_one(resid[h], __ldg(&hbytes[h]), to);
             }
-            return mine;
+            const int32_t base = (r < nw ? r : 0) * nin;
+            double acc = 0.0;
+            for (int32_t j = 0; j < nin; ++j) acc += __shfl_sync(kFull, t, base + j);
+            const int32_t rw = __popc(want_nodes & ((1u << want) - 1u));
+            return __shfl_sync(kFull, acc, rw * nin);
         }
+        double mine = 0.0;
         for (unsigned wn = want_nodes; wn; wn &= wn - 1) {
             const int32_t to = __ffs(wn) - 1;
             double acc = 0.0;
@@ -292,25 +296,25 @@ struct Sim {
             pop1 += m == 1;
             pop2 += m == 2;
         }
-        const int32_t* q = queue + static_cast<int64_t>(w) * qcap;
+        const int64_t qo = static_cast<int64_t>(w) * qcap;
+        const int32_t* q = queue + qo;
         uint64_t b0 = 0, b1 = 0, b2 = 0;
         int32_t bpos = INT_MAX;
         for (int32_t i = lane; i < ql; i += 32) {
-            const int32_t t = q[i] & 0xffffff;
             uint64_t k0, k1;
             if (policy == TBSIM_POLICY_DMDAP) {
                 k0 = k1 = 1;
             } else if (m == TBSIM_MODE_ABILITY) {
-                k0 = ord_f64(ability ? static_cast<double>(__ldg(&ability[t0 + t])) : 0.0);
+                k0 = ord_f64(static_cast<double>(qab[qo + i]));
                 k1 = ord_f64(0.0);
             } else if (m == TBSIM_MODE_EFFICIENCY) {
-                k0 = ord_f64(efficiency ? static_cast<double>(__ldg(&efficiency[t0 + t])) : 0.0);
+                k0 = ord_f64(static_cast<double>(qef[qo + i]));
                 k1 = ord_f64(0.0);
             } else {
-                k0 = ord_f64(resident_fraction(t, nd));
-                k1 = ord_f64(efficiency ? static_cast<double>(__ldg(&efficiency[t0 + t])) : 0.0);
+                k0 = ord_f64(resident_fraction(q[i] & 0xffffff, nd));
+                k1 = ord_f64(static_cast<double>(qef[qo + i]));
             }
-            const uint64_t k2 = ord_i64(prio ? __ldg(&prio[t0 + t]) : 0);
+            const uint64_t k2 = ord_i64(qprio[qo + i]);
             const bool better = bpos == INT_MAX || k0 > b0 ||
                                 (k0 == b0 && (k1 > b1 || (k1 == b1 && k2 > b2)));
             if (better) { b0 = k0; b1 = k1; b2 = k2; bpos = i; }
@@ -338,14 +342,27 @@ struct Sim {
         nd = __shfl_sync(kFull, nd, owner);
         if (bz || ql == 0) return;
         const int32_t pick = select_entry(w, ql, nd);
-        int32_t* q = queue + static_cast<int64_t>(w) * qcap;
+        const int64_t qo = static_cast<int64_t>(w) * qcap;
+        int32_t* q = queue + qo;
         const uint32_t e = static_cast<uint32_t>(q[pick]);
         __syncwarp();
+        const bool ins = policy == TBSIM_POLICY_INSPIRIT, pri = policy >= TBSIM_POLICY_DMDAP;
         for (int32_t base = pick; base < ql - 1; base += 32) {
             const int32_t i = base + lane;
-            const int32_t val = i < ql - 1 ? q[i + 1] : 0;
+            const bool mv = i < ql - 1;
+            int32_t val = 0, va = 0, ve = 0;
+            int64_t vp = 0;
+            if (mv) {
+                val = q[i + 1];
+                if (ins) { va = qab[qo + i + 1]; ve = qef[qo + i + 1]; }
+                if (pri) vp = qprio[qo + i + 1];
+            }
             __syncwarp();
-            if (i < ql - 1) q[i] = val;
+            if (mv) {
+                q[i] = val;
+                if (ins) { qab[qo + i] = va; qef[qo + i] = ve; }
+                if (pri) qprio[qo + i] = vp;
+            }
             __syncwarp();
         }
         const int32_t task = static_cast<int32_t>(e & 0xffffffu);
@@ -389,8 +406,21 @@ struct Sim {
 
     __device__ __forceinline__ void on_push(int32_t task) {  // engine.cpp:124-141
         const int32_t ty = __ldg(&type[task]);
+        // pop keys of this task, loaded while the push rule runs
+        int32_t ka = 0, ke = 0;
+        int64_t kp = 0;
+        bool too_large = false;
+        if (policy == TBSIM_POLICY_INSPIRIT) {
+            const int64_t a64 = ability ? __ldg(&ability[t0 + task]) : 0;
+            const int64_t e64 = efficiency ? __ldg(&efficiency[t0 + task]) : 0;
+            ka = static_cast<int32_t>(a64);
+            ke = static_cast<int32_t>(e64);
+            too_large = ka != a64 || ke != e64;  // the queue caches int32 keys
+        }
+        if (policy >= TBSIM_POLICY_DMDAP) kp = prio ? __ldg(&prio[t0 + task]) : 0;
         const int32_t w = select_worker(task, ty);
         if (w < 0) { status = GS_NO_WORKER; aux = task; return; }
+        if (too_large) { status = GS_TOO_LARGE; aux = task; return; }
         const int j = w >> 5, owner = w & 31;
         int32_t ovf = 0;
 #pragma unroll
@@ -399,7 +429,10 @@ struct Sim {
                 if (qlen[jj] >= qcap) {
                     ovf = 1;
                 } else {
-                    queue[static_cast<int64_t>(w) * qcap + qlen[jj]] = (ty << 24) | task;
+                    const int64_t at = static_cast<int64_t>(w) * qcap + qlen[jj];
+                    queue[at] = (ty << 24) | task;
+                    if (policy == TBSIM_POLICY_INSPIRIT) { qab[at] = ka; qef[at] = ke; }
+                    if (policy >= TBSIM_POLICY_DMDAP) qprio[at] = kp;
                     qlen[jj] += 1;
                     if (busy[jj] && !fdirty[jj]) fsum[jj] += cost(ty, kind[jj]);
                 }
@@ -531,7 +564,8 @@ __device__ void simulate_impl(const SimParams& p) {
     char* base = p.use_smem ? smem + static_cast<int64_t>(warp_in_block) * p.state_bytes
                             : p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
     const DevBatch& b = p.b;
-    const SimLayout L = sim_layout(b.max_n, b.max_h, p.max_workers, p.qcap, p.ring, p.n_types, p.max_nodes, COMPACT);
+    const SimLayout L = sim_layout(b.max_n, b.max_h, p.max_workers, p.qcap, p.ring, p.n_types, p.max_nodes, COMPACT,
+                                   p.policy);
     using S = Sim<WPL, COMPACT>;
     S s;
     s.P = &p;
@@ -540,6 +574,9 @@ __device__ void simulate_impl(const SimParams& p) {
     s.resid = reinterpret_cast<typename S::ResidT*>(base + L.resid);
     s.ready = reinterpret_cast<typename S::ReadyT*>(base + L.ready);
     s.queue = reinterpret_cast<int32_t*>(base + L.queue);
+    s.qab = reinterpret_cast<int32_t*>(base + L.qab);
+    s.qef = reinterpret_cast<int32_t*>(base + L.qef);
+    s.qprio = reinterpret_cast<int64_t*>(base + L.qprio);
     s.samp_t = reinterpret_cast<double*>(base + L.ring);
     s.samp_n = reinterpret_cast<int64_t*>(base + L.ring + 8 * p.ring);
     s.costs = reinterpret_cast<double*>(base + L.costs);
