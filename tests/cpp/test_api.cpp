@@ -3,6 +3,7 @@
 // GPU_CASEs need a B200 (attributes and simulate run on the device);
 // TEST_CASEs are host-side and also run with --cpu-only.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <filesystem>
 #include <fstream>
@@ -769,6 +770,78 @@ GPU_CASE("run_bench rows, baseline, error rows and overrides") {
     o.regulator.k_inc = 1e9;
     BenchReport ro = run_bench(o);
     CHECK(ro.rows.size() == 2 * 3);
+}
+
+// ----------------------------------------- acceptance gate (tests/acceptance.cpp)
+
+GPU_CASE("acceptance c7: INSPIRIT vs DMDA grid equals the reference's CSV") {
+    std::string csv;
+    for (const char* app : {"autogen", "cholesky", "lu"}) {
+        BenchSpec spec;
+        spec.app = app;
+        spec.sizes = std::string(app) == "autogen" ? std::vector<int64_t>{1000, 5000}
+                     : std::string(app) == "cholesky" ? std::vector<int64_t>{8, 12, 16, 20, 24}
+                                                      : std::vector<int64_t>{8, 12, 16};
+        spec.platforms = {"26cpu_2gpu"};
+        spec.policies = {"dmda", "inspirit"};
+        spec.seed = 7;
+        BenchReport r = run_bench(spec);
+        std::ostringstream out;
+        write_bench_csv(out, r);
+        std::string body = out.str();
+        csv += csv.empty() ? body : body.substr(body.find('\n') + 1);
+        double log_sum = 0.0, mn = 1e300;
+        for (const auto& row : r.rows) {
+            REQUIRE(row.ok);
+            if (row.policy == "inspirit") {
+                log_sum += std::log(row.speedup);
+                mn = std::min(mn, row.speedup);
+            }
+        }
+        CHECK(mn >= 0.95);
+        CHECK(log_sum >= 0.0);
+    }
+    std::ifstream golden(std::string(GOLDEN_DIR) + "/grid_bench.csv");
+    std::stringstream want;
+    want << golden.rdbuf();
+    CHECK(csv == want.str());
+}
+
+GPU_CASE("acceptance c8: reruns are identical") {
+    Platform p = make_preset("26cpu_2gpu");
+    auto g = build_cholesky_dag(12, 960 * 960 * 4);
+    TaskAttributes a = compute_attributes(g, p.costs, PriorityKind::UpwardRank);
+    SimTrace x = run(g, p, "inspirit", a), y = run(g, p, "inspirit", a);
+    CHECK(gantt(g, x) == gantt(g, y));
+    CHECK(x.nready_samples == y.nready_samples);
+    BenchSpec spec;
+    spec.app = "cholesky";
+    spec.sizes = {12};
+    spec.platforms = {"26cpu_2gpu", "homog2"};
+    spec.seed = 3;
+    auto csv = [&spec]() {
+        std::ostringstream out;
+        write_bench_csv(out, run_bench(spec));
+        return out.str();
+    };
+    const std::string first = csv();
+    CHECK(first == csv());
+    spec.jobs = 4;
+    CHECK(first == csv());
+}
+
+GPU_CASE("acceptance c9: calibration stays within eleven evaluations") {
+    CostTable costs = make_preset("26cpu_2gpu").costs;
+    std::vector<TaskGraph> graphs;
+    for (int n : {8, 12, 16, 20, 24}) graphs.push_back(build_cholesky_dag(n, 4096));
+    for (int n : {8, 12, 16}) graphs.push_back(build_lu_dag(n, 4096));
+    for (int n : {1000, 5000}) graphs.push_back(generate_layered_dag(n, 10, 0.05, 7));
+    for (const auto& g : graphs) {
+        CalibrationResult c = calibrate_unit_time(g, costs);
+        CHECK(c.evaluations <= 11);
+        CHECK(c.best_score >= c.w0_score);
+        CHECK(c.unit_time_ms > 0.0);
+    }
 }
 
 int main(int argc, char** argv) { return mt::run_all(argc, argv); }

@@ -89,6 +89,40 @@ def hand_graphs():
     return chain, diamond
 
 
+def _fmt_ms(v):
+    s = "%.6f" % v
+    if "." in s:
+        s = s.rstrip("0")
+        if s.endswith("."):
+            s = s[:-1]
+    return "0" if s == "-0" else s
+
+
+def grid_csv():
+    """The acceptance gate's INSPIRIT-vs-DMDA grid (tests/acceptance.cpp:430-480)
+    as the reference's bench CSV (src/bench.cpp:149-159), cells computed by
+    the reference itself."""
+    pl = P.make_preset("26cpu_2gpu")
+    costs = pl.costs
+    rows = []
+    cells = [("autogen", n, lambda n: pyref.gen_layered(n, 10, 0.05, 7)) for n in (1000, 5000)]
+    cells += [("cholesky", n, lambda n: pyref.gen_cholesky(n, 960 * 960 * 4)) for n in (8, 12, 16, 20, 24)]
+    cells += [("lu", n, lambda n: pyref.gen_lu(n, 160 * 160 * 4)) for n in (8, 12, 16)]
+    for app, n, gen in cells:
+        b = gen(n)
+        a = pyref.attributes(b, costs, abi.ATTR_ALL)
+        ms = {pol: pyref.simulate(b, [pl], pol, attrs=a, record=False)["makespan_ms"][0] for pol in ("dmda", "inspirit")}
+        for pol in ("dmda", "inspirit"):
+            sp = 1.0 if pol == "dmda" else ms["dmda"] / ms[pol]
+            rows.append((app, n, pol, f"{app},{n},26cpu_2gpu,{pol},{_fmt_ms(ms[pol])},{sp:.3f},ok"))
+    rows.sort(key=lambda r: (r[0], r[1], r[2]))
+    with open(os.path.join(HERE, "grid_bench.csv"), "w") as f:
+        f.write("app,size,platform,policy,makespan_ms,speedup_vs_baseline,status\n")
+        for r in rows:
+            f.write(r[3] + "\n")
+    print("wrote grid_bench.csv", len(rows), "rows")
+
+
 def main():
     default = P.default_cost_table()
     # hand graphs of tests/test_attributes.cpp
@@ -122,6 +156,7 @@ def main():
     for b in rnd:
         assert b.type_names[:len(P.TYPE_NAMES)] == P.TYPE_NAMES
     save("random_dag", GraphBatch.concat(rnd), default, ["homog2", "26cpu_2gpu", "2gpu"])
+    grid_csv()
     # README goldens (proj/README.md:81-88,117-125): cholesky 8/12 dmda/inspirit
     # are inside "cholesky" on 26cpu_2gpu; a quick self-check:
     z = np.load(os.path.join(HERE, "cholesky.npz"))
