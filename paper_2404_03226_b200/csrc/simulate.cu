@@ -555,14 +555,17 @@ struct Sim {
     }
 };
 
-template <int WPL, bool COMPACT>
+// SMEM: the per-warp state lives in shared memory (provably, so every state
+// access compiles to 32-bit-addressed LDS/STS); otherwise in HBM.
+template <int WPL, bool COMPACT, bool SMEM>
 __device__ void simulate_impl(const SimParams& p) {
     extern __shared__ __align__(16) char smem[];
     const int lane = threadIdx.x & 31;
     const int warp_in_block = threadIdx.x >> 5;
     const int warps_per_block = blockDim.x >> 5;
-    char* base = p.use_smem ? smem + static_cast<int64_t>(warp_in_block) * p.state_bytes
-                            : p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
+    char* base;
+    if constexpr (SMEM) base = smem + warp_in_block * static_cast<int32_t>(p.state_bytes);
+    else base = p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
     const DevBatch& b = p.b;
     const SimLayout L = sim_layout(b.max_n, b.max_h, p.max_workers, p.qcap, p.ring, p.n_types, p.max_nodes, COMPACT,
                                    p.policy);
@@ -714,9 +717,15 @@ __device__ void simulate_impl(const SimParams& p) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(256, 2) k_simulate_w1c(const __grid_constant__ SimParams p) { simulate_impl<1, true>(p); }
-__global__ void __launch_bounds__(256, 2) k_simulate_w2c(const __grid_constant__ SimParams p) { simulate_impl<2, true>(p); }
-__global__ void __launch_bounds__(256, 2) k_simulate_w1(const __grid_constant__ SimParams p) { simulate_impl<1, false>(p); }
-__global__ void __launch_bounds__(256, 2) k_simulate_w2(const __grid_constant__ SimParams p) { simulate_impl<2, false>(p); }
+#define TBSIM_SIM_KERNEL(NAME, WPL, COMPACT)                                                          \
+    __global__ void __launch_bounds__(256, 2) NAME(const __grid_constant__ SimParams p) {               \
+        if (p.use_smem) simulate_impl<WPL, COMPACT, true>(p);                                          \
+        else simulate_impl<WPL, COMPACT, false>(p);                                                    \
+    }
+TBSIM_SIM_KERNEL(k_simulate_w1c, 1, true)
+TBSIM_SIM_KERNEL(k_simulate_w2c, 2, true)
+TBSIM_SIM_KERNEL(k_simulate_w1, 1, false)
+TBSIM_SIM_KERNEL(k_simulate_w2, 2, false)
+#undef TBSIM_SIM_KERNEL
 
 }  // namespace tbsim_dev
