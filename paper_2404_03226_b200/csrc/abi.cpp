@@ -831,7 +831,8 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
         }
     }
     p.qcap = static_cast<int32_t>(qcap);
-    p.state_bytes = layout(qcap).total;
+    p.layout = layout(qcap);
+    p.state_bytes = p.layout.total;
     p.max_workers = max_workers;
     p.n_items = n_items;
     int grid = static_cast<int>(std::min<int64_t>((n_items + kWarps - 1) / kWarps,

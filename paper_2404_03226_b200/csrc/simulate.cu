@@ -121,18 +121,28 @@ struct Sim {
         const unsigned want_nodes = __reduce_or_sync(kFull, 1u << want);
         const int32_t nw = __popc(want_nodes);
         if (nin * nw <= 32) {
-            const int32_t r = lane / nin, k = lane - r * nin;
+            // r = lane / nin without an integer divide (exact: lane < 32)
+            const int32_t r = __float2int_rz(__fdividef(static_cast<float>(lane) + 0.5f, static_cast<float>(nin)));
+            const int32_t k = lane - r * nin;
             double t = 0.0;
             if (r < nw) {
-                unsigned wn = want_nodes;
-                for (int32_t i = 0; i < r; ++i) wn &= wn - 1;
-                const int32_t to = __ffs(wn) - 1;
+                const int32_t to = __fns(want_nodes, 0, r + 1);
                 const int32_t h = __ldg(&in[k0 + k]);
                 t = transfer_one(resid[h], __ldg(&hbytes[h]), to);
             }
             const int32_t base = (r < nw ? r : 0) * nin;
+            // in-order sum; the shuffles are independent and issued ahead
             double acc = 0.0;
-            for (int32_t j = 0; j < nin; ++j) acc += __shfl_sync(kFull, t, base + j);
+            int32_t j = 0;
+            for (; j + 4 <= nin; j += 4) {
+                const double a0 = __shfl_sync(kFull, t, base + j), a1 = __shfl_sync(kFull, t, base + j + 1);
+                const double a2 = __shfl_sync(kFull, t, base + j + 2), a3 = __shfl_sync(kFull, t, base + j + 3);
+                acc += a0;
+                acc += a1;
+                acc += a2;
+                acc += a3;
+            }
+            for (; j < nin; ++j) acc += __shfl_sync(kFull, t, base + j);
             const int32_t rw = __popc(want_nodes & ((1u << want) - 1u));
             return __shfl_sync(kFull, acc, rw * nin);
         }
@@ -567,8 +577,7 @@ __device__ void simulate_impl(const SimParams& p) {
     if constexpr (SMEM) base = smem + warp_in_block * static_cast<int32_t>(p.state_bytes);
     else base = p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
     const DevBatch& b = p.b;
-    const SimLayout L = sim_layout(b.max_n, b.max_h, p.max_workers, p.qcap, p.ring, p.n_types, p.max_nodes, COMPACT,
-                                   p.policy);
+    const SimLayout& L = p.layout;  // offsets precomputed on the host
     using S = Sim<WPL, COMPACT>;
     S s;
     s.P = &p;

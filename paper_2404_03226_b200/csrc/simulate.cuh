@@ -7,6 +7,38 @@
 
 namespace tbsim_dev {
 
+// Per-warp state layout (bytes, 16-aligned sections).  Compact state
+// (n < 32768, <= 8 memory nodes) stores unmet counts and the ready list as
+// int16 and residency masks as uint8.
+struct SimLayout {
+    int64_t unmet, resid, ready, queue, qab, qef, qprio, ring, costs, bw, total;
+};
+
+// Pop keys cached per queue entry: inspirit (policy 4) ability + efficiency
+// (int32) + static priority (int64); dmdap (3) the priority only.
+__host__ __device__ inline int key_bytes(int32_t policy) { return policy == 4 ? 16 : policy == 3 ? 8 : 0; }
+
+__host__ __device__ inline SimLayout sim_layout(int64_t max_n, int64_t max_h, int64_t max_workers, int64_t qcap,
+                                                int64_t ring, int64_t n_types, int64_t max_nodes, bool compact,
+                                                int32_t policy) {
+    auto al = [](int64_t x) { return (x + 15) & ~int64_t(15); };
+    SimLayout L;
+    int64_t off = 0;
+    L.unmet = off; off += al((compact ? 2 : 4) * max_n);
+    L.resid = off; off += al((compact ? 1 : 4) * max_h);
+    L.ready = off; off += al((compact ? 2 : 4) * max_n);
+    L.queue = off; off += al(4 * max_workers * qcap);
+    const bool ins = policy == 4, pri = policy >= 3;
+    L.qab = off; off += ins ? al(4 * max_workers * qcap) : 0;
+    L.qef = off; off += ins ? al(4 * max_workers * qcap) : 0;
+    L.qprio = off; off += pri ? al(8 * max_workers * qcap) : 0;
+    L.ring = off; off += al(16 * ring);
+    L.costs = off; off += al(16 * n_types);
+    L.bw = off; off += al(8 * max_nodes * max_nodes);
+    L.total = off;
+    return L;
+}
+
 struct SimParams {
     DevBatch b;
     const DevPlatform* platforms;
@@ -40,6 +72,7 @@ struct SimParams {
     int32_t max_nodes;                // platform copy: nodes x nodes bandwidth
     int32_t n_types;                  // platform copy: cost rows
     int32_t ring;                     // regulator sample ring capacity (power of 2)
+    SimLayout layout;                 // per-warp state sections (set by launch_sim)
     const int32_t* graph_list;        // subset of graphs (rerun) or null
     int64_t n_items;                  // graphs to process (list length or G)
     unsigned long long* work_counter;
@@ -49,37 +82,5 @@ __global__ void k_simulate_w1c(const __grid_constant__ SimParams p);  // <= 32 w
 __global__ void k_simulate_w2c(const __grid_constant__ SimParams p);  // <= 64 workers, compact state
 __global__ void k_simulate_w1(const __grid_constant__ SimParams p);   // <= 32 workers, wide state
 __global__ void k_simulate_w2(const __grid_constant__ SimParams p);   // <= 64 workers, wide state
-
-// Per-warp state layout (bytes, 16-aligned sections).  Compact state
-// (n < 32768, <= 8 memory nodes) stores unmet counts and the ready list as
-// int16 and residency masks as uint8.
-struct SimLayout {
-    int64_t unmet, resid, ready, queue, qab, qef, qprio, ring, costs, bw, total;
-};
-
-// Pop keys cached per queue entry: inspirit (policy 4) ability + efficiency
-// (int32) + static priority (int64); dmdap (3) the priority only.
-__host__ __device__ inline int key_bytes(int32_t policy) { return policy == 4 ? 16 : policy == 3 ? 8 : 0; }
-
-__host__ __device__ inline SimLayout sim_layout(int64_t max_n, int64_t max_h, int64_t max_workers, int64_t qcap,
-                                                int64_t ring, int64_t n_types, int64_t max_nodes, bool compact,
-                                                int32_t policy) {
-    auto al = [](int64_t x) { return (x + 15) & ~int64_t(15); };
-    SimLayout L;
-    int64_t off = 0;
-    L.unmet = off; off += al((compact ? 2 : 4) * max_n);
-    L.resid = off; off += al((compact ? 1 : 4) * max_h);
-    L.ready = off; off += al((compact ? 2 : 4) * max_n);
-    L.queue = off; off += al(4 * max_workers * qcap);
-    const bool ins = policy == 4, pri = policy >= 3;
-    L.qab = off; off += ins ? al(4 * max_workers * qcap) : 0;
-    L.qef = off; off += ins ? al(4 * max_workers * qcap) : 0;
-    L.qprio = off; off += pri ? al(8 * max_workers * qcap) : 0;
-    L.ring = off; off += al(16 * ring);
-    L.costs = off; off += al(16 * n_types);
-    L.bw = off; off += al(8 * max_nodes * max_nodes);
-    L.total = off;
-    return L;
-}
 
 }  // namespace tbsim_dev
