@@ -181,10 +181,11 @@ def algorithmic_bytes(gb, dominant):
     T, G, E = gb.n_tasks, gb.n_graphs, gb.n_edges
     I, O, H = int(gb.in_base[-1]), int(gb.out_base[-1]), int(gb.handle_base[-1])
     if dominant == "k_simulate":
-        # succ CSR + dep offsets + inputs/outputs CSR + types + handle bytes
-        # + 3 attribute arrays in; worker/start/end out; makespan per graph
-        return (4 * (T + G) * 4 + 4 * E + 4 * I + 4 * O + 4 * T + 8 * H + 3 * 8 * T
-                + (4 + 8 + 8) * T + 8 * G)
+        # packed task records (32 B: list offset, counts, type, pop keys) and
+        # per-task lists (input bytes 8 B + input handle 4 B per input, 4 B
+        # per output and successor entry) + dependency offsets in; the
+        # 24-byte dispatch log + per-graph makespan/completed/status out
+        return 32 * T + 12 * I + 4 * O + 4 * E + 4 * (T + G) + 24 * T + (8 + 8 + 4 + 4) * G
     # k_sweep: level order, dep offsets, types, predecessor slots in; 4 words
     # of window bins per source out
     return 4 * T + 4 * (T + G) + 4 * T + 4 * E + 32 * T
@@ -321,7 +322,7 @@ def run_c5(args):
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
-    kms = {k: ctx.last_kernel_ms(k) for k in ("k_ingest", "k_structure", "k_sweep", "k_finalize", "k_simulate")}
+    kms = {k: ctx.last_kernel_ms(k) for k in ("k_structure", "k_sweep", "k_finalize", "k_sim_pack", "k_simulate", "k_sim_scatter")}
     for _ in range(args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -368,29 +369,30 @@ def run_c5(args):
     return 0
 
 
-def run_c4(args):
+def c4_measure(steps=3, warmup=1, ctx=None, stream=None):
     """BASELINE configs[3]: one 1M-task layered DAG, attributes only
-    (compute_attributes UpwardRank).  Reports attribute passes per second and
-    the HBM roofline of the bitset closure (ability)."""
+    (compute_attributes UpwardRank).  Returns the measurement dict with the
+    HBM roofline of the bitset closure (ability)."""
     import torch
     from paper_2404_03226_b200 import abi, api
     from paper_2404_03226_b200 import platform as P
     n, layers, p = 1 << 20, 1024, 1.0 / 256
-    ctx = api.Context(0)
-    stream = torch.cuda.current_stream()
-    ctx.set_stream(stream.cuda_stream)
+    if ctx is None:
+        ctx = api.Context(0)
+        stream = torch.cuda.current_stream()
+        ctx.set_stream(stream.cuda_stream)
     t = time.perf_counter()
     hb = api.HostBatch().add_layered(n, layers, p, [1])
     gen_s = time.perf_counter() - t
     gb = hb.view()
     db = ctx.upload(hb)
     costs = P.default_cost_table()
-    for _ in range(max(args.warmup, 1)):
+    for _ in range(max(warmup, 1)):
         res = ctx.attributes(db, costs, abi.ATTR_ALL)
     torch.cuda.synchronize()
     ctx.set_timing(True)
     times, kms = [], []
-    for _ in range(args.steps):
+    for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         res = ctx.attributes(db, costs, abi.ATTR_ALL)
@@ -402,20 +404,16 @@ def run_c4(args):
     ctx.set_timing(False)
     # algorithmic bytes of the closure: every successor's set read from its
     # lower word bound, every node's set written from its own bound (8 B/word)
-    order_level = None
     lvl = ctx.attributes(db, costs, abi.ATTR_LAYERS)["layer"]
     counts = np.bincount(lvl, minlength=layers)
     lstart = np.concatenate([[0], np.cumsum(counts)])
     nw = (n + 63) // 64
     lo_of_level = lstart[1:] // 64
     off, dep = gb.graph_deps(0)
-    deg_out = np.bincount(dep, minlength=n)
-    words_written = (nw - lo_of_level[lvl]).astype(np.int64)
-    words_read = (deg_out * 0).astype(np.int64)
-    # each edge u->v reads set(v) from lo(v)
     v_of_edge = np.repeat(np.arange(n), np.diff(off))
-    words_read = int((nw - lo_of_level[lvl[v_of_edge]]).sum())
-    alg_bytes = 8 * (int(words_written.sum()) + words_read)
+    words_written = int((nw - lo_of_level[lvl]).astype(np.int64).sum())
+    words_read = int((nw - lo_of_level[lvl[v_of_edge]]).astype(np.int64).sum())
+    alg_bytes = 8 * (words_written + words_read)
     closure_ms = statistics.median(k["k_closure"] for k in kms)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -424,19 +422,27 @@ def run_c4(args):
     ab, ef = res["ability"], res["efficiency"]
     props = {"efficiency_le_ability": bool(np.all(ef <= ab)),
              "ability_monotone": bool(np.all(ab[dep] >= ab[v_of_edge] + 1))}
-    total_ms = statistics.median(times)
-    line = {"metric": "attribute passes/sec (1M-task DAG)", "value": 1e3 / total_ms, "unit": "DAGs/s",
-            "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": total_ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic generate_layered_dag(1048576, 1024, 1/256, seed 1)",
-            "config": {"workload": "C4: single 1M-task DAG, compute_attributes(UpwardRank)", "n_tasks": n,
-                       "n_edges": gb.n_edges, "host_generation_s": gen_s},
+    db.free()
+    return {"ms_per_pass": statistics.median(times), "n_tasks": n, "n_edges": gb.n_edges,
+            "host_generation_s": gen_s,
             "kernel_ms": {k: statistics.median(x[k] for x in kms) for k in kms[0]},
             "roofline": {"bound": "hbm", "kernel": "k_closure", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "algorithmic_bytes": alg_bytes, "kernel_ms": closure_ms,
-                         "note": "trimmed descendant sets (level-ordered bit space); L2 reuse of the level cut can "
-                                 "push algorithmic GB/s above the DRAM copy peak"},
+                         "note": "trimmed descendant sets (level-ordered bit space); L2 reuse of the level cut "
+                                 "can push algorithmic GB/s above the DRAM copy peak"},
             "properties": props, "unit_time_ms": float(res["unit_time_ms"][0])}
+
+
+def run_c4(args):
+    m = c4_measure(args.steps, args.warmup)
+    line = {"metric": "attribute passes/sec (1M-task DAG)", "value": 1e3 / m["ms_per_pass"], "unit": "DAGs/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 1), "ms_per_step": m["ms_per_pass"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic generate_layered_dag(1048576, 1024, 1/256, seed 1)",
+            "config": {"workload": "C4: single 1M-task DAG, compute_attributes(UpwardRank)", "n_tasks": m["n_tasks"],
+                       "n_edges": m["n_edges"], "host_generation_s": m["host_generation_s"]},
+            "kernel_ms": m["kernel_ms"], "roofline": m["roofline"], "properties": m["properties"],
+            "unit_time_ms": m["unit_time_ms"]}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -449,6 +455,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n-dags", type=int, default=WORKLOAD["n_dags"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the 1M-task attribute roofline probe")
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     args = ap.parse_args()
     if args.impl == "reference":
@@ -532,8 +539,8 @@ def main():
     ctx.set_timing(True)
     value_step()
     torch.cuda.synchronize()
-    kms = {k: ctx.last_kernel_ms(k) for k in ("k_ingest", "k_structure", "k_tile_plan", "k_sweep",
-                                             "k_finalize", "k_structure_out", "k_simulate")}
+    kms = {k: ctx.last_kernel_ms(k) for k in ("k_structure", "k_tile_plan", "k_sweep", "k_finalize",
+                                             "k_structure_out", "k_sim_pack", "k_simulate", "k_sim_scatter")}
     ctx.set_timing(False)
     dominant = max(("k_sweep", "k_simulate"), key=lambda k: kms[k])
     alg = algorithmic_bytes(gb, dominant)
@@ -619,6 +626,17 @@ def main():
                          f"({cpu_model()}), {secs:.1f} s",
                "makespans_match_gpu": bool(np.array_equal(got, ref_ms[:len(got)]))}
 
+    # ---------------- attribute-kernel HBM roofline: the 1M-task C4 DAG
+    c4 = None
+    if rank == 0 and world == 1 and not args.no_c4:
+        try:
+            del db
+            m = c4_measure(2, 1, ctx, stream)
+            c4 = {"workload": "C4: one 1M-task DAG, compute_attributes", "ms_per_pass": m["ms_per_pass"],
+                  "kernel_ms": m["kernel_ms"], "roofline": m["roofline"], "properties": m["properties"]}
+        except Exception as e:  # pragma: no cover
+            c4 = {"error": str(e)}
+
     if rank == 0:
         line = {
             "metric": "DAGs scheduled/sec", "value": value, "unit": "DAGs/s", "n_gpus": world,
@@ -642,6 +660,7 @@ def main():
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "parity": parity,
+            "c4_attributes": c4,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

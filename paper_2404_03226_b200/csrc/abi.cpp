@@ -854,9 +854,31 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
 
 // Runs the simulator over every graph, reruns queue overflows with full
 // capacity in HBM, and raises the first graph's error.
-void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t max_workers) {
-    const int64_t G = b->d.G;
+struct SimKeys {
+    const int64_t* ability = nullptr;
+    const int64_t* efficiency = nullptr;
+    const int64_t* prio = nullptr;
+};
+
+void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t max_workers, const SimKeys& keys) {
+    const DevBatch& d = b->d;
+    const int64_t G = d.G;
     if (G == 0) return;
+    // packed simulation graph: one record per task + contiguous lists
+    const int64_t adj_bytes = sim_adj_bytes(d.T, d.I, d.O, d.E);
+    if (adj_bytes >= (int64_t(1) << 35)) raise(TBSIM_E_INVALID_ARGUMENT, "batch too large for the packed simulation graph");
+    SimTaskHdr* hdr = ctx->buf("s_hdr").as<SimTaskHdr>(std::max<int64_t>(d.T, 1));
+    char* adj = static_cast<char*>(ctx->buf("s_adj").get(static_cast<size_t>(adj_bytes)));
+    p.hdr = hdr;
+    p.adj = adj;
+    p.log = ctx->buf("s_log").as<SimLog>(std::max<int64_t>(d.T, 1));
+    p.n_disp = ctx->buf("s_ndisp").as<int32_t>(G);
+    if (d.T > 0) {
+        const int grid = static_cast<int>(std::min<int64_t>((d.T + 255) / 256, 16LL * ctx->n_sms));
+        ctx->begin("k_sim_pack");
+        k_sim_pack<<<grid, 256, 0, ctx->stream>>>(d, keys.ability, keys.efficiency, keys.prio, p.policy, hdr, adj);
+        ctx->end("k_sim_pack");
+    }
     p.graph_list = nullptr;
     p.qcap = 0;
     launch_sim(ctx, p, max_workers, G);
@@ -880,6 +902,12 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
         cuda_check(cudaMemcpyAsync(aux.data(), p.status_aux, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H aux");
         ctx->sync();
     }
+    if (d.T > 0) {  // dispatch logs -> per-task worker/start/end
+        const int grid = static_cast<int>(std::min<int64_t>((d.T + 255) / 256, 16LL * ctx->n_sms));
+        ctx->begin("k_sim_scatter");
+        k_sim_scatter<<<grid, 256, 0, ctx->stream>>>(d, p.log, p.n_disp, p.worker, p.start_ms, p.end_ms);
+        ctx->end("k_sim_scatter");
+    }
     for (int64_t g = 0; g < G; ++g) {
         if (status[g] == GS_OK) continue;
         const int64_t t0 = b->task_base[g], n = b->task_base[g + 1] - t0;
@@ -891,8 +919,9 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
         switch (status[g]) {
             case GS_NO_WORKER: raise(TBSIM_E_RUNTIME, "no worker can run task type " + ty_at(aux[g]));
             case GS_TOO_LARGE:
-                raise(TBSIM_E_INVALID_ARGUMENT, "ability/efficiency of task " + std::to_string(task_ident(b, g, aux[g])) +
-                                                    " exceeds the device's int32 queue keys");
+                raise(TBSIM_E_INVALID_ARGUMENT, "task " + std::to_string(task_ident(b, g, aux[g])) +
+                                                    " exceeds the device simulator's limits (ability/efficiency "
+                                                    "beyond its int32 queue keys, or 2^24 successor entries)");
             case GS_DEGENERATE_TIME:
                 raise(TBSIM_E_RUNTIME, "event of task " + std::to_string(task_ident(b, g, aux[g])) +
                                            " would fire at the current time (transfer/exec below FP64 resolution)");
@@ -1007,10 +1036,11 @@ extern "C" tbsim_status tbsim_simulate(tbsim_ctx* ctx, const tbsim_batch* b, con
             cuda_check(cudaMemcpyAsync(dv, a, T * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D attrs");
             return dv;
         };
+        SimKeys keys;
         if (attrs) {
-            p.ability = up_attr(attrs->ability, "s_ab");
-            p.efficiency = up_attr(attrs->efficiency, "s_ef");
-            p.prio = up_attr(attrs->static_priority, "s_pr");
+            keys.ability = up_attr(attrs->ability, "s_ab");
+            keys.efficiency = up_attr(attrs->efficiency, "s_ef");
+            keys.prio = up_attr(attrs->static_priority, "s_pr");
         }
         p.worker = scratch_if_null(ctx, "s_worker", sim_out_ptr(ctx, st, "s_worker", out->worker, T, dev), T);
         p.start_ms = scratch_if_null(ctx, "s_start", sim_out_ptr(ctx, st, "s_start", out->start_ms, T, dev), T);
@@ -1032,7 +1062,7 @@ extern "C" tbsim_status tbsim_simulate(tbsim_ctx* ctx, const tbsim_batch* b, con
         }
         p.status = ctx->buf("s_status").as<int32_t>(G);
         p.status_aux = ctx->buf("s_aux").as<int32_t>(G);
-        run_simulation(ctx, b, p, maxw);
+        run_simulation(ctx, b, p, maxw, keys);
         for (const auto& c : st.copies)
             cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
         ctx->sync();
@@ -1102,9 +1132,10 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         p.reg = nullptr;
         p.median = run.s.median;
         p.median_stride = 1;
-        p.ability = o.ability;
-        p.efficiency = o.efficiency;
-        p.prio = o.static_priority;
+        SimKeys keys;
+        keys.ability = o.ability;
+        keys.efficiency = o.efficiency;
+        keys.prio = o.static_priority;
         p.worker = scratch_if_null(ctx, "s_worker", sim_out_ptr(ctx, st, "s_worker", out->worker, T, dev), T);
         p.start_ms = scratch_if_null(ctx, "s_start", sim_out_ptr(ctx, st, "s_start", out->start_ms, T, dev), T);
         p.end_ms = scratch_if_null(ctx, "s_end", sim_out_ptr(ctx, st, "s_end", out->end_ms, T, dev), T);
@@ -1114,7 +1145,7 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         p.reg_state = sim_out_ptr(ctx, st, "s_rstate", out->reg_state, G, dev, true);
         p.status = ctx->buf("s_status").as<int32_t>(G);
         p.status_aux = ctx->buf("s_aux").as<int32_t>(G);
-        run_simulation(ctx, b, p, maxw);
+        run_simulation(ctx, b, p, maxw, keys);
         for (const auto& c : ast.copies)
             cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
         for (const auto& c : st.copies)

@@ -43,7 +43,9 @@ __device__ __forceinline__ uint64_t ord_i64(int64_t x) {
     return static_cast<uint64_t>(x) ^ 0x8000000000000000ull;
 }
 
-template <int WPL, bool COMPACT>
+// POL >= 0 fixes the policy at compile time; POL < 0 (the shipped kernels)
+// reads it at run time -- specialising saved <1% of the code.
+template <int WPL, bool COMPACT, int POL>
 struct Sim {
     using UnmetT = typename std::conditional<COMPACT, int16_t, int32_t>::type;
     using ResidT = typename std::conditional<COMPACT, uint8_t, uint32_t>::type;
@@ -51,12 +53,13 @@ struct Sim {
     // ---- graph
     int64_t g, t0;
     int32_t n, nh;
-    const int32_t *doff, *soff, *succ, *ioff, *in, *ooff, *out, *type;
-    const int64_t* hbytes;
+    const int32_t* doff;
+    const SimTaskHdr* hdr;  // this graph's packed records
+    const char* adj;        // packed list base
     int32_t W, nn;
     double lat;
-    int32_t policy;
-    const int64_t *ability, *efficiency, *prio;
+    int32_t policy_rt;
+    __device__ __forceinline__ int32_t pol() const { return POL >= 0 ? POL : policy_rt; }
     // ---- per-warp state memory (shared memory when it fits)
     UnmetT* unmet;
     ResidT* resid;
@@ -96,6 +99,14 @@ struct Sim {
 
     __device__ __forceinline__ double cost(int32_t ty, int32_t k) const { return costs[2 * ty + k]; }
 
+    // first half of a packed record: (adj8, nin, nout, nsucc | type << 24)
+    __device__ __forceinline__ int4 head(int32_t task) const {
+        return __ldg(reinterpret_cast<const int4*>(hdr + task));
+    }
+    __device__ __forceinline__ const char* lists(const int4& h) const {
+        return adj + 8ull * static_cast<uint32_t>(h.x);
+    }
+
     // transfer_one_ms (engine.cpp:86-103): fastest resident copy, ties to the
     // lowest node; Platform::transfer_time_ms (platform.cpp:56-63).
     __device__ __forceinline__ double transfer_one(uint32_t m, int64_t bytes, int32_t to) const {
@@ -114,9 +125,8 @@ struct Sim {
     // lane).  Lanes hold (node, input) pairs, so every per-input transfer is
     // computed once and in parallel; each node's total is then summed in
     // input order by one shuffle chain shared by all nodes.
-    __device__ __forceinline__ double transfer_total_lanes(int32_t task, int32_t want) const {
-        const int32_t k0 = __ldg(&ioff[task]), k1 = __ldg(&ioff[task + 1]);
-        const int32_t nin = k1 - k0;
+    __device__ __forceinline__ double transfer_total_lanes(const int64_t* inb, const int32_t* inh, int32_t nin,
+                                                           int32_t want) const {
         if (nin == 0) return 0.0;
         const unsigned want_nodes = __reduce_or_sync(kFull, 1u << want);
         const int32_t nw = __popc(want_nodes);
@@ -126,9 +136,10 @@ struct Sim {
             const int32_t k = lane - r * nin;
             double t = 0.0;
             if (r < nw) {
-                const int32_t to = __fns(want_nodes, 0, r + 1);
-                const int32_t h = __ldg(&in[k0 + k]);
-                t = transfer_one(resid[h], __ldg(&hbytes[h]), to);
+                unsigned m = want_nodes;  // r-th set bit (few nodes; __fns is emulated)
+                for (int32_t i = 0; i < r; ++i) m &= m - 1;
+                const int32_t to = __ffs(m) - 1;
+                t = transfer_one(resid[__ldg(&inh[k])], __ldg(&inb[k]), to);
             }
             const int32_t base = (r < nw ? r : 0) * nin;
             // in-order sum; the shuffles are independent and issued ahead
@@ -153,10 +164,7 @@ struct Sim {
             for (int32_t base = 0; base < nin; base += 32) {
                 const int32_t cnt = min(32, nin - base);
                 double t = 0.0;
-                if (lane < cnt) {
-                    const int32_t h = __ldg(&in[k0 + base + lane]);
-                    t = transfer_one(resid[h], __ldg(&hbytes[h]), to);
-                }
+                if (lane < cnt) t = transfer_one(resid[__ldg(&inh[base + lane])], __ldg(&inb[base + lane]), to);
                 for (int32_t j = 0; j < cnt; ++j) acc += __shfl_sync(kFull, t, j);
             }
             if (want == to) mine = acc;
@@ -166,14 +174,16 @@ struct Sim {
 
     // resident_fraction (engine.cpp:63-74)
     __device__ __forceinline__ double resident_fraction(int32_t task, int32_t nd) const {
-        const int32_t k0 = __ldg(&ioff[task]), k1 = __ldg(&ioff[task + 1]);
-        if (k0 == k1) return 1.0;
+        const int4 hd = head(task);
+        const int32_t nin = hd.y;
+        if (nin == 0) return 1.0;
+        const int64_t* inb = reinterpret_cast<const int64_t*>(lists(hd));
+        const int32_t* inh = reinterpret_cast<const int32_t*>(inb + nin);
         int64_t total = 0, local = 0;
-        for (int32_t k = k0; k < k1; ++k) {
-            const int32_t h = __ldg(&in[k]);
-            const int64_t by = __ldg(&hbytes[h]);
+        for (int32_t k = 0; k < nin; ++k) {
+            const int64_t by = __ldg(&inb[k]);
             total += by;
-            if ((static_cast<uint32_t>(resid[h]) >> nd) & 1u) local += by;
+            if ((static_cast<uint32_t>(resid[__ldg(&inh[k])]) >> nd) & 1u) local += by;
         }
         return static_cast<double>(local) / static_cast<double>(total);
     }
@@ -182,6 +192,7 @@ struct Sim {
     __device__ __forceinline__ double calculate_k() const {  // policies.cpp:153-169
         if (r_count < 2) return 0.0;
         double sx = 0.0, sy = 0.0;
+#pragma unroll 1
         for (int i = 0; i < r_count; ++i) {
             const int idx = (r_head + i) & ring_mask;
             sx += samp_t[idx];
@@ -190,6 +201,7 @@ struct Sim {
         const double dn = static_cast<double>(r_count);
         const double mx = sx / dn, my = sy / dn;
         double sxx = 0.0, sxy = 0.0;
+#pragma unroll 1
         for (int i = 0; i < r_count; ++i) {
             const int idx = (r_head + i) & ring_mask;
             const double dx = samp_t[idx] - mx;
@@ -239,7 +251,7 @@ struct Sim {
             P->sample_nready[2 * t0 + n_samp] = nready;
         }
         ++n_samp;
-        if (policy == TBSIM_POLICY_INSPIRIT) regulator_step(nready);
+        if (pol() == TBSIM_POLICY_INSPIRIT) regulator_step(nready);
     }
 
     // ---------------------------------------------------------- push rules
@@ -259,14 +271,14 @@ struct Sim {
 
     // push_fifo / push_dm / push_dmda (policies.cpp:37-72): argmin over
     // capable workers, strict < so ties keep the lowest id.
-    __device__ __forceinline__ int32_t select_worker(int32_t task, int32_t ty) {
-        if (policy != TBSIM_POLICY_FIFO) refresh_free();
+    __device__ __forceinline__ int32_t select_worker(const int64_t* inb, const int32_t* inh, int32_t nin, int32_t ty) {
+        if (pol() != TBSIM_POLICY_FIFO) refresh_free();
         double xfer[WPL];
 #pragma unroll
         for (int j = 0; j < WPL; ++j) xfer[j] = 0.0;
-        if (policy >= TBSIM_POLICY_DMDA) {
+        if (pol() >= TBSIM_POLICY_DMDA) {
 #pragma unroll
-            for (int j = 0; j < WPL; ++j) xfer[j] = transfer_total_lanes(task, node[j]);
+            for (int j = 0; j < WPL; ++j) xfer[j] = transfer_total_lanes(inb, inh, nin, node[j]);
         }
         uint64_t bk = ~0ull;
         int32_t bwk = INT_MAX;
@@ -277,12 +289,12 @@ struct Sim {
             const double ce = cost(ty, kind[j]);
             if (!(ce > 0.0)) continue;
             double key;
-            if (policy == TBSIM_POLICY_FIFO) {
+            if (pol() == TBSIM_POLICY_FIFO) {
                 key = static_cast<double>(qlen[j]) + (busy[j] ? 1.0 : 0.0);
             } else {
                 const double fa = busy[j] ? fsum[j] : now;
                 const double st = now < fa ? fa : now;  // std::max(now, free_at)
-                if (policy == TBSIM_POLICY_DM) key = st + ce;
+                if (pol() == TBSIM_POLICY_DM) key = st + ce;
                 else key = (st + xfer[j]) + ce;
             }
             const uint64_t kb = ord_f64(key);
@@ -298,9 +310,9 @@ struct Sim {
     // lexicographic argmax over (k0, k1, static priority, -seq); queue
     // position is insertion (= seq) order.
     __device__ __forceinline__ int32_t select_entry(int32_t w, int32_t ql, int32_t nd) {
-        if (policy <= TBSIM_POLICY_DMDA) return 0;
+        if (pol() <= TBSIM_POLICY_DMDA) return 0;
         int32_t m = TBSIM_MODE_EFFICIENCY;
-        if (policy == TBSIM_POLICY_INSPIRIT) {
+        if (pol() == TBSIM_POLICY_INSPIRIT) {
             m = mode;
             pop0 += m == 0;
             pop1 += m == 1;
@@ -312,7 +324,7 @@ struct Sim {
         int32_t bpos = INT_MAX;
         for (int32_t i = lane; i < ql; i += 32) {
             uint64_t k0, k1;
-            if (policy == TBSIM_POLICY_DMDAP) {
+            if (pol() == TBSIM_POLICY_DMDAP) {
                 k0 = k1 = 1;
             } else if (m == TBSIM_MODE_ABILITY) {
                 k0 = ord_f64(static_cast<double>(qab[qo + i]));
@@ -356,7 +368,7 @@ struct Sim {
         int32_t* q = queue + qo;
         const uint32_t e = static_cast<uint32_t>(q[pick]);
         __syncwarp();
-        const bool ins = policy == TBSIM_POLICY_INSPIRIT, pri = policy >= TBSIM_POLICY_DMDAP;
+        const bool ins = pol() == TBSIM_POLICY_INSPIRIT, pri = pol() >= TBSIM_POLICY_DMDAP;
         for (int32_t base = pick; base < ql - 1; base += 32) {
             const int32_t i = base + lane;
             const bool mv = i < ql - 1;
@@ -377,15 +389,18 @@ struct Sim {
         }
         const int32_t task = static_cast<int32_t>(e & 0xffffffu);
         const int32_t ty = static_cast<int32_t>(e >> 24);
+        const int4 hd = head(task);  // issued before the queue bookkeeping
         nready -= 1;
+        const int64_t slot = t0 + n_pop;
         if (P->pop_time && lane == 0) {
-            P->pop_time[t0 + n_pop] = now;
-            P->pop_task[t0 + n_pop] = task;
-            P->pop_worker[t0 + n_pop] = w;
+            P->pop_time[slot] = now;
+            P->pop_task[slot] = task;
+            P->pop_worker[slot] = w;
         }
         ++n_pop;
         queue_event();
-        const double xfer = transfer_total_lanes(task, nd);
+        const int64_t* inb = reinterpret_cast<const int64_t*>(lists(hd));
+        const double xfer = transfer_total_lanes(inb, reinterpret_cast<const int32_t*>(inb + hd.y), hd.y, nd);
         const double exec = cost(ty, kd);
         const double start = now + xfer;
         const double end = start + exec;
@@ -394,10 +409,11 @@ struct Sim {
             aux = task;
             return;
         }
-        if (lane == 0) {
-            P->worker[t0 + task] = w;
-            P->start_ms[t0 + task] = start;
-            P->end_ms[t0 + task] = end;
+        if (lane == 0) {  // dispatch log: sequential, scattered by k_sim_scatter
+            SimLog* lg = P->log + slot;
+            *reinterpret_cast<int2*>(lg) = make_int2(task, w);
+            lg->start = start;
+            lg->end = end;
         }
         const uint32_t sx = seq;
         if (xfer > 0.0) ++seq;
@@ -414,23 +430,22 @@ struct Sim {
             }
     }
 
-    __device__ __forceinline__ void on_push(int32_t task) {  // engine.cpp:124-141
-        const int32_t ty = __ldg(&type[task]);
-        // pop keys of this task, loaded while the push rule runs
-        int32_t ka = 0, ke = 0;
-        int64_t kp = 0;
-        bool too_large = false;
-        if (policy == TBSIM_POLICY_INSPIRIT) {
-            const int64_t a64 = ability ? __ldg(&ability[t0 + task]) : 0;
-            const int64_t e64 = efficiency ? __ldg(&efficiency[t0 + task]) : 0;
-            ka = static_cast<int32_t>(a64);
-            ke = static_cast<int32_t>(e64);
-            too_large = ka != a64 || ke != e64;  // the queue caches int32 keys
-        }
-        if (policy >= TBSIM_POLICY_DMDAP) kp = prio ? __ldg(&prio[t0 + task]) : 0;
-        const int32_t w = select_worker(task, ty);
-        if (w < 0) { status = GS_NO_WORKER; aux = task; return; }
-        if (too_large) { status = GS_TOO_LARGE; aux = task; return; }
+    // push rule + queue insert; returns the chosen worker (dispatch follows
+    // in run(), so the dispatch code exists once in the kernel)
+    __device__ __forceinline__ int32_t on_push(int32_t task) {  // engine.cpp:124-141
+        // the whole record in two 16-byte loads of one sector; the pop keys
+        // ride along while the push rule runs
+        const int4 hd = head(task);
+        const int4 kk = __ldg(reinterpret_cast<const int4*>(hdr + task) + 1);
+        const int32_t ty = static_cast<int32_t>(static_cast<uint32_t>(hd.w) >> 24);
+        const int32_t ka = kk.x, ke = kk.y;
+        const int64_t kp = static_cast<int64_t>((static_cast<uint64_t>(static_cast<uint32_t>(kk.w)) << 32) |
+                                                static_cast<uint32_t>(kk.z));
+        const bool too_large = ka < 0;  // pop keys beyond int32 or > 2^24 successor entries
+        const int64_t* inb = reinterpret_cast<const int64_t*>(lists(hd));
+        const int32_t w = select_worker(inb, reinterpret_cast<const int32_t*>(inb + hd.y), hd.y, ty);
+        if (w < 0) { status = GS_NO_WORKER; aux = task; return -1; }
+        if (too_large) { status = GS_TOO_LARGE; aux = task; return -1; }
         const int j = w >> 5, owner = w & 31;
         int32_t ovf = 0;
 #pragma unroll
@@ -441,13 +456,13 @@ struct Sim {
                 } else {
                     const int64_t at = static_cast<int64_t>(w) * qcap + qlen[jj];
                     queue[at] = (ty << 24) | task;
-                    if (policy == TBSIM_POLICY_INSPIRIT) { qab[at] = ka; qef[at] = ke; }
-                    if (policy >= TBSIM_POLICY_DMDAP) qprio[at] = kp;
+                    if (pol() == TBSIM_POLICY_INSPIRIT) { qab[at] = ka; qef[at] = ke; }
+                    if (pol() >= TBSIM_POLICY_DMDAP) qprio[at] = kp;
                     qlen[jj] += 1;
                     if (busy[jj] && !fdirty[jj]) fsum[jj] += cost(ty, kind[jj]);
                 }
             }
-        if (__shfl_sync(kFull, ovf, owner)) { status = GS_QUEUE_OVERFLOW; aux = task; return; }
+        if (__shfl_sync(kFull, ovf, owner)) { status = GS_QUEUE_OVERFLOW; aux = task; return -1; }
         __syncwarp();
         nready += 1;
         if (P->push_time && lane == 0) {
@@ -456,7 +471,7 @@ struct Sim {
         }
         ++n_push;
         queue_event();
-        maybe_dispatch(w);
+        return w;
     }
 
     __device__ __forceinline__ void run() {  // Simulation::run, engine.cpp:207-248
@@ -476,23 +491,34 @@ struct Sim {
         }
         for (int32_t h = lane; h < nh; h += 32) resid[h] = 1u;  // engine.cpp:215-216
         __syncwarp();
+        // One loop, one dispatch site: phase A pushes the tasks made ready
+        // at `now` in creation order (2)+(3); phase B drains the worker
+        // events stamped `now` in enqueue order (1), then time advances.
+        int32_t r = 0;
+        bool events = false;
+        uint64_t mt = 0;
         for (;;) {
-            // (2)+(3): pushes of the tasks made ready at `now`, creation order
-            for (int32_t r = 0; r < rcount && status == GS_OK; ++r) on_push(ready[r]);
-            rcount = 0;
-            if (status != GS_OK) return;
-            // next worker-event time
-            uint64_t lt = ~0ull;
+            int32_t w;
+            if (!events) {
+                if (r < rcount) {
+                    w = on_push(ready[r++]);
+                    if (status != GS_OK) return;
+                } else {
+                    rcount = r = 0;
+                    // next worker-event time
+                    uint64_t lt = ~0ull;
 #pragma unroll
-            for (int j = 0; j < WPL; ++j) {
-                if (xs[j] != kNone) lt = min(lt, dbits(xt[j]));
-                if (ds[j] != kNone) lt = min(lt, dbits(dt[j]));
-            }
-            const uint64_t mt = warp_min_u64(lt);
-            if (mt == ~0ull) break;
-            now = __longlong_as_double(static_cast<long long>(mt));
-            // (1): every worker event at `now`, enqueue order
-            for (;;) {
+                    for (int j = 0; j < WPL; ++j) {
+                        if (xs[j] != kNone) lt = min(lt, dbits(xt[j]));
+                        if (ds[j] != kNone) lt = min(lt, dbits(dt[j]));
+                    }
+                    mt = warp_min_u64(lt);
+                    if (mt == ~0ull) break;
+                    now = __longlong_as_double(static_cast<long long>(mt));
+                    events = true;
+                    continue;
+                }
+            } else {
                 uint32_t ls = kNone;
 #pragma unroll
                 for (int j = 0; j < WPL; ++j) {
@@ -500,7 +526,10 @@ struct Sim {
                     if (ds[j] != kNone && dbits(dt[j]) == mt) ls = min(ls, ds[j]);
                 }
                 const uint32_t ms = __reduce_min_sync(kFull, ls);
-                if (ms == kNone) break;
+                if (ms == kNone) {
+                    events = false;
+                    continue;
+                }
                 const int owner = __ffs(__ballot_sync(kFull, ls == ms)) - 1;
                 int32_t info = 0;
                 if (lane == owner) {
@@ -512,7 +541,7 @@ struct Sim {
                 }
                 info = __shfl_sync(kFull, info, owner);
                 const int32_t task = info & 0xffffff;
-                const int32_t w = owner + 32 * (static_cast<uint32_t>(info) >> 30);
+                w = owner + 32 * (static_cast<uint32_t>(info) >> 30);
                 const bool is_done = (info >> 29) & 1;
                 int32_t nd = 0;
 #pragma unroll
@@ -520,17 +549,21 @@ struct Sim {
                     if (j == (w >> 5)) nd = node[j];
                 nd = __shfl_sync(kFull, nd, owner);
                 const uint32_t bit = 1u << nd;
+                const int4 hd = head(task);
+                const int32_t nin = hd.y, nout = hd.z;
+                const int32_t* inh = reinterpret_cast<const int32_t*>(lists(hd) + 8ull * nin);
                 if (!is_done) {  // TransferDone: inputs resident (engine.cpp:168-172)
-                    for (int32_t k = __ldg(&ioff[task]) + lane; k < __ldg(&ioff[task + 1]); k += 32) {
-                        const int32_t h = __ldg(&in[k]);
+                    for (int32_t k = lane; k < nin; k += 32) {
+                        const int32_t h = __ldg(&inh[k]);
                         resid[h] = static_cast<ResidT>(resid[h] | bit);
                     }
                     __syncwarp();
                     continue;
                 }
                 // TaskDone (engine.cpp:174-185)
-                for (int32_t k = __ldg(&ooff[task]) + lane; k < __ldg(&ooff[task + 1]); k += 32) {
-                    const int32_t h = __ldg(&out[k]);
+                const int32_t* outl = inh + nin;
+                for (int32_t k = lane; k < nout; k += 32) {
+                    const int32_t h = __ldg(&outl[k]);
                     resid[h] = static_cast<ResidT>(resid[h] | bit);
                 }
 #pragma unroll
@@ -540,11 +573,12 @@ struct Sim {
                 makespan = now > makespan ? now : makespan;
                 // successors: sorted, multi-edges adjacent; the lowest lane of
                 // each run of equal ids decrements by the run length
-                const int32_t s0 = __ldg(&soff[task]), s1 = __ldg(&soff[task + 1]);
-                for (int32_t base = s0; base < s1; base += 32) {
+                const int32_t* succl = outl + nout;
+                const int32_t s1 = static_cast<int32_t>(static_cast<uint32_t>(hd.w) & 0xffffffu);
+                for (int32_t base = 0; base < s1; base += 32) {
                     const int32_t k = base + lane;
                     const bool valid = k < s1;
-                    const int32_t sv = valid ? __ldg(&succ[k]) : -1 - lane;
+                    const int32_t sv = valid ? __ldg(&succl[k]) : -1 - lane;
                     const unsigned peers = __match_any_sync(kFull, sv);
                     bool rdy = false;
                     if (valid && (__ffs(peers) - 1) == lane) {
@@ -558,16 +592,16 @@ struct Sim {
                     __syncwarp();
                 }
                 __syncwarp();
-                maybe_dispatch(w);
-                if (status != GS_OK) return;
             }
+            maybe_dispatch(w);
+            if (status != GS_OK) return;
         }
     }
 };
 
 // SMEM: the per-warp state lives in shared memory (provably, so every state
 // access compiles to 32-bit-addressed LDS/STS); otherwise in HBM.
-template <int WPL, bool COMPACT, bool SMEM>
+template <int WPL, bool COMPACT, int POL, bool SMEM>
 __device__ void simulate_impl(const SimParams& p) {
     extern __shared__ __align__(16) char smem[];
     const int lane = threadIdx.x & 31;
@@ -578,7 +612,7 @@ __device__ void simulate_impl(const SimParams& p) {
     else base = p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
     const DevBatch& b = p.b;
     const SimLayout& L = p.layout;  // offsets precomputed on the host
-    using S = Sim<WPL, COMPACT>;
+    using S = Sim<WPL, COMPACT, POL>;
     S s;
     s.P = &p;
     s.lane = lane;
@@ -595,7 +629,7 @@ __device__ void simulate_impl(const SimParams& p) {
     s.bw = reinterpret_cast<double*>(base + L.bw);
     s.qcap = p.qcap;
     s.ring_mask = p.ring - 1;
-    s.policy = p.policy;
+    s.policy_rt = p.policy;
     int32_t loaded_pf = -1;
 
     for (;;) {
@@ -609,14 +643,8 @@ __device__ void simulate_impl(const SimParams& p) {
         s.n = static_cast<int32_t>(b.task_base[g + 1] - s.t0);
         s.nh = static_cast<int32_t>(b.handle_base[g + 1] - b.handle_base[g]);
         s.doff = b.dep_off + s.t0 + g;
-        s.soff = b.succ_off + s.t0 + g;
-        s.succ = b.succ + b.edge_base[g];
-        s.ioff = b.in_off + s.t0 + g;
-        s.in = b.in + b.in_base[g];
-        s.ooff = b.out_off + s.t0 + g;
-        s.out = b.out + b.out_base[g];
-        s.type = b.type + s.t0;
-        s.hbytes = b.handle_bytes + b.handle_base[g];
+        s.hdr = p.hdr + s.t0;
+        s.adj = p.adj;
         const int32_t pfi = p.platform_of ? p.platform_of[g] : 0;
         const DevPlatform* pf = p.platforms + pfi;
         s.W = pf->n_workers;
@@ -632,9 +660,6 @@ __device__ void simulate_impl(const SimParams& p) {
             __syncwarp();
             loaded_pf = pfi;
         }
-        s.ability = p.ability;
-        s.efficiency = p.efficiency;
-        s.prio = p.prio;
 #pragma unroll
         for (int j = 0; j < WPL; ++j) {
             const int32_t w = lane + 32 * j;
@@ -685,13 +710,28 @@ __device__ void simulate_impl(const SimParams& p) {
             s.mode = TBSIM_MODE_EFFICIENCY; s.phase = TBSIM_PHASE_INC; s.peak = 0; s.prev_nready = 0;
             s.last_trigger = 0; s.s_dec_count = 1; s.cur_k = 0.0; s.r_head = 0; s.r_count = 0;
         }
-        for (int32_t v = lane; v < s.n; v += 32) {
-            p.worker[s.t0 + v] = -1;
-            p.start_ms[s.t0 + v] = 0.0;
-            p.end_ms[s.t0 + v] = 0.0;
-        }
         __syncwarp();
         s.run();
+        if (s.status == GS_OK && s.completed == s.n) {
+            if (lane == 0) p.n_disp[g] = static_cast<int32_t>(s.n_pop);
+        } else {
+            // failed graph: outputs written here (undispatched tasks keep
+            // worker -1), k_sim_scatter skips it
+            __syncwarp();
+            for (int32_t v = lane; v < s.n; v += 32) {
+                p.worker[s.t0 + v] = -1;
+                p.start_ms[s.t0 + v] = 0.0;
+                p.end_ms[s.t0 + v] = 0.0;
+            }
+            __syncwarp();
+            for (int64_t i = lane; i < s.n_pop; i += 32) {
+                const SimLog e = p.log[s.t0 + i];
+                p.worker[s.t0 + e.task] = e.worker;
+                p.start_ms[s.t0 + e.task] = e.start;
+                p.end_ms[s.t0 + e.task] = e.end;
+            }
+            if (lane == 0) p.n_disp[g] = -1;
+        }
         if (lane == 0) {
             int32_t st = s.status;
             if (st == GS_OK && s.completed != s.n) st = GS_STUCK;
@@ -724,17 +764,95 @@ __device__ void simulate_impl(const SimParams& p) {
     }
 }
 
+__device__ __forceinline__ int64_t graph_of(const DevBatch& b, int64_t t) {
+    // largest g with task_base[g] <= t (empty graphs share a base and sort first)
+    int64_t lo = 0, hi = b.G;
+    while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(&b.task_base[mid]) <= t) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
 }  // namespace
 
-#define TBSIM_SIM_KERNEL(NAME, WPL, COMPACT)                                                          \
-    __global__ void __launch_bounds__(256, 2) NAME(const __grid_constant__ SimParams p) {               \
-        if (p.use_smem) simulate_impl<WPL, COMPACT, true>(p);                                          \
-        else simulate_impl<WPL, COMPACT, false>(p);                                                    \
+__global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* ability, const int64_t* efficiency,
+                                                  const int64_t* prio, int32_t policy, SimTaskHdr* hdr, char* adj) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < b.T; t += stride) {
+        const int64_t g = graph_of(b, t);
+        const int64_t t0 = __ldg(&b.task_base[g]);
+        const int64_t v = t - t0;
+        const int32_t* ioff = b.in_off + t0 + g;
+        const int32_t* ooff = b.out_off + t0 + g;
+        const int32_t* soff = b.succ_off + t0 + g;
+        const int32_t i0 = __ldg(&ioff[v]), i1 = __ldg(&ioff[v + 1]);
+        const int32_t o0 = __ldg(&ooff[v]), o1 = __ldg(&ooff[v + 1]);
+        const int32_t s0 = soff[v], s1 = soff[v + 1];  // written by k_ingest
+        const int64_t ib = __ldg(&b.in_base[g]), ob = __ldg(&b.out_base[g]), eb = __ldg(&b.edge_base[g]);
+        const int64_t hb = __ldg(&b.handle_base[g]);
+        // closed-form list offset: 4 bytes of slack per task absorb the
+        // 8-byte alignment of the input-bytes section
+        const int64_t x = 4 * (t0 + v) + 12 * (ib + i0) + 4 * (ob + o0) + 4 * (eb + s0);
+        const int64_t x8 = (x + 7) & ~int64_t(7);
+        const int32_t nin = i1 - i0, nout = o1 - o0, nsucc = s1 - s0;
+        int32_t ka = 0, ke = 0;
+        int64_t kp = prio && policy >= TBSIM_POLICY_DMDAP ? prio[t] : 0;
+        bool bad = nsucc >= (1 << 24);
+        if (policy == TBSIM_POLICY_INSPIRIT) {
+            const int64_t a64 = ability ? ability[t] : 0, e64 = efficiency ? efficiency[t] : 0;
+            ka = static_cast<int32_t>(a64);
+            ke = static_cast<int32_t>(e64);
+            bad = bad || ka != a64 || ke != e64 || ka < 0;
+        }
+        if (bad) ka = -1;
+        int4* h = reinterpret_cast<int4*>(hdr + t);
+        h[0] = make_int4(static_cast<int32_t>(x8 >> 3), nin, nout,
+                         static_cast<int32_t>((static_cast<uint32_t>(__ldg(&b.type[t])) << 24) |
+                                              (static_cast<uint32_t>(nsucc) & 0xffffffu)));
+        h[1] = make_int4(ka, ke, static_cast<int32_t>(static_cast<uint64_t>(kp)),
+                         static_cast<int32_t>(static_cast<uint64_t>(kp) >> 32));
+        int64_t* inb = reinterpret_cast<int64_t*>(adj + x8);
+        int32_t* inh = reinterpret_cast<int32_t*>(inb + nin);
+        const int32_t* in = b.in + ib + i0;
+        for (int32_t k = 0; k < nin; ++k) {
+            const int32_t hd = __ldg(&in[k]);
+            inh[k] = hd;
+            inb[k] = __ldg(&b.handle_bytes[hb + hd]);
+        }
+        int32_t* outl = inh + nin;
+        const int32_t* out = b.out + ob + o0;
+        for (int32_t k = 0; k < nout; ++k) outl[k] = __ldg(&out[k]);
+        int32_t* succl = outl + nout;
+        const int32_t* succ = b.succ + eb + s0;
+        for (int32_t k = 0; k < nsucc; ++k) succl[k] = succ[k];
     }
-TBSIM_SIM_KERNEL(k_simulate_w1c, 1, true)
-TBSIM_SIM_KERNEL(k_simulate_w2c, 2, true)
-TBSIM_SIM_KERNEL(k_simulate_w1, 1, false)
-TBSIM_SIM_KERNEL(k_simulate_w2, 2, false)
+}
+
+__global__ void __launch_bounds__(256) k_sim_scatter(DevBatch b, const SimLog* log, const int32_t* n_disp,
+                                                     int32_t* worker, double* start_ms, double* end_ms) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < b.T; t += stride) {
+        const int64_t g = graph_of(b, t);
+        const int64_t t0 = __ldg(&b.task_base[g]);
+        if (t - t0 >= __ldg(&n_disp[g])) continue;  // -1: written by the simulator
+        const SimLog e = log[t];
+        worker[t0 + e.task] = e.worker;
+        start_ms[t0 + e.task] = e.start;
+        end_ms[t0 + e.task] = e.end;
+    }
+}
+
+#define TBSIM_SIM_KERNEL(NAME, WPL, COMPACT, POL)                                                     \
+    __global__ void __launch_bounds__(256, 2) NAME(const __grid_constant__ SimParams p) {               \
+        if (p.use_smem) simulate_impl<WPL, COMPACT, POL, true>(p);                                     \
+        else simulate_impl<WPL, COMPACT, POL, false>(p);                                               \
+    }
+TBSIM_SIM_KERNEL(k_simulate_w1c, 1, true, -1)
+TBSIM_SIM_KERNEL(k_simulate_w2c, 2, true, -1)
+TBSIM_SIM_KERNEL(k_simulate_w1, 1, false, -1)
+TBSIM_SIM_KERNEL(k_simulate_w2, 2, false, -1)
 #undef TBSIM_SIM_KERNEL
 
 }  // namespace tbsim_dev

@@ -39,6 +39,36 @@ __host__ __device__ inline SimLayout sim_layout(int64_t max_n, int64_t max_h, in
     return L;
 }
 
+// Per-task record of the packed simulation graph (k_sim_pack): everything a
+// push, dispatch or completion reads about one task in one 32-byte sector,
+// plus a byte offset (in 8-byte units) to the task's contiguous lists
+//   [input bytes: int64 x nin][input handles: int32 x nin][outputs: int32 x nout][successors: int32 x nsucc]
+// The CSR sections of the batch are scattered over ten arrays; packed, a task
+// touches ~3 consecutive sectors instead of ~25 scattered ones.
+struct alignas(16) SimTaskHdr {
+    uint32_t adj8;      // list offset / 8 from the adjacency base
+    uint32_t nin;
+    uint32_t nout;
+    uint32_t nsucc_ty;  // successors (24 bits) | type << 24
+    int32_t ab, ef;     // inspirit pop keys (int32 queue keys; ab < 0: does not fit)
+    int64_t prio;       // static priority
+};
+static_assert(sizeof(SimTaskHdr) == 32, "one sector per task");
+
+// Dispatch log entry: the simulator appends one per dispatch in dispatch
+// order (sequential stores); k_sim_scatter moves them to the per-task output
+// arrays afterwards.
+struct SimLog {
+    int32_t task, worker;
+    double start, end;
+};
+
+// Byte size of the adjacency region for a batch (closed-form per-task
+// offsets: 4 bytes of alignment slack per task).
+__host__ __device__ inline int64_t sim_adj_bytes(int64_t T, int64_t I, int64_t O, int64_t E) {
+    return 4 * T + 12 * I + 4 * O + 4 * E + 16;
+}
+
 struct SimParams {
     DevBatch b;
     const DevPlatform* platforms;
@@ -47,9 +77,10 @@ struct SimParams {
     const tbsim_regulator_cfg* reg;   // [G] or null -> default from median
     const double* median;             // [G] lower-median GPU time (default cfg)
     int32_t median_stride;            // elements between consecutive graphs' medians
-    const int64_t* ability;           // [T] or null
-    const int64_t* efficiency;        // [T] or null
-    const int64_t* prio;              // [T] or null
+    const SimTaskHdr* hdr;            // [T] packed task records (k_sim_pack)
+    const char* adj;                  // packed per-task lists
+    SimLog* log;                      // [T] dispatch log
+    int32_t* n_disp;                  // [G] log length, -1: outputs written directly
     // outputs
     int32_t* worker;
     double* start_ms;
@@ -77,6 +108,13 @@ struct SimParams {
     int64_t n_items;                  // graphs to process (list length or G)
     unsigned long long* work_counter;
 };
+
+// Builds the packed records and lists; one thread per task.
+__global__ void k_sim_pack(DevBatch b, const int64_t* ability, const int64_t* efficiency, const int64_t* prio,
+                           int32_t policy, SimTaskHdr* hdr, char* adj);
+// Moves the dispatch logs into worker/start/end; one thread per log slot.
+__global__ void k_sim_scatter(DevBatch b, const SimLog* log, const int32_t* n_disp, int32_t* worker, double* start_ms,
+                              double* end_ms);
 
 __global__ void k_simulate_w1c(const __grid_constant__ SimParams p);  // <= 32 workers, compact state
 __global__ void k_simulate_w2c(const __grid_constant__ SimParams p);  // <= 64 workers, compact state

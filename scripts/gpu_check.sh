@@ -10,10 +10,10 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 if [ "${PROFILE:-1}" = "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
-     --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
+     --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-c4 > /dev/null 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_simulate -s 1 -c 1 \
-     -o gpurun_out/prof_sim -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_sim.log 2>&1
+     -o gpurun_out/prof_sim -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-c4 > gpurun_out/ncu_sim.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 1 -c 1 \
-     -o gpurun_out/prof_sweep -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_sweep.log 2>&1
+     -o gpurun_out/prof_sweep -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-c4 > gpurun_out/ncu_sweep.log 2>&1
 fi
 ls -la gpurun_out
