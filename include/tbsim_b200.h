@@ -118,6 +118,13 @@ tbsim_status tbsim_ctx_destroy(tbsim_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch.cuda.current_stream()). NULL
  * restores the context's own stream. */
 tbsim_status tbsim_ctx_set_stream(tbsim_ctx* ctx, void* cuda_stream);
+/* Stream for batch uploads (H2D copies + successor ingest).  When set and
+ * different from the compute stream, tbsim_batch_upload returns at once and
+ * every compute call on the batch waits for its copies on the device, so the
+ * next batch's upload overlaps the current batch's kernels.  Freed batch
+ * memory is reused by a later upload only after the compute stream has
+ * finished with it.  NULL: uploads run on the compute stream. */
+tbsim_status tbsim_ctx_set_upload_stream(tbsim_ctx* ctx, void* cuda_stream);
 tbsim_status tbsim_ctx_synchronize(tbsim_ctx* ctx);
 /* Single graphs with at least this many tasks (default 65536) take the
  * large-graph attribute path: ability by the HBM bitset closure, the

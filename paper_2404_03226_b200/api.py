@@ -175,6 +175,11 @@ class Context:
     def set_stream(self, stream_ptr: int | None):
         _check(load().tbsim_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
 
+    def set_upload_stream(self, stream_ptr: int | None):
+        """Run batch uploads on this stream (overlapping the compute stream's
+        kernels); compute calls wait for a batch's copies on the device."""
+        _check(load().tbsim_ctx_set_upload_stream(self.h, C.c_void_p(stream_ptr or 0)))
+
     def synchronize(self):
         _check(load().tbsim_ctx_synchronize(self.h))
 

@@ -106,20 +106,32 @@ struct tbsim_ctx {
     std::map<std::string, DevBuf> bufs;
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
-    std::vector<std::pair<void*, size_t>> batch_pool;  // freed batch allocations for reuse
+    cudaStream_t upload = nullptr;  // batch uploads (null: the compute stream)
+    struct PoolEntry {
+        void* p;
+        size_t bytes;
+        cudaEvent_t freed;  // compute-stream point after the last reader
+    };
+    std::vector<PoolEntry> batch_pool;  // freed batch allocations for reuse
     int64_t large_threshold = 65536;  // single graphs at least this large take the closure path
 
     DevBuf& buf(const std::string& name) { return bufs[name]; }
     void* batch_alloc(size_t bytes, size_t* got) {
         size_t best = batch_pool.size();
         for (size_t i = 0; i < batch_pool.size(); ++i)
-            if (batch_pool[i].second >= bytes && (best == batch_pool.size() || batch_pool[i].second < batch_pool[best].second))
+            if (batch_pool[i].bytes >= bytes && (best == batch_pool.size() || batch_pool[i].bytes < batch_pool[best].bytes))
                 best = i;
         if (best < batch_pool.size()) {
-            void* p = batch_pool[best].first;
-            *got = batch_pool[best].second;
+            const PoolEntry e = batch_pool[best];
             batch_pool.erase(batch_pool.begin() + static_cast<std::ptrdiff_t>(best));
-            return p;
+            // the writer (this stream) waits for the kernels that read the
+            // freed batch on the compute stream
+            if (e.freed) {
+                cuda_check(cudaStreamWaitEvent(stream, e.freed, 0), "cudaStreamWaitEvent(pool)");
+                cudaEventDestroy(e.freed);
+            }
+            *got = e.bytes;
+            return e.p;
         }
         void* p = nullptr;
         cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(batch)");
@@ -171,6 +183,7 @@ struct tbsim_batch {
     std::vector<int64_t> task_id;      // host copy (messages)
     std::vector<std::string> type_names;
     int32_t max_workers_seen = 0;
+    cudaEvent_t ready = nullptr;  // recorded on the upload stream when it is not the compute stream
 };
 
 namespace {
@@ -219,6 +232,22 @@ DevPlatform to_dev_platform(const tbsim_platform_desc& p, int32_t n_types_batch)
     return d;
 }
 
+// Routes a batch upload onto ctx->upload for its duration.
+struct UploadStream {
+    tbsim_ctx* ctx;
+    cudaStream_t saved;
+    explicit UploadStream(tbsim_ctx* c) : ctx(c), saved(c->stream) {
+        if (c->upload) c->stream = c->upload;
+    }
+    ~UploadStream() { ctx->stream = saved; }
+    bool active() const { return ctx->stream != saved; }
+};
+
+// Compute on a batch uploaded on another stream waits for its copies.
+void wait_batch(tbsim_ctx* ctx, const tbsim_batch* b) {
+    if (b && b->ready) cuda_check(cudaStreamWaitEvent(ctx->stream, b->ready, 0), "cudaStreamWaitEvent(batch)");
+}
+
 }  // namespace
 
 extern "C" {
@@ -255,7 +284,11 @@ tbsim_status tbsim_ctx_destroy(tbsim_ctx* ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         for (auto& [k, b] : ctx->bufs) b.release();
-        for (auto& pb : ctx->batch_pool) cudaFree(pb.first);
+        if (ctx->upload) cudaStreamSynchronize(ctx->upload);
+        for (auto& pb : ctx->batch_pool) {
+            cudaFree(pb.p);
+            if (pb.freed) cudaEventDestroy(pb.freed);
+        }
         for (auto& [k, ev] : ctx->events) {
             cudaEventDestroy(ev.first);
             cudaEventDestroy(ev.second);
@@ -268,6 +301,10 @@ tbsim_status tbsim_ctx_destroy(tbsim_ctx* ctx) {
 
 tbsim_status tbsim_ctx_set_stream(tbsim_ctx* ctx, void* s) {
     return guarded([&] { ctx->stream = s ? static_cast<cudaStream_t>(s) : ctx->own; });
+}
+
+tbsim_status tbsim_ctx_set_upload_stream(tbsim_ctx* ctx, void* s) {
+    return guarded([&] { ctx->upload = static_cast<cudaStream_t>(s); });
 }
 
 tbsim_status tbsim_ctx_synchronize(tbsim_ctx* ctx) {
@@ -296,6 +333,8 @@ tbsim_status tbsim_ctx_last_kernel_ms(const tbsim_ctx* ctx, const char* kernel, 
 tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim_batch** out) {
     return guarded([&] {
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        // copies + ingest on the upload stream; compute calls wait on b->ready
+        UploadStream us(ctx);
         const int64_t G = h->n_graphs;
         if (G < 0) raise(TBSIM_E_INVALID_ARGUMENT, "negative graph count");
         auto b = std::make_unique<tbsim_batch>();
@@ -363,6 +402,10 @@ tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim
             k_ingest<<<grid, 256, 0, ctx->stream>>>(d, cursor);
             ctx->end("k_ingest");
         }
+        if (us.active()) {
+            cuda_check(cudaEventCreateWithFlags(&b->ready, cudaEventDisableTiming), "cudaEventCreate");
+            cuda_check(cudaEventRecord(b->ready, ctx->stream), "cudaEventRecord(ready)");
+        }
         *out = b.release();
     });
 }
@@ -371,14 +414,22 @@ tbsim_status tbsim_batch_free(tbsim_ctx* ctx, tbsim_batch* b) {
     return guarded([&] {
         if (!b) return;
         if (ctx) {
-            // stream-ordered reuse: later uploads on this stream run after
-            // every kernel that reads this batch
-            if (b->mem) ctx->batch_pool.push_back({b->mem, b->mem_bytes});
-            if (b->mem2) ctx->batch_pool.push_back({b->mem2, b->mem2_bytes});
+            // stream-ordered reuse: a later upload waits for every kernel
+            // that reads this batch (all on the compute stream)
+            for (auto [m, bytes] : {std::make_pair(b->mem, b->mem_bytes), std::make_pair(b->mem2, b->mem2_bytes)}) {
+                if (!m) continue;
+                cudaEvent_t ev = nullptr;
+                if (ctx->upload && ctx->upload != ctx->stream) {
+                    cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+                    cuda_check(cudaEventRecord(ev, ctx->stream), "cudaEventRecord(freed)");
+                }
+                ctx->batch_pool.push_back({m, bytes, ev});
+            }
         } else {
             if (b->mem) cudaFree(b->mem);
             if (b->mem2) cudaFree(b->mem2);
         }
+        if (b->ready) cudaEventDestroy(b->ready);
         delete b;
     });
 }
@@ -393,6 +444,7 @@ tbsim_status tbsim_batch_sizes(const tbsim_batch* b, int64_t* s) {
 
 tbsim_status tbsim_batch_download(tbsim_ctx* ctx, const tbsim_batch* b, tbsim_batch_desc* h) {
     return guarded([&] {
+        wait_batch(ctx, b);
         const DevBatch& d = b->d;
         const int64_t G = d.G, T = d.T;
         auto cp = [&](const void* dst, const void* src, size_t bytes) {
@@ -711,6 +763,7 @@ extern "C" tbsim_status tbsim_attributes(tbsim_ctx* ctx, const tbsim_batch* b, c
                                          int32_t request, int32_t priority_kind, tbsim_attr_out* out) {
     return guarded([&] {
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        wait_batch(ctx, b);
         const DevBatch& d = b->d;
         const int64_t T = d.T, G = d.G;
         const bool dev = out->on_device != 0;
@@ -991,6 +1044,7 @@ extern "C" tbsim_status tbsim_simulate(tbsim_ctx* ctx, const tbsim_batch* b, con
                                        const tbsim_regulator_cfg* reg, const tbsim_attr_in* attrs, tbsim_sim_out* out) {
     return guarded([&] {
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        wait_batch(ctx, b);
         if (policy < 0 || policy > TBSIM_POLICY_INSPIRIT) raise(TBSIM_E_RUNTIME, "unknown policy id");
         const DevBatch& d = b->d;
         const int64_t T = d.T, G = d.G;
@@ -1075,6 +1129,7 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
                                        int32_t priority_kind, tbsim_attr_out* attr_out, tbsim_sim_out* out) {
     return guarded([&] {
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        wait_batch(ctx, b);
         if (policy < 0 || policy > TBSIM_POLICY_INSPIRIT) raise(TBSIM_E_RUNTIME, "unknown policy id");
         const DevBatch& d = b->d;
         const int64_t T = d.T, G = d.G;

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(HERE, "libtbsim_b200.so")
 # Every symbol the header declares (tests check the .so exports all of them).
 EXPORTS = [
     "tbsim_last_error", "tbsim_abi_version",
-    "tbsim_ctx_create", "tbsim_ctx_destroy", "tbsim_ctx_set_stream", "tbsim_ctx_synchronize",
+    "tbsim_ctx_create", "tbsim_ctx_destroy", "tbsim_ctx_set_stream", "tbsim_ctx_set_upload_stream", "tbsim_ctx_synchronize",
     "tbsim_ctx_launch_count", "tbsim_ctx_set_timing", "tbsim_ctx_last_kernel_ms",
     "tbsim_ctx_set_large_graph_threshold",
     "tbsim_batch_upload", "tbsim_batch_free", "tbsim_batch_h2d_bytes", "tbsim_batch_generate_layered",
@@ -51,6 +51,7 @@ def load():
     L.tbsim_ctx_create.argtypes = [C.c_int, P(vp)]
     L.tbsim_ctx_destroy.argtypes = [vp]
     L.tbsim_ctx_set_stream.argtypes = [vp, vp]
+    L.tbsim_ctx_set_upload_stream.argtypes = [vp, vp]
     L.tbsim_ctx_synchronize.argtypes = [vp]
     L.tbsim_ctx_launch_count.argtypes = [vp]
     L.tbsim_ctx_launch_count.restype = i64

@@ -281,3 +281,29 @@ def test_device_generated_batch_schedules_like_host_batch(ctx):
     b = ctx.schedule(ctx.upload(api.HostBatch().add_layered(1000, 10, 0.05, seeds)), pl, "inspirit")
     for k in ("worker", "start_ms", "end_ms", "makespan_ms", "attr_efficiency", "attr_ability"):
         eq(a[k], b[k], k)
+
+
+def test_upload_stream_pipeline_matches_serial(ctx):
+    """Uploads on a second stream (step k+1's copies overlapping step k's
+    kernels, freed batch memory recycled through the pool) give the same
+    schedules as serial upload-then-compute."""
+    import torch
+    pl = [P.assemble("8c2g", 8, 2)]
+    batches = [api.HostBatch().add_layered(600 + 37 * i, 6 + i, 0.04 + 0.01 * i, np.arange(50 * i, 50 * i + 64))
+               for i in range(4)]
+    serial = [ctx.schedule(ctx.upload(hb), pl, "inspirit") for hb in batches]
+    up = torch.cuda.Stream()
+    ctx.set_upload_stream(up.cuda_stream)
+    try:
+        for _ in range(2):  # second pass reuses pooled batch memory
+            nxt = ctx.upload(batches[0])
+            for i in range(len(batches)):
+                cur = nxt
+                if i + 1 < len(batches):
+                    nxt = ctx.upload(batches[i + 1])
+                got = ctx.schedule(cur, pl, "inspirit")
+                cur.free()
+                for k in ("worker", "start_ms", "end_ms", "makespan_ms", "attr_efficiency", "attr_ability"):
+                    eq(got[k], serial[i][k], f"{k} batch {i}")
+    finally:
+        ctx.set_upload_stream(None)
