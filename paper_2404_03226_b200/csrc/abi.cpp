@@ -604,6 +604,7 @@ AttrScratch alloc_attr_scratch(tbsim_ctx* ctx, const DevBatch& d) {
     s.median = ctx->buf("a_median").as<double>(G);
     s.tile_base = ctx->buf("a_tilebase").as<int64_t>(G + 1);
     s.tile_s = ctx->buf("a_tiles").as<int32_t>(G);
+    s.tile_graph = ctx->buf("a_tilegraph").as<int32_t>(T / 8 + G + 1);
     s.opos = ctx->buf("a_opos").as<int32_t>(T);
     s.firstuse = ctx->buf("a_firstuse").as<int32_t>(T);
     s.rslot = ctx->buf("a_rslot").as<int32_t>(T);

@@ -430,28 +430,37 @@ __device__ __forceinline__ int bin_t(double d, const Thresholds& th) {
     }
 }
 
-// Flush 8-bit per-lane bin counters into the CTA's 21-bit accumulators.
-__device__ __forceinline__ void flush8(uint32_t (&h)[3], unsigned long long* dst) {
-    uint64_t h21[4] = {0, 0, 0, 0};
+// Per-lane window-bin counters: 12 fields of 5 bits in one u64 per source.
+// A pair that is not counted shifts by 64, which PTX defines as 0 (no
+// select on the increment).  Flushed into per-bin u32 shared counters
+// (native ATOMS.ADD; the 64-bit shared atomic is a CAS loop) every 31 visits.
+constexpr int kFieldBits = 5;
+constexpr int kFlushEvery = (1 << kFieldBits) - 1;
+
+__device__ __forceinline__ uint64_t shl64(uint64_t x, uint32_t sh) {
+    uint64_t r;
+    asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(sh));
+    return r;
+}
+
+__device__ __forceinline__ void flush5(uint64_t& h, uint32_t* dst) {
 #pragma unroll
     for (int bn = 0; bn < kBins; ++bn) {
-        const uint64_t c = (h[bn >> 2] >> (8 * (bn & 3))) & 0xffu;
-        h21[bn / 3] += c << (21 * (bn % 3));
+        const uint32_t c = static_cast<uint32_t>(h >> (kFieldBits * bn)) & kFlushEvery;
+        if (c) atomicAdd(&dst[bn], c);
     }
-#pragma unroll
-    for (int w = 0; w < 4; ++w)
-        if (h21[w]) atomicAdd(&dst[w], static_cast<unsigned long long>(h21[w]));
-    h[0] = h[1] = h[2] = 0;
+    h = 0;
 }
 
 // Group of GL lanes handles one node for S sources (S/GL per lane).  Node
 // records are read in level order (order-major arrays); the sources' distance
-// columns live in shared memory, win[slot][S].  Window bins are counted in
-// 8-bit fields (three u32 per source) and flushed every 255 node visits.
+// columns live in shared memory, win[slot][S], with each lane's pairs of
+// sources interleaved across the group so every double2 access is contiguous
+// over the lanes (conflict-free 128-bit LDS/STS).
 template <int S, bool SMEM, int TMODE>
 __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                            double* gwin, int32_t P, const Thresholds& th,
-                                           unsigned long long* s_hist, int32_t prune_span) {
+                                           uint32_t* s_hist, int32_t prune_span) {
     extern __shared__ double win_smem[];
     double* win = SMEM ? win_smem : gwin;
     constexpr int GL = S < 32 ? S : 32;   // lanes per node group
@@ -472,14 +481,18 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     const int32_t first = tile * S;
     const int32_t nsrc = min(S, gi.processed - first);
 
-    for (int64_t i = threadIdx.x; i < static_cast<int64_t>(P) * S; i += blockDim.x) win[i] = -1.0;
-    for (int i = threadIdx.x; i < S * 4; i += blockDim.x) s_hist[i] = 0ull;
-    uint32_t hist[SPL][3];
+    {
+        double2* w2 = reinterpret_cast<double2*>(win);
+        const double2 neg = make_double2(-1.0, -1.0);
+        for (int64_t i = threadIdx.x; i < static_cast<int64_t>(P) * (S / 2); i += blockDim.x) w2[i] = neg;
+    }
+    for (int i = threadIdx.x; i < S * kBins; i += blockDim.x) s_hist[i] = 0u;
+    uint64_t hist[SPL];
 #pragma unroll
-    for (int q = 0; q < SPL; ++q) hist[q][0] = hist[q][1] = hist[q][2] = 0;
+    for (int q = 0; q < SPL; ++q) hist[q] = 0;
     int32_t visits = 0;  // node visits since the last flush (uniform per group)
     const int32_t La = s.level[t0 + s.order[t0 + first]];
-    const int32_t my_first = first + gl * SPL;  // order position of this lane's first source
+    auto src = [&](int q) { return SPL >= 2 ? (q >> 1) * 2 * GL + 2 * gl + (q & 1) : gl; };
     // Pruning (large graphs, ability computed elsewhere): distances only grow
     // along paths, so once no distance within the largest window was written
     // in the last `prune_span` levels (the longest edge span), no later node
@@ -501,52 +514,55 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
             double m[SPL];
 #pragma unroll
             for (int q = 0; q < SPL; ++q) m[q] = -1.0;
+            // plain compare-select: operands are -1 or non-negative, never NaN
+            auto relax = [&](int32_t ps) {
+                const double* row = win + ps * S;
+                if constexpr (SPL >= 2) {
+#pragma unroll
+                    for (int q = 0; q < SPL; q += 2) {
+                        const double2 x = *reinterpret_cast<const double2*>(row + src(q));
+                        m[q] = x.x > m[q] ? x.x : m[q];
+                        m[q + 1] = x.y > m[q + 1] ? x.y : m[q + 1];
+                    }
+                } else {
+                    const double x = row[gl];
+                    m[0] = x > m[0] ? x : m[0];
+                }
+            };
             for (int32_t c = 0; c < deg; c += GL) {
                 const int32_t myps = (c + gl < deg) ? __ldg(&om_ps[p0 + c + gl]) : 0;
                 const int32_t lim = min(GL, deg - c);
-                for (int32_t j = 0; j < lim; ++j) {
-                    const int32_t ps = __shfl_sync(gmask, myps, grp * GL + j);
-                    const double* row = win + ps * S + gl * SPL;
-                    // plain compare-select: operands are -1 or non-negative, never NaN
-                    if constexpr (SPL >= 2) {
-#pragma unroll
-                        for (int q = 0; q < SPL; q += 2) {
-                            const double2 x = *reinterpret_cast<const double2*>(row + q);
-                            m[q] = x.x > m[q] ? x.x : m[q];
-                            m[q + 1] = x.y > m[q + 1] ? x.y : m[q + 1];
-                        }
-                    } else {
-                        const double x = row[0];
-                        m[0] = x > m[0] ? x : m[0];
-                    }
+                int32_t j = 0;
+                for (; j + 2 <= lim; j += 2) {  // two predecessors in flight
+                    const int32_t ps0 = __shfl_sync(gmask, myps, grp * GL + j);
+                    const int32_t ps1 = __shfl_sync(gmask, myps, grp * GL + j + 1);
+                    relax(ps0);
+                    relax(ps1);
                 }
+                if (j < lim) relax(__shfl_sync(gmask, myps, grp * GL + j));
             }
             double d[SPL];
 #pragma unroll
             for (int q = 0; q < SPL; ++q) {
-                const bool is_src = i == my_first + q;
+                const bool is_src = i == first + src(q);
                 const double reach = m[q] + gv;
                 const bool counted = !is_src && m[q] >= 0.0;
                 d[q] = is_src ? 0.0 : (m[q] < 0.0 ? -1.0 : reach);
                 const int bn = bin_t<TMODE>(reach, th);
-                const uint32_t inc = counted ? 1u << (8 * (bn & 3)) : 0u;
-                const int w = bn >> 2;
-                hist[q][0] += w == 0 ? inc : 0u;
-                hist[q][1] += w == 1 ? inc : 0u;
-                hist[q][2] += w == 2 ? inc : 0u;
+                hist[q] += shl64(1ull, counted ? static_cast<uint32_t>(kFieldBits * bn) : 64u);
                 small |= d[q] >= 0.0 && d[q] <= wmax;
             }
-            double* outp = win + sl * S + gl * SPL;
+            double* outp = win + sl * S;
             if constexpr (SPL >= 2) {
 #pragma unroll
-                for (int q = 0; q < SPL; q += 2) *reinterpret_cast<double2*>(outp + q) = make_double2(d[q], d[q + 1]);
+                for (int q = 0; q < SPL; q += 2) *reinterpret_cast<double2*>(outp + src(q)) = make_double2(d[q], d[q + 1]);
             } else {
-                outp[0] = d[0];
+                outp[gl] = d[0];
             }
-            if (++visits == 255) {
+            if (++visits == kFlushEvery) {
 #pragma unroll
                 for (int q = 0; q < SPL; ++q)
-                    if (gl * SPL + q < nsrc) flush8(hist[q], s_hist + (gl * SPL + q) * 4);
+                    if (src(q) < nsrc) flush5(hist[q], s_hist + src(q) * kBins);
                 visits = 0;
             }
         }
@@ -559,17 +575,21 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     }
 #pragma unroll
     for (int q = 0; q < SPL; ++q)
-        if (gl * SPL + q < nsrc) flush8(hist[q], s_hist + (gl * SPL + q) * 4);
+        if (src(q) < nsrc) flush5(hist[q], s_hist + src(q) * kBins);
     __syncthreads();
+    // per source: 12 bins as 21-bit fields in four words (k_finalize)
     const int32_t* order = s.order + t0;
-    for (int i = threadIdx.x; i < nsrc * 4; i += blockDim.x)
-        s.hist[(t0 + order[first + i / 4]) * 4 + (i & 3)] = s_hist[i];
+    for (int i = threadIdx.x; i < nsrc * 4; i += blockDim.x) {
+        const uint32_t* c = s_hist + (i >> 2) * kBins + 3 * (i & 3);
+        s.hist[(t0 + order[first + (i >> 2)]) * 4 + (i & 3)] =
+            static_cast<uint64_t>(c[0]) | (static_cast<uint64_t>(c[1]) << 21) | (static_cast<uint64_t>(c[2]) << 42);
+    }
 }
 
 template <int S, bool SMEM>
 __device__ __forceinline__ void sweep_tile_mode(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                                 double* gwin, int32_t P, const Thresholds& th,
-                                                unsigned long long* s_hist, int32_t prune_span) {
+                                                uint32_t* s_hist, int32_t prune_span) {
     if (th.mode == 0) sweep_tile<S, SMEM, 0>(b, s, g, tile, gwin, P, th, s_hist, prune_span);
     else if (th.mode == 2) sweep_tile<S, SMEM, 2>(b, s, g, tile, gwin, P, th, s_hist, 0);
     else sweep_tile<S, SMEM, 1>(b, s, g, tile, gwin, P, th, s_hist, prune_span);
@@ -581,51 +601,48 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
                                               int64_t total_tiles, unsigned long long* work_counter,
                                               int64_t smem_bytes, double* gwin, int64_t gwin_stride,
                                               int32_t prune) {
-    __shared__ int64_t s_item;
-    __shared__ unsigned long long s_hist[128 * 4];
+    __shared__ int64_t s_item[2];
+    __shared__ uint32_t s_hist[128 * kBins];
     (void)costs_g;
     (void)cost_idx;
     if (total_tiles < 0) total_tiles = s.tile_base[b.G];
-    for (;;) {
-        if (threadIdx.x == 0) s_item = atomicAdd(work_counter, 1ull);
-        __syncthreads();
-        const int64_t item = s_item;
-        __syncthreads();
+    if (threadIdx.x == 0) s_item[0] = atomicAdd(work_counter, 1ull);
+    __syncthreads();
+    for (int k = 0;; k ^= 1) {
+        const int64_t item = s_item[k];
         if (item >= total_tiles) break;
-        // locate graph: tile_base is [G+1] prefix of tiles per graph
-        int64_t lo = 0, hi = b.G;
-        while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (s.tile_base[mid] <= item) lo = mid; else hi = mid;
-        }
-        const int64_t g = lo;
+        // the next item is claimed while this tile runs
+        if (threadIdx.x == 0) s_item[k ^ 1] = atomicAdd(work_counter, 1ull);
+        const int64_t g = s.tile_graph[item];
         const int32_t tile = static_cast<int32_t>(item - s.tile_base[g]);
         const GraphInfo gi = s.info[g];
-        if (gi.processed != static_cast<int32_t>(b.task_base[g + 1] - b.task_base[g])) continue;  // cyclic
-        const int32_t P = max(gi.peak_slots, 1);
-        Thresholds th;
-        if (sweep_mode == SWEEP_SINGLE) th = make_thresholds(SWEEP_SINGLE, unit_time[g]);
-        else th = make_thresholds(sweep_mode, 2.0 * gi.median);
-        const int32_t S = s.tile_s[g];
-        double* gw = gwin + blockIdx.x * gwin_stride;
-        // prune only when the edge span fits the 64-level history
-        const int32_t prune_span = (prune && gi.max_span > 0 && gi.max_span < 64) ? gi.max_span : 0;
-        if (static_cast<int64_t>(P) * S * 8 > smem_bytes) {
-            sweep_tile_mode<32, false>(b, s, g, tile, gw, P, th, s_hist, prune_span);
-        } else {
-            switch (S) {
-                case 128: sweep_tile_mode<128, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
-                case 64: sweep_tile_mode<64, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
-                case 32: sweep_tile_mode<32, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
-                case 16: sweep_tile_mode<16, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
-                default: sweep_tile_mode<8, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+        if (gi.processed == static_cast<int32_t>(b.task_base[g + 1] - b.task_base[g])) {  // else cyclic
+            const int32_t P = max(gi.peak_slots, 1);
+            Thresholds th;
+            if (sweep_mode == SWEEP_SINGLE) th = make_thresholds(SWEEP_SINGLE, unit_time[g]);
+            else th = make_thresholds(sweep_mode, 2.0 * gi.median);
+            const int32_t S = s.tile_s[g];
+            double* gw = gwin + blockIdx.x * gwin_stride;
+            // prune only when the edge span fits the 64-level history
+            const int32_t prune_span = (prune && gi.max_span > 0 && gi.max_span < 64) ? gi.max_span : 0;
+            if (static_cast<int64_t>(P) * S * 8 > smem_bytes) {
+                sweep_tile_mode<32, false>(b, s, g, tile, gw, P, th, s_hist, prune_span);
+            } else {
+                switch (S) {
+                    case 128: sweep_tile_mode<128, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+                    case 64: sweep_tile_mode<64, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+                    case 32: sweep_tile_mode<32, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+                    case 16: sweep_tile_mode<16, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+                    default: sweep_tile_mode<8, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+                }
             }
         }
         __syncthreads();
     }
 }
 
-// Tiles per graph and their prefix (single CTA; G can be large).
+// Tiles per graph, their prefix and the tile -> graph map (single CTA; G can
+// be large).
 __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s) {
     __shared__ int32_t warp_tot[32];
     __shared__ int64_t carry;
@@ -650,10 +667,18 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
         }
         int32_t tot;
         const int32_t inc = block_inclusive_scan(tiles, warp_tot, &tot);
-        if (g < b.G) s.tile_base[g] = carry + inc - tiles;
+        const int64_t tb = carry + inc - tiles;
+        if (g < b.G) s.tile_base[g] = tb;
         __syncthreads();
         if (threadIdx.x == 0) carry += tot;
         __syncthreads();
+        // tile -> graph: a warp per graph of this chunk, lanes over its tiles
+        const int lane = threadIdx.x & 31;
+        for (int64_t gg = base + (threadIdx.x >> 5); gg < b.G && gg < base + static_cast<int64_t>(blockDim.x); gg += blockDim.x >> 5) {
+            const int64_t t_begin = s.tile_base[gg];
+            const int32_t nt = (s.info[gg].processed + s.tile_s[gg] - 1) / s.tile_s[gg];
+            for (int32_t t = lane; t < nt; t += 32) s.tile_graph[t_begin + t] = static_cast<int32_t>(gg);
+        }
     }
     if (threadIdx.x == 0) s.tile_base[b.G] = carry;
 }

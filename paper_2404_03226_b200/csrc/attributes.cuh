@@ -53,6 +53,7 @@ struct AttrScratch {
     double* median;      // [G] lower-median GPU time (regulator defaults)
     int64_t* tile_base;  // [G+1]
     int32_t* tile_s;     // [G]
+    int32_t* tile_graph; // [tiles] graph of each sweep tile (<= T/8 + G)
 };
 
 struct AttrOutDev {
