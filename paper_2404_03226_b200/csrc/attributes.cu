@@ -26,6 +26,7 @@
 //                fractions (attributes.cpp:205-217), the strict-> winner, and the
 //                per-task efficiency / ability.
 #include <cooperative_groups.h>
+#include <math_constants.h>
 
 #include <cfloat>
 #include <cstdint>
@@ -416,10 +417,11 @@ __device__ Thresholds make_thresholds(int32_t mode_req, double w0_or_unit) {
 template <int TMODE>
 __device__ __forceinline__ int bin_t(double d, const Thresholds& th) {
     if constexpr (TMODE == 0) {
+        // first k with d <= W_k: ceil(delta / 2^52) clamped to [0, 11]
+        // (arithmetic shift; no overflow for any double incl. -inf, +inf)
         const int64_t delta = __double_as_longlong(d) - th.w0bits;
-        if (delta <= 0) return 0;
-        const int k = static_cast<int>(static_cast<uint64_t>(delta - 1) >> 52) + 1;
-        return k > kWindows ? kWindows : k;
+        const int k = static_cast<int>((delta + ((int64_t(1) << 52) - 1)) >> 52);
+        return min(max(k, 0), kWindows);
     } else if constexpr (TMODE == 2) {
         return kWindows;
     } else {
@@ -483,7 +485,7 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
 
     {
         double2* w2 = reinterpret_cast<double2*>(win);
-        const double2 neg = make_double2(-1.0, -1.0);
+        const double2 neg = make_double2(-CUDART_INF, -CUDART_INF);  // unreachable
         for (int64_t i = threadIdx.x; i < static_cast<int64_t>(P) * (S / 2); i += blockDim.x) w2[i] = neg;
     }
     for (int i = threadIdx.x; i < S * kBins; i += blockDim.x) s_hist[i] = 0u;
@@ -513,8 +515,8 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
             const int32_t sl = __ldg(&om_slot[i]);
             double m[SPL];
 #pragma unroll
-            for (int q = 0; q < SPL; ++q) m[q] = -1.0;
-            // plain compare-select: operands are -1 or non-negative, never NaN
+            for (int q = 0; q < SPL; ++q) m[q] = -CUDART_INF;
+            // plain compare-select: operands are -inf or non-negative, never NaN
             auto relax = [&](int32_t ps) {
                 const double* row = win + ps * S;
                 if constexpr (SPL >= 2) {
@@ -529,9 +531,7 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
                     m[0] = x > m[0] ? x : m[0];
                 }
             };
-            for (int32_t c = 0; c < deg; c += GL) {
-                const int32_t myps = (c + gl < deg) ? __ldg(&om_ps[p0 + c + gl]) : 0;
-                const int32_t lim = min(GL, deg - c);
+            auto relax_chunk = [&](int32_t myps, int32_t lim) {
                 int32_t j = 0;
                 for (; j + 2 <= lim; j += 2) {  // two predecessors in flight
                     const int32_t ps0 = __shfl_sync(gmask, myps, grp * GL + j);
@@ -540,17 +540,34 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
                     relax(ps1);
                 }
                 if (j < lim) relax(__shfl_sync(gmask, myps, grp * GL + j));
+            };
+            if (deg <= GL) {  // the common case: one chunk of predecessors
+                relax_chunk(gl < deg ? __ldg(&om_ps[p0 + gl]) : 0, deg);
+            } else {
+                for (int32_t c = 0; c < deg; c += GL)
+                    relax_chunk((c + gl < deg) ? __ldg(&om_ps[p0 + c + gl]) : 0, min(GL, deg - c));
             }
+            // unreachable stays -inf (-inf + gv); reachable distances are >= 0
             double d[SPL];
+            const bool node_is_src = static_cast<uint32_t>(i - first) < static_cast<uint32_t>(S);
 #pragma unroll
             for (int q = 0; q < SPL; ++q) {
-                const bool is_src = i == first + src(q);
-                const double reach = m[q] + gv;
-                const bool counted = !is_src && m[q] >= 0.0;
-                d[q] = is_src ? 0.0 : (m[q] < 0.0 ? -1.0 : reach);
-                const int bn = bin_t<TMODE>(reach, th);
+                d[q] = m[q] + gv;
+                const bool counted = d[q] >= 0.0;
+                const int bn = bin_t<TMODE>(d[q], th);
                 hist[q] += shl64(1ull, counted ? static_cast<uint32_t>(kFieldBits * bn) : 64u);
-                small |= d[q] >= 0.0 && d[q] <= wmax;
+            }
+            if (node_is_src) {  // the source itself: distance 0, not its own descendant
+#pragma unroll
+                for (int q = 0; q < SPL; ++q)
+                    if (i == first + src(q)) {
+                        if (d[q] >= 0.0) hist[q] -= shl64(1ull, static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d[q], th)));
+                        d[q] = 0.0;
+                    }
+            }
+            if (prune_span > 0) {
+#pragma unroll
+                for (int q = 0; q < SPL; ++q) small |= d[q] >= 0.0 && d[q] <= wmax;
             }
             double* outp = win + sl * S;
             if constexpr (SPL >= 2) {
