@@ -145,6 +145,7 @@ struct Sim {
             // in-order sum; the shuffles are independent and issued ahead
             double acc = 0.0;
             int32_t j = 0;
+#pragma unroll 1
             for (; j + 4 <= nin; j += 4) {
                 const double a0 = __shfl_sync(kFull, t, base + j), a1 = __shfl_sync(kFull, t, base + j + 1);
                 const double a2 = __shfl_sync(kFull, t, base + j + 2), a3 = __shfl_sync(kFull, t, base + j + 3);
@@ -153,6 +154,7 @@ struct Sim {
                 acc += a2;
                 acc += a3;
             }
+#pragma unroll 1
             for (; j < nin; ++j) acc += __shfl_sync(kFull, t, base + j);
             const int32_t rw = __popc(want_nodes & ((1u << want) - 1u));
             return __shfl_sync(kFull, acc, rw * nin);
@@ -165,6 +167,7 @@ struct Sim {
                 const int32_t cnt = min(32, nin - base);
                 double t = 0.0;
                 if (lane < cnt) t = transfer_one(resid[__ldg(&inh[base + lane])], __ldg(&inb[base + lane]), to);
+#pragma unroll 1
                 for (int32_t j = 0; j < cnt; ++j) acc += __shfl_sync(kFull, t, j);
             }
             if (want == to) mine = acc;
