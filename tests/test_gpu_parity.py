@@ -96,6 +96,38 @@ def test_random_graphs_all_policies_platform_mix(ctx):
             eq(g[k], o[k], f"{pol}/{k}")
 
 
+def odd_platform(name, bw_rows, latency=0.02):
+    """4 CPUs on node 0, one GPU per further node, custom bandwidths."""
+    nn = len(bw_rows)
+    workers = [(0, 0)] * 4 + [(1, k) for k in range(1, nn)]
+    return P.Platform(name, workers, P.default_cost_table(), nn, latency, bw_rows)
+
+
+def test_transfers_on_custom_bandwidth_matrices(ctx):
+    """Fastest-copy transfers (engine.cpp:86-110) on asymmetric bandwidth
+    matrices with 1..5 distinct values and a zero bandwidth, alone and mixed
+    in one batch, give the reference's schedules."""
+    b = random_graphs(11, 30)
+    two = [[0, 7e6, 9e6], [7e6, 0, 9e6], [9e6, 9e6, 0]]
+    one = [[0, 5e6], [5e6, 0]]
+    three = [[0, 3e6, 5e6, 7e6], [3e6, 0, 7e6, 5e6], [5e6, 7e6, 0, 3e6], [7e6, 5e6, 3e6, 0]]
+    five = [[0, 1e6, 2e6, 3e6], [1e6, 0, 4e6, 5e6], [2e6, 4e6, 0, 5e6], [3e6, 5e6, 4e6, 0]]
+    zero = [[0, 0.0, 9e6], [6e6, 0, 9e6], [9e6, 9e6, 0]]
+    costs = P.default_cost_table()
+    oa = po.attributes(b, costs, abi.ATTR_ALL)
+    db = ctx.upload(b)
+    for pls in ([odd_platform("one", one)], [odd_platform("two", two)], [odd_platform("three", three)],
+                [odd_platform("five", five)], [odd_platform("zero", zero)],
+                [odd_platform("two", two), odd_platform("five", five), odd_platform("three", three)]):
+        pof = np.arange(b.n_graphs) % len(pls)
+        reg = [po.default_regulator_config(b, g, pls[pof[g]]) for g in range(b.n_graphs)]
+        for pol in ("dmda", "inspirit"):
+            g = ctx.simulate(db, pls, pol, reg, platform_of=pof, attrs=oa, record=True)
+            o = po.simulate(b, pls, pol, platform_of=pof, reg=reg, attrs=oa, record=True)
+            for k in SIM_KEYS:
+                eq(g[k], o[k], f"{[p.name for p in pls]}/{pol}/{k}")
+
+
 def test_schedule_pipeline_matches_oracle(ctx):
     hb = api.HostBatch().add_cholesky(10, 960 * 960 * 4).add_layered(1000, 10, 0.05, [3, 4, 5])
     hb.add_lu(12, 160 * 160 * 4).add_qr(10, 160 * 160 * 4)
