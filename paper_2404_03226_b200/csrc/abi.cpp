@@ -632,9 +632,28 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
     // pruned at the largest window.  Batches: ability inside the sweep.
     const bool large = G == 1 && d.max_n >= ctx->large_threshold && do_sweep;
     const int grid_g = static_cast<int>(std::min<int64_t>(G, 4LL * ctx->n_sms));
-    ctx->begin("k_structure");
-    k_structure<<<grid_g, 512, 0, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, want_rank ? 1 : 0, large ? 1 : 0);
-    ctx->end("k_structure");
+    if (G == 1 && d.max_n >= ctx->large_threshold) {
+        // one large graph: the structure pass with the whole GPU
+        static int per_sm = 0;
+        if (!per_sm)
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_structure_large, 512, 0), "occupancy");
+        const int grid = std::max(1, std::min(per_sm, 2)) * ctx->n_sms;
+        const size_t ctl_bytes = sizeof(LargeCtl) + 4 * static_cast<size_t>(grid);
+        LargeCtl* ctl = static_cast<LargeCtl*>(ctx->buf("a_large_ctl").get(ctl_bytes));
+        cuda_check(cudaMemsetAsync(ctl, 0, ctl_bytes, ctx->stream), "memset");
+        DevBatch dv = d;
+        AttrScratch sv = run.s;
+        int32_t wr = want_rank ? 1 : 0;
+        void* args[] = {&dv, const_cast<DevCosts**>(&d_costs), const_cast<int32_t**>(&d_cost_idx), &sv, &wr, &ctl};
+        ctx->begin("k_structure");
+        cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_structure_large), grid, 512, args, 0, ctx->stream),
+                   "cudaLaunchCooperativeKernel(k_structure_large)");
+        ctx->end("k_structure");
+    } else {
+        ctx->begin("k_structure");
+        k_structure<<<grid_g, 512, 0, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, want_rank ? 1 : 0, large ? 1 : 0);
+        ctx->end("k_structure");
+    }
     bool ability_done = false;
     if (large && o.ability) {
         GraphInfo gi;
@@ -690,10 +709,30 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         ctx->end("k_sweep");
         const int64_t cls_stride = static_cast<int64_t>(d.max_n) * (3 * kWindows + 1) + 16;
         int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride * grid_g);
-        ctx->begin("k_finalize");
-        k_finalize<<<grid_g, 256, 0, ctx->stream>>>(d, run.s, sweep_mode, d_unit_time, o, cls_scratch, cls_stride,
-                                                    (large || ability_done) ? 0 : 1);
-        ctx->end("k_finalize");
+        const int32_t write_ab = (large || ability_done) ? 0 : 1;
+        if (G == 1 && d.max_n >= ctx->large_threshold) {
+            static int per_sm = 0;
+            if (!per_sm)
+                cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_finalize_large, 512, 0), "occupancy");
+            const int grid = std::max(1, std::min(per_sm, 2)) * ctx->n_sms;
+            int64_t tab_cap = 1;
+            while (tab_cap < 2 * static_cast<int64_t>(d.max_n)) tab_cap <<= 1;
+            int32_t* tab = ctx->buf("a_fin_tab").as<int32_t>(tab_cap * kWindows);
+            int32_t* score = ctx->buf("a_fin_score").as<int32_t>(kWindows);
+            DevBatch dv = d;
+            AttrScratch sv = run.s;
+            int32_t sm = sweep_mode, wa = write_ab;
+            void* args[] = {&dv, &sv, &sm, &o, &cls_scratch, &tab, &tab_cap, &score, &wa};
+            ctx->begin("k_finalize");
+            cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_finalize_large), grid, 512, args, 0, ctx->stream),
+                       "cudaLaunchCooperativeKernel(k_finalize_large)");
+            ctx->end("k_finalize");
+        } else {
+            ctx->begin("k_finalize");
+            k_finalize<<<grid_g, 256, 0, ctx->stream>>>(d, run.s, sweep_mode, d_unit_time, o, cls_scratch, cls_stride,
+                                                        write_ab);
+            ctx->end("k_finalize");
+        }
     }
     if (o.layer || o.depth || (want_prio && o.static_priority)) {
         const int grid = static_cast<int>(std::min<int64_t>((d.T + 255) / 256, 16LL * ctx->n_sms));

@@ -97,27 +97,29 @@ __global__ void __launch_bounds__(256) k_ingest(DevBatch b, int32_t* cursor_scra
 // free slots (stack) or fresh ones; a node's slot is released after level
 // key[v] has been processed.  reverse = walk levels from the last to the
 // first.  Returns the number of slots used (peak live set).
+// order/lstart/key are read through L2 (__ldcg): in the cooperative
+// large-graph kernel they were written by other CTAs earlier in the launch.
 __device__ int32_t assign_slots(const int32_t* order, const int32_t* lstart, int32_t L, int32_t processed,
                                 const int32_t* key, bool reverse, int32_t* slot, int32_t* cnt, int32_t* cur,
                                 int32_t* rel_order, int32_t* fstack, int32_t* warp_tot) {
     const int tid = threadIdx.x, nthr = blockDim.x;
     for (int32_t i = tid; i <= L; i += nthr) cnt[i] = 0;
     __syncthreads();
-    for (int32_t i = tid; i < processed; i += nthr) atomicAdd(&cnt[key[order[i]]], 1);
+    for (int32_t i = tid; i < processed; i += nthr) atomicAdd(&cnt[__ldcg(&key[__ldcg(&order[i])])], 1);
     __syncthreads();
     block_exclusive_scan_inplace(cnt, L + 1, warp_tot);
     for (int32_t i = tid; i <= L; i += nthr) cur[i] = cnt[i];
     __syncthreads();
     for (int32_t i = tid; i < processed; i += nthr) {
-        const int32_t v = order[i];
-        rel_order[atomicAdd(&cur[key[v]], 1)] = v;
+        const int32_t v = __ldcg(&order[i]);
+        rel_order[atomicAdd(&cur[__ldcg(&key[v])], 1)] = v;
     }
     __syncthreads();
     int32_t fs = 0, P = 0;
     for (int32_t step = 0; step < L; ++step) {
         const int32_t lv = reverse ? L - 1 - step : step;
-        const int32_t a0 = lstart[lv], a = lstart[lv + 1] - a0;
-        for (int32_t i = tid; i < a; i += nthr) slot[order[a0 + i]] = i < fs ? fstack[fs - 1 - i] : P + (i - fs);
+        const int32_t a0 = __ldcg(&lstart[lv]), a = __ldcg(&lstart[lv + 1]) - a0;
+        for (int32_t i = tid; i < a; i += nthr) slot[__ldcg(&order[a0 + i])] = i < fs ? fstack[fs - 1 - i] : P + (i - fs);
         __syncthreads();
         const int32_t nfs = max(fs - a, 0);
         P += max(a - fs, 0);
@@ -127,6 +129,45 @@ __device__ int32_t assign_slots(const int32_t* order, const int32_t* lstart, int
         fs = nfs + r;
     }
     return P;
+}
+
+// median_gpu_time_ms (platform.cpp:233-240): the lower median of the tasks'
+// GPU times, from the per-type task counts -- present types sorted by GPU
+// time, counts walked to rank (n-1)/2.
+__device__ double lower_median_gpu(const DevCosts& sc, const int32_t* tcount, int32_t NT, int32_t n) {
+    int32_t ids[kMaxTypes];
+    int32_t m = 0;
+    for (int32_t t = 0; t < NT && t < kMaxTypes; ++t)
+        if (tcount[t] > 0) {
+            int32_t j = m++;
+            while (j > 0 && sc.gpu[ids[j - 1]] > sc.gpu[t]) { ids[j] = ids[j - 1]; --j; }
+            ids[j] = t;
+        }
+    const int32_t want = (n - 1) / 2;
+    int32_t acc = 0;
+    for (int32_t j = 0; j < m; ++j) {
+        acc += tcount[ids[j]];
+        if (acc > want) return sc.gpu[ids[j]];
+    }
+    return 0.0;
+}
+
+// Cost table of graph g into shared memory, plus mean_ms per type
+// (platform.cpp:39-50: ((0 + cpu) + gpu) / count).
+__device__ void load_costs(const DevCosts* costs_g, int32_t ci, DevCosts& sc, double* s_mean) {
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    __syncthreads();
+    for (int i = tid; i < static_cast<int>(sizeof(DevCosts) / 8); i += nthr)
+        reinterpret_cast<double*>(&sc)[i] = reinterpret_cast<const double*>(costs_g + ci)[i];
+    __syncthreads();
+    if (tid < kMaxTypes) {
+        double sum = 0.0;
+        int cnt = 0;
+        if (tid < sc.n_types && sc.cpu[tid] > 0.0) { sum += sc.cpu[tid]; ++cnt; }
+        if (tid < sc.n_types && sc.gpu[tid] > 0.0) { sum += sc.gpu[tid]; ++cnt; }
+        s_mean[tid] = cnt ? sum / cnt : 0.0;
+    }
+    __syncthreads();
 }
 
 __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* costs_g,
@@ -159,18 +200,7 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
         // cost table of this graph (per-platform tables in a schedule batch)
         const int32_t ci = cost_idx ? cost_idx[g] : 0;
         if (ci != loaded) {
-            __syncthreads();
-            for (int i = tid; i < static_cast<int>(sizeof(DevCosts) / 8); i += nthr)
-                reinterpret_cast<double*>(&sc)[i] = reinterpret_cast<const double*>(costs_g + ci)[i];
-            __syncthreads();
-            if (tid < kMaxTypes) {
-                // mean_ms (platform.cpp:39-50): ((0 + cpu) + gpu) / count
-                double sum = 0.0;
-                int cnt = 0;
-                if (tid < sc.n_types && sc.cpu[tid] > 0.0) { sum += sc.cpu[tid]; ++cnt; }
-                if (tid < sc.n_types && sc.gpu[tid] > 0.0) { sum += sc.gpu[tid]; ++cnt; }
-                s_mean[tid] = cnt ? sum / cnt : 0.0;
-            }
+            load_costs(costs_g, ci, sc, s_mean);
             loaded = ci;
         }
         const int32_t NT = b.n_types;
@@ -318,28 +348,292 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
             gi.n_classes = n_cls;
             gi.miss_gpu = s_miss_gpu == INT32_MAX ? -1 : s_miss_gpu;
             gi.miss_any = s_miss_any == INT32_MAX ? -1 : s_miss_any;
-            gi.median = 0.0;
-            if (n > 0 && gi.miss_gpu < 0) {
-                // sort present types by GPU time; walk counts to rank (n-1)/2
-                int32_t ids[kMaxTypes];
-                int32_t m = 0;
-                for (int32_t t = 0; t < NT && t < kMaxTypes; ++t)
-                    if (s_tcount[t] > 0) {
-                        int32_t j = m++;
-                        while (j > 0 && sc.gpu[ids[j - 1]] > sc.gpu[t]) { ids[j] = ids[j - 1]; --j; }
-                        ids[j] = t;
-                    }
-                const int32_t want = (n - 1) / 2;
-                int32_t acc = 0;
-                for (int32_t j = 0; j < m; ++j) {
-                    acc += s_tcount[ids[j]];
-                    if (acc > want) { gi.median = sc.gpu[ids[j]]; break; }
-                }
-            }
+            gi.median = (n > 0 && gi.miss_gpu < 0) ? lower_median_gpu(sc, s_tcount, NT, n) : 0.0;
             s.info[g] = gi;
             s.median[g] = gi.median;
         }
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------- structure, one large graph
+
+namespace cg = cooperative_groups;
+
+// Exclusive scan of a[0..len) in place across a cooperative grid: each CTA
+// owns one contiguous chunk; chunk totals go through part[gridDim.x].
+// Returns the grand total.  All threads of the grid must call it.
+__device__ int32_t grid_exclusive_scan(cg::grid_group& grid, int32_t* a, int64_t len, int32_t* part,
+                                       int32_t* warp_tot) {
+    const int64_t nb = gridDim.x;
+    const int64_t chunk = (len + nb - 1) / nb;
+    const int64_t lo = min(len, static_cast<int64_t>(blockIdx.x) * chunk), hi = min(len, lo + chunk);
+    int32_t sum = 0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) sum += __ldcg(&a[i]);
+    int32_t tot;
+    block_inclusive_scan(sum, warp_tot, &tot);
+    if (threadIdx.x == 0) part[blockIdx.x] = tot;
+    grid.sync();
+    int32_t before = 0, all = 0;
+    for (int64_t j = threadIdx.x; j < nb; j += blockDim.x) {
+        const int32_t x = __ldcg(&part[j]);
+        all += x;
+        if (j < blockIdx.x) before += x;
+    }
+    int32_t carry, total;
+    block_inclusive_scan(before, warp_tot, &carry);  // CTA sums: chunks before this one
+    block_inclusive_scan(all, warp_tot, &total);
+    for (int64_t base = lo; base < hi; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const int32_t x = i < hi ? __ldcg(&a[i]) : 0;
+        int32_t t;
+        const int32_t inc = block_inclusive_scan(x, warp_tot, &t);
+        if (i < hi) a[i] = carry + inc - x;
+        carry += t;
+    }
+    grid.sync();
+    return total;
+}
+
+// Warp-aggregated append of the lanes with `pred` to list[base + *ctr ...]
+// (any active-lane mask).  Returns the slot of this lane (or -1).
+__device__ __forceinline__ int32_t warp_append(bool pred, int32_t* ctr) {
+    const unsigned am = __activemask();
+    const unsigned bal = __ballot_sync(am, pred);
+    if (!bal) return -1;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(am) - 1;
+    int32_t base = 0;
+    if (lane == leader) base = atomicAdd(ctr, __popc(bal));
+    base = __shfl_sync(am, base, leader);
+    return pred ? base + __popc(bal & ((1u << lane) - 1u)) : -1;
+}
+
+__device__ __forceinline__ double warp_max_f64(double x) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
+
+// k_structure for ONE graph with the whole GPU (cooperative launch): the
+// same outputs as k_structure (levels, level order, height/depth, upward
+// rank, live-range slots, order-major records, calibration classes, lower
+// median), level-synchronous across the grid with one grid barrier per level
+// instead of one CTA walking a million-task graph.  A warp owns a frontier
+// node, its lanes the node's successors (warp-aggregated appends to the next
+// level).  Level order inside a level is arbitrary; every consumer is
+// order-free (max-plus, max, set union).  Live-range slots: when every live
+// set fits in a ring over level-order positions (R = widest window of
+// span+1 consecutive levels, at most twice the widest two-level window),
+// slot = position mod R -- a node is live only while positions within R of
+// it are being processed; otherwise CTA 0 runs the stack allocator.
+// Everything written by other CTAs inside this launch is read through L2.
+__global__ void __launch_bounds__(512) k_structure_large(DevBatch b, const DevCosts* costs_g, const int32_t* cost_idx,
+                                                        AttrScratch s, int32_t want_rank, LargeCtl* ctl) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ DevCosts sc;
+    __shared__ double s_mean[kMaxTypes];
+    __shared__ int32_t s_tc[kMaxTypes];
+    __shared__ int32_t warp_tot[32];
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31;
+    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * nthr + tid;
+    const int64_t gthreads = static_cast<int64_t>(gridDim.x) * nthr;
+    const int64_t gwarp = gtid >> 5, gwarps = gthreads >> 5;
+    constexpr int64_t g = 0;
+    const int64_t t0 = b.task_base[g];
+    const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
+    const int32_t* doff = b.dep_off + t0 + g;
+    const int32_t* dep = b.dep + b.edge_base[g];
+    const int32_t* soff = b.succ_off + t0 + g;
+    const int32_t* succ = b.succ + b.edge_base[g];
+    const int32_t* type = b.type + t0;
+    int32_t* indeg = s.tmp + t0 + g;
+    int32_t* order = s.order + t0;
+    int32_t* level = s.level + t0;
+    int32_t* lstart = s.lstart + t0 + g;
+    int32_t* height = s.height + t0;
+    int32_t* lastuse = s.lastuse + t0;
+    int32_t* slot = s.slot + t0;
+    int32_t* opos = s.opos + t0;
+    int32_t* firstuse = s.firstuse + t0;
+    int32_t* rslot = s.rslot + t0;
+    double* rank = s.rank + t0;
+    const int32_t NT = b.n_types;
+
+    load_costs(costs_g, cost_idx ? cost_idx[g] : 0, sc, s_mean);
+    if (tid < kMaxTypes) s_tc[tid] = 0;
+    __syncthreads();
+    // ---- entries, cost diagnostics, type histogram, roots
+    for (int64_t v = gtid; v < n; v += gthreads) {
+        const int32_t deg = doff[v + 1] - doff[v];
+        indeg[v] = deg;
+        level[v] = 0;
+        const int32_t ty = type[v];
+        const bool has_gpu = ty < NT && sc.gpu[ty] > 0.0;
+        const bool has_cpu = ty < NT && sc.cpu[ty] > 0.0;
+        if (!has_gpu) atomicMax(&ctl->miss_gpu, n - static_cast<int32_t>(v));
+        if (!has_gpu && !has_cpu) atomicMax(&ctl->miss_any, n - static_cast<int32_t>(v));
+        if (has_gpu) atomicAdd(&s_tc[ty], 1);
+        const int32_t at = warp_append(deg == 0, &ctl->ctr[0]);
+        if (at >= 0) order[at] = static_cast<int32_t>(v);
+    }
+    __syncthreads();
+    if (tid < kMaxTypes && s_tc[tid]) atomicAdd(&ctl->tcount[tid], s_tc[tid]);
+    grid.sync();
+    // ---- level-synchronous Kahn (topological_layers, taskgraph.cpp:197-219).
+    // Three rotating counters: level L appends to ctr[(L+1)%3] while
+    // ctr[(L+2)%3] (read two levels ago) is reset.
+    int32_t begin = 0, L = 0;
+    int32_t cnt = __ldcg(&ctl->ctr[0]);
+    if (gtid == 0) lstart[0] = 0;
+    while (cnt > 0) {
+        const int32_t end = begin + cnt;
+        if (gtid == 0) {
+            lstart[L + 1] = end;
+            ctl->ctr[(L + 2) % 3] = 0;
+        }
+        int32_t* nxt = &ctl->ctr[(L + 1) % 3];
+        for (int64_t i = begin + gwarp; i < end; i += gwarps) {
+            const int32_t u = __ldcg(&order[i]);
+            const int32_t k1 = soff[u + 1];
+            for (int32_t k = soff[u] + lane; k - lane < k1; k += 32) {
+                bool rdy = false;
+                int32_t v = 0;
+                if (k < k1) {
+                    v = succ[k];
+                    rdy = atomicSub(&indeg[v], 1) == 1;
+                }
+                const int32_t at = warp_append(rdy, nxt);
+                if (at >= 0) {
+                    level[v] = L + 1;
+                    order[end + at] = v;
+                }
+            }
+        }
+        grid.sync();
+        begin = end;
+        ++L;
+        cnt = __ldcg(&ctl->ctr[L % 3]);
+    }
+    const int32_t processed = begin;
+    // ---- reverse level sweep: height (depth), upward rank, last use
+    for (int32_t lv = L - 1; lv >= 0; --lv) {
+        const int32_t a0 = __ldcg(&lstart[lv]), a1 = __ldcg(&lstart[lv + 1]);
+        for (int64_t i = a0 + gwarp; i < a1; i += gwarps) {
+            const int32_t u = __ldcg(&order[i]);
+            int32_t h = 0, lu = lv;
+            double best = 0.0;
+            for (int32_t k = soff[u] + lane; k < soff[u + 1]; k += 32) {
+                const int32_t v = succ[k];
+                h = max(h, __ldcg(&height[v]) + 1);
+                best = fmax(best, __ldcg(&rank[v]));
+                lu = max(lu, __ldcg(&level[v]));
+            }
+            h = __reduce_max_sync(0xffffffffu, h);
+            lu = __reduce_max_sync(0xffffffffu, lu);
+            if (want_rank) best = warp_max_f64(best);
+            if (lane == 0) {
+                height[u] = h;
+                lastuse[u] = lu;
+                if (want_rank) rank[u] = s_mean[type[u] < kMaxTypes ? type[u] : 0] + best;
+            }
+        }
+        grid.sync();
+    }
+    // ---- inverse order, first use, edge level span
+    for (int64_t i = gtid; i < processed; i += gthreads) opos[__ldcg(&order[i])] = static_cast<int32_t>(i);
+    for (int64_t v = gtid; v < n; v += gthreads) {
+        const int32_t lvv = __ldcg(&level[v]);
+        int32_t fu = lvv, sp = 1;
+        for (int32_t k = doff[v]; k < doff[v + 1]; ++k) {
+            const int32_t lu = __ldcg(&level[dep[k]]);
+            fu = min(fu, lu);
+            sp = max(sp, lvv - lu);
+        }
+        firstuse[v] = fu;
+        const unsigned am = __activemask();
+        sp = __reduce_max_sync(am, sp);
+        if (lane == __ffs(am) - 1) atomicMax(&ctl->span, sp);
+    }
+    grid.sync();
+    const int32_t span = max(__ldcg(&ctl->span), 1);
+    // widest window of span+1 consecutive levels (ring size), and of two
+    for (int64_t lv = gtid; lv < L; lv += gthreads) {
+        const int32_t hi = __ldcg(&lstart[lv + 1]);
+        const int32_t r = hi - __ldcg(&lstart[lv > span ? lv - span : 0]);
+        const int32_t w2 = __ldcg(&lstart[lv + 2 < L ? lv + 2 : L]) - __ldcg(&lstart[lv]);
+        atomicMax(&ctl->ring, r);
+        atomicMax(&ctl->wide2, w2);
+    }
+    grid.sync();
+    const int32_t R = max(__ldcg(&ctl->ring), 1);
+    const bool ring = static_cast<int64_t>(R) <= 2 * static_cast<int64_t>(max(__ldcg(&ctl->wide2), 1));
+    int32_t P = R, Pr = R;
+    if (ring) {
+        for (int64_t i = gtid; i < processed; i += gthreads) {
+            const int32_t v = __ldcg(&order[i]);
+            slot[v] = static_cast<int32_t>(i % R);
+            rslot[v] = static_cast<int32_t>(i % R);
+        }
+    } else if (blockIdx.x == 0) {
+        P = assign_slots(order, lstart, L, processed, lastuse, false, slot, indeg, s.tmp2 + t0 + g,
+                         s.rel_order + t0, s.fstack + t0, warp_tot);
+        Pr = assign_slots(order, lstart, L, processed, firstuse, true, rslot, indeg, s.tmp2 + t0 + g,
+                          s.rel_order + t0, s.fstack + t0, warp_tot);
+    }
+    grid.sync();
+    // ---- order-major node records for the sweep
+    int32_t* om_slot = s.om_slot + t0;
+    double* om_gpu = s.om_gpu + t0;
+    int32_t* om_poff = s.om_poff + t0 + g;
+    int32_t* om_ps = s.om_pslot + b.edge_base[g];
+    for (int64_t i = gtid; i < processed; i += gthreads) {
+        const int32_t v = __ldcg(&order[i]);
+        om_slot[i] = __ldcg(&slot[v]);
+        const int32_t ty = type[v];
+        om_gpu[i] = ty < NT ? sc.gpu[ty] : 0.0;
+        om_poff[i] = doff[v + 1] - doff[v];
+    }
+    if (gtid == 0) om_poff[processed] = 0;
+    grid.sync();
+    grid_exclusive_scan(grid, om_poff, processed + 1, ctl->part, warp_tot);
+    for (int64_t i = gtid; i < processed; i += gthreads) {
+        const int32_t v = __ldcg(&order[i]);
+        const int32_t o = __ldcg(&om_poff[i]) - doff[v];
+        for (int32_t k = doff[v]; k < doff[v + 1]; ++k) om_ps[o + k] = __ldcg(&slot[dep[k]]);
+    }
+    // ---- calibration classes: dense ids of present (layer, type) pairs
+    int32_t* mark = s.cls_mark + t0 * NT;
+    const int64_t nkeys = static_cast<int64_t>(L) * NT;
+    for (int64_t i = gtid; i < nkeys; i += gthreads) mark[i] = 0;
+    grid.sync();
+    for (int64_t v = gtid; v < n; v += gthreads) {
+        const int32_t ty = type[v];
+        if (ty < NT) mark[static_cast<int64_t>(__ldcg(&level[v])) * NT + ty] = 1;
+    }
+    grid.sync();
+    const int32_t n_cls = grid_exclusive_scan(grid, mark, nkeys, ctl->part, warp_tot);
+    for (int64_t v = gtid; v < n; v += gthreads) {
+        const int32_t ty = type[v];
+        s.cls[t0 + v] = ty < NT ? __ldcg(&mark[static_cast<int64_t>(__ldcg(&level[v])) * NT + ty]) : 0;
+    }
+    // ---- per-graph scalars
+    if (blockIdx.x == 0 && tid == 0) {
+        int32_t tc[kMaxTypes];
+        for (int t = 0; t < kMaxTypes; ++t) tc[t] = __ldcg(&ctl->tcount[t]);
+        const int32_t mg = __ldcg(&ctl->miss_gpu), ma = __ldcg(&ctl->miss_any);
+        GraphInfo gi;
+        gi.n_levels = L;
+        gi.processed = processed;
+        gi.peak_slots = P;
+        gi.peak_rslots = Pr;
+        gi.max_span = span;
+        gi.n_classes = n_cls;
+        gi.miss_gpu = mg > 0 ? n - mg : -1;
+        gi.miss_any = ma > 0 ? n - ma : -1;
+        gi.median = (n > 0 && gi.miss_gpu < 0) ? lower_median_gpu(sc, tc, NT, n) : 0.0;
+        s.info[g] = gi;
+        s.median[g] = gi.median;
     }
 }
 
@@ -790,6 +1084,105 @@ __global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int
             if (o.ability && write_ability) o.ability[t0 + v] = abil;
         }
         __syncthreads();
+    }
+}
+
+// k_finalize for ONE large graph with the whole GPU (cooperative launch).
+// Same results as k_finalize; the phases are grid-wide: per-class window
+// sums (L2 atomics), reduced fractions per (class, window), distinct
+// fractions per window by insertion into an open-addressing table (a slot,
+// once claimed by a class, never changes, so equal fractions meet on the
+// same probe sequence), then per-task efficiency / ability.
+// scratch: [C*11] sums, [C] counts, [C*11] numerators, [C*11] denominators;
+// tab: 11 tables of `tab_size` int32 (power of two >= 2C), score[11].
+__global__ void __launch_bounds__(512) k_finalize_large(DevBatch b, AttrScratch s, int32_t sweep_mode, AttrOutDev o,
+                                                       int64_t* scratch, int32_t* tab, int64_t tab_cap,
+                                                       int32_t* score, int32_t write_ability) {
+    cg::grid_group grid = cg::this_grid();
+    constexpr int64_t g = 0;
+    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t t0 = b.task_base[g];
+    const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
+    const GraphInfo gi = s.info[g];
+    if (gi.processed != n) return;  // uniform: cyclic graphs are reported by the host
+    const uint64_t* hist = s.hist + t0 * 4;
+    int best = 0;
+    if (sweep_mode == SWEEP_CALIBRATE) {
+        const int64_t C = gi.n_classes;
+        int64_t* sums = scratch;
+        int64_t* cnt = sums + C * kWindows;
+        int64_t* fa = cnt + C;
+        int64_t* fq = fa + C * kWindows;
+        int64_t ts = 1;
+        while (ts < 2 * C) ts <<= 1;
+        ts = min(ts, tab_cap);
+        for (int64_t i = gtid; i < C * (kWindows + 1); i += gthreads) sums[i] = 0;
+        for (int64_t i = gtid; i < ts * kWindows; i += gthreads) tab[i] = 0;
+        if (gtid < kWindows) score[gtid] = 0;
+        grid.sync();
+        for (int64_t v = gtid; v < n; v += gthreads) {
+            const int32_t c = s.cls[t0 + v];
+            const uint64_t* h = hist + v * 4;
+            int64_t acc = 0;
+            for (int k = 0; k < kWindows; ++k) {
+                acc += field(h, k);
+                if (acc) atomicAdd(reinterpret_cast<unsigned long long*>(&sums[static_cast<int64_t>(c) * kWindows + k]),
+                                   static_cast<unsigned long long>(acc));
+            }
+            atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[c]), 1ull);
+        }
+        grid.sync();
+        for (int64_t item = gtid; item < C * kWindows; item += gthreads) {
+            const int64_t c = item / kWindows;
+            const int64_t sc_ = __ldcg(&sums[item]), cc = __ldcg(&cnt[c]);
+            const int64_t d = gcd64(sc_ == 0 ? cc : sc_, cc);
+            fa[item] = sc_ / d;
+            fq[item] = cc / d;
+        }
+        grid.sync();
+        for (int64_t item = gtid; item < C * kWindows; item += gthreads) {
+            const int64_t c = item / kWindows;
+            const int k = static_cast<int>(item - c * kWindows);
+            const int64_t a = __ldcg(&fa[item]), q = __ldcg(&fq[item]);
+            int32_t* t = tab + static_cast<int64_t>(k) * ts;
+            uint64_t hsh = static_cast<uint64_t>(a) * 0x9E3779B97F4A7C15ull ^ (static_cast<uint64_t>(q) * 0xC2B2AE3D27D4EB4Full);
+            hsh ^= hsh >> 29;
+            int64_t pos = static_cast<int64_t>(hsh & static_cast<uint64_t>(ts - 1));
+            for (;;) {
+                const int32_t cur = atomicCAS(&t[pos], 0, static_cast<int32_t>(c) + 1);
+                if (cur == 0) { atomicAdd(&score[k], 1); break; }
+                const int64_t oi = static_cast<int64_t>(cur - 1) * kWindows + k;
+                if (__ldcg(&fa[oi]) == a && __ldcg(&fq[oi]) == q) break;
+                pos = (pos + 1) & (ts - 1);
+            }
+        }
+        grid.sync();
+        int64_t best_score = -1;
+        int32_t sk[kWindows];
+        for (int k = 0; k < kWindows; ++k) {
+            sk[k] = __ldcg(&score[k]);
+            if (sk[k] > best_score) { best_score = sk[k]; best = k; }  // strict >: ties keep the smaller W
+        }
+        if (gtid == 0) {
+            const double w0 = 2.0 * gi.median;
+            if (o.unit_time_ms) o.unit_time_ms[g] = ldexp(w0, best - 4);
+            if (o.w0_ms) o.w0_ms[g] = w0;
+            if (o.best_score) o.best_score[g] = best_score;
+            if (o.w0_score) o.w0_score[g] = sk[4];
+            if (o.evaluations) o.evaluations[g] = kWindows;
+        }
+    }
+    for (int64_t v = gtid; v < n; v += gthreads) {
+        const uint64_t* h = hist + v * 4;
+        int64_t eff = 0, abil = 0;
+        for (int k = 0; k < kBins; ++k) {
+            const int64_t f = field(h, k);
+            if (k <= best) eff += f;
+            abil += f;
+        }
+        if (o.efficiency && sweep_mode != SWEEP_ABILITY) o.efficiency[t0 + v] = eff;
+        if (o.ability && write_ability) o.ability[t0 + v] = abil;
     }
 }
 

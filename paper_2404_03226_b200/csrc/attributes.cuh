@@ -56,6 +56,20 @@ struct AttrScratch {
     int32_t* tile_graph; // [tiles] graph of each sweep tile (<= T/8 + G)
 };
 
+// Grid-wide counters of k_structure_large (zeroed before the launch),
+// followed by gridDim.x ints of scan partials.
+struct LargeCtl {
+    int32_t ctr[4];      // rotating per-level append counters
+    int32_t miss_gpu;    // max (n - v) over tasks without a GPU cost (0: none)
+    int32_t miss_any;    // same, tasks without any cost
+    int32_t span;        // max level(v) - level(u) over edges
+    int32_t ring;        // widest window of span+1 consecutive levels
+    int32_t wide2;       // widest window of two consecutive levels
+    int32_t pad[7];
+    int32_t tcount[kMaxTypes];
+    int32_t part[1];     // [gridDim.x]
+};
+
 struct AttrOutDev {
     int64_t* ability;
     int64_t* efficiency;
@@ -72,6 +86,8 @@ struct AttrOutDev {
 __global__ void k_ingest(DevBatch b, int32_t* cursor_scratch);
 __global__ void k_structure(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                             int32_t want_rank, int32_t want_large);
+__global__ void k_structure_large(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
+                                  int32_t want_rank, LargeCtl* ctl);
 __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s);
 __global__ void k_sweep(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                         int32_t sweep_mode,
@@ -79,6 +95,8 @@ __global__ void k_sweep(DevBatch b, const DevCosts* costs, const int32_t* cost_i
                         int64_t smem_bytes, double* gwin, int64_t gwin_stride, int32_t prune);
 __global__ void k_finalize(DevBatch b, AttrScratch s, int32_t sweep_mode, const double* unit_time_in,
                            AttrOutDev o, int64_t* cls_scratch, int64_t cls_stride, int32_t write_ability);
+__global__ void k_finalize_large(DevBatch b, AttrScratch s, int32_t sweep_mode, AttrOutDev o, int64_t* scratch,
+                                 int32_t* tab, int64_t tab_cap, int32_t* score, int32_t write_ability);
 template <int CH>
 __global__ void k_closure(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets, int64_t nw,
                           unsigned long long* ability);

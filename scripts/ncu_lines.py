@@ -6,7 +6,7 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+out = subprocess.run(["ncu", "-i", rep] + (["-k", sys.argv[3]] if len(sys.argv) > 3 else []) + [ "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 cur = None
 agg, ins, src = collections.Counter(), collections.Counter(), {}
