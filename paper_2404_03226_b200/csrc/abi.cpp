@@ -898,7 +898,13 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
     auto layout = [&](int64_t qcap) {
         return sim_layout(d.max_n, d.max_h, max_workers, qcap, p.ring, p.n_types, p.max_nodes, compact, p.policy);
     };
-    const bool forced = p.qcap > 0;  // rerun of queue overflows: HBM state, full capacity
+    // HBM state with full queues: reruns of queue overflows, and batches of
+    // a few large DAGs (fewer warps than SMs, so shared memory buys no
+    // occupancy, and their ready queues outgrow it: C3's LU/QR overflow a
+    // shared-memory queue and measured 150 ms in HBM vs 167 ms in a 1-warp
+    // shared-memory CTA)
+    const bool few_large = n_items < ctx->n_sms && d.max_n >= 4096;
+    const bool forced = p.qcap > 0 || few_large;
     int64_t qcap = qcap_full;
     int ctas_per_sm = 2;
     p.use_smem = 0;

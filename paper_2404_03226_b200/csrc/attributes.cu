@@ -906,6 +906,152 @@ __device__ __forceinline__ void sweep_tile_mode(const DevBatch& b, const AttrScr
     else sweep_tile<S, SMEM, 1>(b, s, g, tile, gwin, P, th, s_hist, prune_span);
 }
 
+// Lane-per-node sweep for narrow tiles (S = 8, 16: graphs whose live set is
+// wide, e.g. the 1M-task C4 DAG).  One lane relaxes all S distance columns of
+// its node from each predecessor's row (S contiguous doubles), so the
+// per-node work -- record loads, binning, the row store -- is paid once per
+// node instead of once per (node, source) lane.  Lanes walk a row's 16-byte
+// chunks starting at a lane-dependent chunk, which spreads a warp's LDS.128 /
+// STS.128 over the banks; the accumulators stay in that rotated order (chunk
+// (j + rot) % NC lives in m[j]), so no register is indexed dynamically.  The
+// next level's node record is loaded while the current level runs.
+template <int S, int TMODE>
+__device__ __forceinline__ void sweep_tile_lanes(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
+                                                 int32_t P, const Thresholds& th, uint32_t* s_hist,
+                                                 int32_t prune_span) {
+    extern __shared__ double win_smem[];
+    constexpr int NC = S / 2;  // 16-byte chunks per row
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int rot = tid & (NC - 1);
+    const int64_t t0 = b.task_base[g];
+    const int32_t* lstart = s.lstart + t0 + g;
+    const int32_t* om_slot = s.om_slot + t0;
+    const double* om_gpu = s.om_gpu + t0;
+    const int32_t* om_poff = s.om_poff + t0 + g;
+    const int32_t* om_ps = s.om_pslot + b.edge_base[g];
+    const GraphInfo gi = s.info[g];
+    const int32_t first = tile * S;
+    const int32_t nsrc = min(S, gi.processed - first);
+    double2* w2 = reinterpret_cast<double2*>(win_smem);
+    {
+        const double2 neg = make_double2(-CUDART_INF, -CUDART_INF);  // unreachable
+        for (int64_t i = tid; i < static_cast<int64_t>(P) * NC; i += nthr) w2[i] = neg;
+    }
+    for (int i = tid; i < S * kBins; i += nthr) s_hist[i] = 0u;
+    uint64_t hist[S];  // hist[2j+e]: source 2*((j+rot)%NC)+e
+#pragma unroll
+    for (int q = 0; q < S; ++q) hist[q] = 0;
+    auto src_of = [&](int j, int e) { return 2 * ((j + rot) & (NC - 1)) + e; };
+    int32_t visits = 0;
+    const int32_t La = s.level[t0 + s.order[t0 + first]];
+    const double wmax = th.w[kWindows - 1];
+    const uint64_t span_mask = prune_span >= 64 ? ~0ull : ((1ull << prune_span) - 1ull);
+    uint64_t recent = 0;
+    struct Rec {
+        int32_t p0, p1, sl;
+        double gv;
+    };
+    auto load_rec = [&](int32_t i) {
+        Rec r;
+        r.p0 = __ldg(&om_poff[i]);
+        r.p1 = __ldg(&om_poff[i + 1]);
+        r.sl = __ldg(&om_slot[i]);
+        r.gv = TMODE == 2 ? 1.0 : __ldg(&om_gpu[i]);
+        return r;
+    };
+    Rec nx{0, 0, 0, 0.0};
+    if (lstart[La] + tid < lstart[La + 1]) nx = load_rec(lstart[La] + tid);
+    __syncthreads();
+
+    for (int32_t lv = La; lv < gi.n_levels; ++lv) {
+        int small = 0;
+        const int32_t a0 = lstart[lv], a1 = lstart[lv + 1];
+        const int32_t a2 = lv + 1 < gi.n_levels ? lstart[lv + 2] : a1;
+        const Rec cur = nx;
+        if (a1 + tid < a2) nx = load_rec(a1 + tid);  // next level's first node of this lane
+        for (int32_t i = a0 + tid; i < a1; i += nthr) {
+            const Rec r = i == a0 + tid ? cur : load_rec(i);
+            double2 m[NC];
+#pragma unroll
+            for (int j = 0; j < NC; ++j) m[j] = make_double2(-CUDART_INF, -CUDART_INF);
+            // plain compare-select: operands are -inf or non-negative, never NaN
+            auto relax = [&](int32_t ps) {
+                const double2* row = w2 + static_cast<int64_t>(ps) * NC;
+#pragma unroll
+                for (int j = 0; j < NC; ++j) {
+                    const double2 x = row[(j + rot) & (NC - 1)];
+                    m[j].x = x.x > m[j].x ? x.x : m[j].x;
+                    m[j].y = x.y > m[j].y ? x.y : m[j].y;
+                }
+            };
+            int32_t k = r.p0;
+            for (; k + 2 <= r.p1; k += 2) {  // two predecessors in flight
+                const int32_t ps0 = __ldg(&om_ps[k]), ps1 = __ldg(&om_ps[k + 1]);
+                relax(ps0);
+                relax(ps1);
+            }
+            if (k < r.p1) relax(__ldg(&om_ps[k]));
+            const int32_t si = i - first;  // this node's own source column, if it is one
+            double2* outp = w2 + static_cast<int64_t>(r.sl) * NC;
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+                double d0 = m[j].x + r.gv, d1 = m[j].y + r.gv;
+                const bool c0 = d0 >= 0.0, c1 = d1 >= 0.0;
+                hist[2 * j] += shl64(1ull, c0 ? static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d0, th)) : 64u);
+                hist[2 * j + 1] += shl64(1ull, c1 ? static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d1, th)) : 64u);
+                if (static_cast<uint32_t>(si) < static_cast<uint32_t>(S)) {
+                    // the source itself: distance 0, not its own descendant
+                    if (src_of(j, 0) == si) {
+                        if (c0) hist[2 * j] -= shl64(1ull, static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d0, th)));
+                        d0 = 0.0;
+                    }
+                    if (src_of(j, 1) == si) {
+                        if (c1) hist[2 * j + 1] -= shl64(1ull, static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d1, th)));
+                        d1 = 0.0;
+                    }
+                }
+                if (prune_span > 0) small |= (d0 >= 0.0 && d0 <= wmax) || (d1 >= 0.0 && d1 <= wmax);
+                outp[(j + rot) & (NC - 1)] = make_double2(d0, d1);
+            }
+            if (++visits == kFlushEvery) {
+#pragma unroll
+                for (int j = 0; j < NC; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        if (src_of(j, e) < nsrc) flush5(hist[2 * j + e], s_hist + src_of(j, e) * kBins);
+                visits = 0;
+            }
+        }
+        if (prune_span > 0) {
+            recent = (recent << 1) | static_cast<uint64_t>(__syncthreads_or(small) != 0);
+            if (lv - La + 1 >= prune_span && (recent & span_mask) == 0) break;
+        } else {
+            __syncthreads();
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NC; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+            if (src_of(j, e) < nsrc) flush5(hist[2 * j + e], s_hist + src_of(j, e) * kBins);
+    __syncthreads();
+    const int32_t* order = s.order + t0;
+    for (int i = tid; i < nsrc * 4; i += nthr) {
+        const uint32_t* c = s_hist + (i >> 2) * kBins + 3 * (i & 3);
+        s.hist[(t0 + order[first + (i >> 2)]) * 4 + (i & 3)] =
+            static_cast<uint64_t>(c[0]) | (static_cast<uint64_t>(c[1]) << 21) | (static_cast<uint64_t>(c[2]) << 42);
+    }
+}
+
+template <int S>
+__device__ __forceinline__ void sweep_tile_lanes_mode(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
+                                                      int32_t P, const Thresholds& th, uint32_t* s_hist,
+                                                      int32_t prune_span) {
+    if (th.mode == 0) sweep_tile_lanes<S, 0>(b, s, g, tile, P, th, s_hist, prune_span);
+    else if (th.mode == 2) sweep_tile_lanes<S, 2>(b, s, g, tile, P, th, s_hist, 0);
+    else sweep_tile_lanes<S, 1>(b, s, g, tile, P, th, s_hist, prune_span);
+}
+
 __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs_g,
                                               const int32_t* cost_idx, AttrScratch s,
                                               int32_t sweep_mode, const double* unit_time,
@@ -943,8 +1089,8 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
                     case 128: sweep_tile_mode<128, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
                     case 64: sweep_tile_mode<64, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
                     case 32: sweep_tile_mode<32, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
-                    case 16: sweep_tile_mode<16, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
-                    default: sweep_tile_mode<8, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
+                    case 16: sweep_tile_lanes_mode<16>(b, s, g, tile, P, th, s_hist, prune_span); break;
+                    default: sweep_tile_lanes_mode<8>(b, s, g, tile, P, th, s_hist, prune_span); break;
                 }
             }
         }
