@@ -884,17 +884,25 @@ int32_t pow2_at_least(int32_t x) {
     return r;
 }
 
-// Picks the per-warp state placement: shared memory (compact types when the
-// batch allows) with 16 then 8 warps per SM, else HBM with full queues.
+// Picks the per-warp state placement and launch shape.  Up to 32 workers
+// with compact state (k_simulate_w1c, <= 72 registers) runs 4-warp CTAs, up
+// to 7 per SM (28 warps: the 4096 DAGs of C2 in one wave on 148 SMs); the
+// state goes to shared memory when a queue capacity of >= 32 entries fits,
+// else to HBM.  Wider platforms (k_simulate_w2*) and wide state run 8-warp
+// CTAs, two per SM.
 void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_items) {
+    const DevBatch& d = p.b;
+    const bool compact = !p.force_wide && d.max_n < 32768 && p.max_nodes <= 8;
+    const bool w2 = max_workers > 32;
+    const bool tight = compact && !w2;
+    const int max_warps = tight ? 4 : 8;
+    const int max_ctas = tight ? 7 : 2;
     // Few DAGs (e.g. two 22k-task tiled factorizations): fewer warps per CTA
-    // so each warp gets more shared memory; many DAGs: 8 warps per CTA.
-    int kWarps = 8;
+    // so each warp gets more shared memory; many DAGs: full CTAs.
+    int kWarps = max_warps;
     while (kWarps > 1 && n_items < static_cast<int64_t>(kWarps) * ctx->n_sms) kWarps >>= 1;
     const int kThreads = 32 * kWarps;
-    const DevBatch& d = p.b;
     const int64_t qcap_full = std::max<int32_t>(d.max_n, 1);
-    const bool compact = d.max_n < 32768 && p.max_nodes <= 8;
     auto layout = [&](int64_t qcap) {
         return sim_layout(d.max_n, d.max_h, max_workers, qcap, p.ring, p.n_types, p.max_nodes, compact, p.policy);
     };
@@ -906,11 +914,11 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
     const bool few_large = n_items < ctx->n_sms && d.max_n >= 4096;
     const bool forced = p.qcap > 0 || few_large;
     int64_t qcap = qcap_full;
-    int ctas_per_sm = 2;
+    int ctas_per_sm = max_ctas;
     p.use_smem = 0;
     if (!forced) {
         const int64_t per_sm = static_cast<int64_t>(ctx->smem_optin) + 1024;  // 228 KB per SM
-        for (int c : {2, 1}) {
+        for (int c = max_ctas; c >= 1; --c) {
             const int64_t per_warp = (per_sm / c - 1024) / kWarps;
             if (layout(qcap_full).total <= per_warp) {
                 qcap = qcap_full;
@@ -918,10 +926,10 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
                 p.use_smem = 1;
                 break;
             }
-            const int64_t cap = (per_warp - layout(0).total - 64) / ((4 + key_bytes(p.policy)) * max_workers);
+            const int64_t cap = (per_warp - layout(0).total - 64) / ((4 + key_bytes(p.policy, compact)) * max_workers);
             // short queues are the common case (C2: <= 27 entries); a graph
             // that overflows is re-run exactly with HBM state
-            if (cap >= (c == 2 ? 32 : 64)) {
+            if (cap >= 32) {
                 qcap = std::min<int64_t>(cap & ~int64_t(3), qcap_full);
                 ctas_per_sm = c;
                 p.use_smem = 1;
@@ -929,6 +937,7 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
             }
         }
     }
+    if (!p.use_smem) qcap = qcap_full;
     p.qcap = static_cast<int32_t>(qcap);
     p.layout = layout(qcap);
     p.state_bytes = p.layout.total;
@@ -942,7 +951,6 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
     unsigned long long* counter = ctx->buf("s_counter").as<unsigned long long>(1);
     cuda_check(cudaMemsetAsync(counter, 0, 8, ctx->stream), "memset");
     p.work_counter = counter;
-    const bool w2 = max_workers > 32;
     auto kern = compact ? (w2 ? k_simulate_w2c : k_simulate_w1c) : (w2 ? k_simulate_w2 : k_simulate_w1);
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "cudaFuncSetAttribute(k_simulate)");
@@ -996,6 +1004,7 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
         SimParams q = p;
         q.graph_list = d_list;
         q.qcap = std::max<int32_t>(b->d.max_n, 1);
+        q.force_wide = 1;  // also covers priorities beyond the compact int32 keys
         launch_sim(ctx, q, max_workers, static_cast<int64_t>(rerun.size()));
         cuda_check(cudaMemcpyAsync(status.data(), p.status, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
         cuda_check(cudaMemcpyAsync(aux.data(), p.status_aux, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H aux");

@@ -45,34 +45,45 @@ __device__ __forceinline__ uint64_t ord_i64(int64_t x) {
 
 // POL >= 0 fixes the policy at compile time; POL < 0 (the shipped kernels)
 // reads it at run time -- specialising saved <1% of the code.
+//
+// Register budget: only the state every event touches lives in registers
+// (time, counters, the lane's workers); regulator state, counters and graph
+// ids live in the warp's SimCold record, and state sections are addressed
+// from one base plus the launch's layout offsets (kernel parameters).
 template <int WPL, bool COMPACT, int POL>
 struct Sim {
     using UnmetT = typename std::conditional<COMPACT, int16_t, int32_t>::type;
     using ResidT = typename std::conditional<COMPACT, uint8_t, uint32_t>::type;
-    using ReadyT = UnmetT;
+    using KeyT = typename std::conditional<COMPACT, int16_t, int32_t>::type;
+    using PrioT = typename std::conditional<COMPACT, int32_t, int64_t>::type;
+    const SimParams* P;
+    char* base;  // this warp's state memory
     // ---- graph
-    int64_t g, t0;
-    int32_t n, nh;
-    const int32_t* doff;
+    int32_t n;
     const SimTaskHdr* hdr;  // this graph's packed records
-    const char* adj;        // packed list base
     int32_t W, nn;
     double lat;
-    int32_t policy_rt;
-    __device__ __forceinline__ int32_t pol() const { return POL >= 0 ? POL : policy_rt; }
-    // ---- per-warp state memory (shared memory when it fits)
-    UnmetT* unmet;
-    ResidT* resid;
-    ReadyT* ready;
-    int32_t* queue;
-    int32_t* qab;    // cached pop keys per queue entry (inspirit)
-    int32_t* qef;
-    int64_t* qprio;  // (dmdap, inspirit)
-    double* samp_t;
-    int64_t* samp_n;
-    double* costs;   // [2*NT]: cpu, gpu per type
-    double* bw;      // [nn*nn]
-    int32_t qcap, ring_mask;
+    __device__ __forceinline__ int32_t pol() const { return POL >= 0 ? POL : P->policy; }
+    // ---- state sections
+    __device__ __forceinline__ SimCold& cold() const { return *reinterpret_cast<SimCold*>(base + P->layout.cold); }
+    __device__ __forceinline__ UnmetT* unmet() const { return reinterpret_cast<UnmetT*>(base + P->layout.unmet); }
+    __device__ __forceinline__ ResidT* resid() const { return reinterpret_cast<ResidT*>(base + P->layout.resid); }
+    __device__ __forceinline__ int32_t* queue(int32_t w) const {
+        return reinterpret_cast<int32_t*>(base + P->layout.queue) + w * P->qcap;
+    }
+    __device__ __forceinline__ KeyT* qab(int32_t w) const { return reinterpret_cast<KeyT*>(base + P->layout.qab) + w * P->qcap; }
+    __device__ __forceinline__ KeyT* qef(int32_t w) const { return reinterpret_cast<KeyT*>(base + P->layout.qef) + w * P->qcap; }
+    __device__ __forceinline__ PrioT* qprio(int32_t w) const {
+        return reinterpret_cast<PrioT*>(base + P->layout.qprio) + w * P->qcap;
+    }
+    __device__ __forceinline__ double* samp_t() const { return reinterpret_cast<double*>(base + P->layout.ring); }
+    __device__ __forceinline__ int64_t* samp_n() const {
+        return reinterpret_cast<int64_t*>(base + P->layout.ring + 8 * P->ring);
+    }
+    __device__ __forceinline__ double cost(int32_t ty, int32_t k) const {
+        return reinterpret_cast<const double*>(base + P->layout.costs)[2 * ty + k];
+    }
+    __device__ __forceinline__ double bw(int32_t i) const { return reinterpret_cast<const double*>(base + P->layout.bw)[i]; }
     // ---- lane-owned workers
     int32_t kind[WPL], node[WPL], qlen[WPL];
     bool busy[WPL], fdirty[WPL];
@@ -80,31 +91,27 @@ struct Sim {
     double xt[WPL], dt[WPL];
     uint32_t xs[WPL], ds[WPL];
     int32_t xtask[WPL], dtask[WPL];
-    // ---- warp-uniform scalars
+    // ---- warp-uniform hot scalars
     int lane;
-    double now, makespan;
+    double now;
     int64_t nready;
-    int32_t completed, rcount;
+    int32_t completed, rcount, rhead, rtail;  // ready list: rcount tasks linked from rhead
     uint32_t seq;
-    int64_t n_push, n_pop, n_samp;
-    int64_t pop0, pop1, pop2;
-    int32_t status, aux;
-    // regulator (RegulatorState, policies.hpp:89-98) + ring of samples
-    int32_t mode, phase;
-    int64_t peak, prev_nready, last_trigger, s_dec_count;
-    double cur_k;
-    int32_t r_head, r_count;
-    tbsim_regulator_cfg cfg;
-    const SimParams* P;
+    int32_t n_pop;
+    int32_t status;
+    int32_t mode;
 
-    __device__ __forceinline__ double cost(int32_t ty, int32_t k) const { return costs[2 * ty + k]; }
+    __device__ __forceinline__ void fail(int32_t st, int32_t task) {
+        status = st;
+        if (lane == 0) cold().aux = task;
+    }
 
     // first half of a packed record: (adj8, nin, nout, nsucc | type << 24)
     __device__ __forceinline__ int4 head(int32_t task) const {
         return __ldg(reinterpret_cast<const int4*>(hdr + task));
     }
     __device__ __forceinline__ const char* lists(const int4& h) const {
-        return adj + 8ull * static_cast<uint32_t>(h.x);
+        return P->adj + 8ull * static_cast<uint32_t>(h.x);
     }
 
     // transfer_one_ms (engine.cpp:86-103): fastest resident copy, ties to the
@@ -115,10 +122,10 @@ struct Sim {
         double bbw = -1.0;
         for (uint32_t mm = m; mm; mm &= mm - 1) {
             const int32_t nd = __ffs(mm) - 1;
-            const double b = bw[nd * nn + to];
+            const double b = bw(nd * nn + to);
             if (b > bbw) { bbw = b; best = nd; }
         }
-        return lat + static_cast<double>(bytes) / bw[best * nn + to];
+        return lat + static_cast<double>(bytes) / bw(best * nn + to);
     }
 
     // transfer_total_ms (engine.cpp:105-110) for node `want` (may differ per
@@ -130,6 +137,7 @@ struct Sim {
         if (nin == 0) return 0.0;
         const unsigned want_nodes = __reduce_or_sync(kFull, 1u << want);
         const int32_t nw = __popc(want_nodes);
+        const ResidT* rs = resid();
         if (nin * nw <= 32) {
             // r = lane / nin without an integer divide (exact: lane < 32)
             const int32_t r = __float2int_rz(__fdividef(static_cast<float>(lane) + 0.5f, static_cast<float>(nin)));
@@ -139,23 +147,23 @@ struct Sim {
                 unsigned m = want_nodes;  // r-th set bit (few nodes; __fns is emulated)
                 for (int32_t i = 0; i < r; ++i) m &= m - 1;
                 const int32_t to = __ffs(m) - 1;
-                t = transfer_one(resid[__ldg(&inh[k])], __ldg(&inb[k]), to);
+                t = transfer_one(rs[__ldg(&inh[k])], __ldg(&inb[k]), to);
             }
-            const int32_t base = (r < nw ? r : 0) * nin;
+            const int32_t b0 = (r < nw ? r : 0) * nin;
             // in-order sum; the shuffles are independent and issued ahead
             double acc = 0.0;
             int32_t j = 0;
 #pragma unroll 1
             for (; j + 4 <= nin; j += 4) {
-                const double a0 = __shfl_sync(kFull, t, base + j), a1 = __shfl_sync(kFull, t, base + j + 1);
-                const double a2 = __shfl_sync(kFull, t, base + j + 2), a3 = __shfl_sync(kFull, t, base + j + 3);
+                const double a0 = __shfl_sync(kFull, t, b0 + j), a1 = __shfl_sync(kFull, t, b0 + j + 1);
+                const double a2 = __shfl_sync(kFull, t, b0 + j + 2), a3 = __shfl_sync(kFull, t, b0 + j + 3);
                 acc += a0;
                 acc += a1;
                 acc += a2;
                 acc += a3;
             }
 #pragma unroll 1
-            for (; j < nin; ++j) acc += __shfl_sync(kFull, t, base + j);
+            for (; j < nin; ++j) acc += __shfl_sync(kFull, t, b0 + j);
             const int32_t rw = __popc(want_nodes & ((1u << want) - 1u));
             return __shfl_sync(kFull, acc, rw * nin);
         }
@@ -163,10 +171,10 @@ struct Sim {
         for (unsigned wn = want_nodes; wn; wn &= wn - 1) {
             const int32_t to = __ffs(wn) - 1;
             double acc = 0.0;
-            for (int32_t base = 0; base < nin; base += 32) {
-                const int32_t cnt = min(32, nin - base);
+            for (int32_t b0 = 0; b0 < nin; b0 += 32) {
+                const int32_t cnt = min(32, nin - b0);
                 double t = 0.0;
-                if (lane < cnt) t = transfer_one(resid[__ldg(&inh[base + lane])], __ldg(&inb[base + lane]), to);
+                if (lane < cnt) t = transfer_one(rs[__ldg(&inh[b0 + lane])], __ldg(&inb[b0 + lane]), to);
 #pragma unroll 1
                 for (int32_t j = 0; j < cnt; ++j) acc += __shfl_sync(kFull, t, j);
             }
@@ -182,78 +190,113 @@ struct Sim {
         if (nin == 0) return 1.0;
         const int64_t* inb = reinterpret_cast<const int64_t*>(lists(hd));
         const int32_t* inh = reinterpret_cast<const int32_t*>(inb + nin);
+        const ResidT* rs = resid();
         int64_t total = 0, local = 0;
         for (int32_t k = 0; k < nin; ++k) {
             const int64_t by = __ldg(&inb[k]);
             total += by;
-            if ((static_cast<uint32_t>(resid[__ldg(&inh[k])]) >> nd) & 1u) local += by;
+            if ((static_cast<uint32_t>(rs[__ldg(&inh[k])]) >> nd) & 1u) local += by;
         }
         return static_cast<double>(local) / static_cast<double>(total);
     }
 
     // ---------------------------------------------------------- regulator
-    __device__ __forceinline__ double calculate_k() const {  // policies.cpp:153-169
-        if (r_count < 2) return 0.0;
+    __device__ __forceinline__ double calculate_k(const SimCold& c) const {  // policies.cpp:153-169
+        if (c.r_count < 2) return 0.0;
+        const int ring_mask = P->ring - 1;
+        const double* st = samp_t();
+        const int64_t* sn = samp_n();
         double sx = 0.0, sy = 0.0;
 #pragma unroll 1
-        for (int i = 0; i < r_count; ++i) {
-            const int idx = (r_head + i) & ring_mask;
-            sx += samp_t[idx];
-            sy += static_cast<double>(samp_n[idx]);
+        for (int i = 0; i < c.r_count; ++i) {
+            const int idx = (c.r_head + i) & ring_mask;
+            sx += st[idx];
+            sy += static_cast<double>(sn[idx]);
         }
-        const double dn = static_cast<double>(r_count);
+        const double dn = static_cast<double>(c.r_count);
         const double mx = sx / dn, my = sy / dn;
         double sxx = 0.0, sxy = 0.0;
 #pragma unroll 1
-        for (int i = 0; i < r_count; ++i) {
-            const int idx = (r_head + i) & ring_mask;
-            const double dx = samp_t[idx] - mx;
+        for (int i = 0; i < c.r_count; ++i) {
+            const int idx = (c.r_head + i) & ring_mask;
+            const double dx = st[idx] - mx;
             sxx += dx * dx;
-            sxy += dx * (static_cast<double>(samp_n[idx]) - my);
+            sxy += dx * (static_cast<double>(sn[idx]) - my);
         }
         if (sxx == 0.0) return 0.0;
         return sxy / sxx;
     }
 
-    __device__ __forceinline__ void regulator_step(int64_t cur) {  // policies.cpp:171-203
-        __syncwarp();
+    // regulator_step (policies.cpp:171-203).  Every lane computes the same
+    // values; lane 0 writes them back (the reads below come after the
+    // __syncwarp of the previous step).
+    __device__ __forceinline__ void regulator_step(int64_t cur) {
+        SimCold& c = cold();
+        const int ring_mask = P->ring - 1;
+        int32_t r_head = c.r_head, r_count = c.r_count;
         const int idx = (r_head + r_count) & ring_mask;
-        if (lane == 0) { samp_t[idx] = now; samp_n[idx] = cur; }
-        __syncwarp();
         if (r_count <= ring_mask) ++r_count;
         else r_head = (r_head + 1) & ring_mask;
-        while (r_count > cfg.slope_samples) {
+        while (r_count > c.cfg.slope_samples) {
             r_head = (r_head + 1) & ring_mask;
             --r_count;
         }
-        const int64_t d = cur - last_trigger;
-        if ((d < 0 ? -d : d) < cfg.task_window) return;
-        last_trigger = cur;
+        const int64_t last = c.last_trigger;
+        const int64_t d = cur - last;
+        __syncwarp();
+        if (lane == 0) {
+            samp_t()[idx] = now;
+            samp_n()[idx] = cur;
+            c.r_head = r_head;
+            c.r_count = r_count;
+        }
+        if ((d < 0 ? -d : d) < c.cfg.task_window) {
+            __syncwarp();
+            return;
+        }
+        int64_t peak = c.peak, s_dec_count = c.s_dec_count;
         peak = cur > peak ? cur : peak;
-        phase = cur >= peak - cfg.dec_step ? TBSIM_PHASE_INC : TBSIM_PHASE_DEC;
+        const int32_t phase = cur >= peak - c.cfg.dec_step ? TBSIM_PHASE_INC : TBSIM_PHASE_DEC;
+        double cur_k = c.cur_k;
         if (phase == TBSIM_PHASE_INC) {
-            if (cur - prev_nready >= cfg.s_inc) {
-                cur_k = calculate_k();
-                if (cur_k < cfg.k_inc) mode = TBSIM_MODE_EFFICIENCY;
-                else if (cur_k > cfg.k_inc) mode = TBSIM_MODE_ABILITY;
+            if (cur - c.prev_nready >= c.cfg.s_inc) {
+                __syncwarp();  // the sample just written
+                cur_k = calculate_k(c);
+                if (cur_k < c.cfg.k_inc) mode = TBSIM_MODE_EFFICIENCY;
+                else if (cur_k > c.cfg.k_inc) mode = TBSIM_MODE_ABILITY;
             }
         } else {
-            if (cur > peak - cfg.s_dec * s_dec_count) {
+            if (cur > peak - c.cfg.s_dec * s_dec_count) {
                 mode = TBSIM_MODE_ABILITY;
-            } else if (cur <= peak - cfg.s_dec * (s_dec_count + 1) + cfg.c) {
+            } else if (cur <= peak - c.cfg.s_dec * (s_dec_count + 1) + c.cfg.c) {
                 mode = TBSIM_MODE_LOCALITY;
-                if (cur <= peak - cfg.s_dec * (s_dec_count + 1)) s_dec_count += 1;
+                if (cur <= peak - c.cfg.s_dec * (s_dec_count + 1)) s_dec_count += 1;
             }
         }
-        prev_nready = cur;
+        __syncwarp();
+        if (lane == 0) {
+            c.last_trigger = cur;
+            c.peak = peak;
+            c.phase = phase;
+            c.cur_k = cur_k;
+            c.s_dec_count = s_dec_count;
+            c.prev_nready = cur;
+        }
+        __syncwarp();
     }
 
     __device__ __forceinline__ void queue_event() {
-        if (P->sample_time && lane == 0) {
-            P->sample_time[2 * t0 + n_samp] = now;
-            P->sample_nready[2 * t0 + n_samp] = nready;
+        SimCold& c = cold();
+        if (P->sample_time) {
+            const int64_t ns = c.n_samp;
+            __syncwarp();
+            if (lane == 0) {
+                P->sample_time[2 * c.t0 + ns] = now;
+                P->sample_nready[2 * c.t0 + ns] = nready;
+                c.n_samp = ns + 1;
+            }
+            __syncwarp();
         }
-        ++n_samp;
         if (pol() == TBSIM_POLICY_INSPIRIT) regulator_step(nready);
     }
 
@@ -264,7 +307,7 @@ struct Sim {
             const int32_t w = lane + 32 * j;
             if (w < W && busy[j] && fdirty[j]) {
                 double t = busy_until[j];
-                const int32_t* q = queue + static_cast<int64_t>(w) * qcap;
+                const int32_t* q = queue(w);
                 for (int32_t i = 0; i < qlen[j]; ++i) t += cost(static_cast<uint32_t>(q[i]) >> 24, kind[j]);
                 fsum[j] = t;
                 fdirty[j] = false;
@@ -317,12 +360,17 @@ struct Sim {
         int32_t m = TBSIM_MODE_EFFICIENCY;
         if (pol() == TBSIM_POLICY_INSPIRIT) {
             m = mode;
-            pop0 += m == 0;
-            pop1 += m == 1;
-            pop2 += m == 2;
+            if (lane == 0) {
+                SimCold& c = cold();
+                if (m == 0) c.pop0 += 1;
+                else if (m == 1) c.pop1 += 1;
+                else c.pop2 += 1;
+            }
         }
-        const int64_t qo = static_cast<int64_t>(w) * qcap;
-        const int32_t* q = queue + qo;
+        const int32_t* q = queue(w);
+        const KeyT* ka = qab(w);
+        const KeyT* ke = qef(w);
+        const PrioT* kp = qprio(w);
         uint64_t b0 = 0, b1 = 0, b2 = 0;
         int32_t bpos = INT_MAX;
         for (int32_t i = lane; i < ql; i += 32) {
@@ -330,16 +378,16 @@ struct Sim {
             if (pol() == TBSIM_POLICY_DMDAP) {
                 k0 = k1 = 1;
             } else if (m == TBSIM_MODE_ABILITY) {
-                k0 = ord_f64(static_cast<double>(qab[qo + i]));
+                k0 = ord_f64(static_cast<double>(ka[i]));
                 k1 = ord_f64(0.0);
             } else if (m == TBSIM_MODE_EFFICIENCY) {
-                k0 = ord_f64(static_cast<double>(qef[qo + i]));
+                k0 = ord_f64(static_cast<double>(ke[i]));
                 k1 = ord_f64(0.0);
             } else {
                 k0 = ord_f64(resident_fraction(q[i] & 0xffffff, nd));
-                k1 = ord_f64(static_cast<double>(qef[qo + i]));
+                k1 = ord_f64(static_cast<double>(ke[i]));
             }
-            const uint64_t k2 = ord_i64(qprio[qo + i]);
+            const uint64_t k2 = ord_i64(static_cast<int64_t>(kp[i]));
             const bool better = bpos == INT_MAX || k0 > b0 ||
                                 (k0 == b0 && (k1 > b1 || (k1 == b1 && k2 > b2)));
             if (better) { b0 = k0; b1 = k1; b2 = k2; bpos = i; }
@@ -367,26 +415,29 @@ struct Sim {
         nd = __shfl_sync(kFull, nd, owner);
         if (bz || ql == 0) return;
         const int32_t pick = select_entry(w, ql, nd);
-        const int64_t qo = static_cast<int64_t>(w) * qcap;
-        int32_t* q = queue + qo;
+        int32_t* q = queue(w);
+        KeyT* ka = qab(w);
+        KeyT* ke = qef(w);
+        PrioT* kp = qprio(w);
         const uint32_t e = static_cast<uint32_t>(q[pick]);
         __syncwarp();
         const bool ins = pol() == TBSIM_POLICY_INSPIRIT, pri = pol() >= TBSIM_POLICY_DMDAP;
-        for (int32_t base = pick; base < ql - 1; base += 32) {
-            const int32_t i = base + lane;
+        for (int32_t b0 = pick; b0 < ql - 1; b0 += 32) {
+            const int32_t i = b0 + lane;
             const bool mv = i < ql - 1;
-            int32_t val = 0, va = 0, ve = 0;
-            int64_t vp = 0;
+            int32_t val = 0;
+            KeyT va = 0, ve = 0;
+            PrioT vp = 0;
             if (mv) {
                 val = q[i + 1];
-                if (ins) { va = qab[qo + i + 1]; ve = qef[qo + i + 1]; }
-                if (pri) vp = qprio[qo + i + 1];
+                if (ins) { va = ka[i + 1]; ve = ke[i + 1]; }
+                if (pri) vp = kp[i + 1];
             }
             __syncwarp();
             if (mv) {
                 q[i] = val;
-                if (ins) { qab[qo + i] = va; qef[qo + i] = ve; }
-                if (pri) qprio[qo + i] = vp;
+                if (ins) { ka[i] = va; ke[i] = ve; }
+                if (pri) kp[i] = vp;
             }
             __syncwarp();
         }
@@ -394,6 +445,7 @@ struct Sim {
         const int32_t ty = static_cast<int32_t>(e >> 24);
         const int4 hd = head(task);  // issued before the queue bookkeeping
         nready -= 1;
+        const int64_t t0 = cold().t0;
         const int64_t slot = t0 + n_pop;
         if (P->pop_time && lane == 0) {
             P->pop_time[slot] = now;
@@ -408,8 +460,7 @@ struct Sim {
         const double start = now + xfer;
         const double end = start + exec;
         if ((xfer > 0.0 && !(start > now)) || !(end > now)) {
-            status = GS_DEGENERATE_TIME;
-            aux = task;
+            fail(GS_DEGENERATE_TIME, task);
             return;
         }
         if (lane == 0) {  // dispatch log: sequential, scattered by k_sim_scatter
@@ -447,67 +498,108 @@ struct Sim {
         const bool too_large = ka < 0;  // pop keys beyond int32 or > 2^24 successor entries
         const int64_t* inb = reinterpret_cast<const int64_t*>(lists(hd));
         const int32_t w = select_worker(inb, reinterpret_cast<const int32_t*>(inb + hd.y), hd.y, ty);
-        if (w < 0) { status = GS_NO_WORKER; aux = task; return -1; }
-        if (too_large) { status = GS_TOO_LARGE; aux = task; return -1; }
+        if (w < 0) { fail(GS_NO_WORKER, task); return -1; }
+        if (too_large) { fail(GS_TOO_LARGE, task); return -1; }
+        // compact keys: ability/efficiency < n < 2^15 always fit; a priority
+        // beyond int32 sends the graph to the wide rerun
+        if (COMPACT && pol() >= TBSIM_POLICY_DMDAP && kp != static_cast<int64_t>(static_cast<PrioT>(kp))) {
+            fail(GS_QUEUE_OVERFLOW, task);
+            return -1;
+        }
         const int j = w >> 5, owner = w & 31;
         int32_t ovf = 0;
 #pragma unroll
         for (int jj = 0; jj < WPL; ++jj)
             if (jj == j && lane == owner) {
-                if (qlen[jj] >= qcap) {
+                if (qlen[jj] >= P->qcap) {
                     ovf = 1;
                 } else {
-                    const int64_t at = static_cast<int64_t>(w) * qcap + qlen[jj];
-                    queue[at] = (ty << 24) | task;
-                    if (pol() == TBSIM_POLICY_INSPIRIT) { qab[at] = ka; qef[at] = ke; }
-                    if (pol() >= TBSIM_POLICY_DMDAP) qprio[at] = kp;
+                    const int32_t at = qlen[jj];
+                    queue(w)[at] = (ty << 24) | task;
+                    if (pol() == TBSIM_POLICY_INSPIRIT) {
+                        qab(w)[at] = static_cast<KeyT>(ka);
+                        qef(w)[at] = static_cast<KeyT>(ke);
+                    }
+                    if (pol() >= TBSIM_POLICY_DMDAP) qprio(w)[at] = static_cast<PrioT>(kp);
                     qlen[jj] += 1;
                     if (busy[jj] && !fdirty[jj]) fsum[jj] += cost(ty, kind[jj]);
                 }
             }
-        if (__shfl_sync(kFull, ovf, owner)) { status = GS_QUEUE_OVERFLOW; aux = task; return -1; }
+        if (__shfl_sync(kFull, ovf, owner)) { fail(GS_QUEUE_OVERFLOW, task); return -1; }
         __syncwarp();
         nready += 1;
-        if (P->push_time && lane == 0) {
-            P->push_time[t0 + n_push] = now;
-            P->push_task[t0 + n_push] = task;
+        if (P->push_time) {
+            SimCold& c = cold();
+            const int64_t np = c.n_push;
+            __syncwarp();
+            if (lane == 0) {
+                P->push_time[c.t0 + np] = now;
+                P->push_task[c.t0 + np] = task;
+                c.n_push = np + 1;
+            }
+            __syncwarp();
         }
-        ++n_push;
         queue_event();
         return w;
     }
 
+    // Appends the lanes with `rdy` (task v) to the ready list in lane order:
+    // each ready task's unmet slot (now dead) links to the next ready task.
+    __device__ __forceinline__ void ready_append(bool rdy, int32_t v) {
+        const unsigned bal = __ballot_sync(kFull, rdy);
+        if (!bal) return;
+        UnmetT* um = unmet();
+        const unsigned above = bal & ~((2u << lane) - 1u);  // (2u << 31) == 0: no lanes above 31
+        const int32_t nv = __shfl_sync(kFull, v, above ? __ffs(above) - 1 : lane);
+        const int first = __ffs(bal) - 1, last = 31 - __clz(bal);
+        if (rdy && above) um[v] = static_cast<UnmetT>(nv);
+        if (lane == first && rcount > 0) um[rtail] = static_cast<UnmetT>(v);
+        const int32_t fv = __shfl_sync(kFull, v, first);
+        rtail = __shfl_sync(kFull, v, last);
+        if (rcount == 0) rhead = fv;
+        rcount += __popc(bal);
+    }
+
     __device__ __forceinline__ void run() {  // Simulation::run, engine.cpp:207-248
         // roots in position order (engine.cpp:218-221)
+        UnmetT* um = unmet();
+        ResidT* rs = resid();
+        const int32_t* doff = P->b.dep_off + cold().t0 + cold().g;
         rcount = 0;
-        for (int32_t base = 0; base < n; base += 32) {
-            const int32_t v = base + lane;
+        for (int32_t b0 = 0; b0 < n; b0 += 32) {
+            const int32_t v = b0 + lane;
             bool root = false;
             if (v < n) {
                 const int32_t deg = __ldg(&doff[v + 1]) - __ldg(&doff[v]);
-                unmet[v] = static_cast<UnmetT>(deg);
+                um[v] = static_cast<UnmetT>(deg);
                 root = deg == 0;
             }
-            const unsigned bal = __ballot_sync(kFull, root);
-            if (root) ready[rcount + __popc(bal & ((1u << lane) - 1u))] = static_cast<ReadyT>(v);
-            rcount += __popc(bal);
+            __syncwarp();
+            ready_append(root, v);
+            __syncwarp();
         }
-        for (int32_t h = lane; h < nh; h += 32) resid[h] = 1u;  // engine.cpp:215-216
+        {
+            const int64_t g = cold().g;
+            const int32_t nh = static_cast<int32_t>(P->b.handle_base[g + 1] - P->b.handle_base[g]);
+            for (int32_t h = lane; h < nh; h += 32) rs[h] = 1u;  // engine.cpp:215-216
+        }
         __syncwarp();
         // One loop, one dispatch site: phase A pushes the tasks made ready
         // at `now` in creation order (2)+(3); phase B drains the worker
         // events stamped `now` in enqueue order (1), then time advances.
-        int32_t r = 0;
         bool events = false;
         uint64_t mt = 0;
         for (;;) {
             int32_t w;
             if (!events) {
-                if (r < rcount) {
-                    w = on_push(ready[r++]);
+                if (rcount > 0) {
+                    const int32_t v = rhead;
+                    const int32_t nx = rcount > 1 ? static_cast<int32_t>(um[v]) : 0;
+                    --rcount;
+                    w = on_push(v);
+                    rhead = nx;
                     if (status != GS_OK) return;
                 } else {
-                    rcount = r = 0;
                     // next worker-event time
                     uint64_t lt = ~0ull;
 #pragma unroll
@@ -558,7 +650,7 @@ struct Sim {
                 if (!is_done) {  // TransferDone: inputs resident (engine.cpp:168-172)
                     for (int32_t k = lane; k < nin; k += 32) {
                         const int32_t h = __ldg(&inh[k]);
-                        resid[h] = static_cast<ResidT>(resid[h] | bit);
+                        rs[h] = static_cast<ResidT>(rs[h] | bit);
                     }
                     __syncwarp();
                     continue;
@@ -567,31 +659,29 @@ struct Sim {
                 const int32_t* outl = inh + nin;
                 for (int32_t k = lane; k < nout; k += 32) {
                     const int32_t h = __ldg(&outl[k]);
-                    resid[h] = static_cast<ResidT>(resid[h] | bit);
+                    rs[h] = static_cast<ResidT>(rs[h] | bit);
                 }
 #pragma unroll
                 for (int j = 0; j < WPL; ++j)
                     if (j == (w >> 5) && lane == owner) busy[j] = false;
                 completed += 1;
-                makespan = now > makespan ? now : makespan;
                 // successors: sorted, multi-edges adjacent; the lowest lane of
                 // each run of equal ids decrements by the run length
                 const int32_t* succl = outl + nout;
                 const int32_t s1 = static_cast<int32_t>(static_cast<uint32_t>(hd.w) & 0xffffffu);
-                for (int32_t base = 0; base < s1; base += 32) {
-                    const int32_t k = base + lane;
+                for (int32_t b0 = 0; b0 < s1; b0 += 32) {
+                    const int32_t k = b0 + lane;
                     const bool valid = k < s1;
                     const int32_t sv = valid ? __ldg(&succl[k]) : -1 - lane;
                     const unsigned peers = __match_any_sync(kFull, sv);
                     bool rdy = false;
                     if (valid && (__ffs(peers) - 1) == lane) {
-                        const int32_t left = static_cast<int32_t>(unmet[sv]) - __popc(peers);
-                        unmet[sv] = static_cast<UnmetT>(left);
+                        const int32_t left = static_cast<int32_t>(um[sv]) - __popc(peers);
+                        um[sv] = static_cast<UnmetT>(left);
                         rdy = left == 0;
                     }
-                    const unsigned bal = __ballot_sync(kFull, rdy);
-                    if (rdy) ready[rcount + __popc(bal & ((1u << lane) - 1u))] = static_cast<ReadyT>(sv);
-                    rcount += __popc(bal);
+                    __syncwarp();
+                    ready_append(rdy, sv);
                     __syncwarp();
                 }
                 __syncwarp();
@@ -614,25 +704,12 @@ __device__ void simulate_impl(const SimParams& p) {
     if constexpr (SMEM) base = smem + warp_in_block * static_cast<int32_t>(p.state_bytes);
     else base = p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
     const DevBatch& b = p.b;
-    const SimLayout& L = p.layout;  // offsets precomputed on the host
     using S = Sim<WPL, COMPACT, POL>;
     S s;
     s.P = &p;
+    s.base = base;
     s.lane = lane;
-    s.unmet = reinterpret_cast<typename S::UnmetT*>(base + L.unmet);
-    s.resid = reinterpret_cast<typename S::ResidT*>(base + L.resid);
-    s.ready = reinterpret_cast<typename S::ReadyT*>(base + L.ready);
-    s.queue = reinterpret_cast<int32_t*>(base + L.queue);
-    s.qab = reinterpret_cast<int32_t*>(base + L.qab);
-    s.qef = reinterpret_cast<int32_t*>(base + L.qef);
-    s.qprio = reinterpret_cast<int64_t*>(base + L.qprio);
-    s.samp_t = reinterpret_cast<double*>(base + L.ring);
-    s.samp_n = reinterpret_cast<int64_t*>(base + L.ring + 8 * p.ring);
-    s.costs = reinterpret_cast<double*>(base + L.costs);
-    s.bw = reinterpret_cast<double*>(base + L.bw);
-    s.qcap = p.qcap;
-    s.ring_mask = p.ring - 1;
-    s.policy_rt = p.policy;
+    SimCold& c = s.cold();
     int32_t loaded_pf = -1;
 
     for (;;) {
@@ -641,26 +718,23 @@ __device__ void simulate_impl(const SimParams& p) {
         item = __shfl_sync(kFull, item, 0);
         if (item >= static_cast<unsigned long long>(p.n_items)) break;
         const int64_t g = p.graph_list ? p.graph_list[item] : static_cast<int64_t>(item);
-        s.g = g;
-        s.t0 = b.task_base[g];
-        s.n = static_cast<int32_t>(b.task_base[g + 1] - s.t0);
-        s.nh = static_cast<int32_t>(b.handle_base[g + 1] - b.handle_base[g]);
-        s.doff = b.dep_off + s.t0 + g;
-        s.hdr = p.hdr + s.t0;
-        s.adj = p.adj;
+        const int64_t t0 = b.task_base[g];
+        s.n = static_cast<int32_t>(b.task_base[g + 1] - t0);
+        s.hdr = p.hdr + t0;
         const int32_t pfi = p.platform_of ? p.platform_of[g] : 0;
         const DevPlatform* pf = p.platforms + pfi;
         s.W = pf->n_workers;
         s.nn = pf->n_nodes;
         s.lat = pf->latency_ms;
+        __syncwarp();
         if (pfi != loaded_pf) {  // platform tables into this warp's state
-            __syncwarp();
+            double* costs = reinterpret_cast<double*>(base + p.layout.costs);
+            double* bw = reinterpret_cast<double*>(base + p.layout.bw);
             for (int i = lane; i < p.n_types; i += 32) {
-                s.costs[2 * i] = pf->costs.cpu[i];
-                s.costs[2 * i + 1] = pf->costs.gpu[i];
+                costs[2 * i] = pf->costs.cpu[i];
+                costs[2 * i + 1] = pf->costs.gpu[i];
             }
-            for (int i = lane; i < s.nn * s.nn; i += 32) s.bw[i] = pf->bw[(i / s.nn) * kMaxNodes + i % s.nn];
-            __syncwarp();
+            for (int i = lane; i < s.nn * s.nn; i += 32) bw[i] = pf->bw[(i / s.nn) * kMaxNodes + i % s.nn];
             loaded_pf = pfi;
         }
 #pragma unroll
@@ -678,60 +752,71 @@ __device__ void simulate_impl(const SimParams& p) {
             s.xtask[j] = s.dtask[j] = 0;
         }
         s.now = 0.0;
-        s.makespan = 0.0;
         s.nready = 0;
         s.completed = 0;
+        s.rcount = s.rhead = s.rtail = 0;
         s.seq = 0;
-        s.n_push = s.n_pop = s.n_samp = 0;
-        s.pop0 = s.pop1 = s.pop2 = 0;
+        s.n_pop = 0;
         s.status = GS_OK;
-        s.aux = -1;
-        // regulator config: explicit, or default_regulator_config
-        // (policies.cpp:139-151) from the worker count and the median
-        if (p.reg) {
-            s.cfg = p.reg[g];
-        } else {
-            const int64_t nw = s.W;
-            const int64_t tw = (nw + 3) / 4 > 2 ? (nw + 3) / 4 : 2;
-            s.cfg.task_window = tw;
-            s.cfg.s_inc = nw;
-            s.cfg.k_inc = static_cast<double>(nw) / p.median[g * p.median_stride];
-            s.cfg.s_dec = tw;
-            s.cfg.c = (tw + 1) / 2;
-            s.cfg.dec_step = tw;
-            s.cfg.slope_samples = 8;
+        if (lane == 0) {
+            c.g = g;
+            c.t0 = t0;
+            c.n_push = c.n_samp = 0;
+            c.pop0 = c.pop1 = c.pop2 = 0;
+            c.aux = -1;
+            // regulator config: explicit, or default_regulator_config
+            // (policies.cpp:139-151) from the worker count and the median
+            if (p.reg) {
+                c.cfg = p.reg[g];
+            } else {
+                const int64_t nw = s.W;
+                const int64_t tw = (nw + 3) / 4 > 2 ? (nw + 3) / 4 : 2;
+                c.cfg.task_window = tw;
+                c.cfg.s_inc = nw;
+                c.cfg.k_inc = static_cast<double>(nw) / p.median[g * p.median_stride];
+                c.cfg.s_dec = tw;
+                c.cfg.c = (tw + 1) / 2;
+                c.cfg.dec_step = tw;
+                c.cfg.slope_samples = 8;
+            }
         }
         // regulator state: caller-provided (in/out) or RegulatorState{}
         if (p.reg_state) {
             const tbsim_regulator_state& rs = p.reg_state[g];
-            s.mode = rs.mode; s.phase = rs.phase; s.peak = rs.peak; s.prev_nready = rs.prev_nready;
-            s.last_trigger = rs.last_trigger_nready; s.s_dec_count = rs.s_dec_count; s.cur_k = rs.cur_k;
-            s.r_head = 0;
-            s.r_count = rs.n_samples;
-            for (int i = lane; i < rs.n_samples; i += 32) { s.samp_t[i] = rs.sample_time[i]; s.samp_n[i] = rs.sample_nready[i]; }
+            s.mode = rs.mode;
+            if (lane == 0) {
+                c.phase = rs.phase; c.peak = rs.peak; c.prev_nready = rs.prev_nready;
+                c.last_trigger = rs.last_trigger_nready; c.s_dec_count = rs.s_dec_count; c.cur_k = rs.cur_k;
+                c.r_head = 0;
+                c.r_count = rs.n_samples;
+            }
+            for (int i = lane; i < rs.n_samples; i += 32) { s.samp_t()[i] = rs.sample_time[i]; s.samp_n()[i] = rs.sample_nready[i]; }
         } else {
-            s.mode = TBSIM_MODE_EFFICIENCY; s.phase = TBSIM_PHASE_INC; s.peak = 0; s.prev_nready = 0;
-            s.last_trigger = 0; s.s_dec_count = 1; s.cur_k = 0.0; s.r_head = 0; s.r_count = 0;
+            s.mode = TBSIM_MODE_EFFICIENCY;
+            if (lane == 0) {
+                c.phase = TBSIM_PHASE_INC; c.peak = 0; c.prev_nready = 0;
+                c.last_trigger = 0; c.s_dec_count = 1; c.cur_k = 0.0; c.r_head = 0; c.r_count = 0;
+            }
         }
         __syncwarp();
         s.run();
+        __syncwarp();
         if (s.status == GS_OK && s.completed == s.n) {
-            if (lane == 0) p.n_disp[g] = static_cast<int32_t>(s.n_pop);
+            if (lane == 0) p.n_disp[g] = s.n_pop;
         } else {
             // failed graph: outputs written here (undispatched tasks keep
             // worker -1), k_sim_scatter skips it
-            __syncwarp();
             for (int32_t v = lane; v < s.n; v += 32) {
-                p.worker[s.t0 + v] = -1;
-                p.start_ms[s.t0 + v] = 0.0;
-                p.end_ms[s.t0 + v] = 0.0;
+                p.worker[t0 + v] = -1;
+                p.start_ms[t0 + v] = 0.0;
+                p.end_ms[t0 + v] = 0.0;
             }
             __syncwarp();
             for (int64_t i = lane; i < s.n_pop; i += 32) {
-                const SimLog e = p.log[s.t0 + i];
-                p.worker[s.t0 + e.task] = e.worker;
-                p.start_ms[s.t0 + e.task] = e.start;
-                p.end_ms[s.t0 + e.task] = e.end;
+                const SimLog e = p.log[t0 + i];
+                p.worker[t0 + e.task] = e.worker;
+                p.start_ms[t0 + e.task] = e.start;
+                p.end_ms[t0 + e.task] = e.end;
             }
             if (lane == 0) p.n_disp[g] = -1;
         }
@@ -739,28 +824,31 @@ __device__ void simulate_impl(const SimParams& p) {
             int32_t st = s.status;
             if (st == GS_OK && s.completed != s.n) st = GS_STUCK;
             p.status[g] = st;
-            p.status_aux[g] = s.aux;
-            p.makespan[g] = s.makespan;
+            p.status_aux[g] = c.aux;
+            // makespan: the last completion (times only grow; a completed
+            // graph's last event is a TaskDone)
+            p.makespan[g] = s.completed > 0 ? s.now : 0.0;
             p.completed[g] = s.completed;
             if (p.pop_counts) {
-                p.pop_counts[3 * g + 0] = s.pop0;
-                p.pop_counts[3 * g + 1] = s.pop1;
-                p.pop_counts[3 * g + 2] = s.pop2;
+                p.pop_counts[3 * g + 0] = c.pop0;
+                p.pop_counts[3 * g + 1] = c.pop1;
+                p.pop_counts[3 * g + 2] = c.pop2;
             }
             if (p.reg_state && p.policy == TBSIM_POLICY_INSPIRIT && s.status == GS_OK) {
                 tbsim_regulator_state& rs = p.reg_state[g];
-                rs.mode = s.mode; rs.phase = s.phase; rs.peak = s.peak; rs.prev_nready = s.prev_nready;
-                rs.last_trigger_nready = s.last_trigger; rs.s_dec_count = s.s_dec_count; rs.cur_k = s.cur_k;
-                rs.n_samples = s.r_count;
+                rs.mode = s.mode; rs.phase = c.phase; rs.peak = c.peak; rs.prev_nready = c.prev_nready;
+                rs.last_trigger_nready = c.last_trigger; rs.s_dec_count = c.s_dec_count; rs.cur_k = c.cur_k;
+                rs.n_samples = c.r_count;
             }
         }
+        __syncwarp();
         if (p.reg_state && p.policy == TBSIM_POLICY_INSPIRIT && s.status == GS_OK) {
-            __syncwarp();
             tbsim_regulator_state& rs = p.reg_state[g];
-            for (int i = lane; i < s.r_count; i += 32) {
-                const int idx = (s.r_head + i) & s.ring_mask;
-                rs.sample_time[i] = s.samp_t[idx];
-                rs.sample_nready[i] = s.samp_n[idx];
+            const int ring_mask = p.ring - 1;
+            for (int i = lane; i < c.r_count; i += 32) {
+                const int idx = (c.r_head + i) & ring_mask;
+                rs.sample_time[i] = s.samp_t()[idx];
+                rs.sample_nready[i] = s.samp_n()[idx];
             }
         }
         __syncwarp();
@@ -847,15 +935,16 @@ __global__ void __launch_bounds__(256) k_sim_scatter(DevBatch b, const SimLog* l
     }
 }
 
-#define TBSIM_SIM_KERNEL(NAME, WPL, COMPACT, POL)                                                     \
-    __global__ void __launch_bounds__(256, 2) NAME(const __grid_constant__ SimParams p) {               \
+#define TBSIM_SIM_KERNEL(NAME, WPL, COMPACT, POL, THREADS, MINB)                                     \
+    __global__ void __launch_bounds__(THREADS, MINB) NAME(const __grid_constant__ SimParams p) {        \
         if (p.use_smem) simulate_impl<WPL, COMPACT, POL, true>(p);                                     \
         else simulate_impl<WPL, COMPACT, POL, false>(p);                                               \
     }
-TBSIM_SIM_KERNEL(k_simulate_w1c, 1, true, -1)
-TBSIM_SIM_KERNEL(k_simulate_w2c, 2, true, -1)
-TBSIM_SIM_KERNEL(k_simulate_w1, 1, false, -1)
-TBSIM_SIM_KERNEL(k_simulate_w2, 2, false, -1)
+// <= 32 workers, compact: 4-warp CTAs, 7 per SM (<= 72 registers)
+TBSIM_SIM_KERNEL(k_simulate_w1c, 1, true, -1, 128, 7)
+TBSIM_SIM_KERNEL(k_simulate_w2c, 2, true, -1, 256, 2)
+TBSIM_SIM_KERNEL(k_simulate_w1, 1, false, -1, 256, 2)
+TBSIM_SIM_KERNEL(k_simulate_w2, 2, false, -1, 256, 2)
 #undef TBSIM_SIM_KERNEL
 
 }  // namespace tbsim_dev

@@ -7,16 +7,33 @@
 
 namespace tbsim_dev {
 
+// Rarely touched per-warp scalars (regulator, counters, graph ids) live in
+// the warp's state memory instead of registers: the event loop keeps only
+// the hot state in registers, which lets more warps share an SM.
+struct SimCold {
+    tbsim_regulator_cfg cfg;
+    int64_t peak, prev_nready, last_trigger, s_dec_count;
+    double cur_k;
+    int64_t n_push, n_samp, pop0, pop1, pop2;
+    int64_t g, t0;
+    int32_t phase, r_head, r_count, aux;
+};
+
 // Per-warp state layout (bytes, 16-aligned sections).  Compact state
-// (n < 32768, <= 8 memory nodes) stores unmet counts and the ready list as
-// int16 and residency masks as uint8.
+// (n < 32768, <= 8 memory nodes) stores unmet counts as int16, residency
+// masks as uint8, and queue keys narrowed: ability/efficiency int16, static
+// priority int32 (a priority beyond int32 sends the graph to a wide rerun).
+// The ready list has no section: it is a linked list threaded through the
+// unmet counters of ready tasks (a ready task's counter is never read again).
 struct SimLayout {
-    int64_t unmet, resid, ready, queue, qab, qef, qprio, ring, costs, bw, total;
+    int64_t cold, unmet, resid, queue, qab, qef, qprio, ring, costs, bw, total;
 };
 
 // Pop keys cached per queue entry: inspirit (policy 4) ability + efficiency
-// (int32) + static priority (int64); dmdap (3) the priority only.
-__host__ __device__ inline int key_bytes(int32_t policy) { return policy == 4 ? 16 : policy == 3 ? 8 : 0; }
+// + static priority; dmdap (3) the priority only.
+__host__ __device__ inline int key_bytes(int32_t policy, bool compact) {
+    return policy == 4 ? (compact ? 8 : 16) : policy == 3 ? (compact ? 4 : 8) : 0;
+}
 
 __host__ __device__ inline SimLayout sim_layout(int64_t max_n, int64_t max_h, int64_t max_workers, int64_t qcap,
                                                 int64_t ring, int64_t n_types, int64_t max_nodes, bool compact,
@@ -24,14 +41,15 @@ __host__ __device__ inline SimLayout sim_layout(int64_t max_n, int64_t max_h, in
     auto al = [](int64_t x) { return (x + 15) & ~int64_t(15); };
     SimLayout L;
     int64_t off = 0;
+    L.cold = off; off += al(static_cast<int64_t>(sizeof(SimCold)));
     L.unmet = off; off += al((compact ? 2 : 4) * max_n);
     L.resid = off; off += al((compact ? 1 : 4) * max_h);
-    L.ready = off; off += al((compact ? 2 : 4) * max_n);
     L.queue = off; off += al(4 * max_workers * qcap);
     const bool ins = policy == 4, pri = policy >= 3;
-    L.qab = off; off += ins ? al(4 * max_workers * qcap) : 0;
-    L.qef = off; off += ins ? al(4 * max_workers * qcap) : 0;
-    L.qprio = off; off += pri ? al(8 * max_workers * qcap) : 0;
+    const int kb = compact ? 2 : 4;
+    L.qab = off; off += ins ? al(kb * max_workers * qcap) : 0;
+    L.qef = off; off += ins ? al(kb * max_workers * qcap) : 0;
+    L.qprio = off; off += pri ? al(2 * kb * max_workers * qcap) : 0;
     L.ring = off; off += al(16 * ring);
     L.costs = off; off += al(16 * n_types);
     L.bw = off; off += al(8 * max_nodes * max_nodes);
@@ -99,6 +117,7 @@ struct SimParams {
     int64_t state_bytes;              // bytes per warp state
     int32_t qcap;                     // queue capacity per worker
     int32_t use_smem;
+    int32_t force_wide;               // rerun: wide (non-compact) state and keys
     int32_t max_workers;
     int32_t max_nodes;                // platform copy: nodes x nodes bandwidth
     int32_t n_types;                  // platform copy: cost rows
@@ -116,7 +135,7 @@ __global__ void k_sim_pack(DevBatch b, const int64_t* ability, const int64_t* ef
 __global__ void k_sim_scatter(DevBatch b, const SimLog* log, const int32_t* n_disp, int32_t* worker, double* start_ms,
                               double* end_ms);
 
-__global__ void k_simulate_w1c(const __grid_constant__ SimParams p);  // <= 32 workers, compact state
+__global__ void k_simulate_w1c(const __grid_constant__ SimParams p);  // <= 32 workers, compact state (128-thread CTAs)
 __global__ void k_simulate_w2c(const __grid_constant__ SimParams p);  // <= 64 workers, compact state
 __global__ void k_simulate_w1(const __grid_constant__ SimParams p);   // <= 32 workers, wide state
 __global__ void k_simulate_w2(const __grid_constant__ SimParams p);   // <= 64 workers, wide state
