@@ -61,8 +61,6 @@ struct Sim {
     // ---- graph
     int32_t n;
     const SimTaskHdr* hdr;  // this graph's packed records
-    int32_t W, nn;
-    double lat;
     __device__ __forceinline__ int32_t pol() const { return POL >= 0 ? POL : P->policy; }
     // ---- state sections
     __device__ __forceinline__ SimCold& cold() const { return *reinterpret_cast<SimCold*>(base + P->layout.cold); }
@@ -84,17 +82,31 @@ struct Sim {
         return reinterpret_cast<const double*>(base + P->layout.costs)[2 * ty + k];
     }
     __device__ __forceinline__ double bw(int32_t i) const { return reinterpret_cast<const double*>(base + P->layout.bw)[i]; }
-    // ---- lane-owned workers
-    int32_t kind[WPL], node[WPL], qlen[WPL];
-    bool busy[WPL], fdirty[WPL];
+    // ---- lane-owned workers.  wk packs valid (w < W) | gpu kind << 1 |
+    // busy << 2 | free_at dirty << 3 | memory node << 4; a pending
+    // TransferDone / TaskDone is (time, seq << kSeqShift | task) -- compact
+    // graphs have < 2^15 tasks and < 2^16 events, so that is one 32-bit word
+    using SlotT = typename std::conditional<COMPACT, uint32_t, uint64_t>::type;
+    static constexpr int kSeqShift = COMPACT ? 16 : 32;
+    static constexpr SlotT kNoSlot = ~SlotT(0);
+    uint32_t wk[WPL];
+    int32_t qlen[WPL];
     double busy_until[WPL], fsum[WPL];
     double xt[WPL], dt[WPL];
-    uint32_t xs[WPL], ds[WPL];
-    int32_t xtask[WPL], dtask[WPL];
+    SlotT xs[WPL], ds[WPL];
+    __device__ __forceinline__ static SlotT mk_slot(uint32_t sq, int32_t task) {
+        return (static_cast<SlotT>(sq) << kSeqShift) | static_cast<SlotT>(static_cast<uint32_t>(task));
+    }
+    __device__ __forceinline__ static int32_t slot_task(SlotT x) {
+        return static_cast<int32_t>(x & ((static_cast<SlotT>(1) << kSeqShift) - 1));
+    }
+    __device__ __forceinline__ int32_t kind_of(int j) const { return (wk[j] >> 1) & 1u; }
+    __device__ __forceinline__ bool busy_of(int j) const { return (wk[j] >> 2) & 1u; }
+    __device__ __forceinline__ int32_t node_of(int j) const { return static_cast<int32_t>(wk[j] >> 4); }
     // ---- warp-uniform hot scalars
     int lane;
     double now;
-    int64_t nready;
+    int32_t nready;
     int32_t completed, rcount, rhead, rtail;  // ready list: rcount tasks linked from rhead
     uint32_t seq;
     int32_t n_pop;
@@ -118,6 +130,7 @@ struct Sim {
     // lowest node; Platform::transfer_time_ms (platform.cpp:56-63).
     __device__ __forceinline__ double transfer_one(uint32_t m, int64_t bytes, int32_t to) const {
         if ((m >> to) & 1u) return 0.0;
+        const int32_t nn = cold().nn;
         int32_t best = 0;
         double bbw = -1.0;
         for (uint32_t mm = m; mm; mm &= mm - 1) {
@@ -125,7 +138,7 @@ struct Sim {
             const double b = bw(nd * nn + to);
             if (b > bbw) { bbw = b; best = nd; }
         }
-        return lat + static_cast<double>(bytes) / bw(best * nn + to);
+        return cold().lat + static_cast<double>(bytes) / bw(best * nn + to);
     }
 
     // transfer_total_ms (engine.cpp:105-110) for node `want` (may differ per
@@ -292,12 +305,12 @@ struct Sim {
             __syncwarp();
             if (lane == 0) {
                 P->sample_time[2 * c.t0 + ns] = now;
-                P->sample_nready[2 * c.t0 + ns] = nready;
+                P->sample_nready[2 * c.t0 + ns] = static_cast<int64_t>(nready);
                 c.n_samp = ns + 1;
             }
             __syncwarp();
         }
-        if (pol() == TBSIM_POLICY_INSPIRIT) regulator_step(nready);
+        if (pol() == TBSIM_POLICY_INSPIRIT) regulator_step(static_cast<int64_t>(nready));
     }
 
     // ---------------------------------------------------------- push rules
@@ -305,12 +318,13 @@ struct Sim {
 #pragma unroll
         for (int j = 0; j < WPL; ++j) {
             const int32_t w = lane + 32 * j;
-            if (w < W && busy[j] && fdirty[j]) {
+            if ((wk[j] & 13u) == 13u) {  // valid, busy, dirty
                 double t = busy_until[j];
                 const int32_t* q = queue(w);
-                for (int32_t i = 0; i < qlen[j]; ++i) t += cost(static_cast<uint32_t>(q[i]) >> 24, kind[j]);
+                const int32_t kd = kind_of(j);
+                for (int32_t i = 0; i < qlen[j]; ++i) t += cost(static_cast<uint32_t>(q[i]) >> 24, kd);
                 fsum[j] = t;
-                fdirty[j] = false;
+                wk[j] &= ~8u;
             }
         }
     }
@@ -324,21 +338,21 @@ struct Sim {
         for (int j = 0; j < WPL; ++j) xfer[j] = 0.0;
         if (pol() >= TBSIM_POLICY_DMDA) {
 #pragma unroll
-            for (int j = 0; j < WPL; ++j) xfer[j] = transfer_total_lanes(inb, inh, nin, node[j]);
+            for (int j = 0; j < WPL; ++j) xfer[j] = transfer_total_lanes(inb, inh, nin, node_of(j));
         }
         uint64_t bk = ~0ull;
         int32_t bwk = INT_MAX;
 #pragma unroll
         for (int j = 0; j < WPL; ++j) {
             const int32_t w = lane + 32 * j;
-            if (w >= W) continue;
-            const double ce = cost(ty, kind[j]);
+            if (!(wk[j] & 1u)) continue;
+            const double ce = cost(ty, kind_of(j));
             if (!(ce > 0.0)) continue;
             double key;
             if (pol() == TBSIM_POLICY_FIFO) {
-                key = static_cast<double>(qlen[j]) + (busy[j] ? 1.0 : 0.0);
+                key = static_cast<double>(qlen[j]) + (busy_of(j) ? 1.0 : 0.0);
             } else {
-                const double fa = busy[j] ? fsum[j] : now;
+                const double fa = busy_of(j) ? fsum[j] : now;
                 const double st = now < fa ? fa : now;  // std::max(now, free_at)
                 if (pol() == TBSIM_POLICY_DM) key = st + ce;
                 else key = (st + xfer[j]) + ce;
@@ -408,7 +422,7 @@ struct Sim {
         int32_t ql = 0, bz = 0, kd = 0, nd = 0;
 #pragma unroll
         for (int jj = 0; jj < WPL; ++jj)
-            if (jj == j) { ql = qlen[jj]; bz = busy[jj]; kd = kind[jj]; nd = node[jj]; }
+            if (jj == j) { ql = qlen[jj]; bz = busy_of(jj); kd = kind_of(jj); nd = node_of(jj); }
         ql = __shfl_sync(kFull, ql, owner);
         bz = __shfl_sync(kFull, bz, owner);
         kd = __shfl_sync(kFull, kd, owner);
@@ -476,11 +490,10 @@ struct Sim {
         for (int jj = 0; jj < WPL; ++jj)
             if (jj == j && lane == owner) {
                 qlen[jj] -= 1;
-                busy[jj] = true;
+                wk[jj] |= 12u;  // busy, free_at dirty
                 busy_until[jj] = end;
-                fdirty[jj] = true;
-                if (xfer > 0.0) { xt[jj] = start; xs[jj] = sx; xtask[jj] = task; }
-                dt[jj] = end; ds[jj] = sd; dtask[jj] = task;
+                if (xfer > 0.0) { xt[jj] = start; xs[jj] = mk_slot(sx, task); }
+                dt[jj] = end; ds[jj] = mk_slot(sd, task);
             }
     }
 
@@ -522,7 +535,7 @@ struct Sim {
                     }
                     if (pol() >= TBSIM_POLICY_DMDAP) qprio(w)[at] = static_cast<PrioT>(kp);
                     qlen[jj] += 1;
-                    if (busy[jj] && !fdirty[jj]) fsum[jj] += cost(ty, kind[jj]);
+                    if ((wk[jj] & 12u) == 4u) fsum[jj] += cost(ty, kind_of(jj));  // busy, not dirty
                 }
             }
         if (__shfl_sync(kFull, ovf, owner)) { fail(GS_QUEUE_OVERFLOW, task); return -1; }
@@ -604,8 +617,8 @@ struct Sim {
                     uint64_t lt = ~0ull;
 #pragma unroll
                     for (int j = 0; j < WPL; ++j) {
-                        if (xs[j] != kNone) lt = min(lt, dbits(xt[j]));
-                        if (ds[j] != kNone) lt = min(lt, dbits(dt[j]));
+                        if (xs[j] != kNoSlot) lt = min(lt, dbits(xt[j]));
+                        if (ds[j] != kNoSlot) lt = min(lt, dbits(dt[j]));
                     }
                     mt = warp_min_u64(lt);
                     if (mt == ~0ull) break;
@@ -614,14 +627,17 @@ struct Sim {
                     continue;
                 }
             } else {
-                uint32_t ls = kNone;
+                // the earliest-enqueued event stamped `now`: slots order by seq
+                SlotT ls = kNoSlot;
 #pragma unroll
                 for (int j = 0; j < WPL; ++j) {
-                    if (xs[j] != kNone && dbits(xt[j]) == mt) ls = min(ls, xs[j]);
-                    if (ds[j] != kNone && dbits(dt[j]) == mt) ls = min(ls, ds[j]);
+                    if (xs[j] != kNoSlot && dbits(xt[j]) == mt) ls = min(ls, xs[j]);
+                    if (ds[j] != kNoSlot && dbits(dt[j]) == mt) ls = min(ls, ds[j]);
                 }
-                const uint32_t ms = __reduce_min_sync(kFull, ls);
-                if (ms == kNone) {
+                SlotT ms;
+                if constexpr (COMPACT) ms = __reduce_min_sync(kFull, ls);
+                else ms = warp_min_u64(ls);
+                if (ms == kNoSlot) {
                     events = false;
                     continue;
                 }
@@ -630,19 +646,15 @@ struct Sim {
                 if (lane == owner) {
 #pragma unroll
                     for (int j = 0; j < WPL; ++j) {
-                        if (xs[j] == ms) { info = (j << 30) | xtask[j]; xs[j] = kNone; }
-                        if (ds[j] == ms) { info = (1 << 29) | (j << 30) | dtask[j]; ds[j] = kNone; }
+                        if (xs[j] == ms) { info = (j << 30) | node_of(j); xs[j] = kNoSlot; }
+                        if (ds[j] == ms) { info = (1 << 29) | (j << 30) | node_of(j); ds[j] = kNoSlot; }
                     }
                 }
                 info = __shfl_sync(kFull, info, owner);
-                const int32_t task = info & 0xffffff;
+                const int32_t task = slot_task(ms);
                 w = owner + 32 * (static_cast<uint32_t>(info) >> 30);
                 const bool is_done = (info >> 29) & 1;
-                int32_t nd = 0;
-#pragma unroll
-                for (int j = 0; j < WPL; ++j)
-                    if (j == (w >> 5)) nd = node[j];
-                nd = __shfl_sync(kFull, nd, owner);
+                const int32_t nd = info & 0xff;
                 const uint32_t bit = 1u << nd;
                 const int4 hd = head(task);
                 const int32_t nin = hd.y, nout = hd.z;
@@ -663,7 +675,7 @@ struct Sim {
                 }
 #pragma unroll
                 for (int j = 0; j < WPL; ++j)
-                    if (j == (w >> 5) && lane == owner) busy[j] = false;
+                    if (j == (w >> 5) && lane == owner) wk[j] &= ~4u;
                 completed += 1;
                 // successors: sorted, multi-edges adjacent; the lowest lane of
                 // each run of equal ids decrements by the run length
@@ -723,9 +735,7 @@ __device__ void simulate_impl(const SimParams& p) {
         s.hdr = p.hdr + t0;
         const int32_t pfi = p.platform_of ? p.platform_of[g] : 0;
         const DevPlatform* pf = p.platforms + pfi;
-        s.W = pf->n_workers;
-        s.nn = pf->n_nodes;
-        s.lat = pf->latency_ms;
+        const int32_t W = pf->n_workers, nn = pf->n_nodes;
         __syncwarp();
         if (pfi != loaded_pf) {  // platform tables into this warp's state
             double* costs = reinterpret_cast<double*>(base + p.layout.costs);
@@ -734,22 +744,18 @@ __device__ void simulate_impl(const SimParams& p) {
                 costs[2 * i] = pf->costs.cpu[i];
                 costs[2 * i + 1] = pf->costs.gpu[i];
             }
-            for (int i = lane; i < s.nn * s.nn; i += 32) bw[i] = pf->bw[(i / s.nn) * kMaxNodes + i % s.nn];
+            for (int i = lane; i < nn * nn; i += 32) bw[i] = pf->bw[(i / nn) * kMaxNodes + i % nn];
             loaded_pf = pfi;
         }
 #pragma unroll
         for (int j = 0; j < WPL; ++j) {
             const int32_t w = lane + 32 * j;
-            s.kind[j] = w < s.W ? pf->kind[w] : 0;
-            s.node[j] = w < s.W ? pf->node[w] : 0;
+            s.wk[j] = w < W ? (1u | (pf->kind[w] ? 2u : 0u) | (static_cast<uint32_t>(pf->node[w]) << 4)) : 0u;
             s.qlen[j] = 0;
-            s.busy[j] = false;
-            s.fdirty[j] = false;
             s.busy_until[j] = 0.0;
             s.fsum[j] = 0.0;
             s.xt[j] = s.dt[j] = 0.0;
-            s.xs[j] = s.ds[j] = kNone;
-            s.xtask[j] = s.dtask[j] = 0;
+            s.xs[j] = s.ds[j] = S::kNoSlot;
         }
         s.now = 0.0;
         s.nready = 0;
@@ -761,6 +767,8 @@ __device__ void simulate_impl(const SimParams& p) {
         if (lane == 0) {
             c.g = g;
             c.t0 = t0;
+            c.nn = nn;
+            c.lat = pf->latency_ms;
             c.n_push = c.n_samp = 0;
             c.pop0 = c.pop1 = c.pop2 = 0;
             c.aux = -1;
@@ -769,7 +777,7 @@ __device__ void simulate_impl(const SimParams& p) {
             if (p.reg) {
                 c.cfg = p.reg[g];
             } else {
-                const int64_t nw = s.W;
+                const int64_t nw = W;
                 const int64_t tw = (nw + 3) / 4 > 2 ? (nw + 3) / 4 : 2;
                 c.cfg.task_window = tw;
                 c.cfg.s_inc = nw;

@@ -14,9 +14,11 @@ struct SimCold {
     tbsim_regulator_cfg cfg;
     int64_t peak, prev_nready, last_trigger, s_dec_count;
     double cur_k;
+    double lat;          // platform transfer latency (ms)
     int64_t n_push, n_samp, pop0, pop1, pop2;
     int64_t g, t0;
     int32_t phase, r_head, r_count, aux;
+    int32_t nn, pad;     // platform memory nodes
 };
 
 // Per-warp state layout (bytes, 16-aligned sections).  Compact state
