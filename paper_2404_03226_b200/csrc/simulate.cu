@@ -107,9 +107,8 @@ struct Sim {
     int lane;
     double now;
     int32_t nready;
-    int32_t completed, rcount, rhead, rtail;  // ready list: rcount tasks linked from rhead
+    int32_t rcount, rhead;  // ready list: rcount tasks linked from rhead (tail in SimCold)
     uint32_t seq;
-    int32_t n_pop;
     int32_t status;
     int32_t mode;
 
@@ -459,14 +458,18 @@ struct Sim {
         const int32_t ty = static_cast<int32_t>(e >> 24);
         const int4 hd = head(task);  // issued before the queue bookkeeping
         nready -= 1;
-        const int64_t t0 = cold().t0;
-        const int64_t slot = t0 + n_pop;
-        if (P->pop_time && lane == 0) {
-            P->pop_time[slot] = now;
-            P->pop_task[slot] = task;
-            P->pop_worker[slot] = w;
+        // dispatch counter and log slot: lane 0 only (cold state)
+        int64_t slot = 0;
+        if (lane == 0) {
+            SimCold& c = cold();
+            slot = c.t0 + c.n_pop;
+            c.n_pop += 1;
+            if (P->pop_time) {
+                P->pop_time[slot] = now;
+                P->pop_task[slot] = task;
+                P->pop_worker[slot] = w;
+            }
         }
-        ++n_pop;
         queue_event();
         const int64_t* inb = reinterpret_cast<const int64_t*>(lists(hd));
         const double xfer = transfer_total_lanes(inb, reinterpret_cast<const int32_t*>(inb + hd.y), hd.y, nd);
@@ -566,9 +569,10 @@ struct Sim {
         const int32_t nv = __shfl_sync(kFull, v, above ? __ffs(above) - 1 : lane);
         const int first = __ffs(bal) - 1, last = 31 - __clz(bal);
         if (rdy && above) um[v] = static_cast<UnmetT>(nv);
-        if (lane == first && rcount > 0) um[rtail] = static_cast<UnmetT>(v);
+        if (lane == first && rcount > 0) um[cold().rtail] = static_cast<UnmetT>(v);
+        __syncwarp();
+        if (lane == last) cold().rtail = v;
         const int32_t fv = __shfl_sync(kFull, v, first);
-        rtail = __shfl_sync(kFull, v, last);
         if (rcount == 0) rhead = fv;
         rcount += __popc(bal);
     }
@@ -601,7 +605,6 @@ struct Sim {
         // at `now` in creation order (2)+(3); phase B drains the worker
         // events stamped `now` in enqueue order (1), then time advances.
         bool events = false;
-        uint64_t mt = 0;
         for (;;) {
             int32_t w;
             if (!events) {
@@ -620,7 +623,7 @@ struct Sim {
                         if (xs[j] != kNoSlot) lt = min(lt, dbits(xt[j]));
                         if (ds[j] != kNoSlot) lt = min(lt, dbits(dt[j]));
                     }
-                    mt = warp_min_u64(lt);
+                    const uint64_t mt = warp_min_u64(lt);
                     if (mt == ~0ull) break;
                     now = __longlong_as_double(static_cast<long long>(mt));
                     events = true;
@@ -629,6 +632,7 @@ struct Sim {
             } else {
                 // the earliest-enqueued event stamped `now`: slots order by seq
                 SlotT ls = kNoSlot;
+                const uint64_t mt = dbits(now);
 #pragma unroll
                 for (int j = 0; j < WPL; ++j) {
                     if (xs[j] != kNoSlot && dbits(xt[j]) == mt) ls = min(ls, xs[j]);
@@ -676,7 +680,6 @@ struct Sim {
 #pragma unroll
                 for (int j = 0; j < WPL; ++j)
                     if (j == (w >> 5) && lane == owner) wk[j] &= ~4u;
-                completed += 1;
                 // successors: sorted, multi-edges adjacent; the lowest lane of
                 // each run of equal ids decrements by the run length
                 const int32_t* succl = outl + nout;
@@ -759,10 +762,8 @@ __device__ void simulate_impl(const SimParams& p) {
         }
         s.now = 0.0;
         s.nready = 0;
-        s.completed = 0;
-        s.rcount = s.rhead = s.rtail = 0;
+        s.rcount = s.rhead = 0;
         s.seq = 0;
-        s.n_pop = 0;
         s.status = GS_OK;
         if (lane == 0) {
             c.g = g;
@@ -770,6 +771,7 @@ __device__ void simulate_impl(const SimParams& p) {
             c.nn = nn;
             c.lat = pf->latency_ms;
             c.n_push = c.n_samp = 0;
+            c.n_pop = 0;
             c.pop0 = c.pop1 = c.pop2 = 0;
             c.aux = -1;
             // regulator config: explicit, or default_regulator_config
@@ -809,8 +811,11 @@ __device__ void simulate_impl(const SimParams& p) {
         __syncwarp();
         s.run();
         __syncwarp();
-        if (s.status == GS_OK && s.completed == s.n) {
-            if (lane == 0) p.n_disp[g] = s.n_pop;
+        // every dispatched task has completed once no event is pending, so
+        // the dispatch count is the completion count (engine.cpp:235-246)
+        const int32_t done = c.n_pop;
+        if (s.status == GS_OK && done == s.n) {
+            if (lane == 0) p.n_disp[g] = done;
         } else {
             // failed graph: outputs written here (undispatched tasks keep
             // worker -1), k_sim_scatter skips it
@@ -820,7 +825,7 @@ __device__ void simulate_impl(const SimParams& p) {
                 p.end_ms[t0 + v] = 0.0;
             }
             __syncwarp();
-            for (int64_t i = lane; i < s.n_pop; i += 32) {
+            for (int64_t i = lane; i < done; i += 32) {
                 const SimLog e = p.log[t0 + i];
                 p.worker[t0 + e.task] = e.worker;
                 p.start_ms[t0 + e.task] = e.start;
@@ -830,13 +835,13 @@ __device__ void simulate_impl(const SimParams& p) {
         }
         if (lane == 0) {
             int32_t st = s.status;
-            if (st == GS_OK && s.completed != s.n) st = GS_STUCK;
+            if (st == GS_OK && done != s.n) st = GS_STUCK;
             p.status[g] = st;
             p.status_aux[g] = c.aux;
             // makespan: the last completion (times only grow; a completed
             // graph's last event is a TaskDone)
-            p.makespan[g] = s.completed > 0 ? s.now : 0.0;
-            p.completed[g] = s.completed;
+            p.makespan[g] = done > 0 ? s.now : 0.0;
+            p.completed[g] = done;
             if (p.pop_counts) {
                 p.pop_counts[3 * g + 0] = c.pop0;
                 p.pop_counts[3 * g + 1] = c.pop1;

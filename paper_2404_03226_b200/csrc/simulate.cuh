@@ -18,7 +18,9 @@ struct SimCold {
     int64_t n_push, n_samp, pop0, pop1, pop2;
     int64_t g, t0;
     int32_t phase, r_head, r_count, aux;
-    int32_t nn, pad;     // platform memory nodes
+    int32_t nn;          // platform memory nodes
+    int32_t n_pop;       // dispatches so far (log slot)
+    int32_t rtail;       // last task of the ready list
 };
 
 // Per-warp state layout (bytes, 16-aligned sections).  Compact state
