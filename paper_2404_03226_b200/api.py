@@ -190,6 +190,10 @@ class Context:
     def set_large_graph_threshold(self, n_tasks: int):
         _check(load().tbsim_ctx_set_large_graph_threshold(self.h, n_tasks))
 
+    def set_sweep_tile(self, sources: int):
+        """Force the efficiency sweep's sources per tile (0: automatic)."""
+        _check(load().tbsim_ctx_set_sweep_tile(self.h, sources))
+
     def set_timing(self, on: bool):
         _check(load().tbsim_ctx_set_timing(self.h, int(on)))
 

@@ -47,6 +47,19 @@ def _stale(obj, srcs):
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
+def _run(cmd, attempts: int = 3) -> None:
+    """Run a compiler command; a crash (signal) is retried -- nvcc 12.9 has
+    been seen to segfault intermittently in this image.  Compile errors
+    raise immediately."""
+    for i in range(attempts):
+        rc = subprocess.call(cmd)
+        if rc == 0:
+            return
+        if rc > 0 and rc != 139:
+            break
+    raise subprocess.CalledProcessError(rc, cmd)
+
+
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
@@ -59,7 +72,7 @@ def build(verbose: bool = False) -> str:
             cmd = [NVCC] + ARCH + CU_FLAGS + ["-rdc=false", "-x", "cu", "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd))
-            subprocess.check_call(cmd)
+            _run(cmd)
         objs.append(o)
     cxx = _host_cxx()
     for src in CXX_SRCS:

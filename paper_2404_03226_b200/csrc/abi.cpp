@@ -114,6 +114,7 @@ struct tbsim_ctx {
     };
     std::vector<PoolEntry> batch_pool;  // freed batch allocations for reuse
     int64_t large_threshold = 65536;  // single graphs at least this large take the closure path
+    int32_t sweep_tile = 0;           // forced sources per sweep tile (0: widest that fits)
 
     DevBuf& buf(const std::string& name) { return bufs[name]; }
     void* batch_alloc(size_t bytes, size_t* got) {
@@ -315,6 +316,14 @@ int64_t tbsim_ctx_launch_count(const tbsim_ctx* ctx) { return ctx ? ctx->launche
 
 tbsim_status tbsim_ctx_set_large_graph_threshold(tbsim_ctx* ctx, int64_t n_tasks) {
     return guarded([&] { ctx->large_threshold = n_tasks; });
+}
+
+tbsim_status tbsim_ctx_set_sweep_tile(tbsim_ctx* ctx, int32_t sources) {
+    return guarded([&] {
+        if (sources != 0 && sources != 8 && sources != 16 && sources != 32 && sources != 64 && sources != 128)
+            raise(TBSIM_E_INVALID_ARGUMENT, "sweep tile must be 0, 8, 16, 32, 64 or 128 sources");
+        ctx->sweep_tile = sources;
+    });
 }
 
 tbsim_status tbsim_ctx_set_timing(tbsim_ctx* ctx, int enable) {
@@ -682,7 +691,7 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
     if (do_sweep && !(large && sweep_mode == SWEEP_ABILITY)) {
         const int64_t smem = sweep_smem_bytes(ctx);
         ctx->begin("k_tile_plan");
-        k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, run.s, smem, 0);
+        k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, run.s, smem, ctx->sweep_tile);
         ctx->end("k_tile_plan");
         // graphs whose distance window exceeds shared memory use a global
         // window; size it from the worst case (every node live)

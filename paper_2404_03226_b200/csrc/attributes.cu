@@ -906,23 +906,30 @@ __device__ __forceinline__ void sweep_tile_mode(const DevBatch& b, const AttrScr
     else sweep_tile<S, SMEM, 1>(b, s, g, tile, gwin, P, th, s_hist, prune_span);
 }
 
-// Lane-per-node sweep for narrow tiles (S = 8, 16: graphs whose live set is
-// wide, e.g. the 1M-task C4 DAG).  One lane relaxes all S distance columns of
-// its node from each predecessor's row (S contiguous doubles), so the
-// per-node work -- record loads, binning, the row store -- is paid once per
-// node instead of once per (node, source) lane.  Lanes walk a row's 16-byte
-// chunks starting at a lane-dependent chunk, which spreads a warp's LDS.128 /
-// STS.128 over the banks; the accumulators stay in that rotated order (chunk
-// (j + rot) % NC lives in m[j]), so no register is indexed dynamically.  The
-// next level's node record is loaded while the current level runs.
-template <int S, int TMODE>
-__device__ __forceinline__ void sweep_tile_lanes(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
-                                                 int32_t P, const Thresholds& th, uint32_t* s_hist,
-                                                 int32_t prune_span) {
+// Row-per-group sweep: a group of GL lanes (GL = 1, 2, 4, 8) owns one node
+// and relaxes all S distance columns of it from each predecessor's row; each
+// lane holds SPL = S / GL columns in registers.  The per-node work --
+// record loads, binning, the row store -- is paid once per node and lane
+// for SPL sources, and predecessor slots need no shuffles (the group's lanes
+// load the same address).  A lane reads its columns as NCL = SPL / 2 16-byte
+// chunks, chunk ((j + rot) mod NCL) * GL + gl at step j, where rot is the
+// group index: the groups of a warp start at different chunks, which spreads
+// a warp's LDS.128 / STS.128 over the banks.  The accumulators stay in that
+// rotated order (m[j]), so no register is indexed dynamically.  The next
+// level's first node record of each group is loaded while the current level
+// runs.
+template <int S, int GL, int TMODE>
+__device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
+                                                int32_t P, const Thresholds& th, uint32_t* s_hist,
+                                                int32_t prune_span) {
     extern __shared__ double win_smem[];
-    constexpr int NC = S / 2;  // 16-byte chunks per row
+    constexpr int SPL = S / GL;   // columns per lane
+    constexpr int NCL = SPL / 2;  // 16-byte chunks per lane
+    constexpr int NC = S / 2;     // chunks per row
+    static_assert(NCL >= 1 && (NCL & (NCL - 1)) == 0, "power-of-two chunks per lane");
     const int tid = threadIdx.x, nthr = blockDim.x;
-    const int rot = tid & (NC - 1);
+    const int gl = tid % GL, gidx = tid / GL, ngroups = nthr / GL;
+    const int rot = gidx & (NCL - 1);
     const int64_t t0 = b.task_base[g];
     const int32_t* lstart = s.lstart + t0 + g;
     const int32_t* om_slot = s.om_slot + t0;
@@ -938,10 +945,10 @@ __device__ __forceinline__ void sweep_tile_lanes(const DevBatch& b, const AttrSc
         for (int64_t i = tid; i < static_cast<int64_t>(P) * NC; i += nthr) w2[i] = neg;
     }
     for (int i = tid; i < S * kBins; i += nthr) s_hist[i] = 0u;
-    uint64_t hist[S];  // hist[2j+e]: source 2*((j+rot)%NC)+e
+    uint64_t hist[SPL];  // hist[2j+e]: source 2*chunk(j)+e
 #pragma unroll
-    for (int q = 0; q < S; ++q) hist[q] = 0;
-    auto src_of = [&](int j, int e) { return 2 * ((j + rot) & (NC - 1)) + e; };
+    for (int q = 0; q < SPL; ++q) hist[q] = 0;
+    auto chunk = [&](int j) { return ((j + rot) & (NCL - 1)) * GL + gl; };
     int32_t visits = 0;
     const int32_t La = s.level[t0 + s.order[t0 + first]];
     const double wmax = th.w[kWindows - 1];
@@ -960,7 +967,7 @@ __device__ __forceinline__ void sweep_tile_lanes(const DevBatch& b, const AttrSc
         return r;
     };
     Rec nx{0, 0, 0, 0.0};
-    if (lstart[La] + tid < lstart[La + 1]) nx = load_rec(lstart[La] + tid);
+    if (lstart[La] + gidx < lstart[La + 1]) nx = load_rec(lstart[La] + gidx);
     __syncthreads();
 
     for (int32_t lv = La; lv < gi.n_levels; ++lv) {
@@ -968,18 +975,18 @@ __device__ __forceinline__ void sweep_tile_lanes(const DevBatch& b, const AttrSc
         const int32_t a0 = lstart[lv], a1 = lstart[lv + 1];
         const int32_t a2 = lv + 1 < gi.n_levels ? lstart[lv + 2] : a1;
         const Rec cur = nx;
-        if (a1 + tid < a2) nx = load_rec(a1 + tid);  // next level's first node of this lane
-        for (int32_t i = a0 + tid; i < a1; i += nthr) {
-            const Rec r = i == a0 + tid ? cur : load_rec(i);
-            double2 m[NC];
+        if (a1 + gidx < a2) nx = load_rec(a1 + gidx);  // next level's first node of this group
+        for (int32_t i = a0 + gidx; i < a1; i += ngroups) {
+            const Rec r = i == a0 + gidx ? cur : load_rec(i);
+            double2 m[NCL];
 #pragma unroll
-            for (int j = 0; j < NC; ++j) m[j] = make_double2(-CUDART_INF, -CUDART_INF);
+            for (int j = 0; j < NCL; ++j) m[j] = make_double2(-CUDART_INF, -CUDART_INF);
             // plain compare-select: operands are -inf or non-negative, never NaN
             auto relax = [&](int32_t ps) {
                 const double2* row = w2 + static_cast<int64_t>(ps) * NC;
 #pragma unroll
-                for (int j = 0; j < NC; ++j) {
-                    const double2 x = row[(j + rot) & (NC - 1)];
+                for (int j = 0; j < NCL; ++j) {
+                    const double2 x = row[chunk(j)];
                     m[j].x = x.x > m[j].x ? x.x : m[j].x;
                     m[j].y = x.y > m[j].y ? x.y : m[j].y;
                 }
@@ -994,31 +1001,31 @@ __device__ __forceinline__ void sweep_tile_lanes(const DevBatch& b, const AttrSc
             const int32_t si = i - first;  // this node's own source column, if it is one
             double2* outp = w2 + static_cast<int64_t>(r.sl) * NC;
 #pragma unroll
-            for (int j = 0; j < NC; ++j) {
+            for (int j = 0; j < NCL; ++j) {
                 double d0 = m[j].x + r.gv, d1 = m[j].y + r.gv;
                 const bool c0 = d0 >= 0.0, c1 = d1 >= 0.0;
                 hist[2 * j] += shl64(1ull, c0 ? static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d0, th)) : 64u);
                 hist[2 * j + 1] += shl64(1ull, c1 ? static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d1, th)) : 64u);
                 if (static_cast<uint32_t>(si) < static_cast<uint32_t>(S)) {
                     // the source itself: distance 0, not its own descendant
-                    if (src_of(j, 0) == si) {
+                    if (2 * chunk(j) == si) {
                         if (c0) hist[2 * j] -= shl64(1ull, static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d0, th)));
                         d0 = 0.0;
                     }
-                    if (src_of(j, 1) == si) {
+                    if (2 * chunk(j) + 1 == si) {
                         if (c1) hist[2 * j + 1] -= shl64(1ull, static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d1, th)));
                         d1 = 0.0;
                     }
                 }
                 if (prune_span > 0) small |= (d0 >= 0.0 && d0 <= wmax) || (d1 >= 0.0 && d1 <= wmax);
-                outp[(j + rot) & (NC - 1)] = make_double2(d0, d1);
+                outp[chunk(j)] = make_double2(d0, d1);
             }
             if (++visits == kFlushEvery) {
 #pragma unroll
-                for (int j = 0; j < NC; ++j)
+                for (int j = 0; j < NCL; ++j)
 #pragma unroll
                     for (int e = 0; e < 2; ++e)
-                        if (src_of(j, e) < nsrc) flush5(hist[2 * j + e], s_hist + src_of(j, e) * kBins);
+                        if (2 * chunk(j) + e < nsrc) flush5(hist[2 * j + e], s_hist + (2 * chunk(j) + e) * kBins);
                 visits = 0;
             }
         }
@@ -1030,10 +1037,10 @@ __device__ __forceinline__ void sweep_tile_lanes(const DevBatch& b, const AttrSc
         }
     }
 #pragma unroll
-    for (int j = 0; j < NC; ++j)
+    for (int j = 0; j < NCL; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-            if (src_of(j, e) < nsrc) flush5(hist[2 * j + e], s_hist + src_of(j, e) * kBins);
+            if (2 * chunk(j) + e < nsrc) flush5(hist[2 * j + e], s_hist + (2 * chunk(j) + e) * kBins);
     __syncthreads();
     const int32_t* order = s.order + t0;
     for (int i = tid; i < nsrc * 4; i += nthr) {
@@ -1043,13 +1050,13 @@ __device__ __forceinline__ void sweep_tile_lanes(const DevBatch& b, const AttrSc
     }
 }
 
-template <int S>
-__device__ __forceinline__ void sweep_tile_lanes_mode(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
-                                                      int32_t P, const Thresholds& th, uint32_t* s_hist,
-                                                      int32_t prune_span) {
-    if (th.mode == 0) sweep_tile_lanes<S, 0>(b, s, g, tile, P, th, s_hist, prune_span);
-    else if (th.mode == 2) sweep_tile_lanes<S, 2>(b, s, g, tile, P, th, s_hist, 0);
-    else sweep_tile_lanes<S, 1>(b, s, g, tile, P, th, s_hist, prune_span);
+template <int S, int GL>
+__device__ __forceinline__ void sweep_tile_rows_mode(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
+                                                     int32_t P, const Thresholds& th, uint32_t* s_hist,
+                                                     int32_t prune_span) {
+    if (th.mode == 0) sweep_tile_rows<S, GL, 0>(b, s, g, tile, P, th, s_hist, prune_span);
+    else if (th.mode == 2) sweep_tile_rows<S, GL, 2>(b, s, g, tile, P, th, s_hist, 0);
+    else sweep_tile_rows<S, GL, 1>(b, s, g, tile, P, th, s_hist, prune_span);
 }
 
 __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs_g,
@@ -1086,11 +1093,16 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
                 sweep_tile_mode<32, false>(b, s, g, tile, gw, P, th, s_hist, prune_span);
             } else {
                 switch (S) {
+                    // measured on B200 (C2 graphs forced to each width; C5):
+                    // 128 sources -- one node per warp, 4 columns per lane
+                    // (9.0 ms vs 10.0 for 16-lane rows); 64 and 32 -- rows of
+                    // 8 / 4 lanes (C2: 12.3 vs 13.9 ms, 16.1 vs 23.7 ms; C5
+                    // k_sweep 1012 -> 743 ms); 16 and 8 -- one lane per node
                     case 128: sweep_tile_mode<128, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
-                    case 64: sweep_tile_mode<64, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
-                    case 32: sweep_tile_mode<32, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
-                    case 16: sweep_tile_lanes_mode<16>(b, s, g, tile, P, th, s_hist, prune_span); break;
-                    default: sweep_tile_lanes_mode<8>(b, s, g, tile, P, th, s_hist, prune_span); break;
+                    case 64: sweep_tile_rows_mode<64, 8>(b, s, g, tile, P, th, s_hist, prune_span); break;
+                    case 32: sweep_tile_rows_mode<32, 4>(b, s, g, tile, P, th, s_hist, prune_span); break;
+                    case 16: sweep_tile_rows_mode<16, 1>(b, s, g, tile, P, th, s_hist, prune_span); break;
+                    default: sweep_tile_rows_mode<8, 1>(b, s, g, tile, P, th, s_hist, prune_span); break;
                 }
             }
         }

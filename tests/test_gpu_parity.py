@@ -96,6 +96,37 @@ def test_random_graphs_all_policies_platform_mix(ctx):
             eq(g[k], o[k], f"{pol}/{k}")
 
 
+@pytest.mark.parametrize("tile", [8, 16, 32, 64, 128])
+def test_every_sweep_tile_width_matches_oracle(ctx, tile):
+    """Each tile width runs its own kernel shape (one node per warp at 128
+    sources, rows of 8 / 4 lanes at 64 / 32, a lane per node at 16 / 8):
+    attributes equal the oracle's for all of them, on random graphs and on
+    layered ones wide enough to need several tiles per level."""
+    b = random_graphs(23, 30)
+    lay = api.HostBatch().add_layered(700, 7, 0.08, [3, 4]).view()
+    costs = P.default_cost_table()
+    for batch in (b, lay):
+        db = ctx.upload(batch)
+        oa = po.attributes(batch, costs, abi.ATTR_ALL)
+        o3 = po.attributes(batch, costs, abi.ATTR_EFFICIENCY, unit_time=np.full(batch.n_graphs, 3.0))
+        ctx.set_sweep_tile(tile)
+        try:
+            ga = ctx.attributes(db, costs, abi.ATTR_ALL)
+            g3 = ctx.attributes(db, costs, abi.ATTR_EFFICIENCY, unit_time=np.full(batch.n_graphs, 3.0))
+            gb = ctx.attributes(db, costs, abi.ATTR_ABILITY)
+        finally:
+            ctx.set_sweep_tile(0)
+        for k in ("ability", "efficiency", "static_priority", "unit_time_ms"):
+            eq(ga[k], oa[k], f"S={tile} {k}")
+        eq(g3["efficiency"], o3["efficiency"], f"S={tile} efficiency@3")
+        eq(gb["ability"], oa["ability"], f"S={tile} ability only")
+
+
+def test_sweep_tile_rejects_other_widths(ctx):
+    with pytest.raises(ValueError):
+        ctx.set_sweep_tile(24)
+
+
 def odd_platform(name, bw_rows, latency=0.02):
     """4 CPUs on node 0, one GPU per further node, custom bandwidths."""
     nn = len(bw_rows)
