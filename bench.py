@@ -323,6 +323,7 @@ def run_c5(args):
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
     kms = {k: ctx.last_kernel_ms(k) for k in ("k_structure", "k_sweep", "k_finalize", "k_sim_pack", "k_simulate", "k_sim_scatter")}
+    c5_relax = ctx.last_sweep_relaxations()
     for _ in range(args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -360,6 +361,7 @@ def run_c5(args):
                                        "(4c1g, 8c2g, 16c2g, 32c4g), inspirit", "n_dags_per_gpu": G,
                            "tasks_per_dag": n},
                 "decisions_per_sec": value * 2 * n, "kernel_ms": kms, "generation_ms": gen_ms,
+                "sweep_roofline": sweep_roofline(ctx, c5_relax, kms["k_sweep"]),
                 "e2e": {"value": G * world * args.steps / (float(tot[1]) / 1e3), "unit": "DAGs/s",
                         "h2d_bytes_per_step": int(G * 8), "d2h_bytes_per_step": int(G * 8 + G * n * 20)},
                 "cpu_baseline": cpu}
@@ -367,6 +369,19 @@ def run_c5(args):
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def sweep_roofline(ctx, relaxations, sweep_ms):
+    """The efficiency sweep's roofline: it is bound by shared-memory reads of
+    predecessor rows + FP64 compare-select, not HBM, so its denominator is
+    the same inner loop with no graph around it (k_probe_relax, measured
+    live on this GPU)."""
+    peak = ctx.probe_sweep_peak(3)
+    achieved = relaxations / (sweep_ms / 1e3) if sweep_ms > 0 else 0.0
+    return {"bound": "smem rows + fp64 compare-select", "kernel": "k_sweep", "achieved": achieved, "peak": peak,
+            "unit": "relaxations/s", "frac": achieved / peak if peak > 0 else None,
+            "relaxations_per_launch": int(relaxations), "kernel_ms": sweep_ms,
+            "peak_source": "k_probe_relax (the sweep's inner loop alone, 128-column rows, one 512-thread CTA per SM)"}
 
 
 def c4_measure(steps=3, warmup=1, ctx=None, stream=None):
@@ -401,6 +416,7 @@ def c4_measure(steps=3, warmup=1, ctx=None, stream=None):
         times.append(e0.elapsed_time(e1))
         kms.append({k: ctx.last_kernel_ms(k) for k in ("k_ingest", "k_structure", "k_closure", "k_tile_plan",
                                                        "k_sweep", "k_finalize", "k_structure_out")})
+    sweep_relax = ctx.last_sweep_relaxations()
     ctx.set_timing(False)
     # algorithmic bytes of the closure: every successor's set read from its
     # lower word bound, every node's set written from its own bound (8 B/word)
@@ -430,6 +446,7 @@ def c4_measure(steps=3, warmup=1, ctx=None, stream=None):
                          "frac": achieved / peak, "algorithmic_bytes": alg_bytes, "kernel_ms": closure_ms,
                          "note": "trimmed descendant sets (level-ordered bit space); L2 reuse of the level cut "
                                  "can push algorithmic GB/s above the DRAM copy peak"},
+            "sweep_roofline": sweep_roofline(ctx, sweep_relax, kms[-1]["k_sweep"]),
             "properties": props, "unit_time_ms": float(res["unit_time_ms"][0])}
 
 
@@ -441,8 +458,8 @@ def run_c4(args):
             "data": "synthetic generate_layered_dag(1048576, 1024, 1/256, seed 1)",
             "config": {"workload": "C4: single 1M-task DAG, compute_attributes(UpwardRank)", "n_tasks": m["n_tasks"],
                        "n_edges": m["n_edges"], "host_generation_s": m["host_generation_s"]},
-            "kernel_ms": m["kernel_ms"], "roofline": m["roofline"], "properties": m["properties"],
-            "unit_time_ms": m["unit_time_ms"]}
+            "kernel_ms": m["kernel_ms"], "roofline": m["roofline"], "sweep_roofline": m["sweep_roofline"],
+            "properties": m["properties"], "unit_time_ms": m["unit_time_ms"]}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -541,7 +558,9 @@ def main():
     torch.cuda.synchronize()
     kms = {k: ctx.last_kernel_ms(k) for k in ("k_structure", "k_tile_plan", "k_sweep", "k_finalize",
                                              "k_structure_out", "k_sim_pack", "k_simulate", "k_sim_scatter")}
+    sweep_relax = ctx.last_sweep_relaxations()
     ctx.set_timing(False)
+    sweep_roof = sweep_roofline(ctx, sweep_relax, kms["k_sweep"])
     dominant = max(("k_sweep", "k_simulate"), key=lambda k: kms[k])
     alg = algorithmic_bytes(gb, dominant)
     peaks = {}
@@ -649,7 +668,8 @@ def main():
             del db
             m = c4_measure(2, 1, ctx, stream)
             c4 = {"workload": "C4: one 1M-task DAG, compute_attributes", "ms_per_pass": m["ms_per_pass"],
-                  "kernel_ms": m["kernel_ms"], "roofline": m["roofline"], "properties": m["properties"]}
+                  "kernel_ms": m["kernel_ms"], "roofline": m["roofline"], "sweep_roofline": m["sweep_roofline"],
+                  "properties": m["properties"]}
         except Exception as e:  # pragma: no cover
             c4 = {"error": str(e)}
 
@@ -670,6 +690,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650 GB/s",
                          "note": "latency/issue-bound event simulation and FP64 sweep; see DESIGN.md §4"},
             "kernel_ms": kms,
+            "sweep_roofline": sweep_roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "DAGs/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),

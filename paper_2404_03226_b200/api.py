@@ -190,6 +190,18 @@ class Context:
     def set_large_graph_threshold(self, n_tasks: int):
         _check(load().tbsim_ctx_set_large_graph_threshold(self.h, n_tasks))
 
+    def last_sweep_relaxations(self) -> int:
+        """Relaxations executed by the last timed efficiency sweep."""
+        v = C.c_int64(0)
+        _check(load().tbsim_ctx_last_sweep_relaxations(self.h, C.byref(v)))
+        return v.value
+
+    def probe_sweep_peak(self, repeats: int = 3) -> float:
+        """Relaxations/s of the sweep's inner loop alone (its roofline)."""
+        v = C.c_double(0.0)
+        _check(load().tbsim_probe_sweep_peak(self.h, repeats, C.byref(v)))
+        return v.value
+
     def set_sweep_tile(self, sources: int):
         """Force the efficiency sweep's sources per tile (0: automatic)."""
         _check(load().tbsim_ctx_set_sweep_tile(self.h, sources))

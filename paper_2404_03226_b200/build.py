@@ -25,7 +25,7 @@ CU_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPI
 CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off",
              "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I/usr/local/cuda/include"]
 
-CU_SRCS = ["attributes.cu", "simulate.cu", "generate.cu", "abi.cpp"]  # abi.cpp launches kernels: nvcc -x cu
+CU_SRCS = ["attributes.cu", "simulate.cu", "generate.cu", "probe.cu", "abi.cpp"]  # abi.cpp launches kernels: nvcc -x cu
 CXX_SRCS = ["hostbatch.cpp"]
 # the drop-in C++ API (namespace tbsim, include/tbsim/*.hpp) over the C-ABI
 API_SRCS = ["api/taskgraph.cpp", "api/platform.cpp", "api/device.cpp", "api/attributes.cpp",

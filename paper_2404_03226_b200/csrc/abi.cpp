@@ -115,6 +115,8 @@ struct tbsim_ctx {
     std::vector<PoolEntry> batch_pool;  // freed batch allocations for reuse
     int64_t large_threshold = 65536;  // single graphs at least this large take the closure path
     int32_t sweep_tile = 0;           // forced sources per sweep tile (0: widest that fits)
+    unsigned long long* relax_ctr = nullptr;  // device counter of the last timed sweep
+    int64_t last_relax = 0;
 
     DevBuf& buf(const std::string& name) { return bufs[name]; }
     void* batch_alloc(size_t bytes, size_t* got) {
@@ -168,6 +170,11 @@ struct tbsim_ctx {
         for (auto& [k, ev] : events) {
             float ms = 0.f;
             if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) last_ms[k] = ms;
+        }
+        if (relax_ctr) {
+            unsigned long long r = 0;
+            if (cudaMemcpy(&r, relax_ctr, 8, cudaMemcpyDeviceToHost) == cudaSuccess) last_relax = static_cast<int64_t>(r);
+            relax_ctr = nullptr;
         }
     }
     void sync() { cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
@@ -328,6 +335,40 @@ tbsim_status tbsim_ctx_set_sweep_tile(tbsim_ctx* ctx, int32_t sources) {
 
 tbsim_status tbsim_ctx_set_timing(tbsim_ctx* ctx, int enable) {
     return guarded([&] { ctx->timing = enable != 0; });
+}
+
+tbsim_status tbsim_probe_sweep_peak(tbsim_ctx* ctx, int32_t repeats, double* relaxations_per_s) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        constexpr int32_t kRows = 128, kIters = 20000, kThreads = 512;
+        const size_t smem = static_cast<size_t>(kRows) * 64 * 16;  // 128 KB window
+        cuda_check(cudaFuncSetAttribute(tbsim_dev::k_probe_relax, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)), "cudaFuncSetAttribute(k_probe_relax)");
+        double* out = ctx->buf("p_out").as<double>(ctx->n_sms);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        double best = 0.0;
+        for (int32_t r = 0; r < std::max(repeats, 1) + 1; ++r) {  // first launch warms up
+            cudaEventRecord(e0, ctx->stream);
+            ctx->begin("k_probe_relax");
+            tbsim_dev::k_probe_relax<<<ctx->n_sms, kThreads, smem, ctx->stream>>>(kRows - 1, kIters, out);
+            ctx->end("k_probe_relax");
+            cudaEventRecord(e1, ctx->stream);
+            cuda_check(cudaEventSynchronize(e1), "probe");
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            const double relax = static_cast<double>(ctx->n_sms) * kThreads * kIters * 4.0 * 4.0;
+            if (r > 0 && ms > 0.f) best = std::max(best, relax / (ms * 1e-3));
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        *relaxations_per_s = best;
+    });
+}
+
+tbsim_status tbsim_ctx_last_sweep_relaxations(const tbsim_ctx* ctx, int64_t* relaxations) {
+    return guarded([&] { *relaxations = ctx->last_relax; });
 }
 
 tbsim_status tbsim_ctx_last_kernel_ms(const tbsim_ctx* ctx, const char* kernel, double* ms) {
@@ -711,10 +752,18 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
                        "cudaFuncSetAttribute(k_sweep)");
             attr_set = true;
         }
+        // executed relaxations (rows x columns) when timing: the sweep's
+        // achieved rate for bench.py's roofline
+        unsigned long long* relax_ctr = nullptr;
+        if (ctx->timing) {
+            relax_ctr = ctx->buf("a_relax").as<unsigned long long>(1);
+            cuda_check(cudaMemsetAsync(relax_ctr, 0, 8, ctx->stream), "memset");
+            ctx->relax_ctr = relax_ctr;
+        }
         ctx->begin("k_sweep");
         k_sweep<<<sweep_grid, kSweepThreads, smem, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, sweep_mode, d_unit_time,
                                                                   total_tiles, counter, smem, gwin, gwin_stride,
-                                                                  large ? 1 : 0);
+                                                                  large ? 1 : 0, relax_ctr);
         ctx->end("k_sweep");
         const int64_t cls_stride = static_cast<int64_t>(d.max_n) * (3 * kWindows + 1) + 16;
         int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride * grid_g);

@@ -756,9 +756,10 @@ __device__ __forceinline__ void flush5(uint64_t& h, uint32_t* dst) {
 template <int S, bool SMEM, int TMODE>
 __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                            double* gwin, int32_t P, const Thresholds& th,
-                                           uint32_t* s_hist, int32_t prune_span) {
+                                           uint32_t* s_hist, int32_t prune_span, unsigned long long* relax_ctr) {
     extern __shared__ double win_smem[];
     double* win = SMEM ? win_smem : gwin;
+    uint64_t nrel = 0;  // predecessor rows relaxed (x S columns), thread 0
     constexpr int GL = S < 32 ? S : 32;   // lanes per node group
     constexpr int SPL = S / GL;           // sources per lane
     constexpr int GPW = 32 / GL;          // groups per warp
@@ -801,6 +802,7 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     for (int32_t lv = La; lv < gi.n_levels; ++lv) {
         int small = 0;
         const int32_t a1 = lstart[lv + 1];
+        if (relax_ctr && threadIdx.x == 0) nrel += static_cast<uint64_t>(__ldg(&om_poff[a1]) - __ldg(&om_poff[lstart[lv]]));
         // groups are independent: every lane of a group sees the same node
         for (int32_t i = lstart[lv] + warp * GPW + grp; i < a1; i += nwarps * GPW) {
             const int32_t p0 = __ldg(&om_poff[i]);
@@ -888,6 +890,7 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     for (int q = 0; q < SPL; ++q)
         if (src(q) < nsrc) flush5(hist[q], s_hist + src(q) * kBins);
     __syncthreads();
+    if (relax_ctr && threadIdx.x == 0) atomicAdd(relax_ctr, static_cast<unsigned long long>(nrel * S));
     // per source: 12 bins as 21-bit fields in four words (k_finalize)
     const int32_t* order = s.order + t0;
     for (int i = threadIdx.x; i < nsrc * 4; i += blockDim.x) {
@@ -900,10 +903,10 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
 template <int S, bool SMEM>
 __device__ __forceinline__ void sweep_tile_mode(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                                 double* gwin, int32_t P, const Thresholds& th,
-                                                uint32_t* s_hist, int32_t prune_span) {
-    if (th.mode == 0) sweep_tile<S, SMEM, 0>(b, s, g, tile, gwin, P, th, s_hist, prune_span);
-    else if (th.mode == 2) sweep_tile<S, SMEM, 2>(b, s, g, tile, gwin, P, th, s_hist, 0);
-    else sweep_tile<S, SMEM, 1>(b, s, g, tile, gwin, P, th, s_hist, prune_span);
+                                                uint32_t* s_hist, int32_t prune_span, unsigned long long* rc) {
+    if (th.mode == 0) sweep_tile<S, SMEM, 0>(b, s, g, tile, gwin, P, th, s_hist, prune_span, rc);
+    else if (th.mode == 2) sweep_tile<S, SMEM, 2>(b, s, g, tile, gwin, P, th, s_hist, 0, rc);
+    else sweep_tile<S, SMEM, 1>(b, s, g, tile, gwin, P, th, s_hist, prune_span, rc);
 }
 
 // Row-per-group sweep: a group of GL lanes (GL = 1, 2, 4, 8) owns one node
@@ -921,8 +924,9 @@ __device__ __forceinline__ void sweep_tile_mode(const DevBatch& b, const AttrScr
 template <int S, int GL, int TMODE>
 __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                                 int32_t P, const Thresholds& th, uint32_t* s_hist,
-                                                int32_t prune_span) {
+                                                int32_t prune_span, unsigned long long* relax_ctr) {
     extern __shared__ double win_smem[];
+    uint64_t nrel = 0;  // predecessor rows relaxed (x S columns), thread 0
     constexpr int SPL = S / GL;   // columns per lane
     constexpr int NCL = SPL / 2;  // 16-byte chunks per lane
     constexpr int NC = S / 2;     // chunks per row
@@ -976,6 +980,7 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
         const int32_t a2 = lv + 1 < gi.n_levels ? lstart[lv + 2] : a1;
         const Rec cur = nx;
         if (a1 + gidx < a2) nx = load_rec(a1 + gidx);  // next level's first node of this group
+        if (relax_ctr && tid == 0) nrel += static_cast<uint64_t>(__ldg(&om_poff[a1]) - __ldg(&om_poff[a0]));
         for (int32_t i = a0 + gidx; i < a1; i += ngroups) {
             const Rec r = i == a0 + gidx ? cur : load_rec(i);
             double2 m[NCL];
@@ -1042,6 +1047,7 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
         for (int e = 0; e < 2; ++e)
             if (2 * chunk(j) + e < nsrc) flush5(hist[2 * j + e], s_hist + (2 * chunk(j) + e) * kBins);
     __syncthreads();
+    if (relax_ctr && tid == 0) atomicAdd(relax_ctr, static_cast<unsigned long long>(nrel * S));
     const int32_t* order = s.order + t0;
     for (int i = tid; i < nsrc * 4; i += nthr) {
         const uint32_t* c = s_hist + (i >> 2) * kBins + 3 * (i & 3);
@@ -1053,10 +1059,10 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
 template <int S, int GL>
 __device__ __forceinline__ void sweep_tile_rows_mode(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                                      int32_t P, const Thresholds& th, uint32_t* s_hist,
-                                                     int32_t prune_span) {
-    if (th.mode == 0) sweep_tile_rows<S, GL, 0>(b, s, g, tile, P, th, s_hist, prune_span);
-    else if (th.mode == 2) sweep_tile_rows<S, GL, 2>(b, s, g, tile, P, th, s_hist, 0);
-    else sweep_tile_rows<S, GL, 1>(b, s, g, tile, P, th, s_hist, prune_span);
+                                                     int32_t prune_span, unsigned long long* rc) {
+    if (th.mode == 0) sweep_tile_rows<S, GL, 0>(b, s, g, tile, P, th, s_hist, prune_span, rc);
+    else if (th.mode == 2) sweep_tile_rows<S, GL, 2>(b, s, g, tile, P, th, s_hist, 0, rc);
+    else sweep_tile_rows<S, GL, 1>(b, s, g, tile, P, th, s_hist, prune_span, rc);
 }
 
 __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs_g,
@@ -1064,7 +1070,7 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
                                               int32_t sweep_mode, const double* unit_time,
                                               int64_t total_tiles, unsigned long long* work_counter,
                                               int64_t smem_bytes, double* gwin, int64_t gwin_stride,
-                                              int32_t prune) {
+                                              int32_t prune, unsigned long long* relax_ctr) {
     __shared__ int64_t s_item[2];
     __shared__ uint32_t s_hist[128 * kBins];
     (void)costs_g;
@@ -1090,7 +1096,7 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
             // prune only when the edge span fits the 64-level history
             const int32_t prune_span = (prune && gi.max_span > 0 && gi.max_span < 64) ? gi.max_span : 0;
             if (static_cast<int64_t>(P) * S * 8 > smem_bytes) {
-                sweep_tile_mode<32, false>(b, s, g, tile, gw, P, th, s_hist, prune_span);
+                sweep_tile_mode<32, false>(b, s, g, tile, gw, P, th, s_hist, prune_span, relax_ctr);
             } else {
                 switch (S) {
                     // measured on B200 (C2 graphs forced to each width; C5):
@@ -1098,11 +1104,11 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
                     // (9.0 ms vs 10.0 for 16-lane rows); 64 and 32 -- rows of
                     // 8 / 4 lanes (C2: 12.3 vs 13.9 ms, 16.1 vs 23.7 ms; C5
                     // k_sweep 1012 -> 743 ms); 16 and 8 -- one lane per node
-                    case 128: sweep_tile_mode<128, true>(b, s, g, tile, gw, P, th, s_hist, prune_span); break;
-                    case 64: sweep_tile_rows_mode<64, 8>(b, s, g, tile, P, th, s_hist, prune_span); break;
-                    case 32: sweep_tile_rows_mode<32, 4>(b, s, g, tile, P, th, s_hist, prune_span); break;
-                    case 16: sweep_tile_rows_mode<16, 1>(b, s, g, tile, P, th, s_hist, prune_span); break;
-                    default: sweep_tile_rows_mode<8, 1>(b, s, g, tile, P, th, s_hist, prune_span); break;
+                    case 128: sweep_tile_mode<128, true>(b, s, g, tile, gw, P, th, s_hist, prune_span, relax_ctr); break;
+                    case 64: sweep_tile_rows_mode<64, 8>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+                    case 32: sweep_tile_rows_mode<32, 4>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+                    case 16: sweep_tile_rows_mode<16, 1>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+                    default: sweep_tile_rows_mode<8, 1>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
                 }
             }
         }

@@ -92,7 +92,8 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
 __global__ void k_sweep(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                         int32_t sweep_mode,
                         const double* unit_time, int64_t total_tiles, unsigned long long* work_counter,
-                        int64_t smem_bytes, double* gwin, int64_t gwin_stride, int32_t prune);
+                        int64_t smem_bytes, double* gwin, int64_t gwin_stride, int32_t prune,
+                        unsigned long long* relax_ctr);
 __global__ void k_finalize(DevBatch b, AttrScratch s, int32_t sweep_mode, const double* unit_time_in,
                            AttrOutDev o, int64_t* cls_scratch, int64_t cls_stride, int32_t write_ability);
 __global__ void k_finalize_large(DevBatch b, AttrScratch s, int32_t sweep_mode, AttrOutDev o, int64_t* scratch,
@@ -102,5 +103,7 @@ __global__ void k_closure(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets, 
                           unsigned long long* ability);
 __global__ void k_structure_out(DevBatch b, AttrScratch s, AttrOutDev o, int32_t prio_kind,
                                 int32_t want_prio);
+// probe.cu: the sweep's inner loop alone (its roofline denominator)
+__global__ void k_probe_relax(int32_t rows_mask, int32_t iters, double* out);
 
 }  // namespace tbsim_dev
