@@ -126,6 +126,12 @@ tbsim_status tbsim_ctx_set_stream(tbsim_ctx* ctx, void* cuda_stream);
  * finished with it.  NULL: uploads run on the compute stream. */
 tbsim_status tbsim_ctx_set_upload_stream(tbsim_ctx* ctx, void* cuda_stream);
 tbsim_status tbsim_ctx_synchronize(tbsim_ctx* ctx);
+/* Asynchronous results: tbsim_schedule calls with host output arrays return
+ * once the results' device-to-host copies are queued on the context's
+ * download stream (overlapping the next call's kernels); the host arrays are
+ * valid after tbsim_ctx_synchronize.  Errors are still raised by the call.
+ * Default off (results valid on return). */
+tbsim_status tbsim_ctx_set_async_results(tbsim_ctx* ctx, int enable);
 /* Single graphs with at least this many tasks (default 65536) take the
  * large-graph attribute path: ability by the HBM bitset closure, the
  * efficiency sweep pruned at the largest window. */

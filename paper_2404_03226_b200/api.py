@@ -202,6 +202,11 @@ class Context:
         _check(load().tbsim_probe_sweep_peak(self.h, repeats, C.byref(v)))
         return v.value
 
+    def set_async_results(self, on: bool):
+        """schedule() with host outputs returns once their D2H copies are
+        queued (overlapping the next call); read them after synchronize()."""
+        _check(load().tbsim_ctx_set_async_results(self.h, int(on)))
+
     def set_sweep_tile(self, sources: int):
         """Force the efficiency sweep's sources per tile (0: automatic)."""
         _check(load().tbsim_ctx_set_sweep_tile(self.h, sources))

@@ -115,6 +115,15 @@ struct tbsim_ctx {
     std::vector<PoolEntry> batch_pool;  // freed batch allocations for reuse
     int64_t large_threshold = 65536;  // single graphs at least this large take the closure path
     int32_t sweep_tile = 0;           // forced sources per sweep tile (0: widest that fits)
+    // Asynchronous results (tbsim_ctx_set_async_results): host-bound outputs
+    // of tbsim_schedule are staged in one of two device buffer sets and copied
+    // on the download stream, so a call's D2H overlaps the next call's
+    // kernels; a set is rewritten only after its previous copies finished.
+    bool async_results = false;
+    cudaStream_t download = nullptr;
+    cudaEvent_t set_free[2] = {nullptr, nullptr};
+    bool set_pending[2] = {false, false};
+    int parity = 0;
     unsigned long long* relax_ctr = nullptr;  // device counter of the last timed sweep
     int64_t last_relax = 0;
 
@@ -301,6 +310,12 @@ tbsim_status tbsim_ctx_destroy(tbsim_ctx* ctx) {
             cudaEventDestroy(ev.first);
             cudaEventDestroy(ev.second);
         }
+        if (ctx->download) {
+            cudaStreamSynchronize(ctx->download);
+            cudaStreamDestroy(ctx->download);
+        }
+        for (auto& e : ctx->set_free)
+            if (e) cudaEventDestroy(e);
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
         if (ctx->own) cudaStreamDestroy(ctx->own);
         delete ctx;
@@ -316,7 +331,23 @@ tbsim_status tbsim_ctx_set_upload_stream(tbsim_ctx* ctx, void* s) {
 }
 
 tbsim_status tbsim_ctx_synchronize(tbsim_ctx* ctx) {
-    return guarded([&] { ctx->sync(); });
+    return guarded([&] {
+        ctx->sync();
+        if (ctx->download) cuda_check(cudaStreamSynchronize(ctx->download), "cudaStreamSynchronize(download)");
+    });
+}
+
+tbsim_status tbsim_ctx_set_async_results(tbsim_ctx* ctx, int enable) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        if (enable && !ctx->download) {
+            cuda_check(cudaStreamCreateWithFlags(&ctx->download, cudaStreamNonBlocking), "cudaStreamCreate");
+            for (auto& e : ctx->set_free)
+                cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        }
+        if (!enable && ctx->download) cuda_check(cudaStreamSynchronize(ctx->download), "cudaStreamSynchronize");
+        ctx->async_results = enable != 0;
+    });
 }
 
 int64_t tbsim_ctx_launch_count(const tbsim_ctx* ctx) { return ctx ? ctx->launches : 0; }
@@ -1255,6 +1286,17 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         if (policy < 0 || policy > TBSIM_POLICY_INSPIRIT) raise(TBSIM_E_RUNTIME, "unknown policy id");
         const DevBatch& d = b->d;
         const int64_t T = d.T, G = d.G;
+        // host-bound outputs: staged in buffer set `set`, copied on the
+        // download stream when results are asynchronous
+        const bool async = ctx->async_results && !out->on_device;
+        const int set = async ? ctx->parity : 0;
+        if (async) {
+            ctx->parity ^= 1;
+            if (ctx->set_pending[set])
+                cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->set_free[set], 0), "cudaStreamWaitEvent");
+        }
+        const std::string sfx = set ? "_1" : "";
+        auto nm = [&](const char* base) { return std::string(base) + sfx; };
         std::vector<DevPlatform> hp;
         DevPlatform* d_pf = nullptr;
         int32_t max_nodes = 1;
@@ -1277,14 +1319,14 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         const bool adev = ao->on_device != 0;
         OutStage ast;
         AttrOutDev o{};
-        o.ability = scratch_if_null(ctx, "f_ab", stage_out(ctx, ast, "f_ab", ao->ability, T, adev), T);
-        o.efficiency = scratch_if_null(ctx, "f_ef", stage_out(ctx, ast, "f_ef", ao->efficiency, T, adev), T);
-        o.static_priority = scratch_if_null(ctx, "f_pr", stage_out(ctx, ast, "f_pr", ao->static_priority, T, adev), T);
-        o.unit_time_ms = scratch_if_null(ctx, "f_ut", stage_out(ctx, ast, "f_ut", ao->unit_time_ms, G, adev), G);
-        o.w0_ms = stage_out(ctx, ast, "f_w0", ao->w0_ms, G, adev);
-        o.best_score = stage_out(ctx, ast, "f_bs", ao->best_score, G, adev);
-        o.w0_score = stage_out(ctx, ast, "f_ws", ao->w0_score, G, adev);
-        o.evaluations = stage_out(ctx, ast, "f_ev", ao->evaluations, G, adev);
+        o.ability = scratch_if_null(ctx, nm("f_ab").c_str(), stage_out(ctx, ast, nm("f_ab").c_str(), ao->ability, T, adev), T);
+        o.efficiency = scratch_if_null(ctx, nm("f_ef").c_str(), stage_out(ctx, ast, nm("f_ef").c_str(), ao->efficiency, T, adev), T);
+        o.static_priority = scratch_if_null(ctx, nm("f_pr").c_str(), stage_out(ctx, ast, nm("f_pr").c_str(), ao->static_priority, T, adev), T);
+        o.unit_time_ms = scratch_if_null(ctx, nm("f_ut").c_str(), stage_out(ctx, ast, nm("f_ut").c_str(), ao->unit_time_ms, G, adev), G);
+        o.w0_ms = stage_out(ctx, ast, nm("f_w0").c_str(), ao->w0_ms, G, adev);
+        o.best_score = stage_out(ctx, ast, nm("f_bs").c_str(), ao->best_score, G, adev);
+        o.w0_score = stage_out(ctx, ast, nm("f_ws").c_str(), ao->w0_score, G, adev);
+        o.evaluations = stage_out(ctx, ast, nm("f_ev").c_str(), ao->evaluations, G, adev);
         AttrRun run;
         run_attributes(ctx, b, d_costs, d_pof, SWEEP_CALIBRATE, nullptr, priority_kind == TBSIM_PRIO_UPWARD_RANK, true,
                        o, priority_kind, true, run);
@@ -1313,20 +1355,31 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         keys.ability = o.ability;
         keys.efficiency = o.efficiency;
         keys.prio = o.static_priority;
-        p.worker = scratch_if_null(ctx, "s_worker", sim_out_ptr(ctx, st, "s_worker", out->worker, T, dev), T);
-        p.start_ms = scratch_if_null(ctx, "s_start", sim_out_ptr(ctx, st, "s_start", out->start_ms, T, dev), T);
-        p.end_ms = scratch_if_null(ctx, "s_end", sim_out_ptr(ctx, st, "s_end", out->end_ms, T, dev), T);
-        p.makespan = scratch_if_null(ctx, "s_mk", sim_out_ptr(ctx, st, "s_mk", out->makespan_ms, G, dev), G);
-        p.completed = scratch_if_null(ctx, "s_done", sim_out_ptr(ctx, st, "s_done", out->completed, G, dev), G);
-        p.pop_counts = sim_out_ptr(ctx, st, "s_pops", out->pop_mode_counts, 3 * G, dev);
-        p.reg_state = sim_out_ptr(ctx, st, "s_rstate", out->reg_state, G, dev, true);
+        p.worker = scratch_if_null(ctx, nm("s_worker").c_str(), sim_out_ptr(ctx, st, nm("s_worker").c_str(), out->worker, T, dev), T);
+        p.start_ms = scratch_if_null(ctx, nm("s_start").c_str(), sim_out_ptr(ctx, st, nm("s_start").c_str(), out->start_ms, T, dev), T);
+        p.end_ms = scratch_if_null(ctx, nm("s_end").c_str(), sim_out_ptr(ctx, st, nm("s_end").c_str(), out->end_ms, T, dev), T);
+        p.makespan = scratch_if_null(ctx, nm("s_mk").c_str(), sim_out_ptr(ctx, st, nm("s_mk").c_str(), out->makespan_ms, G, dev), G);
+        p.completed = scratch_if_null(ctx, nm("s_done").c_str(), sim_out_ptr(ctx, st, nm("s_done").c_str(), out->completed, G, dev), G);
+        p.pop_counts = sim_out_ptr(ctx, st, nm("s_pops").c_str(), out->pop_mode_counts, 3 * G, dev);
+        p.reg_state = sim_out_ptr(ctx, st, nm("s_rstate").c_str(), out->reg_state, G, dev, true);
         p.status = ctx->buf("s_status").as<int32_t>(G);
         p.status_aux = ctx->buf("s_aux").as<int32_t>(G);
         run_simulation(ctx, b, p, maxw, keys);
+        cudaStream_t dl = ctx->stream;
+        if (async) {  // the copies wait for this call's kernels, not the next call's
+            cudaEvent_t done = ctx->set_free[set];
+            cuda_check(cudaEventRecord(done, ctx->stream), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(ctx->download, done, 0), "cudaStreamWaitEvent");
+            dl = ctx->download;
+        }
         for (const auto& c : ast.copies)
-            cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+            cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, dl), "D2H");
         for (const auto& c : st.copies)
-            cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+            cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, dl), "D2H");
+        if (async) {
+            cuda_check(cudaEventRecord(ctx->set_free[set], ctx->download), "cudaEventRecord");
+            ctx->set_pending[set] = true;
+        }
         ctx->sync();
         ctx->collect_timing();
     });

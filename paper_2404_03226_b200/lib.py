@@ -21,6 +21,7 @@ EXPORTS = [
     "tbsim_ctx_launch_count", "tbsim_ctx_set_timing", "tbsim_ctx_last_kernel_ms",
     "tbsim_ctx_set_large_graph_threshold",
     "tbsim_ctx_set_sweep_tile",
+    "tbsim_ctx_set_async_results",
     "tbsim_ctx_last_sweep_relaxations",
     "tbsim_probe_sweep_peak",
     "tbsim_batch_upload", "tbsim_batch_free", "tbsim_batch_h2d_bytes", "tbsim_batch_generate_layered",
@@ -61,6 +62,7 @@ def load():
     L.tbsim_ctx_set_timing.argtypes = [vp, C.c_int]
     L.tbsim_ctx_set_large_graph_threshold.argtypes = [vp, i64]
     L.tbsim_ctx_set_sweep_tile.argtypes = [vp, i32]
+    L.tbsim_ctx_set_async_results.argtypes = [vp, C.c_int]
     L.tbsim_ctx_last_sweep_relaxations.argtypes = [vp, P(i64)]
     L.tbsim_probe_sweep_peak.argtypes = [vp, i32, P(dbl)]
     L.tbsim_ctx_last_kernel_ms.argtypes = [vp, C.c_char_p, P(dbl)]

@@ -370,3 +370,32 @@ def test_upload_stream_pipeline_matches_serial(ctx):
                     eq(got[k], serial[i][k], f"{k} batch {i}")
     finally:
         ctx.set_upload_stream(None)
+
+
+def test_async_results_match_synchronous(ctx):
+    """Asynchronous results (D2H on the download stream, two staging sets):
+    every call's host arrays hold that call's schedules once synchronized,
+    including arrays reused by a later call."""
+    import torch
+    pl = [P.assemble("8c2g", 8, 2)]
+    batches = [api.HostBatch().add_layered(500 + 41 * i, 7, 0.05, np.arange(40 * i, 40 * i + 48)) for i in range(5)]
+    serial = [ctx.schedule(ctx.upload(hb), pl, "inspirit", want_attrs=False) for hb in batches]
+    keys = ("worker", "start_ms", "end_ms", "makespan_ms", "completed")
+    ctx.set_async_results(True)
+    try:
+        outs = []
+        for i, hb in enumerate(batches):
+            T, G = hb.view().n_tasks, hb.view().n_graphs
+            arr = {"worker": torch.empty(T, dtype=torch.int32, pin_memory=True).numpy(),
+                   "start_ms": torch.empty(T, dtype=torch.float64, pin_memory=True).numpy(),
+                   "end_ms": torch.empty(T, dtype=torch.float64, pin_memory=True).numpy(),
+                   "makespan_ms": torch.empty(G, dtype=torch.float64, pin_memory=True).numpy(),
+                   "completed": torch.empty(G, dtype=torch.int64, pin_memory=True).numpy()}
+            outs.append(ctx.schedule(ctx.upload(hb), pl, "inspirit", want_attrs=False, out_arrays=arr,
+                                     want_states=False))
+        ctx.synchronize()
+        for i, got in enumerate(outs):
+            for k in keys:
+                eq(got[k], serial[i][k], f"async {k} call {i}")
+    finally:
+        ctx.set_async_results(False)
