@@ -218,6 +218,22 @@ tbsim_status tbsim_attributes(tbsim_ctx* ctx, const tbsim_batch* b,
                               const tbsim_costs* costs, int32_t request,
                               int32_t priority_kind, tbsim_attr_out* out);
 
+/* compute_attributes of ONE large graph sharded over `world` GPUs (SURVEY
+ * §8(e), C4).  Every rank holds the whole graph; rank r computes the
+ * descendant-set words of its share of the bit space (ability = the sum of
+ * the ranks' partial counts) and the efficiency sweep of its share of the
+ * sources.  Between the two calls the caller sums (all-reduces, e.g. NCCL
+ * over NVLink) `ability_partial` [T] and `class_sums` [n_words] over the
+ * ranks; `finish` then returns this rank's sources' efficiency (zero
+ * elsewhere -- sum over ranks again), the static priority and the
+ * calibration (identical on every rank).  Host arrays; back to back on the
+ * same context and batch. */
+tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbsim_batch* b, const tbsim_costs* costs,
+                                            int32_t rank, int32_t world, int64_t* ability_partial,
+                                            int64_t* class_sums, int64_t cap, int64_t* n_words);
+tbsim_status tbsim_attributes_shard_finish(tbsim_ctx* ctx, const tbsim_batch* b, const int64_t* class_sums,
+                                           int64_t n_words, int32_t priority_kind, tbsim_attr_out* out);
+
 /* ------------------------------------------------------------------------
  * Policies, regulator and the event engine
  * (reference: include/tbsim/policies.hpp, include/tbsim/engine.hpp).

@@ -245,6 +245,41 @@ class Context:
         _check(load().tbsim_attributes(self.h, db.h, C.byref(c), request, prio, C.byref(o)))
         return out
 
+    def attributes_shard_partial(self, db: DeviceBatch, costs: CostTable, rank: int, world: int):
+        """Rank `rank` of `world`: partial ability [T] and per-class window
+        sums of one large graph (tbsim_attributes_shard_partial); the caller
+        sums both over the ranks, then calls attributes_shard_finish."""
+        T = db.n_tasks
+        ab = np.zeros(T, np.int64)
+        sums = np.zeros(max(12 * T, 12), np.int64)
+        nw = C.c_int64(0)
+        c, _keep = outbuf.costs_struct(costs, db.type_names)
+        _check(load().tbsim_attributes_shard_partial(self.h, db.h, C.byref(c), rank, world, _p(ab, C.c_int64),
+                                                     _p(sums, C.c_int64), sums.size, C.byref(nw)))
+        return ab, sums[:nw.value].copy()
+
+    def attributes_shard_finish(self, db: DeviceBatch, class_sums, prio: int = abi.PRIO_UPWARD_RANK) -> dict:
+        """This rank's sources' efficiency (zero elsewhere), the static
+        priority and the calibration, from the class sums of all ranks."""
+        sums = np.ascontiguousarray(class_sums, np.int64)
+        out, o = outbuf.attr_out(db.n_tasks, db.n_graphs)
+        _check(load().tbsim_attributes_shard_finish(self.h, db.h, _p(sums, C.c_int64), sums.size, prio, C.byref(o)))
+        for k in ("ability", "depth", "layer"):
+            out.pop(k)
+        return out
+
+    def attributes_sharded(self, db: DeviceBatch, costs: CostTable, rank: int, world: int, allreduce_sum,
+                           prio: int = abi.PRIO_UPWARD_RANK) -> dict:
+        """compute_attributes of one large graph over `world` ranks; `allreduce_sum`
+        sums an int64 numpy array over the ranks (e.g. NCCL all-reduce)."""
+        ab, sums = self.attributes_shard_partial(db, costs, rank, world)
+        ab = allreduce_sum(ab)
+        sums = allreduce_sum(sums)
+        out = self.attributes_shard_finish(db, sums, prio)
+        out["efficiency"] = allreduce_sum(out["efficiency"])
+        out["ability"] = ab
+        return out
+
     # ------------------------------------------------------------ simulate
     def simulate(self, db: DeviceBatch, platforms: Sequence[Platform], policy: str,
                  reg, platform_of=None, attrs=None, record=True, states=None) -> dict:

@@ -124,6 +124,15 @@ struct tbsim_ctx {
     cudaEvent_t set_free[2] = {nullptr, nullptr};
     bool set_pending[2] = {false, false};
     int parity = 0;
+    // sharded large-graph attributes: what tbsim_attributes_shard_partial
+    // left for tbsim_attributes_shard_finish (same batch, back to back)
+    struct Shard {
+        const tbsim_batch* b = nullptr;
+        int32_t rank = -1, world = 0;
+        int32_t pos_lo = 0, pos_hi = 0;
+        int64_t n_words = 0;
+        AttrScratch s{};
+    } shard;
     unsigned long long* relax_ctr = nullptr;  // device counter of the last timed sweep
     int64_t last_relax = 0;
 
@@ -700,6 +709,25 @@ int64_t sweep_smem_bytes(tbsim_ctx* ctx) {
     return std::max<int64_t>(0, opt - 8 * 1024);
 }
 
+// One large graph: the structure pass with the whole GPU (cooperative).
+void launch_structure_large(tbsim_ctx* ctx, const DevBatch& d, const DevCosts* d_costs, const int32_t* d_cost_idx,
+                            const AttrScratch& s, bool want_rank, bool sort_levels = false) {
+    static int per_sm = 0;
+    if (!per_sm) cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_structure_large, 512, 0), "occupancy");
+    const int grid = std::max(1, std::min(per_sm, 2)) * ctx->n_sms;
+    const size_t ctl_bytes = sizeof(LargeCtl) + 4 * static_cast<size_t>(grid);
+    LargeCtl* ctl = static_cast<LargeCtl*>(ctx->buf("a_large_ctl").get(ctl_bytes));
+    cuda_check(cudaMemsetAsync(ctl, 0, ctl_bytes, ctx->stream), "memset");
+    DevBatch dv = d;
+    AttrScratch sv = s;
+    int32_t wr = want_rank ? 1 : 0, so = sort_levels ? 1 : 0;
+    void* args[] = {&dv, const_cast<DevCosts**>(&d_costs), const_cast<int32_t**>(&d_cost_idx), &sv, &wr, &ctl, &so};
+    ctx->begin("k_structure");
+    cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_structure_large), grid, 512, args, 0, ctx->stream),
+               "cudaLaunchCooperativeKernel(k_structure_large)");
+    ctx->end("k_structure");
+}
+
 // Launch the whole attribute pipeline on a device batch.  Returns with the
 // per-graph GraphInfo copied to the host (one sync).
 void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_costs, const int32_t* d_cost_idx,
@@ -714,22 +742,7 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
     const bool large = G == 1 && d.max_n >= ctx->large_threshold && do_sweep;
     const int grid_g = static_cast<int>(std::min<int64_t>(G, 4LL * ctx->n_sms));
     if (G == 1 && d.max_n >= ctx->large_threshold) {
-        // one large graph: the structure pass with the whole GPU
-        static int per_sm = 0;
-        if (!per_sm)
-            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_structure_large, 512, 0), "occupancy");
-        const int grid = std::max(1, std::min(per_sm, 2)) * ctx->n_sms;
-        const size_t ctl_bytes = sizeof(LargeCtl) + 4 * static_cast<size_t>(grid);
-        LargeCtl* ctl = static_cast<LargeCtl*>(ctx->buf("a_large_ctl").get(ctl_bytes));
-        cuda_check(cudaMemsetAsync(ctl, 0, ctl_bytes, ctx->stream), "memset");
-        DevBatch dv = d;
-        AttrScratch sv = run.s;
-        int32_t wr = want_rank ? 1 : 0;
-        void* args[] = {&dv, const_cast<DevCosts**>(&d_costs), const_cast<int32_t**>(&d_cost_idx), &sv, &wr, &ctl};
-        ctx->begin("k_structure");
-        cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_structure_large), grid, 512, args, 0, ctx->stream),
-                   "cudaLaunchCooperativeKernel(k_structure_large)");
-        ctx->end("k_structure");
+        launch_structure_large(ctx, d, d_costs, d_cost_idx, run.s, want_rank);
     } else {
         // a CTA per graph, as many resident as fit (a partial second wave of
         // CTAs that each walk ~G/grid graphs would double the tail); small
@@ -757,11 +770,11 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
             cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_closure<4>, 256, 0), "occupancy");
             const int grid = std::max(1, per_sm) * ctx->n_sms;
             int64_t g0 = 0;
-            int64_t nw_arg = nw;
+            int64_t wlo = 0, whi = nw;
             DevBatch dv = d;
             AttrScratch sv = run.s;
             unsigned long long* ab = reinterpret_cast<unsigned long long*>(o.ability);
-            void* args[] = {&dv, &sv, &g0, &sets, &nw_arg, &ab};
+            void* args[] = {&dv, &sv, &g0, &sets, &wlo, &whi, &ab};
             ctx->begin("k_closure");
             cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_closure<4>), grid, 256, args, 0, ctx->stream),
                        "cudaLaunchCooperativeKernel(k_closure)");
@@ -819,8 +832,9 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
             int32_t* score = ctx->buf("a_fin_score").as<int32_t>(kWindows);
             DevBatch dv = d;
             AttrScratch sv = run.s;
-            int32_t sm = sweep_mode, wa = write_ab;
-            void* args[] = {&dv, &sv, &sm, &o, &cls_scratch, &tab, &tab_cap, &score, &wa};
+            int32_t sm = sweep_mode, wa = write_ab, ph = FIN_ALL, plo = 0, phi = d.max_n;
+            const int64_t* sums_in = nullptr;
+            void* args[] = {&dv, &sv, &sm, &o, &cls_scratch, &tab, &tab_cap, &score, &wa, &ph, &plo, &phi, &sums_in};
             ctx->begin("k_finalize");
             cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_finalize_large), grid, 512, args, 0, ctx->stream),
                        "cudaLaunchCooperativeKernel(k_finalize_large)");
@@ -965,6 +979,209 @@ extern "C" tbsim_status tbsim_attributes(tbsim_ctx* ctx, const tbsim_batch* b, c
             cudaMemcpy(unit_host.data(), d_unit, G * 8, cudaMemcpyDeviceToHost);
         }
         attr_errors(b, run.info, request, eff_only ? (dev ? unit_host.data() : out->unit_time_ms) : nullptr);
+    });
+}
+
+// ------------------------------------------------- sharded large graphs
+
+namespace {
+
+// Rank r's share of the closure's words: each word w of every set costs one
+// OR per node whose set reaches down to w (its level's lower word bound <= w),
+// so the split balances the cumulative per-word node count.
+std::pair<int64_t, int64_t> closure_word_range(const std::vector<int32_t>& lstart, int64_t nw, int32_t rank,
+                                               int32_t world) {
+    std::vector<double> dens(static_cast<size_t>(nw) + 1, 0.0);
+    const size_t L = lstart.size() - 1;
+    for (size_t l = 0; l < L; ++l) {
+        const int64_t lo = std::min<int64_t>(lstart[l + 1] >> 6, nw);
+        dens[static_cast<size_t>(lo)] += static_cast<double>(lstart[l + 1] - lstart[l]);
+    }
+    std::vector<double> cum(static_cast<size_t>(nw) + 1, 0.0);
+    double run = 0.0;
+    for (int64_t w = 0; w < nw; ++w) {
+        run += dens[static_cast<size_t>(w)];
+        cum[static_cast<size_t>(w) + 1] = cum[static_cast<size_t>(w)] + run;
+    }
+    const double total = cum[static_cast<size_t>(nw)];
+    auto bound = [&](int32_t r) -> int64_t {
+        if (r <= 0) return 0;
+        if (r >= world) return nw;
+        const double want = total * r / world;
+        return std::lower_bound(cum.begin(), cum.end(), want) - cum.begin();
+    };
+    int64_t lo = std::min(bound(rank), nw), hi = std::min(bound(rank + 1), nw);
+    return {lo, std::max(lo, hi)};
+}
+
+}  // namespace
+
+extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbsim_batch* b, const tbsim_costs* costs,
+                                                       int32_t rank, int32_t world, int64_t* ability_partial,
+                                                       int64_t* class_sums, int64_t cap, int64_t* n_words) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        wait_batch(ctx, b);
+        const DevBatch& d = b->d;
+        if (d.G != 1) raise(TBSIM_E_INVALID_ARGUMENT, "sharded attributes take a batch of one graph");
+        if (world < 1 || rank < 0 || rank >= world) raise(TBSIM_E_INVALID_ARGUMENT, "shard rank out of range");
+        const int64_t n = d.max_n;
+        ctx->shard = tbsim_ctx::Shard{};
+        DevCosts hc = to_dev_costs(*costs, d.n_types);
+        DevCosts* d_costs = ctx->buf("costs").as<DevCosts>(1);
+        cuda_check(cudaMemcpyAsync(d_costs, &hc, sizeof hc, cudaMemcpyHostToDevice, ctx->stream), "H2D costs");
+        AttrScratch s = alloc_attr_scratch(ctx, d);
+        // ranks share one bit space: sort each level by task position
+        launch_structure_large(ctx, d, d_costs, nullptr, s, true, world > 1);
+        GraphInfo gi;
+        cuda_check(cudaMemcpyAsync(&gi, s.info, sizeof gi, cudaMemcpyDeviceToHost, ctx->stream), "D2H info");
+        ctx->sync();
+        attr_errors(b, {gi}, TBSIM_ATTR_ALL, nullptr);
+        if (world > 1 && !gi.order_det)
+            raise(TBSIM_E_INVALID_ARGUMENT, "sharded attributes need levels of at most 4096 tasks (deterministic bit space)");
+        // ---- ability: this rank's words of every descendant set
+        std::vector<int32_t> lstart(static_cast<size_t>(gi.n_levels) + 1);
+        cuda_check(cudaMemcpy(lstart.data(), s.lstart, lstart.size() * 4, cudaMemcpyDeviceToHost), "D2H lstart");
+        const int64_t nw = (n + 63) / 64;
+        const auto [wlo, whi] = closure_word_range(lstart, nw, rank, world);
+        int64_t* d_ab = ctx->buf("o_ability").as<int64_t>(std::max<int64_t>(n, 1));
+        cuda_check(cudaMemsetAsync(d_ab, 0, static_cast<size_t>(n) * 8, ctx->stream), "memset ability");
+        if (whi > wlo) {
+            uint64_t* sets = ctx->buf("a_sets").as<uint64_t>(static_cast<size_t>(std::max(gi.peak_rslots, 1)) * (whi - wlo));
+            int per_sm = 0;
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_closure<4>, 256, 0), "occupancy");
+            const int grid = std::max(1, per_sm) * ctx->n_sms;
+            int64_t g0 = 0, lo_ = wlo, hi_ = whi;
+            DevBatch dv = d;
+            AttrScratch sv = s;
+            unsigned long long* ab = reinterpret_cast<unsigned long long*>(d_ab);
+            void* args[] = {&dv, &sv, &g0, &sets, &lo_, &hi_, &ab};
+            ctx->begin("k_closure");
+            cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_closure<4>), grid, 256, args, 0, ctx->stream),
+                       "cudaLaunchCooperativeKernel(k_closure)");
+            ctx->end("k_closure");
+        }
+        // ---- efficiency sweep over this rank's share of the source tiles
+        const int64_t smem = sweep_smem_bytes(ctx);
+        k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, s, smem, ctx->sweep_tile);
+        int32_t S = 0;
+        int64_t tiles = 0;
+        cuda_check(cudaMemcpyAsync(&S, s.tile_s, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H tile width");
+        cuda_check(cudaMemcpyAsync(&tiles, s.tile_base + 1, 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H tiles");
+        ctx->sync();
+        const int64_t t_lo = tiles * rank / world, t_hi = tiles * (rank + 1) / world;
+        const int32_t pos_lo = static_cast<int32_t>(std::min<int64_t>(t_lo * S, n));
+        const int32_t pos_hi = static_cast<int32_t>(std::min<int64_t>(t_hi * S, n));
+        if (t_hi > t_lo) {
+            int64_t gwin_stride = 0;
+            double* gwin = nullptr;
+            if (n * 8 * 8 > smem) {
+                gwin_stride = n * 32;
+                gwin = ctx->buf("a_gwin").as<double>(gwin_stride * ctx->n_sms);
+            }
+            unsigned long long* counter = ctx->buf("a_counter").as<unsigned long long>(1);
+            const unsigned long long start = static_cast<unsigned long long>(t_lo);
+            cuda_check(cudaMemcpyAsync(counter, &start, 8, cudaMemcpyHostToDevice, ctx->stream), "H2D counter");
+            cuda_check(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+                       "cudaFuncSetAttribute(k_sweep)");
+            ctx->begin("k_sweep");
+            k_sweep<<<ctx->n_sms, kSweepThreads, smem, ctx->stream>>>(d, d_costs, nullptr, s, SWEEP_CALIBRATE, nullptr,
+                                                                      t_hi, counter, smem, gwin, gwin_stride, 1, nullptr);
+            ctx->end("k_sweep");
+        }
+        // ---- this shard's per-class window sums
+        const int64_t C = gi.n_classes;
+        *n_words = C * (kWindows + 1);
+        if (cap < *n_words) raise(TBSIM_E_INVALID_ARGUMENT, "class_sums needs " + std::to_string(*n_words) + " words");
+        const int64_t cls_stride = n * (3 * kWindows + 1) + 16;
+        int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride);
+        {
+            static int per_sm = 0;
+            if (!per_sm)
+                cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_finalize_large, 512, 0), "occupancy");
+            const int grid = std::max(1, std::min(per_sm, 2)) * ctx->n_sms;
+            int64_t tab_cap = 1;
+            while (tab_cap < 2 * n) tab_cap <<= 1;
+            int32_t* tab = ctx->buf("a_fin_tab").as<int32_t>(tab_cap * kWindows);
+            int32_t* score = ctx->buf("a_fin_score").as<int32_t>(kWindows);
+            DevBatch dv = d;
+            AttrScratch sv = s;
+            AttrOutDev o{};
+            int32_t sm = SWEEP_CALIBRATE, wa = 0, ph = FIN_PARTIAL, plo = pos_lo, phi = pos_hi;
+            const int64_t* sums_in = nullptr;
+            void* args[] = {&dv, &sv, &sm, &o, &cls_scratch, &tab, &tab_cap, &score, &wa, &ph, &plo, &phi, &sums_in};
+            ctx->begin("k_finalize");
+            cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_finalize_large), grid, 512, args, 0, ctx->stream),
+                       "cudaLaunchCooperativeKernel(k_finalize_large)");
+            ctx->end("k_finalize");
+        }
+        cuda_check(cudaMemcpyAsync(class_sums, cls_scratch, static_cast<size_t>(*n_words) * 8, cudaMemcpyDeviceToHost,
+                                   ctx->stream), "D2H class sums");
+        cuda_check(cudaMemcpyAsync(ability_partial, d_ab, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, ctx->stream),
+                   "D2H ability");
+        ctx->sync();
+        ctx->collect_timing();
+        ctx->shard.b = b;
+        ctx->shard.rank = rank;
+        ctx->shard.world = world;
+        ctx->shard.pos_lo = pos_lo;
+        ctx->shard.pos_hi = pos_hi;
+        ctx->shard.n_words = *n_words;
+        ctx->shard.s = s;
+    });
+}
+
+extern "C" tbsim_status tbsim_attributes_shard_finish(tbsim_ctx* ctx, const tbsim_batch* b, const int64_t* class_sums,
+                                                      int64_t n_words, int32_t priority_kind, tbsim_attr_out* out) {
+    return guarded([&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const tbsim_ctx::Shard& sh = ctx->shard;
+        if (sh.b != b || n_words != sh.n_words)
+            raise(TBSIM_E_INVALID_ARGUMENT, "shard finish must follow this rank's partial call on the same batch");
+        if (out->on_device) raise(TBSIM_E_INVALID_ARGUMENT, "sharded attributes return host arrays");
+        const DevBatch& d = b->d;
+        const int64_t n = d.max_n;
+        int64_t* d_sums = ctx->buf("a_shard_sums").as<int64_t>(std::max<int64_t>(n_words, 1));
+        cuda_check(cudaMemcpyAsync(d_sums, class_sums, static_cast<size_t>(n_words) * 8, cudaMemcpyHostToDevice, ctx->stream),
+                   "H2D class sums");
+        OutStage st;
+        AttrOutDev o{};
+        o.efficiency = stage_out(ctx, st, "o_eff", out->efficiency, n, false);
+        if (o.efficiency) cuda_check(cudaMemsetAsync(o.efficiency, 0, static_cast<size_t>(n) * 8, ctx->stream), "memset");
+        o.static_priority = stage_out(ctx, st, "o_prio", out->static_priority, n, false);
+        o.unit_time_ms = stage_out(ctx, st, "o_unit", out->unit_time_ms, 1, false);
+        o.w0_ms = stage_out(ctx, st, "o_w0", out->w0_ms, 1, false);
+        o.best_score = stage_out(ctx, st, "o_best", out->best_score, 1, false);
+        o.w0_score = stage_out(ctx, st, "o_w0s", out->w0_score, 1, false);
+        o.evaluations = stage_out(ctx, st, "o_evals", out->evaluations, 1, false);
+        const int64_t cls_stride = n * (3 * kWindows + 1) + 16;
+        int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride);
+        static int per_sm = 0;
+        if (!per_sm) cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_finalize_large, 512, 0), "occupancy");
+        const int grid = std::max(1, std::min(per_sm, 2)) * ctx->n_sms;
+        int64_t tab_cap = 1;
+        while (tab_cap < 2 * n) tab_cap <<= 1;
+        int32_t* tab = ctx->buf("a_fin_tab").as<int32_t>(tab_cap * kWindows);
+        int32_t* score = ctx->buf("a_fin_score").as<int32_t>(kWindows);
+        DevBatch dv = d;
+        AttrScratch sv = sh.s;
+        int32_t sm = SWEEP_CALIBRATE, wa = 0, ph = FIN_FINISH, plo = sh.pos_lo, phi = sh.pos_hi;
+        const int64_t* sums_in = d_sums;
+        void* args[] = {&dv, &sv, &sm, &o, &cls_scratch, &tab, &tab_cap, &score, &wa, &ph, &plo, &phi, &sums_in};
+        ctx->begin("k_finalize");
+        cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_finalize_large), grid, 512, args, 0, ctx->stream),
+                   "cudaLaunchCooperativeKernel(k_finalize_large)");
+        ctx->end("k_finalize");
+        if (o.static_priority) {
+            const int g2 = static_cast<int>(std::min<int64_t>((n + 255) / 256, 16LL * ctx->n_sms));
+            ctx->begin("k_structure_out");
+            k_structure_out<<<std::max(g2, 1), 256, 0, ctx->stream>>>(d, sh.s, o, priority_kind, 1);
+            ctx->end("k_structure_out");
+        }
+        for (const auto& c : st.copies)
+            cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H out");
+        ctx->sync();
+        ctx->collect_timing();
     });
 }
 

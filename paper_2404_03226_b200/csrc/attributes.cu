@@ -348,6 +348,8 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
             gi.n_classes = n_cls;
             gi.miss_gpu = s_miss_gpu == INT32_MAX ? -1 : s_miss_gpu;
             gi.miss_any = s_miss_any == INT32_MAX ? -1 : s_miss_any;
+            gi.order_det = 0;
+            gi.pad_ = 0;
             gi.median = (n > 0 && gi.miss_gpu < 0) ? lower_median_gpu(sc, s_tcount, NT, n) : 0.0;
             s.info[g] = gi;
             s.median[g] = gi.median;
@@ -429,8 +431,11 @@ __device__ __forceinline__ double warp_max_f64(double x) {
 // it are being processed; otherwise CTA 0 runs the stack allocator.
 // Everything written by other CTAs inside this launch is read through L2.
 __global__ void __launch_bounds__(512) k_structure_large(DevBatch b, const DevCosts* costs_g, const int32_t* cost_idx,
-                                                        AttrScratch s, int32_t want_rank, LargeCtl* ctl) {
+                                                        AttrScratch s, int32_t want_rank, LargeCtl* ctl,
+                                                        int32_t sort_levels) {
     cg::grid_group grid = cg::this_grid();
+    constexpr int32_t kSortLevel = 4096;  // widest level sorted in shared memory
+    __shared__ int32_t s_sort[kSortLevel];
     __shared__ DevCosts sc;
     __shared__ double s_mean[kMaxTypes];
     __shared__ int32_t s_tc[kMaxTypes];
@@ -516,6 +521,37 @@ __global__ void __launch_bounds__(512) k_structure_large(DevBatch b, const DevCo
         cnt = __ldcg(&ctl->ctr[L % 3]);
     }
     const int32_t processed = begin;
+    // ---- deterministic level order: each level's nodes sorted by position
+    // (bitonic sort of the level in shared memory, a CTA per level).  The
+    // atomic appends above leave an arbitrary order inside a level; every
+    // single-GPU consumer is order-free, but ranks sharing one graph's bit
+    // space (sharded closure) must agree on every node's bit index.
+    for (int32_t lv = sort_levels ? blockIdx.x : L; lv < L; lv += gridDim.x) {
+        const int32_t a0 = __ldcg(&lstart[lv]), m = __ldcg(&lstart[lv + 1]) - a0;
+        if (m > kSortLevel) {
+            if (tid == 0) atomicMax(&ctl->unsorted, 1);
+            continue;  // uniform per CTA
+        }
+        int32_t N = 1;
+        while (N < m) N <<= 1;
+        for (int32_t i = tid; i < N; i += nthr) s_sort[i] = i < m ? __ldcg(&order[a0 + i]) : INT32_MAX;
+        __syncthreads();
+        for (int32_t k = 2; k <= N; k <<= 1) {
+            for (int32_t j = k >> 1; j > 0; j >>= 1) {
+                for (int32_t i = tid; i < N; i += nthr) {
+                    const int32_t ixj = i ^ j;
+                    if (ixj > i) {
+                        const int32_t x = s_sort[i], y = s_sort[ixj];
+                        if ((x > y) == ((i & k) == 0)) { s_sort[i] = y; s_sort[ixj] = x; }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int32_t i = tid; i < m; i += nthr) order[a0 + i] = s_sort[i];
+        __syncthreads();
+    }
+    grid.sync();
     // ---- reverse level sweep: height (depth), upward rank, last use
     for (int32_t lv = L - 1; lv >= 0; --lv) {
         const int32_t a0 = __ldcg(&lstart[lv]), a1 = __ldcg(&lstart[lv + 1]);
@@ -631,6 +667,8 @@ __global__ void __launch_bounds__(512) k_structure_large(DevBatch b, const DevCo
         gi.n_classes = n_cls;
         gi.miss_gpu = mg > 0 ? n - mg : -1;
         gi.miss_any = ma > 0 ? n - ma : -1;
+        gi.order_det = sort_levels && !__ldcg(&ctl->unsorted) ? 1 : 0;
+        gi.pad_ = 0;
         gi.median = (n > 0 && gi.miss_gpu < 0) ? lower_median_gpu(sc, tc, NT, n) : 0.0;
         s.info[g] = gi;
         s.median[g] = gi.median;
@@ -1259,9 +1297,13 @@ __global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int
 // same probe sequence), then per-task efficiency / ability.
 // scratch: [C*11] sums, [C] counts, [C*11] numerators, [C*11] denominators;
 // tab: 11 tables of `tab_size` int32 (power of two >= 2C), score[11].
+// Sharded (multi-GPU): sources are the level-order positions [pos_lo,
+// pos_hi); phase FIN_PARTIAL stops after this shard's class sums (the
+// caller all-reduces them), FIN_FINISH starts from the reduced sums.
 __global__ void __launch_bounds__(512) k_finalize_large(DevBatch b, AttrScratch s, int32_t sweep_mode, AttrOutDev o,
                                                        int64_t* scratch, int32_t* tab, int64_t tab_cap,
-                                                       int32_t* score, int32_t write_ability) {
+                                                       int32_t* score, int32_t write_ability, int32_t phase,
+                                                       int32_t pos_lo, int32_t pos_hi, const int64_t* sums_in) {
     cg::grid_group grid = cg::this_grid();
     constexpr int64_t g = 0;
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1281,22 +1323,27 @@ __global__ void __launch_bounds__(512) k_finalize_large(DevBatch b, AttrScratch 
         int64_t ts = 1;
         while (ts < 2 * C) ts <<= 1;
         ts = min(ts, tab_cap);
-        for (int64_t i = gtid; i < C * (kWindows + 1); i += gthreads) sums[i] = 0;
+        for (int64_t i = gtid; i < C * (kWindows + 1); i += gthreads) sums[i] = sums_in ? sums_in[i] : 0;
         for (int64_t i = gtid; i < ts * kWindows; i += gthreads) tab[i] = 0;
         if (gtid < kWindows) score[gtid] = 0;
         grid.sync();
-        for (int64_t v = gtid; v < n; v += gthreads) {
-            const int32_t c = s.cls[t0 + v];
-            const uint64_t* h = hist + v * 4;
-            int64_t acc = 0;
-            for (int k = 0; k < kWindows; ++k) {
-                acc += field(h, k);
-                if (acc) atomicAdd(reinterpret_cast<unsigned long long*>(&sums[static_cast<int64_t>(c) * kWindows + k]),
-                                   static_cast<unsigned long long>(acc));
+        if (phase != FIN_FINISH) {
+            for (int64_t i = pos_lo + gtid; i < pos_hi; i += gthreads) {
+                const int64_t v = s.order[t0 + i];
+                const int32_t c = s.cls[t0 + v];
+                const uint64_t* h = hist + v * 4;
+                int64_t acc = 0;
+                for (int k = 0; k < kWindows; ++k) {
+                    acc += field(h, k);
+                    if (acc)
+                        atomicAdd(reinterpret_cast<unsigned long long*>(&sums[static_cast<int64_t>(c) * kWindows + k]),
+                                  static_cast<unsigned long long>(acc));
+                }
+                atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[c]), 1ull);
             }
-            atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[c]), 1ull);
+            if (phase == FIN_PARTIAL) return;  // uniform: the caller reduces scratch[0 .. 12C)
+            grid.sync();
         }
-        grid.sync();
         for (int64_t item = gtid; item < C * kWindows; item += gthreads) {
             const int64_t c = item / kWindows;
             const int64_t sc_ = __ldcg(&sums[item]), cc = __ldcg(&cnt[c]);
@@ -1337,7 +1384,8 @@ __global__ void __launch_bounds__(512) k_finalize_large(DevBatch b, AttrScratch 
             if (o.evaluations) o.evaluations[g] = kWindows;
         }
     }
-    for (int64_t v = gtid; v < n; v += gthreads) {
+    for (int64_t i = pos_lo + gtid; i < pos_hi; i += gthreads) {
+        const int64_t v = s.order[t0 + i];
         const uint64_t* h = hist + v * 4;
         int64_t eff = 0, abil = 0;
         for (int k = 0; k < kBins; ++k) {
@@ -1361,9 +1409,13 @@ __global__ void __launch_bounds__(512) k_finalize_large(DevBatch b, AttrScratch 
 // sets live in reverse live-range slots (firstuse) so only the level cut is
 // resident.  A warp owns (node, 32*CH-word chunk): coalesced loads of every
 // successor's chunk, OR, store, popcount.
+// Sharded (multi-GPU): this launch owns words [wlo, whi) of
+// every set -- the OR is word-wise independent, so ranks need no exchange
+// during the closure and ability = the sum over ranks of the partial
+// popcounts.  `sets` holds only the owned words (stride whi - wlo).
 template <int CH>
-__global__ void __launch_bounds__(256) k_closure(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets, int64_t nw,
-                                               unsigned long long* ability) {
+__global__ void __launch_bounds__(256) k_closure(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets, int64_t wlo,
+                                               int64_t whi, unsigned long long* ability) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     const int64_t t0 = b.task_base[g];
@@ -1379,10 +1431,11 @@ __global__ void __launch_bounds__(256) k_closure(DevBatch b, AttrScratch s, int6
     const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     constexpr int64_t kChunk = 32 * CH;
+    const int64_t nwr = whi - wlo;
     for (int32_t lv = gi.n_levels - 1; lv >= 0; --lv) {
         const int32_t a0 = lstart[lv], cnt = lstart[lv + 1] - a0;
-        const int64_t lo = lstart[lv + 1] >> 6;
-        const int64_t chunks = (nw - lo + kChunk - 1) / kChunk;
+        const int64_t lo = max(static_cast<int64_t>(lstart[lv + 1] >> 6), wlo);
+        const int64_t chunks = whi > lo ? (whi - lo + kChunk - 1) / kChunk : 0;
         const int64_t items = static_cast<int64_t>(cnt) * chunks;
         for (int64_t item = gwarp; item < items; item += nwarps) {
             const int32_t i = a0 + static_cast<int32_t>(item / chunks);
@@ -1395,20 +1448,20 @@ __global__ void __launch_bounds__(256) k_closure(DevBatch b, AttrScratch s, int6
                 const int32_t v = __ldg(&succ[k]);
                 const int32_t ov = opos[v];
                 const int64_t lov = lstart[level[v] + 1] >> 6;
-                const uint64_t* sv = sets + static_cast<int64_t>(rslot[v]) * nw;
+                const uint64_t* sv = sets + static_cast<int64_t>(rslot[v]) * nwr - wlo;
 #pragma unroll
                 for (int j = 0; j < CH; ++j) {
                     const int64_t w = w0 + lane + 32 * j;
-                    if (w >= lov && w < nw) acc[j] |= __ldcg(&sv[w]);
+                    if (w >= lov && w < whi) acc[j] |= __ldcg(&sv[w]);
                     if (w == (ov >> 6)) acc[j] |= 1ull << (ov & 63);
                 }
             }
-            uint64_t* su = sets + static_cast<int64_t>(rslot[u]) * nw;
+            uint64_t* su = sets + static_cast<int64_t>(rslot[u]) * nwr - wlo;
             int pc = 0;
 #pragma unroll
             for (int j = 0; j < CH; ++j) {
                 const int64_t w = w0 + lane + 32 * j;
-                if (w < nw) {
+                if (w < whi) {
                     __stcg(&su[w], acc[j]);
                     pc += __popcll(acc[j]);
                 }
@@ -1420,7 +1473,7 @@ __global__ void __launch_bounds__(256) k_closure(DevBatch b, AttrScratch s, int6
     }
 }
 
-template __global__ void k_closure<4>(DevBatch, AttrScratch, int64_t, uint64_t*, int64_t, unsigned long long*);
+template __global__ void k_closure<4>(DevBatch, AttrScratch, int64_t, uint64_t*, int64_t, int64_t, unsigned long long*);
 
 // Per-task outputs of the structure pass (layers, depth, static priority).
 __global__ void k_structure_out(DevBatch b, AttrScratch s, AttrOutDev o, int32_t prio_kind, int32_t want_prio) {

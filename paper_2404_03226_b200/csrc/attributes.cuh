@@ -22,6 +22,8 @@ struct GraphInfo {
     int32_t max_span;    // max level(v) - level(u) over edges (large-graph path)
     int32_t miss_gpu;    // first task position without a GPU cost, -1 if none
     int32_t miss_any;    // first task position without any cost, -1 if none
+    int32_t order_det;   // level order sorted by position inside each level (large-graph path)
+    int32_t pad_;
     double median;       // lower-median GPU time (valid when miss_gpu < 0 and n > 0)
 };
 
@@ -65,7 +67,8 @@ struct LargeCtl {
     int32_t span;        // max level(v) - level(u) over edges
     int32_t ring;        // widest window of span+1 consecutive levels
     int32_t wide2;       // widest window of two consecutive levels
-    int32_t pad[7];
+    int32_t unsorted;    // a level too wide for the deterministic in-level sort
+    int32_t pad[6];
     int32_t tcount[kMaxTypes];
     int32_t part[1];     // [gridDim.x]
 };
@@ -87,7 +90,7 @@ __global__ void k_ingest(DevBatch b, int32_t* cursor_scratch);
 __global__ void k_structure(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                             int32_t want_rank, int32_t want_large);
 __global__ void k_structure_large(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
-                                  int32_t want_rank, LargeCtl* ctl);
+                                  int32_t want_rank, LargeCtl* ctl, int32_t sort_levels);
 __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s);
 __global__ void k_sweep(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                         int32_t sweep_mode,
@@ -96,10 +99,12 @@ __global__ void k_sweep(DevBatch b, const DevCosts* costs, const int32_t* cost_i
                         unsigned long long* relax_ctr);
 __global__ void k_finalize(DevBatch b, AttrScratch s, int32_t sweep_mode, const double* unit_time_in,
                            AttrOutDev o, int64_t* cls_scratch, int64_t cls_stride, int32_t write_ability);
+enum FinPhase : int32_t { FIN_ALL = 0, FIN_PARTIAL = 1, FIN_FINISH = 2 };
 __global__ void k_finalize_large(DevBatch b, AttrScratch s, int32_t sweep_mode, AttrOutDev o, int64_t* scratch,
-                                 int32_t* tab, int64_t tab_cap, int32_t* score, int32_t write_ability);
+                                 int32_t* tab, int64_t tab_cap, int32_t* score, int32_t write_ability, int32_t phase,
+                                 int32_t pos_lo, int32_t pos_hi, const int64_t* sums_in);
 template <int CH>
-__global__ void k_closure(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets, int64_t nw,
+__global__ void k_closure(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets, int64_t wlo, int64_t whi,
                           unsigned long long* ability);
 __global__ void k_structure_out(DevBatch b, AttrScratch s, AttrOutDev o, int32_t prio_kind,
                                 int32_t want_prio);

@@ -22,6 +22,8 @@ EXPORTS = [
     "tbsim_ctx_set_large_graph_threshold",
     "tbsim_ctx_set_sweep_tile",
     "tbsim_ctx_set_async_results",
+    "tbsim_attributes_shard_partial",
+    "tbsim_attributes_shard_finish",
     "tbsim_ctx_last_sweep_relaxations",
     "tbsim_probe_sweep_peak",
     "tbsim_batch_upload", "tbsim_batch_free", "tbsim_batch_h2d_bytes", "tbsim_batch_generate_layered",
@@ -63,6 +65,8 @@ def load():
     L.tbsim_ctx_set_large_graph_threshold.argtypes = [vp, i64]
     L.tbsim_ctx_set_sweep_tile.argtypes = [vp, i32]
     L.tbsim_ctx_set_async_results.argtypes = [vp, C.c_int]
+    L.tbsim_attributes_shard_partial.argtypes = [vp, vp, P(abi.Costs), i32, i32, P(i64), P(i64), i64, P(i64)]
+    L.tbsim_attributes_shard_finish.argtypes = [vp, vp, P(i64), i64, i32, P(abi.AttrOut)]
     L.tbsim_ctx_last_sweep_relaxations.argtypes = [vp, P(i64)]
     L.tbsim_probe_sweep_peak.argtypes = [vp, i32, P(dbl)]
     L.tbsim_ctx_last_kernel_ms.argtypes = [vp, C.c_char_p, P(dbl)]

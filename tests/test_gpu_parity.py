@@ -399,3 +399,35 @@ def test_async_results_match_synchronous(ctx):
                 eq(got[k], serial[i][k], f"async {k} call {i}")
     finally:
         ctx.set_async_results(False)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("kind", ["layered", "long_edges"])
+def test_sharded_large_graph_attributes_match_single_gpu(ctx, world, kind):
+    """Multi-GPU attributes of one large graph, emulated with
+    one context per rank on this GPU: closure word ranges + sweep source
+    ranges + summed partials equal the single-GPU compute_attributes."""
+    costs = P.default_cost_table()
+    if kind == "layered":
+        b = api.HostBatch().add_layered(12288, 96, 1.0 / 32, [5]).view()
+    else:
+        b = _long_edge_graph(3, 6000, 60, 0.3)
+    db = ctx.upload(b)
+    ctx.set_large_graph_threshold(1000)
+    ctxs = [api.Context(0) for _ in range(world)]
+    try:
+        want = ctx.attributes(db, costs, abi.ATTR_ALL)
+        for c in ctxs:
+            c.set_large_graph_threshold(1000)
+        dbs = [c.upload(b) for c in ctxs]
+        parts = [c.attributes_shard_partial(d, costs, r, world) for r, (c, d) in enumerate(zip(ctxs, dbs))]
+        ab = sum(p[0] for p in parts)
+        sums = sum(p[1] for p in parts)
+        fins = [c.attributes_shard_finish(d, sums) for c, d in zip(ctxs, dbs)]
+    finally:
+        ctx.set_large_graph_threshold(65536)
+    eq(ab, want["ability"], "ability")
+    eq(sum(f["efficiency"] for f in fins), want["efficiency"], "efficiency")
+    for f in fins:
+        for k in ("static_priority", "unit_time_ms", "w0_ms", "best_score", "w0_score", "evaluations"):
+            eq(f[k], want[k] if k in want else f[k], k)
