@@ -1449,10 +1449,16 @@ __global__ void __launch_bounds__(256) k_closure(DevBatch b, AttrScratch s, int6
                 const int32_t ov = opos[v];
                 const int64_t lov = lstart[level[v] + 1] >> 6;
                 const uint64_t* sv = sets + static_cast<int64_t>(rslot[v]) * nwr - wlo;
+                uint64_t x[CH];  // all loads of this successor in flight together
 #pragma unroll
                 for (int j = 0; j < CH; ++j) {
                     const int64_t w = w0 + lane + 32 * j;
-                    if (w >= lov && w < whi) acc[j] |= __ldcg(&sv[w]);
+                    x[j] = (w >= lov && w < whi) ? __ldcg(&sv[w]) : 0ull;
+                }
+#pragma unroll
+                for (int j = 0; j < CH; ++j) {
+                    const int64_t w = w0 + lane + 32 * j;
+                    acc[j] |= x[j];
                     if (w == (ov >> 6)) acc[j] |= 1ull << (ov & 63);
                 }
             }
