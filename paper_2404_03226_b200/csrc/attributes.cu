@@ -1444,22 +1444,36 @@ __global__ void __launch_bounds__(256) k_closure(DevBatch b, AttrScratch s, int6
             uint64_t acc[CH];
 #pragma unroll
             for (int j = 0; j < CH; ++j) acc[j] = 0;
-            for (int32_t k = __ldg(&soff[u]); k < __ldg(&soff[u + 1]); ++k) {
-                const int32_t v = __ldg(&succ[k]);
-                const int32_t ov = opos[v];
-                const int64_t lov = lstart[level[v] + 1] >> 6;
-                const uint64_t* sv = sets + static_cast<int64_t>(rslot[v]) * nwr - wlo;
-                uint64_t x[CH];  // all loads of this successor in flight together
-#pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int64_t w = w0 + lane + 32 * j;
-                    x[j] = (w >= lov && w < whi) ? __ldcg(&sv[w]) : 0ull;
+            // successor metadata for 32 successors at once (a lane each),
+            // then a broadcast per successor: no dependent load chain
+            // between one successor's set reads and the next's
+            const int32_t k0 = __ldg(&soff[u]), k1 = __ldg(&soff[u + 1]);
+            for (int32_t kb = k0; kb < k1; kb += 32) {
+                int32_t m_ov = 0, m_slot = 0, m_lov = 0;
+                if (kb + lane < k1) {
+                    const int32_t v = __ldg(&succ[kb + lane]);
+                    m_ov = opos[v];
+                    m_lov = lstart[level[v] + 1] >> 6;
+                    m_slot = rslot[v];
                 }
+                const int32_t cnt = min(32, k1 - kb);
+                for (int32_t t = 0; t < cnt; ++t) {
+                    const int32_t ov = __shfl_sync(0xffffffffu, m_ov, t);
+                    const int64_t lov = __shfl_sync(0xffffffffu, m_lov, t);
+                    const int32_t slot = __shfl_sync(0xffffffffu, m_slot, t);
+                    const uint64_t* sv = sets + static_cast<int64_t>(slot) * nwr - wlo;
+                    uint64_t x[CH];  // all loads of this successor in flight together
 #pragma unroll
-                for (int j = 0; j < CH; ++j) {
-                    const int64_t w = w0 + lane + 32 * j;
-                    acc[j] |= x[j];
-                    if (w == (ov >> 6)) acc[j] |= 1ull << (ov & 63);
+                    for (int j = 0; j < CH; ++j) {
+                        const int64_t w = w0 + lane + 32 * j;
+                        x[j] = (w >= lov && w < whi) ? __ldcg(&sv[w]) : 0ull;
+                    }
+#pragma unroll
+                    for (int j = 0; j < CH; ++j) {
+                        const int64_t w = w0 + lane + 32 * j;
+                        acc[j] |= x[j];
+                        if (w == (ov >> 6)) acc[j] |= 1ull << (ov & 63);
+                    }
                 }
             }
             uint64_t* su = sets + static_cast<int64_t>(rslot[u]) * nwr - wlo;
