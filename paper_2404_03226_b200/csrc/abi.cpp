@@ -210,9 +210,32 @@ struct tbsim_batch {
     std::vector<std::string> type_names;
     int32_t max_workers_seen = 0;
     cudaEvent_t ready = nullptr;  // recorded on the upload stream when it is not the compute stream
+    // packed simulation graph (k_sim_pack): built once per batch
+    void* mem3 = nullptr;
+    size_t mem3_bytes = 0;
+    tbsim_dev::SimTaskHdr* hdr = nullptr;
+    char* adj = nullptr;
 };
 
 namespace {
+
+// The simulator's packed view of a batch (one 32-byte record per task +
+// contiguous lists), built once on the stream the call runs on -- at upload,
+// after k_ingest, or on a generated batch's first simulation.
+void ensure_packed(tbsim_ctx* ctx, tbsim_batch* b) {
+    const DevBatch& d = b->d;
+    if (b->hdr || d.T == 0) return;
+    const int64_t adj_bytes = sim_adj_bytes(d.T, d.I, d.O, d.E);
+    if (adj_bytes >= (int64_t(1) << 35)) raise(TBSIM_E_INVALID_ARGUMENT, "batch too large for the packed simulation graph");
+    const size_t hdr_bytes = static_cast<size_t>(d.T) * sizeof(SimTaskHdr);
+    b->mem3 = ctx->batch_alloc(hdr_bytes + static_cast<size_t>(adj_bytes) + 256, &b->mem3_bytes);
+    b->hdr = static_cast<SimTaskHdr*>(b->mem3);
+    b->adj = static_cast<char*>(b->mem3) + ((hdr_bytes + 255) & ~size_t(255));
+    const int grid = static_cast<int>(std::min<int64_t>((d.T + 255) / 256, 16LL * ctx->n_sms));
+    ctx->begin("k_sim_pack");
+    k_sim_pack<<<grid, 256, 0, ctx->stream>>>(d, b->hdr, b->adj);
+    ctx->end("k_sim_pack");
+}
 
 std::string type_name(const tbsim_batch* b, int32_t ty) {
     if (ty >= 0 && ty < static_cast<int32_t>(b->type_names.size())) return b->type_names[ty];
@@ -491,6 +514,7 @@ tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim
             ctx->begin("k_ingest");
             k_ingest<<<grid, 256, 0, ctx->stream>>>(d, cursor);
             ctx->end("k_ingest");
+            ensure_packed(ctx, b.get());
         }
         if (us.active()) {
             cuda_check(cudaEventCreateWithFlags(&b->ready, cudaEventDisableTiming), "cudaEventCreate");
@@ -506,7 +530,8 @@ tbsim_status tbsim_batch_free(tbsim_ctx* ctx, tbsim_batch* b) {
         if (ctx) {
             // stream-ordered reuse: a later upload waits for every kernel
             // that reads this batch (all on the compute stream)
-            for (auto [m, bytes] : {std::make_pair(b->mem, b->mem_bytes), std::make_pair(b->mem2, b->mem2_bytes)}) {
+            for (auto [m, bytes] : {std::make_pair(b->mem, b->mem_bytes), std::make_pair(b->mem2, b->mem2_bytes),
+                                    std::make_pair(b->mem3, b->mem3_bytes)}) {
                 if (!m) continue;
                 cudaEvent_t ev = nullptr;
                 if (ctx->upload && ctx->upload != ctx->stream) {
@@ -518,6 +543,7 @@ tbsim_status tbsim_batch_free(tbsim_ctx* ctx, tbsim_batch* b) {
         } else {
             if (b->mem) cudaFree(b->mem);
             if (b->mem2) cudaFree(b->mem2);
+            if (b->mem3) cudaFree(b->mem3);
         }
         if (b->ready) cudaEventDestroy(b->ready);
         delete b;
@@ -1286,20 +1312,17 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
     const DevBatch& d = b->d;
     const int64_t G = d.G;
     if (G == 0) return;
-    // packed simulation graph: one record per task + contiguous lists
-    const int64_t adj_bytes = sim_adj_bytes(d.T, d.I, d.O, d.E);
-    if (adj_bytes >= (int64_t(1) << 35)) raise(TBSIM_E_INVALID_ARGUMENT, "batch too large for the packed simulation graph");
-    SimTaskHdr* hdr = ctx->buf("s_hdr").as<SimTaskHdr>(std::max<int64_t>(d.T, 1));
-    char* adj = static_cast<char*>(ctx->buf("s_adj").get(static_cast<size_t>(adj_bytes)));
-    p.hdr = hdr;
-    p.adj = adj;
+    // packed simulation graph (built once per batch) + this call's pop keys
+    ensure_packed(ctx, const_cast<tbsim_batch*>(b));
+    p.hdr = b->hdr;
+    p.adj = b->adj;
     p.log = ctx->buf("s_log").as<SimLog>(std::max<int64_t>(d.T, 1));
     p.n_disp = ctx->buf("s_ndisp").as<int32_t>(G);
     if (d.T > 0) {
         const int grid = static_cast<int>(std::min<int64_t>((d.T + 255) / 256, 16LL * ctx->n_sms));
-        ctx->begin("k_sim_pack");
-        k_sim_pack<<<grid, 256, 0, ctx->stream>>>(d, keys.ability, keys.efficiency, keys.prio, p.policy, hdr, adj);
-        ctx->end("k_sim_pack");
+        ctx->begin("k_sim_keys");
+        k_sim_keys<<<grid, 256, 0, ctx->stream>>>(d, keys.ability, keys.efficiency, keys.prio, p.policy, b->hdr);
+        ctx->end("k_sim_keys");
     }
     p.graph_list = nullptr;
     p.qcap = 0;

@@ -881,8 +881,10 @@ __device__ __forceinline__ int64_t graph_of(const DevBatch& b, int64_t t) {
 
 }  // namespace
 
-__global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* ability, const int64_t* efficiency,
-                                                  const int64_t* prio, int32_t policy, SimTaskHdr* hdr, char* adj) {
+// Structural half of the packed simulation graph (record words 0-3 and the
+// lists); depends only on the batch, so it is built once per batch, at
+// upload (k_ingest's stream) or on first use.
+__global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, SimTaskHdr* hdr, char* adj) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < b.T; t += stride) {
         const int64_t g = graph_of(b, t);
@@ -901,22 +903,10 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* abi
         const int64_t x = 4 * (t0 + v) + 12 * (ib + i0) + 4 * (ob + o0) + 4 * (eb + s0);
         const int64_t x8 = (x + 7) & ~int64_t(7);
         const int32_t nin = i1 - i0, nout = o1 - o0, nsucc = s1 - s0;
-        int32_t ka = 0, ke = 0;
-        int64_t kp = prio && policy >= TBSIM_POLICY_DMDAP ? prio[t] : 0;
-        bool bad = nsucc >= (1 << 24);
-        if (policy == TBSIM_POLICY_INSPIRIT) {
-            const int64_t a64 = ability ? ability[t] : 0, e64 = efficiency ? efficiency[t] : 0;
-            ka = static_cast<int32_t>(a64);
-            ke = static_cast<int32_t>(e64);
-            bad = bad || ka != a64 || ke != e64 || ka < 0;
-        }
-        if (bad) ka = -1;
         int4* h = reinterpret_cast<int4*>(hdr + t);
         h[0] = make_int4(static_cast<int32_t>(x8 >> 3), nin, nout,
                          static_cast<int32_t>((static_cast<uint32_t>(__ldg(&b.type[t])) << 24) |
                                               (static_cast<uint32_t>(nsucc) & 0xffffffu)));
-        h[1] = make_int4(ka, ke, static_cast<int32_t>(static_cast<uint64_t>(kp)),
-                         static_cast<int32_t>(static_cast<uint64_t>(kp) >> 32));
         int64_t* inb = reinterpret_cast<int64_t*>(adj + x8);
         int32_t* inh = reinterpret_cast<int32_t*>(inb + nin);
         const int32_t* in = b.in + ib + i0;
@@ -931,6 +921,32 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* abi
         int32_t* succl = outl + nout;
         const int32_t* succ = b.succ + eb + s0;
         for (int32_t k = 0; k < nsucc; ++k) succl[k] = succ[k];
+    }
+}
+
+// Pop keys of one simulation call (record words 4-7): ability, efficiency
+// and static priority; ab = -1 flags keys beyond the queue's int32 keys or a
+// task with 2^24 successor entries.
+__global__ void __launch_bounds__(256) k_sim_keys(DevBatch b, const int64_t* ability, const int64_t* efficiency,
+                                                  const int64_t* prio, int32_t policy, SimTaskHdr* hdr) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < b.T; t += stride) {
+        int32_t ka = 0, ke = 0;
+        int64_t kp = prio && policy >= TBSIM_POLICY_DMDAP ? prio[t] : 0;
+        // the 24-bit field holds nsucc mod 2^24; the full count is checked here
+        const int64_t g = graph_of(b, t);
+        const int64_t v = t - __ldg(&b.task_base[g]);
+        const int32_t* soff = b.succ_off + __ldg(&b.task_base[g]) + g;
+        bool bad = soff[v + 1] - soff[v] >= (1 << 24);
+        if (policy == TBSIM_POLICY_INSPIRIT) {
+            const int64_t a64 = ability ? ability[t] : 0, e64 = efficiency ? efficiency[t] : 0;
+            ka = static_cast<int32_t>(a64);
+            ke = static_cast<int32_t>(e64);
+            bad = bad || ka != a64 || ke != e64 || ka < 0;
+        }
+        if (bad) ka = -1;
+        reinterpret_cast<int4*>(hdr + t)[1] = make_int4(ka, ke, static_cast<int32_t>(static_cast<uint64_t>(kp)),
+                                                         static_cast<int32_t>(static_cast<uint64_t>(kp) >> 32));
     }
 }
 

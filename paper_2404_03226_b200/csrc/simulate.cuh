@@ -132,9 +132,11 @@ struct SimParams {
     unsigned long long* work_counter;
 };
 
-// Builds the packed records and lists; one thread per task.
-__global__ void k_sim_pack(DevBatch b, const int64_t* ability, const int64_t* efficiency, const int64_t* prio,
-                           int32_t policy, SimTaskHdr* hdr, char* adj);
+// Builds the packed records' structural words and lists (once per batch);
+// k_sim_keys fills the pop keys of one call.  One thread per task.
+__global__ void k_sim_pack(DevBatch b, SimTaskHdr* hdr, char* adj);
+__global__ void k_sim_keys(DevBatch b, const int64_t* ability, const int64_t* efficiency, const int64_t* prio,
+                           int32_t policy, SimTaskHdr* hdr);
 // Moves the dispatch logs into worker/start/end; one thread per log slot.
 __global__ void k_sim_scatter(DevBatch b, const SimLog* log, const int32_t* n_disp, int32_t* worker, double* start_ms,
                               double* end_ms);
