@@ -745,7 +745,9 @@ def main():
             "config": {"workload": w["name"], "n_dags_per_gpu": G, "tasks_per_dag": w["n_tasks"],
                        "platform": "8 CPU + 2 GPU workers (assemble)", "policy": w["policy"],
                        "priority": "UpwardRank", "parallelism": f"dp{world} (DAG shards, NCCL all-gather)",
-                       "l2": "256 MB buffer written before every timed step; batch CSR > L2"},
+                       "l2": "256 MB buffer written before every timed step; batch CSR > L2",
+                       "resident_input": "value: the batch's device form (CSR, successor CSR, packed task "
+                                         "records) built at upload; e2e uploads + ingests every step"},
             "decisions_per_sec": value * 2 * w["n_tasks"],
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
