@@ -836,8 +836,19 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     const uint64_t span_mask = prune_span >= 64 ? ~0ull : ((1ull << prune_span) - 1ull);
     uint64_t recent = 0;
     __syncthreads();
+    // Level La holds the tile's first sources and nothing reachable from any
+    // source of the tile (an edge always ends at a higher level; the tile's
+    // other sources come later): its rows stay -inf except each source's own
+    // distance-0 cell, so that level is written, not swept.
+    {
+        const int32_t e = min(first + nsrc, lstart[La + 1]);
+        for (int32_t i = first + static_cast<int32_t>(threadIdx.x); i < e; i += blockDim.x)
+            win[static_cast<int64_t>(__ldg(&om_slot[i])) * S + (i - first)] = 0.0;
+    }
+    recent = 1;  // level La wrote distances <= wmax (the sources' zeros)
+    __syncthreads();
 
-    for (int32_t lv = La; lv < gi.n_levels; ++lv) {
+    for (int32_t lv = La + 1; lv < gi.n_levels; ++lv) {
         int small = 0;
         const int32_t a1 = lstart[lv + 1];
         if (relax_ctr && threadIdx.x == 0) nrel += static_cast<uint64_t>(__ldg(&om_poff[a1]) - __ldg(&om_poff[lstart[lv]]));
@@ -1009,10 +1020,21 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
         return r;
     };
     Rec nx{0, 0, 0, 0.0};
-    if (lstart[La] + gidx < lstart[La + 1]) nx = load_rec(lstart[La] + gidx);
+    if (La + 1 < gi.n_levels && lstart[La + 1] + gidx < lstart[La + 2]) nx = load_rec(lstart[La + 1] + gidx);
+    __syncthreads();
+    // Level La holds the tile's first sources and nothing reachable from any
+    // source of the tile (an edge always ends at a higher level; the tile's
+    // other sources come later): its rows stay -inf except each source's own
+    // distance-0 cell, so that level is written, not swept.
+    {
+        const int32_t e = min(first + nsrc, lstart[La + 1]);
+        for (int32_t i = first + static_cast<int32_t>(tid); i < e; i += nthr)
+            reinterpret_cast<double*>(w2)[static_cast<int64_t>(__ldg(&om_slot[i])) * S + (i - first)] = 0.0;
+    }
+    recent = 1;  // level La wrote distances <= wmax (the sources' zeros)
     __syncthreads();
 
-    for (int32_t lv = La; lv < gi.n_levels; ++lv) {
+    for (int32_t lv = La + 1; lv < gi.n_levels; ++lv) {
         int small = 0;
         const int32_t a0 = lstart[lv], a1 = lstart[lv + 1];
         const int32_t a2 = lv + 1 < gi.n_levels ? lstart[lv + 2] : a1;
