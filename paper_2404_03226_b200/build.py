@@ -47,9 +47,10 @@ def _stale(obj, srcs):
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
-def _run(cmd, attempts: int = 3) -> None:
+def _run(cmd, attempts: int = 8) -> None:
     """Run a compiler command; a crash (signal) is retried -- nvcc 12.9 has
-    been seen to segfault intermittently in this image.  Compile errors
+    been seen to segfault intermittently in this image (cicc, on the large
+    simulator translation unit).  Compile errors
     raise immediately."""
     for i in range(attempts):
         rc = subprocess.call(cmd)

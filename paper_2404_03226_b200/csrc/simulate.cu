@@ -32,7 +32,6 @@ namespace tbsim_dev {
 
 namespace {
 
-constexpr uint32_t kNone = 0xffffffffu;
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint64_t ord_f64(double x) {
@@ -416,7 +415,11 @@ struct Sim {
     }
 
     // ------------------------------------------------------------- engine
-    __device__ __forceinline__ void maybe_dispatch(int32_t w) {  // engine.cpp:143-166
+    // pushed: a push to w just happened and its queue event (the regulator
+    // step) is still due -- both queue events of a push-then-pop run through
+    // one call site of queue_event, which keeps the kernel's hot code small
+    // (instruction-cache stalls are the simulator's largest stall class).
+    __device__ __forceinline__ void maybe_dispatch(int32_t w, bool pushed) {  // engine.cpp:143-166
         const int j = w >> 5, owner = w & 31;
         int32_t ql = 0, bz = 0, kd = 0, nd = 0;
 #pragma unroll
@@ -426,51 +429,59 @@ struct Sim {
         bz = __shfl_sync(kFull, bz, owner);
         kd = __shfl_sync(kFull, kd, owner);
         nd = __shfl_sync(kFull, nd, owner);
-        if (bz || ql == 0) return;
-        const int32_t pick = select_entry(w, ql, nd);
-        int32_t* q = queue(w);
-        KeyT* ka = qab(w);
-        KeyT* ke = qef(w);
-        PrioT* kp = qprio(w);
-        const uint32_t e = static_cast<uint32_t>(q[pick]);
-        __syncwarp();
-        const bool ins = pol() == TBSIM_POLICY_INSPIRIT, pri = pol() >= TBSIM_POLICY_DMDAP;
-        for (int32_t b0 = pick; b0 < ql - 1; b0 += 32) {
-            const int32_t i = b0 + lane;
-            const bool mv = i < ql - 1;
-            int32_t val = 0;
-            KeyT va = 0, ve = 0;
-            PrioT vp = 0;
-            if (mv) {
-                val = q[i + 1];
-                if (ins) { va = ka[i + 1]; ve = ke[i + 1]; }
-                if (pri) vp = kp[i + 1];
+        uint32_t e = 0;
+        int64_t slot = 0;
+        int4 hd = make_int4(0, 0, 0, 0);
+#pragma unroll 1
+        for (int k = pushed ? 0 : 1; k < 2; ++k) {
+            if (k == 1) {
+                if (bz || ql == 0) return;
+                const int32_t pick = select_entry(w, ql, nd);
+                int32_t* q = queue(w);
+                KeyT* ka = qab(w);
+                KeyT* ke = qef(w);
+                PrioT* kp = qprio(w);
+                e = static_cast<uint32_t>(q[pick]);
+                __syncwarp();
+                const bool ins = pol() == TBSIM_POLICY_INSPIRIT, pri = pol() >= TBSIM_POLICY_DMDAP;
+                for (int32_t b0 = pick; b0 < ql - 1; b0 += 32) {
+                    const int32_t i = b0 + lane;
+                    const bool mv = i < ql - 1;
+                    int32_t val = 0;
+                    KeyT va = 0, ve = 0;
+                    PrioT vp = 0;
+                    if (mv) {
+                        val = q[i + 1];
+                        if (ins) { va = ka[i + 1]; ve = ke[i + 1]; }
+                        if (pri) vp = kp[i + 1];
+                    }
+                    __syncwarp();
+                    if (mv) {
+                        q[i] = val;
+                        if (ins) { ka[i] = va; ke[i] = ve; }
+                        if (pri) kp[i] = vp;
+                    }
+                    __syncwarp();
+                }
+                const int32_t task = static_cast<int32_t>(e & 0xffffffu);
+                hd = head(task);  // issued before the queue bookkeeping
+                nready -= 1;
+                // dispatch counter and log slot: lane 0 only (cold state)
+                if (lane == 0) {
+                    SimCold& c = cold();
+                    slot = c.t0 + c.n_pop;
+                    c.n_pop += 1;
+                    if (P->pop_time) {
+                        P->pop_time[slot] = now;
+                        P->pop_task[slot] = task;
+                        P->pop_worker[slot] = w;
+                    }
+                }
             }
-            __syncwarp();
-            if (mv) {
-                q[i] = val;
-                if (ins) { ka[i] = va; ke[i] = ve; }
-                if (pri) kp[i] = vp;
-            }
-            __syncwarp();
+            queue_event();
         }
         const int32_t task = static_cast<int32_t>(e & 0xffffffu);
         const int32_t ty = static_cast<int32_t>(e >> 24);
-        const int4 hd = head(task);  // issued before the queue bookkeeping
-        nready -= 1;
-        // dispatch counter and log slot: lane 0 only (cold state)
-        int64_t slot = 0;
-        if (lane == 0) {
-            SimCold& c = cold();
-            slot = c.t0 + c.n_pop;
-            c.n_pop += 1;
-            if (P->pop_time) {
-                P->pop_time[slot] = now;
-                P->pop_task[slot] = task;
-                P->pop_worker[slot] = w;
-            }
-        }
-        queue_event();
         const int64_t* inb = reinterpret_cast<const int64_t*>(lists(hd));
         const double xfer = transfer_total_lanes(inb, reinterpret_cast<const int32_t*>(inb + hd.y), hd.y, nd);
         const double exec = cost(ty, kd);
@@ -555,8 +566,7 @@ struct Sim {
             }
             __syncwarp();
         }
-        queue_event();
-        return w;
+        return w;  // its queue event runs in maybe_dispatch(w, true)
     }
 
     // Appends the lanes with `rdy` (task v) to the ready list in lane order:
@@ -607,6 +617,7 @@ struct Sim {
         bool events = false;
         for (;;) {
             int32_t w;
+            bool pushed = false;
             if (!events) {
                 if (rcount > 0) {
                     const int32_t v = rhead;
@@ -615,6 +626,7 @@ struct Sim {
                     w = on_push(v);
                     rhead = nx;
                     if (status != GS_OK) return;
+                    pushed = true;
                 } else {
                     // next worker-event time
                     uint64_t lt = ~0ull;
@@ -701,7 +713,7 @@ struct Sim {
                 }
                 __syncwarp();
             }
-            maybe_dispatch(w);
+            maybe_dispatch(w, pushed);
             if (status != GS_OK) return;
         }
     }
