@@ -728,8 +728,14 @@ __device__ void simulate_impl(const SimParams& p) {
     const int warp_in_block = threadIdx.x >> 5;
     const int warps_per_block = blockDim.x >> 5;
     char* base;
-    if constexpr (SMEM) base = smem + warp_in_block * static_cast<int32_t>(p.state_bytes);
-    else base = p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
+    if constexpr (SMEM) {
+        // the warp's state offset passes through an opaque move so the
+        // compiler keeps it in a register instead of re-deriving it from
+        // %tid (S2R + shift + multiply) at every state access
+        uint32_t off = static_cast<uint32_t>(warp_in_block) * static_cast<uint32_t>(p.state_bytes);
+        asm volatile("mov.b32 %0, %1;" : "=r"(off) : "r"(off));
+        base = smem + off;
+    } else base = p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
     const DevBatch& b = p.b;
     using S = Sim<WPL, COMPACT, POL>;
     S s;
