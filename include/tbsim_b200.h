@@ -137,8 +137,9 @@ tbsim_status tbsim_ctx_set_async_results(tbsim_ctx* ctx, int enable);
  * efficiency sweep pruned at the largest window. */
 tbsim_status tbsim_ctx_set_large_graph_threshold(tbsim_ctx* ctx, int64_t n_tasks);
 /* Sources per efficiency-sweep tile: 0 (default) picks the widest of
- * 128/64/32/16/8 whose distance window fits shared memory; 8..128 forces it
- * (tests of every tile shape; results do not depend on it). */
+ * 256 (FP32-exact windows only)/128/64/32/16/8 whose distance window fits
+ * shared memory; 8..256 forces it (tests of every tile shape; results do not
+ * depend on it). */
 tbsim_status tbsim_ctx_set_sweep_tile(tbsim_ctx* ctx, int32_t sources);
 /* Number of kernels this context launched since creation (bench evidence). */
 int64_t tbsim_ctx_launch_count(const tbsim_ctx* ctx);

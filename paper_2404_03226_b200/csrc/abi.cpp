@@ -390,8 +390,9 @@ tbsim_status tbsim_ctx_set_large_graph_threshold(tbsim_ctx* ctx, int64_t n_tasks
 
 tbsim_status tbsim_ctx_set_sweep_tile(tbsim_ctx* ctx, int32_t sources) {
     return guarded([&] {
-        if (sources != 0 && sources != 8 && sources != 16 && sources != 32 && sources != 64 && sources != 128)
-            raise(TBSIM_E_INVALID_ARGUMENT, "sweep tile must be 0, 8, 16, 32, 64 or 128 sources");
+        if (sources != 0 && sources != 8 && sources != 16 && sources != 32 && sources != 64 && sources != 128 &&
+            sources != 256)
+            raise(TBSIM_E_INVALID_ARGUMENT, "sweep tile must be 0, 8, 16, 32, 64, 128 or 256 sources");
         ctx->sweep_tile = sources;
     });
 }
@@ -730,9 +731,9 @@ AttrScratch alloc_attr_scratch(tbsim_ctx* ctx, const DevBatch& d) {
 constexpr int kSweepThreads = 512;
 
 int64_t sweep_smem_bytes(tbsim_ctx* ctx) {
-    // leave room for the kernel's static shared memory (costs + histogram)
+    // leave room for the kernel's static shared memory (256-source histogram)
     int64_t opt = static_cast<int64_t>(ctx->smem_optin);
-    return std::max<int64_t>(0, opt - 8 * 1024);
+    return std::max<int64_t>(0, opt - 14 * 1024);
 }
 
 // One large graph: the structure pass with the whole GPU (cooperative).
@@ -811,7 +812,7 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
     if (do_sweep && !(large && sweep_mode == SWEEP_ABILITY)) {
         const int64_t smem = sweep_smem_bytes(ctx);
         ctx->begin("k_tile_plan");
-        k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, run.s, smem, ctx->sweep_tile);
+        k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, run.s, smem, ctx->sweep_tile, d_costs, d_cost_idx, sweep_mode);
         ctx->end("k_tile_plan");
         // graphs whose distance window exceeds shared memory use a global
         // window; size it from the worst case (every node live)
@@ -1089,12 +1090,13 @@ extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbs
         }
         // ---- efficiency sweep over this rank's share of the source tiles
         const int64_t smem = sweep_smem_bytes(ctx);
-        k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, s, smem, ctx->sweep_tile);
+        k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, s, smem, ctx->sweep_tile, d_costs, nullptr, SWEEP_CALIBRATE);
         int32_t S = 0;
         int64_t tiles = 0;
         cuda_check(cudaMemcpyAsync(&S, s.tile_s, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H tile width");
         cuda_check(cudaMemcpyAsync(&tiles, s.tile_base + 1, 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H tiles");
         ctx->sync();
+        S &= kTileWidthMask;
         const int64_t t_lo = tiles * rank / world, t_hi = tiles * (rank + 1) / world;
         const int32_t pos_lo = static_cast<int32_t>(std::min<int64_t>(t_lo * S, n));
         const int32_t pos_hi = static_cast<int32_t>(std::min<int64_t>(t_hi * S, n));

@@ -350,6 +350,9 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
             gi.miss_any = s_miss_any == INT32_MAX ? -1 : s_miss_any;
             gi.order_det = 0;
             gi.pad_ = 0;
+            gi.gpu_types = 0;
+            for (int t = 0; t < kMaxTypes; ++t)
+                if (s_tcount[t] > 0) gi.gpu_types |= 1ull << t;
             gi.median = (n > 0 && gi.miss_gpu < 0) ? lower_median_gpu(sc, s_tcount, NT, n) : 0.0;
             s.info[g] = gi;
             s.median[g] = gi.median;
@@ -669,6 +672,9 @@ __global__ void __launch_bounds__(512) k_structure_large(DevBatch b, const DevCo
         gi.miss_any = ma > 0 ? n - ma : -1;
         gi.order_det = sort_levels && !__ldcg(&ctl->unsorted) ? 1 : 0;
         gi.pad_ = 0;
+        gi.gpu_types = 0;
+        for (int t = 0; t < kMaxTypes; ++t)
+            if (tc[t] > 0) gi.gpu_types |= 1ull << t;
         gi.median = (n > 0 && gi.miss_gpu < 0) ? lower_median_gpu(sc, tc, NT, n) : 0.0;
         s.info[g] = gi;
         s.median[g] = gi.median;
@@ -684,9 +690,22 @@ __global__ void __launch_bounds__(512) k_structure_large(DevBatch b, const DevCo
 // like their bit patterns.
 struct Thresholds {
     int32_t mode;       // 0: calibration grid fast path, 1: ladder, 2: ability only
+    int32_t w0bits32;   // bits((float)W_0) -- FP32 windows (exact there, see k_tile_plan)
     int64_t w0bits;     // bits(W_0)
     double w[kWindows];
 };
+
+// 16 bytes of distance columns: 2 doubles or 4 floats (one LDS/STS.128).
+template <typename T>
+struct __align__(16) Chunk {
+    static constexpr int N = 16 / static_cast<int>(sizeof(T));
+    T v[N];
+};
+
+// max of two distances (-inf or non-negative, never NaN): FMNMX for FP32,
+// compare-select for FP64 (no FP64 min/max instruction)
+__device__ __forceinline__ float dmax(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
 __device__ __forceinline__ int bin_of(double d, const Thresholds& th) {
     if (th.mode == 0) {
@@ -723,6 +742,7 @@ __device__ __forceinline__ void bump16(uint64_t (&h)[3], int bin) {
 
 __device__ Thresholds make_thresholds(int32_t mode_req, double w0_or_unit) {
     Thresholds th;
+    th.w0bits32 = 0;
     if (mode_req == SWEEP_ABILITY) {
         th.mode = 2;
         th.w0bits = 0;
@@ -737,6 +757,7 @@ __device__ Thresholds make_thresholds(int32_t mode_req, double w0_or_unit) {
     }
     for (int j = 0; j < kWindows; ++j) th.w[j] = ldexp(w0_or_unit, j - 4);
     th.w0bits = __double_as_longlong(th.w[0]);
+    th.w0bits32 = __float_as_int(static_cast<float>(th.w[0]));
     const bool normal = th.w[0] >= DBL_MIN && th.w[kWindows - 1] <= DBL_MAX;
     th.mode = normal ? 0 : 1;
     return th;
@@ -746,6 +767,25 @@ __device__ Thresholds make_thresholds(int32_t mode_req, double w0_or_unit) {
 // records are read in level order (order-major arrays), the sources' distance
 // columns live in shared memory: win[slot][S].
 // Window bin with the threshold mode known at compile time.
+// FP32 distances (exact, see k_tile_plan): W_k = W_0 * 2^k are exact floats,
+// bits(W_k) = bits(W_0) + k << 23.
+template <int TMODE>
+__device__ __forceinline__ int bin_t(float d, const Thresholds& th) {
+    if constexpr (TMODE == 0) {
+        const int32_t delta = __float_as_int(d) - th.w0bits32;
+        const int k = (delta + ((1 << 23) - 1)) >> 23;
+        return min(max(k, 0), kWindows);
+    } else if constexpr (TMODE == 2) {
+        return kWindows;
+    } else {
+        int k = 0;
+        const double dd = d;
+#pragma unroll
+        for (int j = 0; j < kWindows; ++j) k += dd > th.w[j];
+        return k;
+    }
+}
+
 template <int TMODE>
 __device__ __forceinline__ int bin_t(double d, const Thresholds& th) {
     if constexpr (TMODE == 0) {
@@ -791,15 +831,19 @@ __device__ __forceinline__ void flush5(uint64_t& h, uint32_t* dst) {
 // columns live in shared memory, win[slot][S], with each lane's pairs of
 // sources interleaved across the group so every double2 access is contiguous
 // over the lanes (conflict-free 128-bit LDS/STS).
-template <int S, bool SMEM, int TMODE>
+// T = float: the FP32-exact window (k_tile_plan) -- half the bytes per
+// column (twice the sources per tile) and FMNMX instead of compare-select.
+template <int S, bool SMEM, int TMODE, typename T = double>
 __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                            double* gwin, int32_t P, const Thresholds& th,
                                            uint32_t* s_hist, int32_t prune_span, unsigned long long* relax_ctr) {
     extern __shared__ double win_smem[];
-    double* win = SMEM ? win_smem : gwin;
+    T* win = SMEM ? reinterpret_cast<T*>(win_smem) : reinterpret_cast<T*>(gwin);
     uint64_t nrel = 0;  // predecessor rows relaxed (x S columns), thread 0
     constexpr int GL = S < 32 ? S : 32;   // lanes per node group
     constexpr int SPL = S / GL;           // sources per lane
+    constexpr int VEC = Chunk<T>::N;      // columns per 16-byte access
+    constexpr bool VECTOR = SPL >= VEC;
     constexpr int GPW = 32 / GL;          // groups per warp
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
@@ -816,10 +860,13 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     const int32_t first = tile * S;
     const int32_t nsrc = min(S, gi.processed - first);
 
+    const T ninf = static_cast<T>(-CUDART_INF);
     {
-        double2* w2 = reinterpret_cast<double2*>(win);
-        const double2 neg = make_double2(-CUDART_INF, -CUDART_INF);  // unreachable
-        for (int64_t i = threadIdx.x; i < static_cast<int64_t>(P) * (S / 2); i += blockDim.x) w2[i] = neg;
+        Chunk<T>* w2 = reinterpret_cast<Chunk<T>*>(win);
+        Chunk<T> neg;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) neg.v[e] = ninf;  // unreachable
+        for (int64_t i = threadIdx.x; i < static_cast<int64_t>(P) * (S / VEC); i += blockDim.x) w2[i] = neg;
     }
     for (int i = threadIdx.x; i < S * kBins; i += blockDim.x) s_hist[i] = 0u;
     uint64_t hist[SPL];
@@ -827,12 +874,14 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     for (int q = 0; q < SPL; ++q) hist[q] = 0;
     int32_t visits = 0;  // node visits since the last flush (uniform per group)
     const int32_t La = s.level[t0 + s.order[t0 + first]];
-    auto src = [&](int q) { return SPL >= 2 ? (q >> 1) * 2 * GL + 2 * gl + (q & 1) : gl; };
+    // column of this lane's q-th source: 16-byte chunks interleaved over the
+    // group's lanes (conflict-free LDS.128 / STS.128)
+    auto src = [&](int q) { return VECTOR ? (q / VEC) * VEC * GL + VEC * gl + (q % VEC) : gl * SPL + q; };
     // Pruning (large graphs, ability computed elsewhere): distances only grow
     // along paths, so once no distance within the largest window was written
     // in the last `prune_span` levels (the longest edge span), no later node
     // can fall inside any window and the tile is done.
-    const double wmax = th.w[kWindows - 1];
+    const T wmax = static_cast<T>(th.w[kWindows - 1]);
     const uint64_t span_mask = prune_span >= 64 ? ~0ull : ((1ull << prune_span) - 1ull);
     uint64_t recent = 0;
     __syncthreads();
@@ -843,7 +892,7 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     {
         const int32_t e = min(first + nsrc, lstart[La + 1]);
         for (int32_t i = first + static_cast<int32_t>(threadIdx.x); i < e; i += blockDim.x)
-            win[static_cast<int64_t>(__ldg(&om_slot[i])) * S + (i - first)] = 0.0;
+            win[static_cast<int64_t>(__ldg(&om_slot[i])) * S + (i - first)] = static_cast<T>(0);
     }
     recent = 1;  // level La wrote distances <= wmax (the sources' zeros)
     __syncthreads();
@@ -856,24 +905,23 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
         for (int32_t i = lstart[lv] + warp * GPW + grp; i < a1; i += nwarps * GPW) {
             const int32_t p0 = __ldg(&om_poff[i]);
             const int32_t deg = __ldg(&om_poff[i + 1]) - p0;
-            const double gv = TMODE == 2 ? 1.0 : __ldg(&om_gpu[i]);
+            const T gv = TMODE == 2 ? static_cast<T>(1) : static_cast<T>(__ldg(&om_gpu[i]));
             const int32_t sl = __ldg(&om_slot[i]);
-            double m[SPL];
+            T m[SPL];
 #pragma unroll
-            for (int q = 0; q < SPL; ++q) m[q] = -CUDART_INF;
-            // plain compare-select: operands are -inf or non-negative, never NaN
+            for (int q = 0; q < SPL; ++q) m[q] = ninf;
             auto relax = [&](int32_t ps) {
-                const double* row = win + ps * S;
-                if constexpr (SPL >= 2) {
+                const T* row = win + ps * S;
+                if constexpr (VECTOR) {
 #pragma unroll
-                    for (int q = 0; q < SPL; q += 2) {
-                        const double2 x = *reinterpret_cast<const double2*>(row + src(q));
-                        m[q] = x.x > m[q] ? x.x : m[q];
-                        m[q + 1] = x.y > m[q + 1] ? x.y : m[q + 1];
+                    for (int q = 0; q < SPL; q += VEC) {
+                        const Chunk<T> x = *reinterpret_cast<const Chunk<T>*>(row + src(q));
+#pragma unroll
+                        for (int e = 0; e < VEC; ++e) m[q + e] = dmax(x.v[e], m[q + e]);
                     }
                 } else {
-                    const double x = row[gl];
-                    m[0] = x > m[0] ? x : m[0];
+#pragma unroll
+                    for (int q = 0; q < SPL; ++q) m[q] = dmax(row[src(q)], m[q]);
                 }
             };
             auto relax_chunk = [&](int32_t myps, int32_t lim) {
@@ -893,12 +941,12 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
                     relax_chunk((c + gl < deg) ? __ldg(&om_ps[p0 + c + gl]) : 0, min(GL, deg - c));
             }
             // unreachable stays -inf (-inf + gv); reachable distances are >= 0
-            double d[SPL];
+            T d[SPL];
             const bool node_is_src = static_cast<uint32_t>(i - first) < static_cast<uint32_t>(S);
 #pragma unroll
             for (int q = 0; q < SPL; ++q) {
                 d[q] = m[q] + gv;
-                const bool counted = d[q] >= 0.0;
+                const bool counted = d[q] >= static_cast<T>(0);
                 const int bn = bin_t<TMODE>(d[q], th);
                 hist[q] += shl64(1ull, counted ? static_cast<uint32_t>(kFieldBits * bn) : 64u);
             }
@@ -906,20 +954,27 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
 #pragma unroll
                 for (int q = 0; q < SPL; ++q)
                     if (i == first + src(q)) {
-                        if (d[q] >= 0.0) hist[q] -= shl64(1ull, static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d[q], th)));
-                        d[q] = 0.0;
+                        if (d[q] >= static_cast<T>(0))
+                            hist[q] -= shl64(1ull, static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d[q], th)));
+                        d[q] = static_cast<T>(0);
                     }
             }
             if (prune_span > 0) {
 #pragma unroll
-                for (int q = 0; q < SPL; ++q) small |= d[q] >= 0.0 && d[q] <= wmax;
+                for (int q = 0; q < SPL; ++q) small |= d[q] >= static_cast<T>(0) && d[q] <= wmax;
             }
-            double* outp = win + sl * S;
-            if constexpr (SPL >= 2) {
+            T* outp = win + sl * S;
+            if constexpr (VECTOR) {
 #pragma unroll
-                for (int q = 0; q < SPL; q += 2) *reinterpret_cast<double2*>(outp + src(q)) = make_double2(d[q], d[q + 1]);
+                for (int q = 0; q < SPL; q += VEC) {
+                    Chunk<T> x;
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) x.v[e] = d[q + e];
+                    *reinterpret_cast<Chunk<T>*>(outp + src(q)) = x;
+                }
             } else {
-                outp[gl] = d[0];
+#pragma unroll
+                for (int q = 0; q < SPL; ++q) outp[src(q)] = d[q];
             }
             if (++visits == kFlushEvery) {
 #pragma unroll
@@ -949,13 +1004,15 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     }
 }
 
-template <int S, bool SMEM>
+// FP32 windows run only in modes 0 and 2 (k_tile_plan never picks them for
+// the ladder of a caller-given window)
+template <int S, bool SMEM, typename T = double>
 __device__ __forceinline__ void sweep_tile_mode(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                                 double* gwin, int32_t P, const Thresholds& th,
                                                 uint32_t* s_hist, int32_t prune_span, unsigned long long* rc) {
-    if (th.mode == 0) sweep_tile<S, SMEM, 0>(b, s, g, tile, gwin, P, th, s_hist, prune_span, rc);
-    else if (th.mode == 2) sweep_tile<S, SMEM, 2>(b, s, g, tile, gwin, P, th, s_hist, 0, rc);
-    else sweep_tile<S, SMEM, 1>(b, s, g, tile, gwin, P, th, s_hist, prune_span, rc);
+    if (th.mode == 0) sweep_tile<S, SMEM, 0, T>(b, s, g, tile, gwin, P, th, s_hist, prune_span, rc);
+    else if (th.mode == 2) sweep_tile<S, SMEM, 2, T>(b, s, g, tile, gwin, P, th, s_hist, 0, rc);
+    else if constexpr (sizeof(T) == 8) sweep_tile<S, SMEM, 1, T>(b, s, g, tile, gwin, P, th, s_hist, prune_span, rc);
 }
 
 // Row-per-group sweep: a group of GL lanes (GL = 1, 2, 4, 8) owns one node
@@ -970,15 +1027,16 @@ __device__ __forceinline__ void sweep_tile_mode(const DevBatch& b, const AttrScr
 // rotated order (m[j]), so no register is indexed dynamically.  The next
 // level's first node record of each group is loaded while the current level
 // runs.
-template <int S, int GL, int TMODE>
+template <int S, int GL, int TMODE, typename T = double>
 __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                                 int32_t P, const Thresholds& th, uint32_t* s_hist,
                                                 int32_t prune_span, unsigned long long* relax_ctr) {
     extern __shared__ double win_smem[];
     uint64_t nrel = 0;  // predecessor rows relaxed (x S columns), thread 0
-    constexpr int SPL = S / GL;   // columns per lane
-    constexpr int NCL = SPL / 2;  // 16-byte chunks per lane
-    constexpr int NC = S / 2;     // chunks per row
+    constexpr int VEC = Chunk<T>::N;  // columns per 16-byte chunk
+    constexpr int SPL = S / GL;       // columns per lane
+    constexpr int NCL = SPL / VEC;    // chunks per lane
+    constexpr int NC = S / VEC;       // chunks per row
     static_assert(NCL >= 1 && (NCL & (NCL - 1)) == 0, "power-of-two chunks per lane");
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int gl = tid % GL, gidx = tid / GL, ngroups = nthr / GL;
@@ -992,34 +1050,37 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
     const GraphInfo gi = s.info[g];
     const int32_t first = tile * S;
     const int32_t nsrc = min(S, gi.processed - first);
-    double2* w2 = reinterpret_cast<double2*>(win_smem);
+    const T ninf = static_cast<T>(-CUDART_INF);
+    Chunk<T>* w2 = reinterpret_cast<Chunk<T>*>(win_smem);
     {
-        const double2 neg = make_double2(-CUDART_INF, -CUDART_INF);  // unreachable
+        Chunk<T> neg;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) neg.v[e] = ninf;  // unreachable
         for (int64_t i = tid; i < static_cast<int64_t>(P) * NC; i += nthr) w2[i] = neg;
     }
     for (int i = tid; i < S * kBins; i += nthr) s_hist[i] = 0u;
-    uint64_t hist[SPL];  // hist[2j+e]: source 2*chunk(j)+e
+    uint64_t hist[SPL];  // hist[VEC*j+e]: source VEC*chunk(j)+e
 #pragma unroll
     for (int q = 0; q < SPL; ++q) hist[q] = 0;
     auto chunk = [&](int j) { return ((j + rot) & (NCL - 1)) * GL + gl; };
     int32_t visits = 0;
     const int32_t La = s.level[t0 + s.order[t0 + first]];
-    const double wmax = th.w[kWindows - 1];
+    const T wmax = static_cast<T>(th.w[kWindows - 1]);
     const uint64_t span_mask = prune_span >= 64 ? ~0ull : ((1ull << prune_span) - 1ull);
     uint64_t recent = 0;
     struct Rec {
         int32_t p0, p1, sl;
-        double gv;
+        T gv;
     };
     auto load_rec = [&](int32_t i) {
         Rec r;
         r.p0 = __ldg(&om_poff[i]);
         r.p1 = __ldg(&om_poff[i + 1]);
         r.sl = __ldg(&om_slot[i]);
-        r.gv = TMODE == 2 ? 1.0 : __ldg(&om_gpu[i]);
+        r.gv = TMODE == 2 ? static_cast<T>(1) : static_cast<T>(__ldg(&om_gpu[i]));
         return r;
     };
-    Rec nx{0, 0, 0, 0.0};
+    Rec nx{0, 0, 0, static_cast<T>(0)};
     if (La + 1 < gi.n_levels && lstart[La + 1] + gidx < lstart[La + 2]) nx = load_rec(lstart[La + 1] + gidx);
     __syncthreads();
     // Level La holds the tile's first sources and nothing reachable from any
@@ -1029,7 +1090,7 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
     {
         const int32_t e = min(first + nsrc, lstart[La + 1]);
         for (int32_t i = first + static_cast<int32_t>(tid); i < e; i += nthr)
-            reinterpret_cast<double*>(w2)[static_cast<int64_t>(__ldg(&om_slot[i])) * S + (i - first)] = 0.0;
+            reinterpret_cast<T*>(w2)[static_cast<int64_t>(__ldg(&om_slot[i])) * S + (i - first)] = static_cast<T>(0);
     }
     recent = 1;  // level La wrote distances <= wmax (the sources' zeros)
     __syncthreads();
@@ -1043,17 +1104,18 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
         if (relax_ctr && tid == 0) nrel += static_cast<uint64_t>(__ldg(&om_poff[a1]) - __ldg(&om_poff[a0]));
         for (int32_t i = a0 + gidx; i < a1; i += ngroups) {
             const Rec r = i == a0 + gidx ? cur : load_rec(i);
-            double2 m[NCL];
+            T m[NCL][VEC];
 #pragma unroll
-            for (int j = 0; j < NCL; ++j) m[j] = make_double2(-CUDART_INF, -CUDART_INF);
-            // plain compare-select: operands are -inf or non-negative, never NaN
+            for (int j = 0; j < NCL; ++j)
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) m[j][e] = ninf;
             auto relax = [&](int32_t ps) {
-                const double2* row = w2 + static_cast<int64_t>(ps) * NC;
+                const Chunk<T>* row = w2 + static_cast<int64_t>(ps) * NC;
 #pragma unroll
                 for (int j = 0; j < NCL; ++j) {
-                    const double2 x = row[chunk(j)];
-                    m[j].x = x.x > m[j].x ? x.x : m[j].x;
-                    m[j].y = x.y > m[j].y ? x.y : m[j].y;
+                    const Chunk<T> x = row[chunk(j)];
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) m[j][e] = dmax(x.v[e], m[j][e]);
                 }
             };
             int32_t k = r.p0;
@@ -1064,33 +1126,32 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
             }
             if (k < r.p1) relax(__ldg(&om_ps[k]));
             const int32_t si = i - first;  // this node's own source column, if it is one
-            double2* outp = w2 + static_cast<int64_t>(r.sl) * NC;
+            Chunk<T>* outp = w2 + static_cast<int64_t>(r.sl) * NC;
 #pragma unroll
             for (int j = 0; j < NCL; ++j) {
-                double d0 = m[j].x + r.gv, d1 = m[j].y + r.gv;
-                const bool c0 = d0 >= 0.0, c1 = d1 >= 0.0;
-                hist[2 * j] += shl64(1ull, c0 ? static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d0, th)) : 64u);
-                hist[2 * j + 1] += shl64(1ull, c1 ? static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d1, th)) : 64u);
-                if (static_cast<uint32_t>(si) < static_cast<uint32_t>(S)) {
-                    // the source itself: distance 0, not its own descendant
-                    if (2 * chunk(j) == si) {
-                        if (c0) hist[2 * j] -= shl64(1ull, static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d0, th)));
-                        d0 = 0.0;
+                Chunk<T> out;
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) {
+                    T d = m[j][e] + r.gv;
+                    const bool c = d >= static_cast<T>(0);
+                    uint64_t& h = hist[VEC * j + e];
+                    h += shl64(1ull, c ? static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d, th)) : 64u);
+                    if (static_cast<uint32_t>(si) < static_cast<uint32_t>(S) && VEC * chunk(j) + e == si) {
+                        // the source itself: distance 0, not its own descendant
+                        if (c) h -= shl64(1ull, static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d, th)));
+                        d = static_cast<T>(0);
                     }
-                    if (2 * chunk(j) + 1 == si) {
-                        if (c1) hist[2 * j + 1] -= shl64(1ull, static_cast<uint32_t>(kFieldBits * bin_t<TMODE>(d1, th)));
-                        d1 = 0.0;
-                    }
+                    if (prune_span > 0) small |= d >= static_cast<T>(0) && d <= wmax;
+                    out.v[e] = d;
                 }
-                if (prune_span > 0) small |= (d0 >= 0.0 && d0 <= wmax) || (d1 >= 0.0 && d1 <= wmax);
-                outp[chunk(j)] = make_double2(d0, d1);
+                outp[chunk(j)] = out;
             }
             if (++visits == kFlushEvery) {
 #pragma unroll
                 for (int j = 0; j < NCL; ++j)
 #pragma unroll
-                    for (int e = 0; e < 2; ++e)
-                        if (2 * chunk(j) + e < nsrc) flush5(hist[2 * j + e], s_hist + (2 * chunk(j) + e) * kBins);
+                    for (int e = 0; e < VEC; ++e)
+                        if (VEC * chunk(j) + e < nsrc) flush5(hist[VEC * j + e], s_hist + (VEC * chunk(j) + e) * kBins);
                 visits = 0;
             }
         }
@@ -1104,8 +1165,8 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
 #pragma unroll
     for (int j = 0; j < NCL; ++j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-            if (2 * chunk(j) + e < nsrc) flush5(hist[2 * j + e], s_hist + (2 * chunk(j) + e) * kBins);
+        for (int e = 0; e < VEC; ++e)
+            if (VEC * chunk(j) + e < nsrc) flush5(hist[VEC * j + e], s_hist + (VEC * chunk(j) + e) * kBins);
     __syncthreads();
     if (relax_ctr && tid == 0) atomicAdd(relax_ctr, static_cast<unsigned long long>(nrel * S));
     const int32_t* order = s.order + t0;
@@ -1116,13 +1177,13 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
     }
 }
 
-template <int S, int GL>
+template <int S, int GL, typename T = double>
 __device__ __forceinline__ void sweep_tile_rows_mode(const DevBatch& b, const AttrScratch& s, int64_t g, int32_t tile,
                                                      int32_t P, const Thresholds& th, uint32_t* s_hist,
                                                      int32_t prune_span, unsigned long long* rc) {
-    if (th.mode == 0) sweep_tile_rows<S, GL, 0>(b, s, g, tile, P, th, s_hist, prune_span, rc);
-    else if (th.mode == 2) sweep_tile_rows<S, GL, 2>(b, s, g, tile, P, th, s_hist, 0, rc);
-    else sweep_tile_rows<S, GL, 1>(b, s, g, tile, P, th, s_hist, prune_span, rc);
+    if (th.mode == 0) sweep_tile_rows<S, GL, 0, T>(b, s, g, tile, P, th, s_hist, prune_span, rc);
+    else if (th.mode == 2) sweep_tile_rows<S, GL, 2, T>(b, s, g, tile, P, th, s_hist, 0, rc);
+    else if constexpr (sizeof(T) == 8) sweep_tile_rows<S, GL, 1, T>(b, s, g, tile, P, th, s_hist, prune_span, rc);
 }
 
 __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs_g,
@@ -1132,7 +1193,7 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
                                               int64_t smem_bytes, double* gwin, int64_t gwin_stride,
                                               int32_t prune, unsigned long long* relax_ctr) {
     __shared__ int64_t s_item[2];
-    __shared__ uint32_t s_hist[128 * kBins];
+    __shared__ uint32_t s_hist[kMaxTile * kBins];
     (void)costs_g;
     (void)cost_idx;
     if (total_tiles < 0) total_tiles = s.tile_base[b.G];
@@ -1151,12 +1212,23 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
             Thresholds th;
             if (sweep_mode == SWEEP_SINGLE) th = make_thresholds(SWEEP_SINGLE, unit_time[g]);
             else th = make_thresholds(sweep_mode, 2.0 * gi.median);
-            const int32_t S = s.tile_s[g];
+            const int32_t S = s.tile_s[g] & kTileWidthMask;
+            const bool f32 = s.tile_s[g] & kTileF32;
             double* gw = gwin + blockIdx.x * gwin_stride;
             // prune only when the edge span fits the 64-level history
             const int32_t prune_span = (prune && gi.max_span > 0 && gi.max_span < 64) ? gi.max_span : 0;
-            if (static_cast<int64_t>(P) * S * 8 > smem_bytes) {
+            if (static_cast<int64_t>(P) * S * (f32 ? 4 : 8) > smem_bytes) {
                 sweep_tile_mode<32, false>(b, s, g, tile, gw, P, th, s_hist, prune_span, relax_ctr);
+            } else if (f32) {
+                // FP32-exact windows: the same kernel shapes at twice the width
+                switch (S) {
+                    case 256: sweep_tile_mode<256, true, float>(b, s, g, tile, gw, P, th, s_hist, prune_span, relax_ctr); break;
+                    case 128: sweep_tile_mode<128, true, float>(b, s, g, tile, gw, P, th, s_hist, prune_span, relax_ctr); break;
+                    case 64: sweep_tile_rows_mode<64, 8, float>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+                    case 32: sweep_tile_rows_mode<32, 4, float>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+                    case 16: sweep_tile_rows_mode<16, 1, float>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+                    default: sweep_tile_rows_mode<8, 1, float>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+                }
             } else {
                 switch (S) {
                     // measured on B200 (C2 graphs forced to each width; C5):
@@ -1176,9 +1248,35 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
     }
 }
 
+// FP32-exact windows: the graph's GPU times (types present) as odd integer
+// m * 2^scale; with the common (smallest) scale e, every time is M * 2^e with
+// M <= the returned maximum (0: a time is not such a dyadic number).
+__device__ double f32_mmax_of(const DevCosts& c, uint64_t types) {
+    int e = INT_MAX;
+    for (uint64_t t = types; t; t &= t - 1) {
+        const double v = c.gpu[__ffsll(static_cast<long long>(t)) - 1];
+        if (!(v >= 1e-30 && v <= 1e30)) return 0.0;
+        int x = 0;
+        const double f = frexp(v, &x);
+        const long long m = static_cast<long long>(ldexp(f, 53));
+        e = min(e, x - 53 + (__ffsll(m) - 1));
+    }
+    double mmax = 0.0;
+    for (uint64_t t = types; t; t &= t - 1) {
+        const double v = c.gpu[__ffsll(static_cast<long long>(t)) - 1];
+        mmax = fmax(mmax, ldexp(v, -e));  // exact: v / 2^e is an integer
+    }
+    return mmax;
+}
+
 // Tiles per graph, their prefix and the tile -> graph map (single CTA; G can
-// be large).
-__global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s) {
+// be large).  FP32 windows when they are exact: every
+// distance of a graph with L levels is M * 2^e with M <= L * f32_mmax < 2^24,
+// and the calibration windows W_0 * 2^k are normal floats -- FP32 max/add
+// then reproduce the FP64 values bit for bit (f32_mmax_of).  Never for a
+// caller-given window (its ladder compares in FP64).
+__global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s,
+                            const DevCosts* costs_g, const int32_t* cost_idx, int32_t sweep_mode) {
     __shared__ int32_t warp_tot[32];
     __shared__ int64_t carry;
     if (threadIdx.x == 0) carry = 0;
@@ -1189,15 +1287,28 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
         if (g < b.G) {
             const GraphInfo gi = s.info[g];
             const int32_t P = max(gi.peak_slots, 1);
+            bool f32 = false;
+            if (sweep_mode == SWEEP_ABILITY) {
+                f32 = gi.n_levels < (1 << 24);
+            } else if (sweep_mode == SWEEP_CALIBRATE && costs_g) {
+                const double mmax = f32_mmax_of(costs_g[cost_idx ? cost_idx[g] : 0], gi.gpu_types);
+                const double w0 = 2.0 * gi.median;
+                f32 = mmax > 0.0 && static_cast<double>(gi.n_levels) * mmax < 16777216.0 &&
+                      w0 >= 1e-30 && w0 * 64.0 <= 1e30;
+            }
+            const int64_t eb = f32 ? 4 : 8;
             int32_t S = 8;
             if (force_s) S = force_s;
-            else if (static_cast<int64_t>(P) * 128 * 8 <= smem_bytes) S = 128;
-            else if (static_cast<int64_t>(P) * 64 * 8 <= smem_bytes) S = 64;
-            else if (static_cast<int64_t>(P) * 32 * 8 <= smem_bytes) S = 32;
-            else if (static_cast<int64_t>(P) * 16 * 8 <= smem_bytes) S = 16;
-            else if (static_cast<int64_t>(P) * 8 * 8 <= smem_bytes) S = 8;
-            else S = 32;  // global-memory window
-            s.tile_s[g] = S;
+            else if (f32 && static_cast<int64_t>(P) * 256 * eb <= smem_bytes) S = 256;
+            else if (static_cast<int64_t>(P) * 128 * eb <= smem_bytes) S = 128;
+            else if (static_cast<int64_t>(P) * 64 * eb <= smem_bytes) S = 64;
+            else if (static_cast<int64_t>(P) * 32 * eb <= smem_bytes) S = 32;
+            else if (static_cast<int64_t>(P) * 16 * eb <= smem_bytes) S = 16;
+            else if (static_cast<int64_t>(P) * 8 * eb <= smem_bytes) S = 8;
+            else { S = 32; f32 = false; }  // global-memory window (FP64)
+            if (S == 256 && !f32) S = 128;  // 256 columns only as FP32
+            if (static_cast<int64_t>(P) * S * (f32 ? 4 : 8) > smem_bytes) { S = 32; f32 = false; }  // forced, too wide
+            s.tile_s[g] = S | (f32 ? kTileF32 : 0);
             tiles = (gi.processed + S - 1) / S;
         }
         int32_t tot;
@@ -1211,7 +1322,8 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
         const int lane = threadIdx.x & 31;
         for (int64_t gg = base + (threadIdx.x >> 5); gg < b.G && gg < base + static_cast<int64_t>(blockDim.x); gg += blockDim.x >> 5) {
             const int64_t t_begin = s.tile_base[gg];
-            const int32_t nt = (s.info[gg].processed + s.tile_s[gg] - 1) / s.tile_s[gg];
+            const int32_t sw = s.tile_s[gg] & kTileWidthMask;
+            const int32_t nt = (s.info[gg].processed + sw - 1) / sw;
             for (int32_t t = lane; t < nt; t += 32) s.tile_graph[t_begin + t] = static_cast<int32_t>(gg);
         }
     }

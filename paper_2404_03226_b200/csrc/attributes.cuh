@@ -7,6 +7,10 @@
 
 namespace tbsim_dev {
 
+constexpr int kMaxTile = 256;                 // widest sweep tile (FP32 windows)
+constexpr int32_t kTileWidthMask = 0xffff;    // tile_s: sources per tile ...
+constexpr int32_t kTileF32 = 1 << 16;         // ... | FP32-exact window
+
 enum SweepMode : int32_t {
     SWEEP_CALIBRATE = 0,  // 11-window calibration grid (also final efficiency + ability)
     SWEEP_SINGLE = 1,     // efficiency at a caller-given window (unit_time_ms[g])
@@ -24,6 +28,7 @@ struct GraphInfo {
     int32_t miss_any;    // first task position without any cost, -1 if none
     int32_t order_det;   // level order sorted by position inside each level (large-graph path)
     int32_t pad_;
+    uint64_t gpu_types;  // task types present (with a GPU time): bit t
     double median;       // lower-median GPU time (valid when miss_gpu < 0 and n > 0)
 };
 
@@ -91,7 +96,8 @@ __global__ void k_structure(DevBatch b, const DevCosts* costs, const int32_t* co
                             int32_t want_rank, int32_t want_large);
 __global__ void k_structure_large(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                                   int32_t want_rank, LargeCtl* ctl, int32_t sort_levels);
-__global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s);
+__global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s, const DevCosts* costs,
+                            const int32_t* cost_idx, int32_t sweep_mode);
 __global__ void k_sweep(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                         int32_t sweep_mode,
                         const double* unit_time, int64_t total_tiles, unsigned long long* work_counter,

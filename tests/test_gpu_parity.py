@@ -96,7 +96,7 @@ def test_random_graphs_all_policies_platform_mix(ctx):
             eq(g[k], o[k], f"{pol}/{k}")
 
 
-@pytest.mark.parametrize("tile", [8, 16, 32, 64, 128])
+@pytest.mark.parametrize("tile", [8, 16, 32, 64, 128, 256])
 def test_every_sweep_tile_width_matches_oracle(ctx, tile):
     """Each tile width runs its own kernel shape (one node per warp at 128
     sources, rows of 8 / 4 lanes at 64 / 32, a lane per node at 16 / 8):
@@ -120,6 +120,31 @@ def test_every_sweep_tile_width_matches_oracle(ctx, tile):
             eq(ga[k], oa[k], f"S={tile} {k}")
         eq(g3["efficiency"], o3["efficiency"], f"S={tile} efficiency@3")
         eq(gb["ability"], oa["ability"], f"S={tile} ability only")
+
+
+@pytest.mark.parametrize("gpu_ms", [(0.5, 1.0, 2.0, 4.0), (1.0 + 2.0 ** -23, 0.5, 2.0, 3.0),
+                                    (0.1, 0.5, 2.0, 4.0), (3.0 * 2.0 ** -40, 2.0 ** -41, 2.0 ** -38, 1.0)])
+def test_fp32_windows_only_when_exact(ctx, gpu_ms):
+    """The sweep keeps distances in FP32 only when every path sum is exact
+    there (dyadic GPU times, levels x largest mantissa < 2^24); otherwise FP64.
+    Either way the attributes equal the oracle's: (1) exact -> FP32; (2)
+    dyadic but 2^23+1 mantissa over 12 levels -> FP64; (3) 0.1 is not dyadic
+    -> FP64; (4) tiny dyadic times with a 2^41 spread -> FP64."""
+    costs = P.CostTable()
+    for name, g in zip(("LAYERK0", "LAYERK1", "LAYERK2", "LAYERK3"), gpu_ms):
+        costs.set(name, P.GPU, g)
+        costs.set(name, P.CPU, 3.0 * g)
+    b = api.HostBatch().add_layered(400, 12, 0.06, [7, 8, 9]).view()
+    db = ctx.upload(b)
+    for tile in (0, 256, 64):
+        ctx.set_sweep_tile(tile)
+        try:
+            ga = ctx.attributes(db, costs, abi.ATTR_ALL)
+        finally:
+            ctx.set_sweep_tile(0)
+        oa = po.attributes(b, costs, abi.ATTR_ALL)
+        for k in ("ability", "efficiency", "unit_time_ms"):
+            eq(ga[k], oa[k], f"tile {tile} {k}")
 
 
 def test_sweep_tile_rejects_other_widths(ctx):
