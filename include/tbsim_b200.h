@@ -150,12 +150,14 @@ tbsim_status tbsim_ctx_last_kernel_ms(const tbsim_ctx* ctx, const char* kernel,
                                       double* ms);
 /* The efficiency sweep's inner-loop peak on this GPU: relaxations per
  * second of k_probe_relax (shared-memory rows + FP64 compare-select, no
- * graph), best of `repeats` launches on the context's stream.  The sweep's
- * roofline denominator (it is not HBM-bound). */
-tbsim_status tbsim_probe_sweep_peak(tbsim_ctx* ctx, int32_t repeats, double* relaxations_per_s);
+ * graph) and of its FP32 twin (FMNMX), best of `repeats` launches on the
+ * context's stream.  The sweep's roofline denominators (it is not
+ * HBM-bound). */
+tbsim_status tbsim_probe_sweep_peak(tbsim_ctx* ctx, int32_t repeats, double* fp64_per_s, double* fp32_per_s);
 /* Relaxations (predecessor row x tile column) the last timed efficiency
- * sweep executed -- the numerator of its achieved rate. */
-tbsim_status tbsim_ctx_last_sweep_relaxations(const tbsim_ctx* ctx, int64_t* relaxations);
+ * sweep executed in FP64 and in FP32-exact windows -- the numerator of its
+ * achieved rate. */
+tbsim_status tbsim_ctx_last_sweep_relaxations(const tbsim_ctx* ctx, int64_t* fp64, int64_t* fp32);
 
 /* ------------------------------------------------------------------------
  * Device-resident batch: CSR ingestion into HBM (one packed H2D copy, the

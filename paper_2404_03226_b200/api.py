@@ -190,17 +190,19 @@ class Context:
     def set_large_graph_threshold(self, n_tasks: int):
         _check(load().tbsim_ctx_set_large_graph_threshold(self.h, n_tasks))
 
-    def last_sweep_relaxations(self) -> int:
-        """Relaxations executed by the last timed efficiency sweep."""
-        v = C.c_int64(0)
-        _check(load().tbsim_ctx_last_sweep_relaxations(self.h, C.byref(v)))
-        return v.value
+    def last_sweep_relaxations(self) -> tuple[int, int]:
+        """Relaxations executed by the last timed efficiency sweep:
+        (in FP64 windows, in FP32-exact windows)."""
+        a, b = C.c_int64(0), C.c_int64(0)
+        _check(load().tbsim_ctx_last_sweep_relaxations(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
-    def probe_sweep_peak(self, repeats: int = 3) -> float:
-        """Relaxations/s of the sweep's inner loop alone (its roofline)."""
-        v = C.c_double(0.0)
-        _check(load().tbsim_probe_sweep_peak(self.h, repeats, C.byref(v)))
-        return v.value
+    def probe_sweep_peak(self, repeats: int = 3) -> tuple[float, float]:
+        """Relaxations/s of the sweep's inner loop alone (its roofline):
+        (FP64 windows, FP32-exact windows)."""
+        a, b = C.c_double(0.0), C.c_double(0.0)
+        _check(load().tbsim_probe_sweep_peak(self.h, repeats, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def set_async_results(self, on: bool):
         """schedule() with host outputs returns once their D2H copies are

@@ -134,7 +134,7 @@ struct tbsim_ctx {
         AttrScratch s{};
     } shard;
     unsigned long long* relax_ctr = nullptr;  // device counter of the last timed sweep
-    int64_t last_relax = 0;
+    int64_t last_relax[2] = {0, 0};  // FP64-window, FP32-window relaxations
 
     DevBuf& buf(const std::string& name) { return bufs[name]; }
     void* batch_alloc(size_t bytes, size_t* got) {
@@ -190,8 +190,11 @@ struct tbsim_ctx {
             if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) last_ms[k] = ms;
         }
         if (relax_ctr) {
-            unsigned long long r = 0;
-            if (cudaMemcpy(&r, relax_ctr, 8, cudaMemcpyDeviceToHost) == cudaSuccess) last_relax = static_cast<int64_t>(r);
+            unsigned long long r[2] = {0, 0};
+            if (cudaMemcpy(r, relax_ctr, 16, cudaMemcpyDeviceToHost) == cudaSuccess) {
+                last_relax[0] = static_cast<int64_t>(r[0]);
+                last_relax[1] = static_cast<int64_t>(r[1]);
+            }
             relax_ctr = nullptr;
         }
     }
@@ -401,38 +404,44 @@ tbsim_status tbsim_ctx_set_timing(tbsim_ctx* ctx, int enable) {
     return guarded([&] { ctx->timing = enable != 0; });
 }
 
-tbsim_status tbsim_probe_sweep_peak(tbsim_ctx* ctx, int32_t repeats, double* relaxations_per_s) {
+tbsim_status tbsim_probe_sweep_peak(tbsim_ctx* ctx, int32_t repeats, double* fp64_per_s, double* fp32_per_s) {
     return guarded([&] {
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
         constexpr int32_t kRows = 128, kIters = 20000, kThreads = 512;
-        const size_t smem = static_cast<size_t>(kRows) * 64 * 16;  // 128 KB window
-        cuda_check(cudaFuncSetAttribute(tbsim_dev::k_probe_relax, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)), "cudaFuncSetAttribute(k_probe_relax)");
         double* out = ctx->buf("p_out").as<double>(ctx->n_sms);
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
-        double best = 0.0;
-        for (int32_t r = 0; r < std::max(repeats, 1) + 1; ++r) {  // first launch warms up
-            cudaEventRecord(e0, ctx->stream);
-            ctx->begin("k_probe_relax");
-            tbsim_dev::k_probe_relax<<<ctx->n_sms, kThreads, smem, ctx->stream>>>(kRows - 1, kIters, out);
-            ctx->end("k_probe_relax");
-            cudaEventRecord(e1, ctx->stream);
-            cuda_check(cudaEventSynchronize(e1), "probe");
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, e0, e1);
-            const double relax = static_cast<double>(ctx->n_sms) * kThreads * kIters * 4.0 * 4.0;
-            if (r > 0 && ms > 0.f) best = std::max(best, relax / (ms * 1e-3));
+        for (int f32 = 0; f32 < 2; ++f32) {
+            const size_t smem = static_cast<size_t>(kRows) * 128 * (f32 ? 4 : 8);
+            auto kern = f32 ? tbsim_dev::k_probe_relax_f32 : tbsim_dev::k_probe_relax;
+            cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+                       "cudaFuncSetAttribute(k_probe_relax)");
+            double best = 0.0;
+            for (int32_t r = 0; r < std::max(repeats, 1) + 1; ++r) {  // first launch warms up
+                cudaEventRecord(e0, ctx->stream);
+                ctx->begin("k_probe_relax");
+                kern<<<ctx->n_sms, kThreads, smem, ctx->stream>>>(kRows - 1, kIters, out);
+                ctx->end("k_probe_relax");
+                cudaEventRecord(e1, ctx->stream);
+                cuda_check(cudaEventSynchronize(e1), "probe");
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, e0, e1);
+                const double relax = static_cast<double>(ctx->n_sms) * kThreads * kIters * 4.0 * 4.0;
+                if (r > 0 && ms > 0.f) best = std::max(best, relax / (ms * 1e-3));
+            }
+            *(f32 ? fp32_per_s : fp64_per_s) = best;
         }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        *relaxations_per_s = best;
     });
 }
 
-tbsim_status tbsim_ctx_last_sweep_relaxations(const tbsim_ctx* ctx, int64_t* relaxations) {
-    return guarded([&] { *relaxations = ctx->last_relax; });
+tbsim_status tbsim_ctx_last_sweep_relaxations(const tbsim_ctx* ctx, int64_t* fp64, int64_t* fp32) {
+    return guarded([&] {
+        *fp64 = ctx->last_relax[0];
+        *fp32 = ctx->last_relax[1];
+    });
 }
 
 tbsim_status tbsim_ctx_last_kernel_ms(const tbsim_ctx* ctx, const char* kernel, double* ms) {
@@ -836,8 +845,8 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         // achieved rate for bench.py's roofline
         unsigned long long* relax_ctr = nullptr;
         if (ctx->timing) {
-            relax_ctr = ctx->buf("a_relax").as<unsigned long long>(1);
-            cuda_check(cudaMemsetAsync(relax_ctr, 0, 8, ctx->stream), "memset");
+            relax_ctr = ctx->buf("a_relax").as<unsigned long long>(2);
+            cuda_check(cudaMemsetAsync(relax_ctr, 0, 16, ctx->stream), "memset");
             ctx->relax_ctr = relax_ctr;
         }
         ctx->begin("k_sweep");

@@ -994,7 +994,8 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     for (int q = 0; q < SPL; ++q)
         if (src(q) < nsrc) flush5(hist[q], s_hist + src(q) * kBins);
     __syncthreads();
-    if (relax_ctr && threadIdx.x == 0) atomicAdd(relax_ctr, static_cast<unsigned long long>(nrel * S));
+    if (relax_ctr && threadIdx.x == 0)  // [0]: FP64 windows, [1]: FP32
+        atomicAdd(relax_ctr + (sizeof(T) == 4 ? 1 : 0), static_cast<unsigned long long>(nrel * S));
     // per source: 12 bins as 21-bit fields in four words (k_finalize)
     const int32_t* order = s.order + t0;
     for (int i = threadIdx.x; i < nsrc * 4; i += blockDim.x) {
@@ -1168,7 +1169,8 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
         for (int e = 0; e < VEC; ++e)
             if (VEC * chunk(j) + e < nsrc) flush5(hist[VEC * j + e], s_hist + (VEC * chunk(j) + e) * kBins);
     __syncthreads();
-    if (relax_ctr && tid == 0) atomicAdd(relax_ctr, static_cast<unsigned long long>(nrel * S));
+    if (relax_ctr && tid == 0)  // [0]: FP64 windows, [1]: FP32
+        atomicAdd(relax_ctr + (sizeof(T) == 4 ? 1 : 0), static_cast<unsigned long long>(nrel * S));
     const int32_t* order = s.order + t0;
     for (int i = tid; i < nsrc * 4; i += nthr) {
         const uint32_t* c = s_hist + (i >> 2) * kBins + 3 * (i & 3);

@@ -116,5 +116,6 @@ __global__ void k_structure_out(DevBatch b, AttrScratch s, AttrOutDev o, int32_t
                                 int32_t want_prio);
 // probe.cu: the sweep's inner loop alone (its roofline denominator)
 __global__ void k_probe_relax(int32_t rows_mask, int32_t iters, double* out);
+__global__ void k_probe_relax_f32(int32_t rows_mask, int32_t iters, double* out);
 
 }  // namespace tbsim_dev

@@ -67,8 +67,8 @@ def load():
     L.tbsim_ctx_set_async_results.argtypes = [vp, C.c_int]
     L.tbsim_attributes_shard_partial.argtypes = [vp, vp, P(abi.Costs), i32, i32, P(i64), P(i64), i64, P(i64)]
     L.tbsim_attributes_shard_finish.argtypes = [vp, vp, P(i64), i64, i32, P(abi.AttrOut)]
-    L.tbsim_ctx_last_sweep_relaxations.argtypes = [vp, P(i64)]
-    L.tbsim_probe_sweep_peak.argtypes = [vp, i32, P(dbl)]
+    L.tbsim_ctx_last_sweep_relaxations.argtypes = [vp, P(i64), P(i64)]
+    L.tbsim_probe_sweep_peak.argtypes = [vp, i32, P(dbl), P(dbl)]
     L.tbsim_ctx_last_kernel_ms.argtypes = [vp, C.c_char_p, P(dbl)]
     L.tbsim_batch_upload.argtypes = [vp, P(abi.BatchDesc), P(vp)]
     L.tbsim_batch_free.argtypes = [vp, vp]
