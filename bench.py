@@ -322,7 +322,7 @@ def run_c5(args):
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
-    kms = {k: ctx.last_kernel_ms(k) for k in ("k_structure", "k_sweep", "k_finalize", "k_sim_pack", "k_sim_keys", "k_simulate", "k_sim_scatter")}
+    kms = {k: ctx.last_kernel_ms(k) for k in ("k_structure", "k_sweep", "k_finalize", "k_sim_pack", "k_sim_keys", "k_simulate", "k_simulate_rerun", "k_sim_scatter")}
     c5_relax = ctx.last_sweep_relaxations()
     for _ in range(args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -619,7 +619,7 @@ def main():
     value_step()
     torch.cuda.synchronize()
     kms = {k: ctx.last_kernel_ms(k) for k in ("k_structure", "k_tile_plan", "k_sweep", "k_finalize",
-                                             "k_structure_out", "k_sim_keys", "k_simulate", "k_sim_scatter")}
+                                             "k_structure_out", "k_sim_keys", "k_simulate", "k_simulate_rerun", "k_sim_scatter")}
     sweep_relax = ctx.last_sweep_relaxations()
     ctx.set_timing(False)
     sweep_roof = sweep_roofline(ctx, sweep_relax, kms["k_sweep"])

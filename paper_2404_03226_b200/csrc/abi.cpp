@@ -1242,7 +1242,8 @@ int32_t pow2_at_least(int32_t x) {
 // state goes to shared memory when a queue capacity of >= 32 entries fits,
 // else to HBM.  Wider platforms (k_simulate_w2*) and wide state run 8-warp
 // CTAs, two per SM.
-void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_items) {
+void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_items,
+                const char* name = "k_simulate") {
     const DevBatch& d = p.b;
     const bool compact = !p.force_wide && d.max_n < 32768 && p.max_nodes <= 8;
     const bool w2 = max_workers > 32;
@@ -1269,8 +1270,15 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
     int ctas_per_sm = max_ctas;
     p.use_smem = 0;
     if (!forced) {
-        const int64_t per_sm = static_cast<int64_t>(ctx->smem_optin) + 1024;  // 228 KB per SM
-        for (int c = max_ctas; c >= 1; --c) {
+        // Shared-memory budgets per SM, tried in order for each CTA count:
+        // 196 KB first -- the 196 KB carveout leaves 60 KB of L1 for the
+        // simulator's register spills and task records (C2: 8.6 -> 8.4 ms)
+        // -- then all of it (228 KB).
+        const int64_t full_sm = static_cast<int64_t>(ctx->smem_optin) + 1024;
+        int c = max_ctas, bi = 0;
+        const int64_t budgets[2] = {tight ? std::min<int64_t>(196 * 1024, full_sm) : full_sm, full_sm};
+        for (int step = 0; step < 2 * max_ctas; ++step, bi ^= 1, c -= bi == 0 ? 1 : 0) {
+            const int64_t per_sm = budgets[bi];
             const int64_t per_warp = (per_sm / c - 1024) / kWarps;
             if (layout(qcap_full).total <= per_warp) {
                 qcap = qcap_full;
@@ -1306,9 +1314,9 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
     auto kern = compact ? (w2 ? k_simulate_w2c : k_simulate_w1c) : (w2 ? k_simulate_w2 : k_simulate_w1);
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "cudaFuncSetAttribute(k_simulate)");
-    ctx->begin("k_simulate");
+    ctx->begin(name);
     kern<<<grid, kThreads, smem, ctx->stream>>>(p);
-    ctx->end("k_simulate");
+    ctx->end(name);
 }
 
 // Runs the simulator over every graph, reruns queue overflows with full
@@ -1319,7 +1327,12 @@ struct SimKeys {
     const int64_t* prio = nullptr;
 };
 
-void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t max_workers, const SimKeys& keys) {
+// pof_host / hp: the graphs' platforms on the host (null: all platform 0).
+// A batch mixing worker counts is dispatched longest-first: graphs on the
+// fewest workers (longest queues, slowest simulations) start first, so they
+// do not pile up at the tail of the atomic DAG queue.
+void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t max_workers, const SimKeys& keys,
+                    const int32_t* pof_host = nullptr, const std::vector<DevPlatform>* hp = nullptr) {
     const DevBatch& d = b->d;
     const int64_t G = d.G;
     if (G == 0) return;
@@ -1337,7 +1350,22 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
     }
     p.graph_list = nullptr;
     p.qcap = 0;
+    if (pof_host && hp && hp->size() > 1 && G >= 2 * ctx->n_sms) {
+        bool mixed = false;
+        for (const auto& pl : *hp) mixed = mixed || pl.n_workers != (*hp)[0].n_workers;
+        if (mixed) {
+            std::vector<int32_t> order(G);
+            for (int64_t g = 0; g < G; ++g) order[g] = static_cast<int32_t>(g);
+            std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+                return (*hp)[pof_host[x]].n_workers < (*hp)[pof_host[y]].n_workers;
+            });
+            int32_t* d_list = ctx->buf("s_order").as<int32_t>(G);
+            cuda_check(cudaMemcpyAsync(d_list, order.data(), G * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D order");
+            p.graph_list = d_list;
+        }
+    }
     launch_sim(ctx, p, max_workers, G);
+    p.graph_list = nullptr;
     std::vector<int32_t> status(G), aux(G);
     cuda_check(cudaMemcpyAsync(status.data(), p.status, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
     cuda_check(cudaMemcpyAsync(aux.data(), p.status_aux, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H aux");
@@ -1354,7 +1382,7 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
         q.graph_list = d_list;
         q.qcap = std::max<int32_t>(b->d.max_n, 1);
         q.force_wide = 1;  // also covers priorities beyond the compact int32 keys
-        launch_sim(ctx, q, max_workers, static_cast<int64_t>(rerun.size()));
+        launch_sim(ctx, q, max_workers, static_cast<int64_t>(rerun.size()), "k_simulate_rerun");
         cuda_check(cudaMemcpyAsync(status.data(), p.status, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
         cuda_check(cudaMemcpyAsync(aux.data(), p.status_aux, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H aux");
         ctx->sync();
@@ -1520,7 +1548,7 @@ extern "C" tbsim_status tbsim_simulate(tbsim_ctx* ctx, const tbsim_batch* b, con
         }
         p.status = ctx->buf("s_status").as<int32_t>(G);
         p.status_aux = ctx->buf("s_aux").as<int32_t>(G);
-        run_simulation(ctx, b, p, maxw, keys);
+        run_simulation(ctx, b, p, maxw, keys, platform_of, &hp);
         for (const auto& c : st.copies)
             cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
         ctx->sync();
@@ -1615,7 +1643,7 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         p.reg_state = sim_out_ptr(ctx, st, nm("s_rstate").c_str(), out->reg_state, G, dev, true);
         p.status = ctx->buf("s_status").as<int32_t>(G);
         p.status_aux = ctx->buf("s_aux").as<int32_t>(G);
-        run_simulation(ctx, b, p, maxw, keys);
+        run_simulation(ctx, b, p, maxw, keys, platform_of, &hp);
         cudaStream_t dl = ctx->stream;
         if (async) {  // the copies wait for this call's kernels, not the next call's
             cudaEvent_t done = ctx->set_free[set];

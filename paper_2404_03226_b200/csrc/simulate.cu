@@ -116,6 +116,13 @@ struct Sim {
         if (lane == 0) cold().aux = task;
     }
 
+    // static priority from the record's second half (compact queues)
+    __device__ __forceinline__ int64_t prio_of(int32_t task) const {
+        const int2 p = __ldg(reinterpret_cast<const int2*>(hdr + task) + 3);
+        return static_cast<int64_t>((static_cast<uint64_t>(static_cast<uint32_t>(p.y)) << 32) |
+                                    static_cast<uint32_t>(p.x));
+    }
+
     // first half of a packed record: (adj8, nin, nout, nsucc | type << 24)
     __device__ __forceinline__ int4 head(int32_t task) const {
         return __ldg(reinterpret_cast<const int4*>(hdr + task));
@@ -399,7 +406,7 @@ struct Sim {
                 k0 = ord_f64(resident_fraction(q[i] & 0xffffff, nd));
                 k1 = ord_f64(static_cast<double>(ke[i]));
             }
-            const uint64_t k2 = ord_i64(static_cast<int64_t>(kp[i]));
+            const uint64_t k2 = ord_i64(COMPACT ? prio_of(q[i] & 0xffffff) : static_cast<int64_t>(kp[i]));
             const bool better = bpos == INT_MAX || k0 > b0 ||
                                 (k0 == b0 && (k1 > b1 || (k1 == b1 && k2 > b2)));
             if (better) { b0 = k0; b1 = k1; b2 = k2; bpos = i; }
@@ -443,7 +450,7 @@ struct Sim {
                 PrioT* kp = qprio(w);
                 e = static_cast<uint32_t>(q[pick]);
                 __syncwarp();
-                const bool ins = pol() == TBSIM_POLICY_INSPIRIT, pri = pol() >= TBSIM_POLICY_DMDAP;
+                const bool ins = pol() == TBSIM_POLICY_INSPIRIT, pri = !COMPACT && pol() >= TBSIM_POLICY_DMDAP;
                 for (int32_t b0 = pick; b0 < ql - 1; b0 += 32) {
                     const int32_t i = b0 + lane;
                     const bool mv = i < ql - 1;
@@ -527,12 +534,8 @@ struct Sim {
         const int32_t w = select_worker(inb, reinterpret_cast<const int32_t*>(inb + hd.y), hd.y, ty);
         if (w < 0) { fail(GS_NO_WORKER, task); return -1; }
         if (too_large) { fail(GS_TOO_LARGE, task); return -1; }
-        // compact keys: ability/efficiency < n < 2^15 always fit; a priority
-        // beyond int32 sends the graph to the wide rerun
-        if (COMPACT && pol() >= TBSIM_POLICY_DMDAP && kp != static_cast<int64_t>(static_cast<PrioT>(kp))) {
-            fail(GS_QUEUE_OVERFLOW, task);
-            return -1;
-        }
+        // compact keys: ability/efficiency < n < 2^15 always fit; the
+        // static priority stays in the task record
         const int j = w >> 5, owner = w & 31;
         int32_t ovf = 0;
 #pragma unroll
@@ -547,7 +550,7 @@ struct Sim {
                         qab(w)[at] = static_cast<KeyT>(ka);
                         qef(w)[at] = static_cast<KeyT>(ke);
                     }
-                    if (pol() >= TBSIM_POLICY_DMDAP) qprio(w)[at] = static_cast<PrioT>(kp);
+                    if (!COMPACT && pol() >= TBSIM_POLICY_DMDAP) qprio(w)[at] = static_cast<PrioT>(kp);
                     qlen[jj] += 1;
                     if ((wk[jj] & 12u) == 4u) fsum[jj] += cost(ty, kind_of(jj));  // busy, not dirty
                 }

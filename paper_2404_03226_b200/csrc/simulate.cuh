@@ -35,8 +35,10 @@ struct SimLayout {
 
 // Pop keys cached per queue entry: inspirit (policy 4) ability + efficiency
 // + static priority; dmdap (3) the priority only.
+// Compact state reads the static priority from the task record instead
+// (smaller queues leave L1 room for the simulator's spills).
 __host__ __device__ inline int key_bytes(int32_t policy, bool compact) {
-    return policy == 4 ? (compact ? 8 : 16) : policy == 3 ? (compact ? 4 : 8) : 0;
+    return policy == 4 ? (compact ? 4 : 16) : policy == 3 ? (compact ? 0 : 8) : 0;
 }
 
 __host__ __device__ inline SimLayout sim_layout(int64_t max_n, int64_t max_h, int64_t max_workers, int64_t qcap,
@@ -53,7 +55,7 @@ __host__ __device__ inline SimLayout sim_layout(int64_t max_n, int64_t max_h, in
     const int kb = compact ? 2 : 4;
     L.qab = off; off += ins ? al(kb * max_workers * qcap) : 0;
     L.qef = off; off += ins ? al(kb * max_workers * qcap) : 0;
-    L.qprio = off; off += pri ? al(2 * kb * max_workers * qcap) : 0;
+    L.qprio = off; off += pri && !compact ? al(2 * kb * max_workers * qcap) : 0;
     L.ring = off; off += al(16 * ring);
     L.costs = off; off += al(16 * n_types);
     L.bw = off; off += al(8 * max_nodes * max_nodes);
