@@ -1245,7 +1245,7 @@ int32_t pow2_at_least(int32_t x) {
 void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_items,
                 const char* name = "k_simulate") {
     const DevBatch& d = p.b;
-    const bool compact = !p.force_wide && d.max_n < 32768 && p.max_nodes <= 8;
+    const bool compact = d.max_n < 32768 && p.max_nodes <= 8;
     const bool w2 = max_workers > 32;
     const bool tight = compact && !w2;
     const int max_warps = tight ? 4 : 8;
@@ -1381,7 +1381,6 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
         SimParams q = p;
         q.graph_list = d_list;
         q.qcap = std::max<int32_t>(b->d.max_n, 1);
-        q.force_wide = 1;  // also covers priorities beyond the compact int32 keys
         launch_sim(ctx, q, max_workers, static_cast<int64_t>(rerun.size()), "k_simulate_rerun");
         cuda_check(cudaMemcpyAsync(status.data(), p.status, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
         cuda_check(cudaMemcpyAsync(aux.data(), p.status_aux, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H aux");

@@ -26,7 +26,7 @@ struct SimCold {
 // Per-warp state layout (bytes, 16-aligned sections).  Compact state
 // (n < 32768, <= 8 memory nodes) stores unmet counts as int16, residency
 // masks as uint8, and queue keys narrowed: ability/efficiency int16, static
-// priority int32 (a priority beyond int32 sends the graph to a wide rerun).
+// priority read from the task record.
 // The ready list has no section: it is a linked list threaded through the
 // unmet counters of ready tasks (a ready task's counter is never read again).
 struct SimLayout {
@@ -123,7 +123,6 @@ struct SimParams {
     int64_t state_bytes;              // bytes per warp state
     int32_t qcap;                     // queue capacity per worker
     int32_t use_smem;
-    int32_t force_wide;               // rerun: wide (non-compact) state and keys
     int32_t max_workers;
     int32_t max_nodes;                // platform copy: nodes x nodes bandwidth
     int32_t n_types;                  // platform copy: cost rows

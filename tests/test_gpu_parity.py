@@ -478,3 +478,28 @@ def test_mixed_width_batch_more_graphs_than_warps(ctx):
     s = ctx.schedule(db, pls, "inspirit", platform_of=pof, want_attrs=False)
     o = po.simulate(b, pls, "inspirit", platform_of=pof, reg=reg, attrs=oa, record=False)
     eq(s["makespan_ms"], o["makespan_ms"], "schedule makespans")
+
+
+def test_queue_overflow_rerun_matches_oracle(ctx):
+    """Many graphs (shared-memory state with short queues) plus two whose
+    first level puts hundreds of tasks on 10 workers at once: those overflow
+    their shared-memory queues and are re-run with HBM state -- every
+    schedule still equals the oracle's."""
+    G = 2 * 148 * 4
+    hb = api.HostBatch().add_layered(120, 6, 0.1, np.arange(G)).add_layered(1500, 2, 0.01, [5, 6])
+    b = hb.view()
+    pl = [P.assemble("8c2g", 8, 2)]
+    costs = P.default_cost_table()
+    db = ctx.upload(b)
+    oa = po.attributes(b, costs, abi.ATTR_ALL)
+    reg = [po.default_regulator_config(b, g, pl[0]) for g in range(b.n_graphs)]
+    ctx.set_timing(True)
+    try:
+        g_ = ctx.simulate(db, pl, "inspirit", reg, attrs=oa, record=True)
+        rerun_ms = ctx.last_kernel_ms("k_simulate_rerun")
+    finally:
+        ctx.set_timing(False)
+    o = po.simulate(b, pl, "inspirit", reg=reg, attrs=oa, record=True)
+    for k in SIM_KEYS:
+        eq(g_[k], o[k], k)
+    assert rerun_ms > 0.0, "the wide graphs were expected to overflow into the HBM rerun"
