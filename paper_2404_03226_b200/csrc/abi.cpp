@@ -731,6 +731,7 @@ AttrScratch alloc_attr_scratch(tbsim_ctx* ctx, const DevBatch& d) {
     s.tile_base = ctx->buf("a_tilebase").as<int64_t>(G + 1);
     s.tile_s = ctx->buf("a_tiles").as<int32_t>(G);
     s.tile_graph = ctx->buf("a_tilegraph").as<int32_t>(T / 8 + G + 1);
+    s.plan_fp32 = ctx->buf("a_planfp32").as<int32_t>(1);
     s.opos = ctx->buf("a_opos").as<int32_t>(T);
     s.firstuse = ctx->buf("a_firstuse").as<int32_t>(T);
     s.rslot = ctx->buf("a_rslot").as<int32_t>(T);
@@ -849,10 +850,19 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
             cuda_check(cudaMemsetAsync(relax_ctr, 0, 16, ctx->stream), "memset");
             ctx->relax_ctr = relax_ctr;
         }
+        static bool attr_set32 = false;
+        if (!attr_set32) {
+            cuda_check(cudaFuncSetAttribute(k_sweep_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+                       "cudaFuncSetAttribute(k_sweep_fp32)");
+            attr_set32 = true;
+        }
+        // both launched: the plan (device) selects one, the other returns
         ctx->begin("k_sweep");
         k_sweep<<<sweep_grid, kSweepThreads, smem, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, sweep_mode, d_unit_time,
                                                                   total_tiles, counter, smem, gwin, gwin_stride,
                                                                   large ? 1 : 0, relax_ctr);
+        k_sweep_fp32<<<sweep_grid, 1024, smem, ctx->stream>>>(d, run.s, sweep_mode, d_unit_time, counter, large ? 1 : 0,
+                                                               relax_ctr);
         ctx->end("k_sweep");
         const int64_t cls_stride = static_cast<int64_t>(d.max_n) * (3 * kWindows + 1) + 16;
         int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride * grid_g);

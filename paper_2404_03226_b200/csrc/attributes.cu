@@ -1188,6 +1188,43 @@ __device__ __forceinline__ void sweep_tile_rows_mode(const DevBatch& b, const At
     else if constexpr (sizeof(T) == 8) sweep_tile_rows<S, GL, 1, T>(b, s, g, tile, P, th, s_hist, prune_span, rc);
 }
 
+// Batches whose every tile is an FP32-exact shape of >= 32 sources (C2, C5)
+// run here instead: the same tile code at 1024 threads per CTA (64 registers)
+// -- twice the warps per SM to hide the record loads and level barriers.
+// k_sweep and k_sweep_fp32 are both launched; the one the plan does not
+// select returns at once (no host round trip between plan and sweep).
+__global__ void __launch_bounds__(1024, 1) k_sweep_fp32(DevBatch b, AttrScratch s, int32_t sweep_mode,
+                                                       const double* unit_time, unsigned long long* work_counter,
+                                                       int32_t prune, unsigned long long* relax_ctr) {
+    __shared__ int64_t s_item[2];
+    __shared__ uint32_t s_hist[kMaxTile * kBins];
+    if (!*s.plan_fp32) return;
+    const int64_t total_tiles = s.tile_base[b.G];
+    if (threadIdx.x == 0) s_item[0] = atomicAdd(work_counter, 1ull);
+    __syncthreads();
+    for (int k = 0;; k ^= 1) {
+        const int64_t item = s_item[k];
+        if (item >= total_tiles) break;
+        if (threadIdx.x == 0) s_item[k ^ 1] = atomicAdd(work_counter, 1ull);
+        const int64_t g = s.tile_graph[item];
+        const int32_t tile = static_cast<int32_t>(item - s.tile_base[g]);
+        const GraphInfo gi = s.info[g];
+        if (gi.processed == static_cast<int32_t>(b.task_base[g + 1] - b.task_base[g])) {  // else cyclic
+            const int32_t P = max(gi.peak_slots, 1);
+            const Thresholds th = make_thresholds(sweep_mode, 2.0 * gi.median);
+            const int32_t prune_span = (prune && gi.max_span > 0 && gi.max_span < 64) ? gi.max_span : 0;
+            switch (s.tile_s[g] & kTileWidthMask) {
+                case 256: sweep_tile_mode<256, true, float>(b, s, g, tile, nullptr, P, th, s_hist, prune_span, relax_ctr); break;
+                case 128: sweep_tile_mode<128, true, float>(b, s, g, tile, nullptr, P, th, s_hist, prune_span, relax_ctr); break;
+                case 64: sweep_tile_rows_mode<64, 8, float>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+                default: sweep_tile_rows_mode<32, 4, float>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+            }
+        }
+        __syncthreads();
+    }
+    (void)unit_time;
+}
+
 __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs_g,
                                               const int32_t* cost_idx, AttrScratch s,
                                               int32_t sweep_mode, const double* unit_time,
@@ -1198,7 +1235,10 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
     __shared__ uint32_t s_hist[kMaxTile * kBins];
     (void)costs_g;
     (void)cost_idx;
-    if (total_tiles < 0) total_tiles = s.tile_base[b.G];
+    if (total_tiles < 0) {  // whole-batch launch: k_sweep_fp32 takes all-FP32 plans
+        if (*s.plan_fp32) return;
+        total_tiles = s.tile_base[b.G];
+    }
     if (threadIdx.x == 0) s_item[0] = atomicAdd(work_counter, 1ull);
     __syncthreads();
     for (int k = 0;; k ^= 1) {
@@ -1281,7 +1321,11 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
                             const DevCosts* costs_g, const int32_t* cost_idx, int32_t sweep_mode) {
     __shared__ int32_t warp_tot[32];
     __shared__ int64_t carry;
-    if (threadIdx.x == 0) carry = 0;
+    __shared__ int32_t all_fp32;
+    if (threadIdx.x == 0) {
+        carry = 0;
+        all_fp32 = 1;
+    }
     __syncthreads();
     for (int64_t base = 0; base < b.G; base += blockDim.x) {
         const int64_t g = base + threadIdx.x;
@@ -1311,6 +1355,7 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
             if (S == 256 && !f32) S = 128;  // 256 columns only as FP32
             if (static_cast<int64_t>(P) * S * (f32 ? 4 : 8) > smem_bytes) { S = 32; f32 = false; }  // forced, too wide
             s.tile_s[g] = S | (f32 ? kTileF32 : 0);
+            if (!f32 || S < 32) atomicAnd(&all_fp32, 0);
             tiles = (gi.processed + S - 1) / S;
         }
         int32_t tot;
@@ -1329,7 +1374,10 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
             for (int32_t t = lane; t < nt; t += 32) s.tile_graph[t_begin + t] = static_cast<int32_t>(gg);
         }
     }
-    if (threadIdx.x == 0) s.tile_base[b.G] = carry;
+    if (threadIdx.x == 0) {
+        s.tile_base[b.G] = carry;
+        *s.plan_fp32 = b.G > 0 ? all_fp32 : 0;
+    }
 }
 
 // ---------------------------------------------------------------- finalize

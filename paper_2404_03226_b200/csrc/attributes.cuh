@@ -61,6 +61,7 @@ struct AttrScratch {
     int64_t* tile_base;  // [G+1]
     int32_t* tile_s;     // [G]
     int32_t* tile_graph; // [tiles] graph of each sweep tile (<= T/8 + G)
+    int32_t* plan_fp32;  // [1] every tile is an FP32-exact shape k_sweep_fp32 runs
 };
 
 // Grid-wide counters of k_structure_large (zeroed before the launch),
@@ -103,6 +104,8 @@ __global__ void k_sweep(DevBatch b, const DevCosts* costs, const int32_t* cost_i
                         const double* unit_time, int64_t total_tiles, unsigned long long* work_counter,
                         int64_t smem_bytes, double* gwin, int64_t gwin_stride, int32_t prune,
                         unsigned long long* relax_ctr);
+__global__ void k_sweep_fp32(DevBatch b, AttrScratch s, int32_t sweep_mode, const double* unit_time,
+                             unsigned long long* work_counter, int32_t prune, unsigned long long* relax_ctr);
 __global__ void k_finalize(DevBatch b, AttrScratch s, int32_t sweep_mode, const double* unit_time_in,
                            AttrOutDev o, int64_t* cls_scratch, int64_t cls_stride, int32_t write_ability);
 enum FinPhase : int32_t { FIN_ALL = 0, FIN_PARTIAL = 1, FIN_FINISH = 2 };
