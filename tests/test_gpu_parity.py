@@ -503,3 +503,24 @@ def test_queue_overflow_rerun_matches_oracle(ctx):
     for k in SIM_KEYS:
         eq(g_[k], o[k], k)
     assert rerun_ms > 0.0, "the wide graphs were expected to overflow into the HBM rerun"
+
+
+def test_c2_every_dag_matches_the_reference(ctx):
+    """BASELINE configs[1] in full: all 4096 layered DAGs of C2 scheduled on
+    the device equal the reference implementation (oracle/_ref, the reference
+    sources compiled unmodified, on all host threads) -- attributes, every
+    assignment, every start/end double and every makespan."""
+    from oracle import pyref
+    if not pyref.available():
+        pytest.skip("oracle/_ref not built")
+    hb = api.HostBatch().add_layered(1000, 10, 0.05, np.arange(4096))
+    b = hb.view()
+    pl = [P.assemble("8c2g", 8, 2)]
+    r = ctx.schedule(ctx.upload(hb), pl, "inspirit")
+    costs = P.default_cost_table()
+    ra = pyref.attributes(b, costs, abi.ATTR_ALL, threads=pyref.max_threads())
+    rs = pyref.simulate(b, pl, "inspirit", attrs=ra, record=False, threads=pyref.max_threads())
+    for k in ("ability", "efficiency", "static_priority"):
+        eq(r["attr_" + k], ra[k], k)
+    for k in ("worker", "start_ms", "end_ms", "makespan_ms"):
+        eq(r[k], rs[k], k)
