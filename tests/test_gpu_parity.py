@@ -524,3 +524,26 @@ def test_c2_every_dag_matches_the_reference(ctx):
         eq(r["attr_" + k], ra[k], k)
     for k in ("worker", "start_ms", "end_ms", "makespan_ms"):
         eq(r[k], rs[k], k)
+
+
+def test_c5_one_percent_sample_matches_the_reference(ctx):
+    """BASELINE configs[4]: a 1% sample (every 100th seed of a GPU's 8192) of
+    the 4096-task layered DAGs on the four worker mixes (seed mod 4),
+    generated on the device, equals the reference implementation."""
+    from oracle import pyref
+    if not pyref.available():
+        pytest.skip("oracle/_ref not built")
+    seeds = np.arange(0, 8192, 100, dtype=np.uint64)
+    mixes = [(4, 1), (8, 2), (16, 2), (32, 4)]
+    pls = [P.assemble(f"{c}c{g}g", c, g) for c, g in mixes]
+    pof = (seeds % 4).astype(np.int32)
+    db = ctx.generate_layered(4096, 10, 0.05, seeds)
+    r = ctx.schedule(db, pls, "inspirit", platform_of=pof)
+    b = api.HostBatch().add_layered(4096, 10, 0.05, seeds).view()
+    costs = P.default_cost_table()
+    ra = pyref.attributes(b, costs, abi.ATTR_ALL, threads=pyref.max_threads())
+    rs = pyref.simulate(b, pls, "inspirit", platform_of=pof, attrs=ra, record=False, threads=pyref.max_threads())
+    for k in ("ability", "efficiency", "static_priority"):
+        eq(r["attr_" + k], ra[k], k)
+    for k in ("worker", "start_ms", "end_ms", "makespan_ms"):
+        eq(r[k], rs[k], k)
