@@ -1342,7 +1342,8 @@ struct SimKeys {
 // fewest workers (longest queues, slowest simulations) start first, so they
 // do not pile up at the tail of the atomic DAG queue.
 void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t max_workers, const SimKeys& keys,
-                    const int32_t* pof_host = nullptr, const std::vector<DevPlatform>* hp = nullptr) {
+                    const int32_t* pof_host = nullptr, const std::vector<DevPlatform>* hp = nullptr,
+                    const AttrRun* attrs_first = nullptr) {
     const DevBatch& d = b->d;
     const int64_t G = d.G;
     if (G == 0) return;
@@ -1380,6 +1381,7 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
     cuda_check(cudaMemcpyAsync(status.data(), p.status, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
     cuda_check(cudaMemcpyAsync(aux.data(), p.status_aux, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H aux");
     ctx->sync();
+    if (attrs_first) attr_errors(b, attrs_first->info, TBSIM_ATTR_ALL, nullptr);
     std::vector<int32_t> rerun;
     for (int64_t g = 0; g < G; ++g)
         if (status[g] == GS_QUEUE_OVERFLOW) rerun.push_back(static_cast<int32_t>(g));
@@ -1618,8 +1620,9 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         AttrRun run;
         run_attributes(ctx, b, d_costs, d_pof, SWEEP_CALIBRATE, nullptr, priority_kind == TBSIM_PRIO_UPWARD_RANK, true,
                        o, priority_kind, true, run);
-        ctx->sync();
-        attr_errors(b, run.info, TBSIM_ATTR_ALL, nullptr);
+        // no host round trip here: compute_attributes' errors are raised
+        // (first, as the reference's bench cell would) at the simulation's
+        // status check
         // ---- default_regulator_config + simulate
         SimStage st;
         const bool dev = out->on_device != 0;
@@ -1652,7 +1655,7 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         p.reg_state = sim_out_ptr(ctx, st, nm("s_rstate").c_str(), out->reg_state, G, dev, true);
         p.status = ctx->buf("s_status").as<int32_t>(G);
         p.status_aux = ctx->buf("s_aux").as<int32_t>(G);
-        run_simulation(ctx, b, p, maxw, keys, platform_of, &hp);
+        run_simulation(ctx, b, p, maxw, keys, platform_of, &hp, &run);
         cudaStream_t dl = ctx->stream;
         if (async) {  // the copies wait for this call's kernels, not the next call's
             cudaEvent_t done = ctx->set_free[set];
