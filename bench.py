@@ -621,6 +621,7 @@ def main():
     kms = {k: ctx.last_kernel_ms(k) for k in ("k_structure", "k_tile_plan", "k_sweep", "k_finalize",
                                              "k_structure_out", "k_sim_keys", "k_simulate", "k_simulate_rerun", "k_sim_scatter")}
     sweep_relax = ctx.last_sweep_relaxations()
+    sim_shape = ctx.last_sim_shape()
     ctx.set_timing(False)
     sweep_roof = sweep_roofline(ctx, sweep_relax, kms["k_sweep"])
     dominant = max(("k_sweep", "k_simulate"), key=lambda k: kms[k])
@@ -755,6 +756,8 @@ def main():
                        "resident_input": "value: the batch's device form (CSR, successor CSR, packed task "
                                          "records) built at upload; e2e uploads + ingests every step"},
             "decisions_per_sec": value * 2 * w["n_tasks"],
+            "simulator": dict(sim_shape, dags_in_flight=sim_shape["warps_per_sm"] * torch.cuda.get_device_properties(dev).multi_processor_count,
+                              note="latency-bound: one warp per DAG, 2n dependent decisions"),
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes": alg, "kernel_ms": kms[dominant],

@@ -154,6 +154,11 @@ tbsim_status tbsim_ctx_last_kernel_ms(const tbsim_ctx* ctx, const char* kernel,
  * context's stream.  The sweep's roofline denominators (it is not
  * HBM-bound). */
 tbsim_status tbsim_probe_sweep_peak(tbsim_ctx* ctx, int32_t repeats, double* fp64_per_s, double* fp32_per_s);
+/* Launch shape of the last simulation: resident warps (DAGs in flight) per
+ * SM, whether the per-warp state sat in shared memory, queue entries per
+ * worker. */
+tbsim_status tbsim_ctx_last_sim_shape(const tbsim_ctx* ctx, int32_t* warps_per_sm, int32_t* state_in_smem,
+                                      int32_t* queue_capacity);
 /* Relaxations (predecessor row x tile column) the last timed efficiency
  * sweep executed in FP64 and in FP32-exact windows -- the numerator of its
  * achieved rate. */

@@ -190,6 +190,12 @@ class Context:
     def set_large_graph_threshold(self, n_tasks: int):
         _check(load().tbsim_ctx_set_large_graph_threshold(self.h, n_tasks))
 
+    def last_sim_shape(self) -> dict:
+        """Launch shape of the last simulation (DAGs in flight per SM, ...)."""
+        a, b, c = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+        _check(load().tbsim_ctx_last_sim_shape(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"warps_per_sm": a.value, "state_in_smem": bool(b.value), "queue_capacity": c.value}
+
     def last_sweep_relaxations(self) -> tuple[int, int]:
         """Relaxations executed by the last timed efficiency sweep:
         (in FP64 windows, in FP32-exact windows)."""

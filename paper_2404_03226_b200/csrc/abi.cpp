@@ -115,6 +115,7 @@ struct tbsim_ctx {
     std::vector<PoolEntry> batch_pool;  // freed batch allocations for reuse
     int64_t large_threshold = 65536;  // single graphs at least this large take the closure path
     int32_t sweep_tile = 0;           // forced sources per sweep tile (0: widest that fits)
+    int32_t sim_warps_per_sm = 0, sim_state_smem = 0, sim_qcap = 0;  // last k_simulate launch shape
     // Asynchronous results (tbsim_ctx_set_async_results): host-bound outputs
     // of tbsim_schedule are staged in one of two device buffer sets and copied
     // on the download stream, so a call's D2H overlaps the next call's
@@ -434,6 +435,15 @@ tbsim_status tbsim_probe_sweep_peak(tbsim_ctx* ctx, int32_t repeats, double* fp6
         }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+    });
+}
+
+tbsim_status tbsim_ctx_last_sim_shape(const tbsim_ctx* ctx, int32_t* warps_per_sm, int32_t* state_in_smem,
+                                      int32_t* queue_capacity) {
+    return guarded([&] {
+        *warps_per_sm = ctx->sim_warps_per_sm;
+        *state_in_smem = ctx->sim_state_smem;
+        *queue_capacity = ctx->sim_qcap;
     });
 }
 
@@ -1316,6 +1326,11 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
     int grid = static_cast<int>(std::min<int64_t>((n_items + kWarps - 1) / kWarps,
                                                   static_cast<int64_t>(ctas_per_sm) * ctx->n_sms));
     grid = std::max(grid, 1);
+    if (std::string(name) == "k_simulate") {
+        ctx->sim_warps_per_sm = ctas_per_sm * kWarps;
+        ctx->sim_state_smem = p.use_smem;
+        ctx->sim_qcap = p.qcap;
+    }
     const size_t smem = p.use_smem ? static_cast<size_t>(p.state_bytes * kWarps) : 0;
     if (!p.use_smem) p.gstate = static_cast<char*>(ctx->buf("s_gstate").get(static_cast<size_t>(p.state_bytes) * kWarps * grid));
     unsigned long long* counter = ctx->buf("s_counter").as<unsigned long long>(1);

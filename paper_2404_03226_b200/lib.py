@@ -25,6 +25,7 @@ EXPORTS = [
     "tbsim_attributes_shard_partial",
     "tbsim_attributes_shard_finish",
     "tbsim_ctx_last_sweep_relaxations",
+    "tbsim_ctx_last_sim_shape",
     "tbsim_probe_sweep_peak",
     "tbsim_batch_upload", "tbsim_batch_free", "tbsim_batch_h2d_bytes", "tbsim_batch_generate_layered",
     "tbsim_batch_sizes", "tbsim_batch_download",
@@ -68,6 +69,7 @@ def load():
     L.tbsim_attributes_shard_partial.argtypes = [vp, vp, P(abi.Costs), i32, i32, P(i64), P(i64), i64, P(i64)]
     L.tbsim_attributes_shard_finish.argtypes = [vp, vp, P(i64), i64, i32, P(abi.AttrOut)]
     L.tbsim_ctx_last_sweep_relaxations.argtypes = [vp, P(i64), P(i64)]
+    L.tbsim_ctx_last_sim_shape.argtypes = [vp, P(i32), P(i32), P(i32)]
     L.tbsim_probe_sweep_peak.argtypes = [vp, i32, P(dbl), P(dbl)]
     L.tbsim_ctx_last_kernel_ms.argtypes = [vp, C.c_char_p, P(dbl)]
     L.tbsim_batch_upload.argtypes = [vp, P(abi.BatchDesc), P(vp)]
