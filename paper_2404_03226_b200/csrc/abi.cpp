@@ -1317,6 +1317,14 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
             }
         }
     }
+    // Latency-bound: DAGs in flight set the throughput.  HBM (L2-resident)
+    // state costs ~1.4x per event (C5 mixes: 42 ms vs 30 ms a wave), so it
+    // wins once it at least doubles the warps per SM (C5's 36-worker batch:
+    // 16 vs 8), and its queues never overflow.
+    if (p.use_smem && !forced && ctas_per_sm * 2 <= max_ctas) {
+        p.use_smem = 0;
+        ctas_per_sm = max_ctas;
+    }
     if (!p.use_smem) qcap = qcap_full;
     p.qcap = static_cast<int32_t>(qcap);
     p.layout = layout(qcap);
@@ -1336,7 +1344,15 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
     unsigned long long* counter = ctx->buf("s_counter").as<unsigned long long>(1);
     cuda_check(cudaMemsetAsync(counter, 0, 8, ctx->stream), "memset");
     p.work_counter = counter;
-    auto kern = compact ? (w2 ? k_simulate_w2c : k_simulate_w1c) : (w2 ? k_simulate_w2 : k_simulate_w1);
+    // tasks reading many inputs (mean inputs x memory nodes > 32, C5: 18 x
+    // up to 5): the transfer sums run in rounds over every node at once and
+    // skip resident inputs.  A separate kernel, because the extra code costs
+    // the few-input kernel 10% (C2) even where it never runs.
+    const bool many_in = d.T > 0 && d.I * p.max_nodes > 32 * d.T && p.policy >= TBSIM_POLICY_DMDA;
+    auto kern = compact ? (w2 ? (many_in ? k_simulate_w2c_mi : k_simulate_w2c)
+                              : many_in ? k_simulate_w1c_mi
+                              : p.policy == TBSIM_POLICY_INSPIRIT ? k_simulate_w1c_ins : k_simulate_w1c)
+                        : (w2 ? k_simulate_w2 : k_simulate_w1);
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "cudaFuncSetAttribute(k_simulate)");
     ctx->begin(name);

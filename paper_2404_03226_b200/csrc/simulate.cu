@@ -49,7 +49,7 @@ __device__ __forceinline__ uint64_t ord_i64(int64_t x) {
 // (time, counters, the lane's workers); regulator state, counters and graph
 // ids live in the warp's SimCold record, and state sections are addressed
 // from one base plus the launch's layout offsets (kernel parameters).
-template <int WPL, bool COMPACT, int POL>
+template <int WPL, bool COMPACT, int POL, bool MANYIN>
 struct Sim {
     using UnmetT = typename std::conditional<COMPACT, int16_t, int32_t>::type;
     using ResidT = typename std::conditional<COMPACT, uint8_t, uint32_t>::type;
@@ -59,6 +59,10 @@ struct Sim {
     char* base;  // this warp's state memory
     // ---- graph
     int32_t n;
+    // queue capacity per worker of this graph: the warp's pool of
+    // qcap x max_workers entries split over the graph's own W workers (a
+    // 5-worker graph in a batch with 36-worker platforms gets 7x longer queues)
+    int32_t qc;
     const SimTaskHdr* hdr;  // this graph's packed records
     __device__ __forceinline__ int32_t pol() const { return POL >= 0 ? POL : P->policy; }
     // ---- state sections
@@ -66,12 +70,12 @@ struct Sim {
     __device__ __forceinline__ UnmetT* unmet() const { return reinterpret_cast<UnmetT*>(base + P->layout.unmet); }
     __device__ __forceinline__ ResidT* resid() const { return reinterpret_cast<ResidT*>(base + P->layout.resid); }
     __device__ __forceinline__ int32_t* queue(int32_t w) const {
-        return reinterpret_cast<int32_t*>(base + P->layout.queue) + w * P->qcap;
+        return reinterpret_cast<int32_t*>(base + P->layout.queue) + w * qc;
     }
-    __device__ __forceinline__ KeyT* qab(int32_t w) const { return reinterpret_cast<KeyT*>(base + P->layout.qab) + w * P->qcap; }
-    __device__ __forceinline__ KeyT* qef(int32_t w) const { return reinterpret_cast<KeyT*>(base + P->layout.qef) + w * P->qcap; }
+    __device__ __forceinline__ KeyT* qab(int32_t w) const { return reinterpret_cast<KeyT*>(base + P->layout.qab) + w * qc; }
+    __device__ __forceinline__ KeyT* qef(int32_t w) const { return reinterpret_cast<KeyT*>(base + P->layout.qef) + w * qc; }
     __device__ __forceinline__ PrioT* qprio(int32_t w) const {
-        return reinterpret_cast<PrioT*>(base + P->layout.qprio) + w * P->qcap;
+        return reinterpret_cast<PrioT*>(base + P->layout.qprio) + w * qc;
     }
     __device__ __forceinline__ double* samp_t() const { return reinterpret_cast<double*>(base + P->layout.ring); }
     __device__ __forceinline__ int64_t* samp_n() const {
@@ -147,58 +151,106 @@ struct Sim {
     }
 
     // transfer_total_ms (engine.cpp:105-110) for node `want` (may differ per
-    // lane).  Lanes hold (node, input) pairs, so every per-input transfer is
-    // computed once and in parallel; each node's total is then summed in
-    // input order by one shuffle chain shared by all nodes.
+    // lane).  Lanes hold (node, input) pairs -- all of them at once when
+    // they fit in 32 lanes, else c = 32 / (distinct nodes) inputs per node
+    // per round -- so every per-input transfer is computed once and in
+    // parallel; each node's lane group then adds its terms in input order.
+    // Over several rounds, zero terms are skipped: a resident input
+    // contributes exactly +0.0 and the sum starts at +0.0 (it can never
+    // become -0.0), so the in-order chain runs over non-resident inputs only.
     __device__ __forceinline__ double transfer_total_lanes(const int64_t* inb, const int32_t* inh, int32_t nin,
                                                            int32_t want) const {
         if (nin == 0) return 0.0;
         const unsigned want_nodes = __reduce_or_sync(kFull, 1u << want);
         const int32_t nw = __popc(want_nodes);
         const ResidT* rs = resid();
-        if (nin * nw <= 32) {
-            // r = lane / nin without an integer divide (exact: lane < 32)
-            const int32_t r = __float2int_rz(__fdividef(static_cast<float>(lane) + 0.5f, static_cast<float>(nin)));
-            const int32_t k = lane - r * nin;
-            double t = 0.0;
-            if (r < nw) {
-                unsigned m = want_nodes;  // r-th set bit (few nodes; __fns is emulated)
-                for (int32_t i = 0; i < r; ++i) m &= m - 1;
-                const int32_t to = __ffs(m) - 1;
-                t = transfer_one(rs[__ldg(&inh[k])], __ldg(&inb[k]), to);
-            }
-            const int32_t b0 = (r < nw ? r : 0) * nin;
-            // in-order sum; the shuffles are independent and issued ahead
-            double acc = 0.0;
-            int32_t j = 0;
-#pragma unroll 1
-            for (; j + 4 <= nin; j += 4) {
-                const double a0 = __shfl_sync(kFull, t, b0 + j), a1 = __shfl_sync(kFull, t, b0 + j + 1);
-                const double a2 = __shfl_sync(kFull, t, b0 + j + 2), a3 = __shfl_sync(kFull, t, b0 + j + 3);
-                acc += a0;
-                acc += a1;
-                acc += a2;
-                acc += a3;
-            }
-#pragma unroll 1
-            for (; j < nin; ++j) acc += __shfl_sync(kFull, t, b0 + j);
-            const int32_t rw = __popc(want_nodes & ((1u << want) - 1u));
-            return __shfl_sync(kFull, acc, rw * nin);
-        }
-        double mine = 0.0;
-        for (unsigned wn = want_nodes; wn; wn &= wn - 1) {
-            const int32_t to = __ffs(wn) - 1;
-            double acc = 0.0;
-            for (int32_t b0 = 0; b0 < nin; b0 += 32) {
-                const int32_t cnt = min(32, nin - b0);
+        if constexpr (!MANYIN) {
+            if (nin * nw <= 32) {  // one round: every (node, input) pair on its own lane
+                // r = lane / nin without an integer divide (exact: lane < 32)
+                const int32_t r = __float2int_rz(__fdividef(static_cast<float>(lane) + 0.5f, static_cast<float>(nin)));
+                const int32_t k = lane - r * nin;
                 double t = 0.0;
-                if (lane < cnt) t = transfer_one(rs[__ldg(&inh[b0 + lane])], __ldg(&inb[b0 + lane]), to);
+                if (r < nw) {
+                    unsigned m = want_nodes;  // r-th set bit (few nodes; __fns is emulated)
+                    for (int32_t i = 0; i < r; ++i) m &= m - 1;
+                    const int32_t to = __ffs(m) - 1;
+                    t = transfer_one(rs[__ldg(&inh[k])], __ldg(&inb[k]), to);
+                }
+                const int32_t b0 = (r < nw ? r : 0) * nin;
+                // in-order sum; the shuffles are independent and issued ahead
+                double acc = 0.0;
+                int32_t j = 0;
 #pragma unroll 1
-                for (int32_t j = 0; j < cnt; ++j) acc += __shfl_sync(kFull, t, j);
+                for (; j + 4 <= nin; j += 4) {
+                    const double a0 = __shfl_sync(kFull, t, b0 + j), a1 = __shfl_sync(kFull, t, b0 + j + 1);
+                    const double a2 = __shfl_sync(kFull, t, b0 + j + 2), a3 = __shfl_sync(kFull, t, b0 + j + 3);
+                    acc += a0;
+                    acc += a1;
+                    acc += a2;
+                    acc += a3;
+                }
+#pragma unroll 1
+                for (; j < nin; ++j) acc += __shfl_sync(kFull, t, b0 + j);
+                const int32_t rw = __popc(want_nodes & ((1u << want) - 1u));
+                return __shfl_sync(kFull, acc, rw * nin);
             }
-            if (want == to) mine = acc;
+            // one pass per node, 32 inputs per round
+            double mine = 0.0;
+            for (unsigned wn = want_nodes; wn; wn &= wn - 1) {
+                const int32_t to = __ffs(wn) - 1;
+                double acc = 0.0;
+                for (int32_t b0 = 0; b0 < nin; b0 += 32) {
+                    const int32_t cnt = min(32, nin - b0);
+                    double t = 0.0;
+                    if (lane < cnt) t = transfer_one(rs[__ldg(&inh[b0 + lane])], __ldg(&inb[b0 + lane]), to);
+#pragma unroll 1
+                    for (int32_t j = 0; j < cnt; ++j) acc += __shfl_sync(kFull, t, j);
+                }
+                if (want == to) mine = acc;
+            }
+            return mine;
+        } else {
+            // rounds of c inputs per node, all nodes at once
+            const int32_t c = 32 / nw;
+            // r = lane / c without an integer divide (exact: lane < 32)
+            const int32_t r = __float2int_rz(__fdividef(static_cast<float>(lane) + 0.5f, static_cast<float>(c)));
+            const int32_t k = lane - r * c;
+            const bool act = r < nw;
+            unsigned m = want_nodes;  // r-th set bit (few nodes; __fns is emulated)
+            for (int32_t i = 0; i < r; ++i) m &= m - 1;
+            const int32_t to = act ? __ffs(m) - 1 : 0;
+            const unsigned gmask = (c == 32 ? kFull : ((1u << c) - 1u)) << (act ? r * c : 0);
+            double acc = 0.0;
+            int32_t h = 0;
+            int64_t by = 0;
+            if (act && k < nin) { h = __ldg(&inh[k]); by = __ldg(&inb[k]); }
+#pragma unroll 1
+            for (int32_t b0 = 0; b0 < nin; b0 += c) {
+                const bool mine = act && b0 + k < nin;
+                const int32_t hc = h;
+                const int64_t bc = by;
+                if (act && b0 + c + k < nin) { h = __ldg(&inh[b0 + c + k]); by = __ldg(&inb[b0 + c + k]); }  // next round
+                const double t = mine ? transfer_one(rs[hc], bc, to) : 0.0;
+                unsigned nz = __ballot_sync(kFull, t != 0.0) & gmask;
+                const int32_t steps = __reduce_max_sync(kFull, static_cast<unsigned>(__popc(nz)));
+                // four shuffles in flight, then four in-order adds (an exhausted
+                // lane adds +0.0, which leaves its sum unchanged)
+#pragma unroll 1
+                for (int32_t s = 0; s < steps; s += 4) {
+                    double a[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        a[u] = __shfl_sync(kFull, t, nz ? __ffs(nz) - 1 : lane);
+                        a[u] = nz ? a[u] : 0.0;
+                        nz &= nz - 1;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc += a[u];
+                }
+            }
+            const int32_t rw = __popc(want_nodes & ((1u << want) - 1u));
+            return __shfl_sync(kFull, acc, rw * c);
         }
-        return mine;
     }
 
     // resident_fraction (engine.cpp:63-74)
@@ -541,7 +593,7 @@ struct Sim {
 #pragma unroll
         for (int jj = 0; jj < WPL; ++jj)
             if (jj == j && lane == owner) {
-                if (qlen[jj] >= P->qcap) {
+                if (qlen[jj] >= qc) {
                     ovf = 1;
                 } else {
                     const int32_t at = qlen[jj];
@@ -724,7 +776,7 @@ struct Sim {
 
 // SMEM: the per-warp state lives in shared memory (provably, so every state
 // access compiles to 32-bit-addressed LDS/STS); otherwise in HBM.
-template <int WPL, bool COMPACT, int POL, bool SMEM>
+template <int WPL, bool COMPACT, int POL, bool MANYIN, bool SMEM>
 __device__ void simulate_impl(const SimParams& p) {
     extern __shared__ __align__(16) char smem[];
     const int lane = threadIdx.x & 31;
@@ -740,7 +792,7 @@ __device__ void simulate_impl(const SimParams& p) {
         base = smem + off;
     } else base = p.gstate + (static_cast<int64_t>(blockIdx.x) * warps_per_block + warp_in_block) * p.state_bytes;
     const DevBatch& b = p.b;
-    using S = Sim<WPL, COMPACT, POL>;
+    using S = Sim<WPL, COMPACT, POL, MANYIN>;
     S s;
     s.P = &p;
     s.base = base;
@@ -760,6 +812,8 @@ __device__ void simulate_impl(const SimParams& p) {
         const int32_t pfi = p.platform_of ? p.platform_of[g] : 0;
         const DevPlatform* pf = p.platforms + pfi;
         const int32_t W = pf->n_workers, nn = pf->n_nodes;
+        s.qc = static_cast<int32_t>(
+            std::min<int64_t>(static_cast<int64_t>(p.qcap) * p.max_workers / (W > 0 ? W : 1), INT32_MAX / 64));
         __syncwarp();
         if (pfi != loaded_pf) {  // platform tables into this warp's state
             double* costs = reinterpret_cast<double*>(base + p.layout.costs);
@@ -985,16 +1039,22 @@ __global__ void __launch_bounds__(256) k_sim_scatter(DevBatch b, const SimLog* l
     }
 }
 
-#define TBSIM_SIM_KERNEL(NAME, WPL, COMPACT, POL, THREADS, MINB)                                     \
+#define TBSIM_SIM_KERNEL(NAME, WPL, COMPACT, POL, MANYIN, THREADS, MINB)                             \
     __global__ void __launch_bounds__(THREADS, MINB) NAME(const __grid_constant__ SimParams p) {        \
-        if (p.use_smem) simulate_impl<WPL, COMPACT, POL, true>(p);                                     \
-        else simulate_impl<WPL, COMPACT, POL, false>(p);                                               \
+        if (p.use_smem) simulate_impl<WPL, COMPACT, POL, MANYIN, true>(p);                             \
+        else simulate_impl<WPL, COMPACT, POL, MANYIN, false>(p);                                       \
     }
 // <= 32 workers, compact: 4-warp CTAs, 7 per SM (<= 72 registers)
-TBSIM_SIM_KERNEL(k_simulate_w1c, 1, true, -1, 128, 7)
-TBSIM_SIM_KERNEL(k_simulate_w2c, 2, true, -1, 256, 2)
-TBSIM_SIM_KERNEL(k_simulate_w1, 1, false, -1, 256, 2)
-TBSIM_SIM_KERNEL(k_simulate_w2, 2, false, -1, 256, 2)
+TBSIM_SIM_KERNEL(k_simulate_w1c, 1, true, -1, false, 128, 7)
+// the same for inspirit only (the policy fixed at compile time)
+TBSIM_SIM_KERNEL(k_simulate_w1c_ins, 1, true, TBSIM_POLICY_INSPIRIT, false, 128, 7)
+// batches whose tasks read many inputs (C5: 18 per task): the multi-round
+// transfer sum that skips resident inputs
+TBSIM_SIM_KERNEL(k_simulate_w1c_mi, 1, true, -1, true, 128, 7)
+TBSIM_SIM_KERNEL(k_simulate_w2c, 2, true, -1, false, 256, 2)
+TBSIM_SIM_KERNEL(k_simulate_w2c_mi, 2, true, -1, true, 256, 2)
+TBSIM_SIM_KERNEL(k_simulate_w1, 1, false, -1, false, 256, 2)
+TBSIM_SIM_KERNEL(k_simulate_w2, 2, false, -1, false, 256, 2)
 #undef TBSIM_SIM_KERNEL
 
 }  // namespace tbsim_dev

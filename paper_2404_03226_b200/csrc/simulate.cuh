@@ -143,7 +143,10 @@ __global__ void k_sim_scatter(DevBatch b, const SimLog* log, const int32_t* n_di
                               double* end_ms);
 
 __global__ void k_simulate_w1c(const __grid_constant__ SimParams p);  // <= 32 workers, compact state (128-thread CTAs)
+__global__ void k_simulate_w1c_ins(const __grid_constant__ SimParams p);  // the same, inspirit only
+__global__ void k_simulate_w1c_mi(const __grid_constant__ SimParams p);   // the same, many inputs per task
 __global__ void k_simulate_w2c(const __grid_constant__ SimParams p);  // <= 64 workers, compact state
+__global__ void k_simulate_w2c_mi(const __grid_constant__ SimParams p);  // the same, many inputs per task
 __global__ void k_simulate_w1(const __grid_constant__ SimParams p);   // <= 32 workers, wide state
 __global__ void k_simulate_w2(const __grid_constant__ SimParams p);   // <= 64 workers, wide state
 

@@ -12,7 +12,8 @@ import os
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtbsim_b200.so")
+# TBSIM_LIB: another in-tree build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.path.join(HERE, os.environ.get("TBSIM_LIB", "libtbsim_b200.so"))
 
 # Every symbol the header declares (tests check the .so exports all of them).
 EXPORTS = [

@@ -480,6 +480,27 @@ def test_mixed_width_batch_more_graphs_than_warps(ctx):
     eq(s["makespan_ms"], o["makespan_ms"], "schedule makespans")
 
 
+@pytest.mark.parametrize("policy", ["dmda", "dmdap", "inspirit"])
+def test_many_input_tasks_match_oracle(ctx, policy):
+    """Tasks reading ~30 inputs on 2..5 memory nodes select the kernels
+    whose transfer sums run in rounds and skip resident inputs (1 and 2
+    worker slots per lane): every schedule equals the oracle's."""
+    hb = api.HostBatch().add_layered(400, 4, 0.3, np.arange(12))
+    b = hb.view()
+    mixes = [(4, 1), (8, 2), (16, 2), (32, 4)]
+    costs = P.default_cost_table()
+    oa = po.attributes(b, costs, abi.ATTR_ALL)
+    db = ctx.upload(b)
+    for sel in ([0, 1, 2], [0, 1, 2, 3]):  # <= 32 workers, then up to 36
+        pls = [P.assemble(f"{c}c{g}g", c, g) for c, g in (mixes[i] for i in sel)]
+        pof = (np.arange(b.n_graphs) % len(sel)).astype(np.int32)
+        reg = [po.default_regulator_config(b, g, pls[pof[g]]) for g in range(b.n_graphs)]
+        g_ = ctx.simulate(db, pls, policy, reg, attrs=oa, record=True, platform_of=pof)
+        o = po.simulate(b, pls, policy, platform_of=pof, reg=reg, attrs=oa, record=True)
+        for k in SIM_KEYS:
+            eq(g_[k], o[k], f"{policy} {sel} {k}")
+
+
 def test_queue_overflow_rerun_matches_oracle(ctx):
     """Many graphs (shared-memory state with short queues) plus two whose
     first level puts hundreds of tasks on 10 workers at once: those overflow
