@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -103,6 +104,7 @@ struct tbsim_ctx {
     bool timing = false;
     std::map<std::string, double> last_ms;
     std::map<std::string, std::pair<cudaEvent_t, cudaEvent_t>> events;
+    std::set<std::string> begun;  // timed names begun since the last collect_timing
     std::map<std::string, DevBuf> bufs;
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
@@ -177,7 +179,8 @@ struct tbsim_ctx {
             cudaEventCreate(&ev.first);
             cudaEventCreate(&ev.second);
         }
-        cudaEventRecord(ev.first, stream);
+        // several launches under one name in one call: first begin to last end
+        if (begun.insert(k).second) cudaEventRecord(ev.first, stream);
     }
     void end(const char* k) {
         cuda_check(cudaGetLastError(), k);
@@ -185,6 +188,7 @@ struct tbsim_ctx {
         cudaEventRecord(events[k].second, stream);
     }
     void collect_timing() {
+        begun.clear();
         if (!timing) return;
         for (auto& [k, ev] : events) {
             float ms = 0.f;
@@ -1392,6 +1396,8 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
     }
     p.graph_list = nullptr;
     p.qcap = 0;
+    int64_t n_lo = G;  // graphs of the first launch (<= 32 workers when split)
+    int32_t max_lo = max_workers;
     if (pof_host && hp && hp->size() > 1 && G >= 2 * ctx->n_sms) {
         bool mixed = false;
         for (const auto& pl : *hp) mixed = mixed || pl.n_workers != (*hp)[0].n_workers;
@@ -1404,9 +1410,27 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
             int32_t* d_list = ctx->buf("s_order").as<int32_t>(G);
             cuda_check(cudaMemcpyAsync(d_list, order.data(), G * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D order");
             p.graph_list = d_list;
+            // graphs on <= 32 workers (a prefix of the order) run in their
+            // own launch of the one-worker-per-lane kernel: ~2x the warps
+            // per SM of the two-worker kernel the > 32-worker graphs need
+            if (max_workers > 32) {
+                int64_t lo = 0;
+                while (lo < G && (*hp)[pof_host[order[lo]]].n_workers <= 32) ++lo;
+                if (lo >= ctx->n_sms && G - lo >= ctx->n_sms) {
+                    n_lo = lo;
+                    max_lo = (*hp)[pof_host[order[lo - 1]]].n_workers;
+                }
+            }
         }
     }
-    launch_sim(ctx, p, max_workers, G);
+    if (n_lo < G) {
+        launch_sim(ctx, p, max_lo, n_lo);
+        p.graph_list += n_lo;
+        p.qcap = 0;  // (set by the first launch; 0 = choose)
+        launch_sim(ctx, p, max_workers, G - n_lo);
+    } else {
+        launch_sim(ctx, p, max_workers, G);
+    }
     p.graph_list = nullptr;
     std::vector<int32_t> status(G), aux(G);
     cuda_check(cudaMemcpyAsync(status.data(), p.status, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");

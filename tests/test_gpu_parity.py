@@ -460,9 +460,10 @@ def test_sharded_large_graph_attributes_match_single_gpu(ctx, world, kind):
 
 def test_mixed_width_batch_more_graphs_than_warps(ctx):
     """A batch mixing <= 32-worker platforms with a 36-worker one (C5's mixes,
-    two workers per lane) and more graphs than resident warps: schedules equal
-    the oracle's for every graph and policy."""
-    G = 2 * 148 + 40
+    two workers per lane) and more graphs than resident warps -- enough of
+    each that the <= 32-worker graphs run in their own launch: schedules and
+    ledgers equal the oracle's for every graph and policy."""
+    G = 4 * 148 + 40
     b = api.HostBatch().add_layered(90, 6, 0.12, np.arange(G)).view()
     pls = [P.assemble(f"{c}c{g}g", c, g) for c, g in ((4, 1), (8, 2), (16, 2), (32, 4))]
     pof = (np.arange(G) % 4).astype(np.int32)
@@ -471,9 +472,9 @@ def test_mixed_width_batch_more_graphs_than_warps(ctx):
     oa = po.attributes(b, costs, abi.ATTR_ALL)
     reg = [po.default_regulator_config(b, g, pls[pof[g]]) for g in range(G)]
     for pol in ("dmda", "inspirit"):
-        g_ = ctx.simulate(db, pls, pol, reg, platform_of=pof, attrs=oa, record=False)
-        o = po.simulate(b, pls, pol, platform_of=pof, reg=reg, attrs=oa, record=False)
-        for k in ("worker", "start_ms", "end_ms", "makespan_ms"):
+        g_ = ctx.simulate(db, pls, pol, reg, platform_of=pof, attrs=oa, record=True)
+        o = po.simulate(b, pls, pol, platform_of=pof, reg=reg, attrs=oa, record=True)
+        for k in SIM_KEYS:
             eq(g_[k], o[k], f"{pol}/{k}")
     s = ctx.schedule(db, pls, "inspirit", platform_of=pof, want_attrs=False)
     o = po.simulate(b, pls, "inspirit", platform_of=pof, reg=reg, attrs=oa, record=False)
