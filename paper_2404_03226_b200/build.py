@@ -26,6 +26,10 @@ CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off",
              "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I/usr/local/cuda/include"]
 
 CU_SRCS = ["attributes.cu", "simulate.cu", "generate.cu", "probe.cu", "abi.cpp"]  # abi.cpp launches kernels: nvcc -x cu
+# NVVM at -O2 for the simulator: cicc -O3 segfaults on most edits of this
+# translation unit (deterministically once ASLR is off), -O2 compiles it and
+# the kernels run as fast
+CU_EXTRA = {"simulate.cu": ["-Xcicc", "-O2"]}
 CXX_SRCS = ["hostbatch.cpp"]
 # the drop-in C++ API (namespace tbsim, include/tbsim/*.hpp) over the C-ABI
 API_SRCS = ["api/taskgraph.cpp", "api/platform.cpp", "api/device.cpp", "api/attributes.cpp",
@@ -70,7 +74,7 @@ def build(verbose: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         if _stale(o, [s] + headers):
-            cmd = [NVCC] + ARCH + CU_FLAGS + ["-rdc=false", "-x", "cu", "-c", s, "-o", o]
+            cmd = [NVCC] + ARCH + CU_FLAGS + CU_EXTRA.get(src, []) + ["-rdc=false", "-x", "cu", "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd))
             _run(cmd)

@@ -65,8 +65,12 @@ __device__ void sort_small(int32_t* a, int32_t len) {
     }
 }
 
-__global__ void __launch_bounds__(256) k_ingest(DevBatch b, int32_t* cursor_scratch) {
+// Successor CSR of each graph (one CTA per graph): count, scan, scatter,
+// sort each list.  Counts and cursors live in shared memory when the graph
+// fits (smem_ints >= n + 1), else in global memory.
+__global__ void __launch_bounds__(256) k_ingest(DevBatch b, int32_t* cursor_scratch, int32_t smem_ints) {
     __shared__ int32_t warp_tot[32];
+    extern __shared__ int32_t s_ctr[];
     for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) {
         const int64_t t0 = b.task_base[g];
         const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
@@ -74,6 +78,27 @@ __global__ void __launch_bounds__(256) k_ingest(DevBatch b, int32_t* cursor_scra
         const int32_t* dep = b.dep + b.edge_base[g];
         int32_t* soff = b.succ_off + t0 + g;
         int32_t* succ = b.succ + b.edge_base[g];
+        if (n + 1 <= smem_ints) {
+            for (int32_t i = threadIdx.x; i <= n; i += blockDim.x) s_ctr[i] = 0;
+            __syncthreads();
+            for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
+                for (int32_t k = __ldg(&doff[v]); k < __ldg(&doff[v + 1]); ++k) atomicAdd(&s_ctr[__ldg(&dep[k])], 1);
+            __syncthreads();
+            block_exclusive_scan_inplace(s_ctr, n + 1, warp_tot);
+            for (int32_t i = threadIdx.x; i <= n; i += blockDim.x) soff[i] = s_ctr[i];
+            __syncthreads();
+            for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
+                for (int32_t k = __ldg(&doff[v]); k < __ldg(&doff[v + 1]); ++k)
+                    succ[atomicAdd(&s_ctr[__ldg(&dep[k])], 1)] = v;
+            __syncthreads();
+            // s_ctr[u] is now the end of u's list
+            for (int32_t u = threadIdx.x; u < n; u += blockDim.x) {
+                const int32_t e = s_ctr[u], s = u == 0 ? 0 : s_ctr[u - 1];
+                sort_small(succ + s, e - s);
+            }
+            __syncthreads();
+            continue;
+        }
         int32_t* cur = cursor_scratch + t0 + g;
         for (int32_t i = threadIdx.x; i <= n; i += blockDim.x) soff[i] = 0;
         __syncthreads();

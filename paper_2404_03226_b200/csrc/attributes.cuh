@@ -92,7 +92,7 @@ struct AttrOutDev {
     int32_t* evaluations;
 };
 
-__global__ void k_ingest(DevBatch b, int32_t* cursor_scratch);
+__global__ void k_ingest(DevBatch b, int32_t* cursor_scratch, int32_t smem_ints);
 __global__ void k_structure(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                             int32_t want_rank, int32_t want_large);
 __global__ void k_structure_large(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,

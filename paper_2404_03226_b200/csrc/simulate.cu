@@ -761,6 +761,8 @@ struct Sim {
                         const int32_t left = static_cast<int32_t>(um[sv]) - __popc(peers);
                         um[sv] = static_cast<UnmetT>(left);
                         rdy = left == 0;
+                        // its push reads the record soon: into L1 now
+                        if (rdy) asm volatile("prefetch.global.L1 [%0];" ::"l"(hdr + sv));
                     }
                     __syncwarp();
                     ready_append(rdy, sv);
@@ -959,11 +961,26 @@ __device__ __forceinline__ int64_t graph_of(const DevBatch& b, int64_t t) {
 // Structural half of the packed simulation graph (record words 0-3 and the
 // lists); depends only on the batch, so it is built once per batch, at
 // upload (k_ingest's stream) or on first use.
+template <int TL>
 __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, SimTaskHdr* hdr, char* adj) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < b.T; t += stride) {
-        const int64_t g = graph_of(b, t);
-        const int64_t t0 = __ldg(&b.task_base[g]);
+    // teams of TL lanes, each over a contiguous range of tasks: the team
+    // copies a task's lists in parallel and follows graph boundaries
+    // incrementally (one search per team)
+    const int tl = threadIdx.x & (TL - 1);
+    const int64_t team = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / TL;
+    const int64_t nteams = static_cast<int64_t>(gridDim.x) * blockDim.x / TL;
+    const int64_t per = (b.T + nteams - 1) / nteams;
+    const int64_t tend = min(b.T, (team + 1) * per);
+    int64_t t = team * per;
+    if (t >= tend) return;
+    int64_t g = graph_of(b, t);
+    int64_t t0 = __ldg(&b.task_base[g]), t1 = __ldg(&b.task_base[g + 1]);
+    for (; t < tend; ++t) {
+        while (t >= t1) {  // next non-empty graph
+            ++g;
+            t0 = t1;
+            t1 = __ldg(&b.task_base[g + 1]);
+        }
         const int64_t v = t - t0;
         const int32_t* ioff = b.in_off + t0 + g;
         const int32_t* ooff = b.out_off + t0 + g;
@@ -975,29 +992,32 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, SimTaskHdr* hdr, c
         const int64_t hb = __ldg(&b.handle_base[g]);
         // closed-form list offset: 4 bytes of slack per task absorb the
         // 8-byte alignment of the input-bytes section
-        const int64_t x = 4 * (t0 + v) + 12 * (ib + i0) + 4 * (ob + o0) + 4 * (eb + s0);
+        const int64_t x = 4 * t + 12 * (ib + i0) + 4 * (ob + o0) + 4 * (eb + s0);
         const int64_t x8 = (x + 7) & ~int64_t(7);
         const int32_t nin = i1 - i0, nout = o1 - o0, nsucc = s1 - s0;
-        int4* h = reinterpret_cast<int4*>(hdr + t);
-        h[0] = make_int4(static_cast<int32_t>(x8 >> 3), nin, nout,
-                         static_cast<int32_t>((static_cast<uint32_t>(__ldg(&b.type[t])) << 24) |
-                                              (static_cast<uint32_t>(nsucc) & 0xffffffu)));
+        if (tl == 0)
+            reinterpret_cast<int4*>(hdr + t)[0] =
+                make_int4(static_cast<int32_t>(x8 >> 3), nin, nout,
+                          static_cast<int32_t>((static_cast<uint32_t>(__ldg(&b.type[t])) << 24) |
+                                               (static_cast<uint32_t>(nsucc) & 0xffffffu)));
         int64_t* inb = reinterpret_cast<int64_t*>(adj + x8);
         int32_t* inh = reinterpret_cast<int32_t*>(inb + nin);
         const int32_t* in = b.in + ib + i0;
-        for (int32_t k = 0; k < nin; ++k) {
+        for (int32_t k = tl; k < nin; k += TL) {
             const int32_t hd = __ldg(&in[k]);
             inh[k] = hd;
             inb[k] = __ldg(&b.handle_bytes[hb + hd]);
         }
         int32_t* outl = inh + nin;
         const int32_t* out = b.out + ob + o0;
-        for (int32_t k = 0; k < nout; ++k) outl[k] = __ldg(&out[k]);
+        for (int32_t k = tl; k < nout; k += TL) outl[k] = __ldg(&out[k]);
         int32_t* succl = outl + nout;
         const int32_t* succ = b.succ + eb + s0;
-        for (int32_t k = 0; k < nsucc; ++k) succl[k] = succ[k];
+        for (int32_t k = tl; k < nsucc; k += TL) succl[k] = succ[k];
     }
 }
+
+template __global__ void k_sim_pack<8>(DevBatch, SimTaskHdr*, char*);
 
 // Pop keys of one simulation call (record words 4-7): ability, efficiency
 // and static priority; ab = -1 flags keys beyond the queue's int32 keys or a

@@ -135,6 +135,7 @@ struct SimParams {
 
 // Builds the packed records' structural words and lists (once per batch);
 // k_sim_keys fills the pop keys of one call.  One thread per task.
+template <int TL>  // lanes per task (8 instantiated)
 __global__ void k_sim_pack(DevBatch b, SimTaskHdr* hdr, char* adj);
 __global__ void k_sim_keys(DevBatch b, const int64_t* ability, const int64_t* efficiency, const int64_t* prio,
                            int32_t policy, SimTaskHdr* hdr);
