@@ -842,6 +842,25 @@ __device__ __forceinline__ uint64_t shl64(uint64_t x, uint32_t sh) {
     return r;
 }
 
+// Final flush of a tile's packed counters without shared atomics.  The
+// distance rows are dead after the last level, so each group has dumped its
+// counter words there: dump[group * S + source].  One thread per (source,
+// part) sums a third of the fields over all groups in registers: fields
+// p, p+3, p+6, p+9 spread to 15-bit lanes (groups x 31 < 32768).
+template <int S>
+__device__ __forceinline__ void dump_reduce(const uint64_t* dump, int32_t ngroups, int32_t nsrc, uint32_t* s_hist) {
+    static_assert(kBins == 12 && kFieldBits == 5, "three 4-field parts per counter word");
+    constexpr uint64_t kPart = 0x1Full | (0x1Full << 15) | (0x1Full << 30) | (0x1Full << 45);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 3 * nsrc; i += blockDim.x) {
+        const int sc = i / 3, p = i - 3 * sc;
+        uint64_t acc = 0;
+        for (int gi = 0; gi < ngroups; ++gi) acc += (dump[gi * S + sc] >> (kFieldBits * p)) & kPart;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s_hist[sc * kBins + p + 3 * k] += static_cast<uint32_t>(acc >> (15 * k)) & 0x7fffu;
+    }
+}
+
 __device__ __forceinline__ void flush5(uint64_t& h, uint32_t* dst) {
 #pragma unroll
     for (int bn = 0; bn < kBins; ++bn) {
@@ -1015,9 +1034,18 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
             __syncthreads();
         }
     }
+    // Final flush: through the dead rows when they hold every warp's
+    // counters (dump_reduce), else atomics per bin.
+    if (SMEM && GPW == 1 && static_cast<int64_t>(P) * sizeof(T) >= static_cast<int64_t>(nwarps) * 8) {
+        uint64_t* dump = reinterpret_cast<uint64_t*>(win);
 #pragma unroll
-    for (int q = 0; q < SPL; ++q)
-        if (src(q) < nsrc) flush5(hist[q], s_hist + src(q) * kBins);
+        for (int q = 0; q < SPL; ++q) dump[warp * S + src(q)] = hist[q];
+        dump_reduce<S>(dump, nwarps, nsrc, s_hist);
+    } else {
+#pragma unroll
+        for (int q = 0; q < SPL; ++q)
+            if (src(q) < nsrc) flush5(hist[q], s_hist + src(q) * kBins);
+    }
     __syncthreads();
     if (relax_ctr && threadIdx.x == 0)  // [0]: FP64 windows, [1]: FP32
         atomicAdd(relax_ctr + (sizeof(T) == 4 ? 1 : 0), static_cast<unsigned long long>(nrel * S));
@@ -1188,11 +1216,23 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
             __syncthreads();
         }
     }
+    // (narrow tiles keep the atomics: 3 x S threads would each sum over
+    // hundreds of groups)
+    if (S >= 32 && static_cast<int64_t>(P) * sizeof(T) >= static_cast<int64_t>(ngroups) * 8 &&
+        ngroups * kFlushEvery < 32768) {
+        uint64_t* dump = reinterpret_cast<uint64_t*>(w2);  // the rows are dead: dump_reduce
 #pragma unroll
-    for (int j = 0; j < NCL; ++j)
+        for (int j = 0; j < NCL; ++j)
 #pragma unroll
-        for (int e = 0; e < VEC; ++e)
-            if (VEC * chunk(j) + e < nsrc) flush5(hist[VEC * j + e], s_hist + (VEC * chunk(j) + e) * kBins);
+            for (int e = 0; e < VEC; ++e) dump[gidx * S + VEC * chunk(j) + e] = hist[VEC * j + e];
+        dump_reduce<S>(dump, ngroups, nsrc, s_hist);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NCL; ++j)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e)
+                if (VEC * chunk(j) + e < nsrc) flush5(hist[VEC * j + e], s_hist + (VEC * chunk(j) + e) * kBins);
+    }
     __syncthreads();
     if (relax_ctr && tid == 0)  // [0]: FP64 windows, [1]: FP32
         atomicAdd(relax_ctr + (sizeof(T) == 4 ? 1 : 0), static_cast<unsigned long long>(nrel * S));
