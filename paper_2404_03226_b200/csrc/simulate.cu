@@ -480,14 +480,15 @@ struct Sim {
     // (instruction-cache stalls are the simulator's largest stall class).
     __device__ __forceinline__ void maybe_dispatch(int32_t w, bool pushed) {  // engine.cpp:143-166
         const int j = w >> 5, owner = w & 31;
-        int32_t ql = 0, bz = 0, kd = 0, nd = 0;
+        // the owner's queue length, busy flag, kind and node in one shuffle
+        // (ql < 2^24 entries, < 32 nodes)
+        uint32_t pk = 0;
 #pragma unroll
         for (int jj = 0; jj < WPL; ++jj)
-            if (jj == j) { ql = qlen[jj]; bz = busy_of(jj); kd = kind_of(jj); nd = node_of(jj); }
-        ql = __shfl_sync(kFull, ql, owner);
-        bz = __shfl_sync(kFull, bz, owner);
-        kd = __shfl_sync(kFull, kd, owner);
-        nd = __shfl_sync(kFull, nd, owner);
+            if (jj == j) pk = (static_cast<uint32_t>(qlen[jj]) << 8) | (wk[jj] & 6u) << 5 | node_of(jj);
+        pk = __shfl_sync(kFull, pk, owner);
+        const int32_t ql = static_cast<int32_t>(pk >> 8), bz = (pk >> 7) & 1, kd = (pk >> 6) & 1,
+                      nd = static_cast<int32_t>(pk & 31u);
         uint32_t e = 0;
         int64_t slot = 0;
         int4 hd = make_int4(0, 0, 0, 0);
