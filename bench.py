@@ -298,27 +298,47 @@ def run_c5(args):
     dev = torch.device("cuda", local)
     gathered = torch.empty(world * G, dtype=torch.float64, device=dev)
 
+    T = G * n
+    # value: the resident batch, results into device buffers (as C2's value);
+    # e2e: generated every step, results into pinned host arrays
+    dout = {"worker": torch.empty(T, dtype=torch.int32, device=dev),
+            "start_ms": torch.empty(T, dtype=torch.float64, device=dev),
+            "end_ms": torch.empty(T, dtype=torch.float64, device=dev),
+            "makespan_ms": torch.empty(G, dtype=torch.float64, device=dev)}
+    dptrs = {k: v.data_ptr() for k, v in dout.items()}
+    pinned = {"worker": torch.empty(T, dtype=torch.int32, pin_memory=True).numpy(),
+              "start_ms": torch.empty(T, dtype=torch.float64, pin_memory=True).numpy(),
+              "end_ms": torch.empty(T, dtype=torch.float64, pin_memory=True).numpy(),
+              "makespan_ms": torch.empty(G, dtype=torch.float64, pin_memory=True).numpy(),
+              "completed": torch.empty(G, dtype=torch.int64, pin_memory=True).numpy()}
+
     def step(db=None):
-        own = db is None
-        if own:
-            db = ctx.generate_layered(n, L, p, seeds)
-        r = ctx.schedule(db, platforms, "inspirit", platform_of=pof, want_attrs=False, want_states=False)
+        if db is not None:
+            ctx.schedule_device(db, platforms, "inspirit", dptrs, platform_of=pof)
+            if dist is not None:
+                dist.all_gather_into_tensor(gathered, dout["makespan_ms"])
+            return None
+        db = ctx.generate_layered(n, L, p, seeds)
+        r = ctx.schedule(db, platforms, "inspirit", platform_of=pof, want_attrs=False, want_states=False,
+                         out_arrays=pinned)
         if dist is not None:
             dist.all_gather_into_tensor(gathered, torch.from_numpy(r["makespan_ms"]).to(dev))
-        if own:
-            db.free()
+        db.free()
         return r
 
     for _ in range(max(args.warmup, 1)):
         step()
     torch.cuda.synchronize()
     resident = ctx.generate_layered(n, L, p, seeds)
+    for _ in range(max(args.warmup, 1)):
+        step(resident)
+    torch.cuda.synchronize()
     ctx.set_timing(True)
     times, e2e = [], []
     for _ in range(args.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        r = step(resident)
+        step(resident)
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
