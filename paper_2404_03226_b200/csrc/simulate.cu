@@ -965,9 +965,12 @@ __device__ __forceinline__ int64_t graph_of(const DevBatch& b, int64_t t) {
 template <int TL>
 __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, SimTaskHdr* hdr, char* adj) {
     // teams of TL lanes, each over a contiguous range of tasks: the team
-    // copies a task's lists in parallel and follows graph boundaries
-    // incrementally (one search per team)
+    // loads the offsets of its next TL tasks at once (lane j: task j, one
+    // coalesced load) and hands them out by shuffles, copies each task's
+    // lists in parallel, and follows graph boundaries incrementally (one
+    // search per team)
     const int tl = threadIdx.x & (TL - 1);
+    const unsigned tmask = (TL == 32 ? 0xffffffffu : ((1u << TL) - 1u)) << ((threadIdx.x & 31) & ~(TL - 1));
     const int64_t team = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / TL;
     const int64_t nteams = static_cast<int64_t>(gridDim.x) * blockDim.x / TL;
     const int64_t per = (b.T + nteams - 1) / nteams;
@@ -976,45 +979,60 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, SimTaskHdr* hdr, c
     if (t >= tend) return;
     int64_t g = graph_of(b, t);
     int64_t t0 = __ldg(&b.task_base[g]), t1 = __ldg(&b.task_base[g + 1]);
-    for (; t < tend; ++t) {
-        while (t >= t1) {  // next non-empty graph
-            ++g;
-            t0 = t1;
-            t1 = __ldg(&b.task_base[g + 1]);
+    int64_t ib = __ldg(&b.in_base[g]), ob = __ldg(&b.out_base[g]), eb = __ldg(&b.edge_base[g]);
+    int64_t hb = __ldg(&b.handle_base[g]);
+    while (t < tend) {
+        if (t >= t1) {  // next non-empty graph
+            do {
+                ++g;
+                t0 = t1;
+                t1 = __ldg(&b.task_base[g + 1]);
+            } while (t >= t1);
+            ib = __ldg(&b.in_base[g]); ob = __ldg(&b.out_base[g]); eb = __ldg(&b.edge_base[g]);
+            hb = __ldg(&b.handle_base[g]);
         }
-        const int64_t v = t - t0;
+        const int32_t nb = static_cast<int32_t>(min(static_cast<int64_t>(TL), min(t1, tend) - t));
+        const int64_t v0 = t - t0;
         const int32_t* ioff = b.in_off + t0 + g;
         const int32_t* ooff = b.out_off + t0 + g;
         const int32_t* soff = b.succ_off + t0 + g;
-        const int32_t i0 = __ldg(&ioff[v]), i1 = __ldg(&ioff[v + 1]);
-        const int32_t o0 = __ldg(&ooff[v]), o1 = __ldg(&ooff[v + 1]);
-        const int32_t s0 = soff[v], s1 = soff[v + 1];  // written by k_ingest
-        const int64_t ib = __ldg(&b.in_base[g]), ob = __ldg(&b.out_base[g]), eb = __ldg(&b.edge_base[g]);
-        const int64_t hb = __ldg(&b.handle_base[g]);
-        // closed-form list offset: 4 bytes of slack per task absorb the
-        // 8-byte alignment of the input-bytes section
-        const int64_t x = 4 * t + 12 * (ib + i0) + 4 * (ob + o0) + 4 * (eb + s0);
-        const int64_t x8 = (x + 7) & ~int64_t(7);
-        const int32_t nin = i1 - i0, nout = o1 - o0, nsucc = s1 - s0;
-        if (tl == 0)
-            reinterpret_cast<int4*>(hdr + t)[0] =
-                make_int4(static_cast<int32_t>(x8 >> 3), nin, nout,
-                          static_cast<int32_t>((static_cast<uint32_t>(__ldg(&b.type[t])) << 24) |
-                                               (static_cast<uint32_t>(nsucc) & 0xffffffu)));
-        int64_t* inb = reinterpret_cast<int64_t*>(adj + x8);
-        int32_t* inh = reinterpret_cast<int32_t*>(inb + nin);
-        const int32_t* in = b.in + ib + i0;
-        for (int32_t k = tl; k < nin; k += TL) {
-            const int32_t hd = __ldg(&in[k]);
-            inh[k] = hd;
-            inb[k] = __ldg(&b.handle_bytes[hb + hd]);
+        int32_t li0 = 0, li1 = 0, lo0 = 0, lo1 = 0, ls0 = 0, ls1 = 0, lty = 0;
+        if (tl < nb) {
+            li0 = __ldg(&ioff[v0 + tl]); li1 = __ldg(&ioff[v0 + tl + 1]);
+            lo0 = __ldg(&ooff[v0 + tl]); lo1 = __ldg(&ooff[v0 + tl + 1]);
+            ls0 = soff[v0 + tl]; ls1 = soff[v0 + tl + 1];  // written by k_ingest
+            lty = __ldg(&b.type[t + tl]);
         }
-        int32_t* outl = inh + nin;
-        const int32_t* out = b.out + ob + o0;
-        for (int32_t k = tl; k < nout; k += TL) outl[k] = __ldg(&out[k]);
-        int32_t* succl = outl + nout;
-        const int32_t* succ = b.succ + eb + s0;
-        for (int32_t k = tl; k < nsucc; k += TL) succl[k] = succ[k];
+        for (int32_t j = 0; j < nb; ++j, ++t) {
+            const int32_t i0 = __shfl_sync(tmask, li0, j, TL), i1 = __shfl_sync(tmask, li1, j, TL);
+            const int32_t o0 = __shfl_sync(tmask, lo0, j, TL), o1 = __shfl_sync(tmask, lo1, j, TL);
+            const int32_t s0 = __shfl_sync(tmask, ls0, j, TL), s1 = __shfl_sync(tmask, ls1, j, TL);
+            const int32_t ty = __shfl_sync(tmask, lty, j, TL);
+            // closed-form list offset: 4 bytes of slack per task absorb the
+            // 8-byte alignment of the input-bytes section
+            const int64_t x = 4 * t + 12 * (ib + i0) + 4 * (ob + o0) + 4 * (eb + s0);
+            const int64_t x8 = (x + 7) & ~int64_t(7);
+            const int32_t nin = i1 - i0, nout = o1 - o0, nsucc = s1 - s0;
+            if (tl == 0)
+                reinterpret_cast<int4*>(hdr + t)[0] =
+                    make_int4(static_cast<int32_t>(x8 >> 3), nin, nout,
+                              static_cast<int32_t>((static_cast<uint32_t>(ty) << 24) |
+                                                   (static_cast<uint32_t>(nsucc) & 0xffffffu)));
+            int64_t* inb = reinterpret_cast<int64_t*>(adj + x8);
+            int32_t* inh = reinterpret_cast<int32_t*>(inb + nin);
+            const int32_t* in = b.in + ib + i0;
+            for (int32_t k = tl; k < nin; k += TL) {
+                const int32_t hd = __ldg(&in[k]);
+                inh[k] = hd;
+                inb[k] = __ldg(&b.handle_bytes[hb + hd]);
+            }
+            int32_t* outl = inh + nin;
+            const int32_t* out = b.out + ob + o0;
+            for (int32_t k = tl; k < nout; k += TL) outl[k] = __ldg(&out[k]);
+            int32_t* succl = outl + nout;
+            const int32_t* succ = b.succ + eb + s0;
+            for (int32_t k = tl; k < nsucc; k += TL) succl[k] = succ[k];
+        }
     }
 }
 
