@@ -808,13 +808,15 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         // CTAs that each walk ~G/grid graphs would double the tail); small
         // graphs use small CTAs -- a level of a 1k-task DAG has ~100 nodes
         const int st_threads = d.max_n <= 4096 ? 128 : 512;
-        static int per_sm_s[2] = {0, 0};
-        int& per_sm = per_sm_s[st_threads == 128 ? 0 : 1];
-        if (!per_sm)
-            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_structure, st_threads, 0), "occupancy");
+        // in-degrees in shared memory for graphs of <= 2048 tasks (8 KB)
+        const int32_t st_ints = d.max_n < 2048 ? ((d.max_n + 1 + 31) & ~31) : 0;
+        int per_sm = 0;
+        cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_structure, st_threads, st_ints * 4),
+                   "occupancy");
         const int grid_s = static_cast<int>(std::min<int64_t>(G, static_cast<int64_t>(std::max(per_sm, 1)) * ctx->n_sms));
         ctx->begin("k_structure");
-        k_structure<<<grid_s, st_threads, 0, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, want_rank ? 1 : 0, large ? 1 : 0);
+        k_structure<<<grid_s, st_threads, static_cast<size_t>(st_ints) * 4, ctx->stream>>>(
+            d, d_costs, d_cost_idx, run.s, want_rank ? 1 : 0, large ? 1 : 0, st_ints);
         ctx->end("k_structure");
     }
     bool ability_done = false;

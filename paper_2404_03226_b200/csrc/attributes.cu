@@ -197,7 +197,8 @@ __device__ void load_costs(const DevCosts* costs_g, int32_t ci, DevCosts& sc, do
 
 __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* costs_g,
                                                   const int32_t* cost_idx, AttrScratch s,
-                                                  int32_t want_rank, int32_t want_large) {
+                                                  int32_t want_rank, int32_t want_large, int32_t smem_ints) {
+    extern __shared__ int32_t s_indeg[];  // [smem_ints]: Kahn's in-degrees when n + 1 fit
     __shared__ DevCosts sc;
     __shared__ double s_mean[kMaxTypes];
     __shared__ int32_t s_tcount[kMaxTypes];
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
         const int32_t* soff = b.succ_off + t0 + g;
         const int32_t* succ = b.succ + b.edge_base[g];
         const int32_t* type = b.type + t0;
-        int32_t* indeg = s.tmp + t0 + g;
+        int32_t* indeg = n + 1 <= smem_ints ? s_indeg : s.tmp + t0 + g;
         int32_t* order = s.order + t0;
         int32_t* level = s.level + t0;
         int32_t* lstart = s.lstart + t0 + g;

@@ -93,8 +93,9 @@ struct AttrOutDev {
 };
 
 __global__ void k_ingest(DevBatch b, int32_t* cursor_scratch, int32_t smem_ints);
+// smem_ints: dynamic shared ints for the in-degree counters (used when n+1 fit)
 __global__ void k_structure(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
-                            int32_t want_rank, int32_t want_large);
+                            int32_t want_rank, int32_t want_large, int32_t smem_ints);
 __global__ void k_structure_large(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                                   int32_t want_rank, LargeCtl* ctl, int32_t sort_levels);
 __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32_t force_s, const DevCosts* costs,
