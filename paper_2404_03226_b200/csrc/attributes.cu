@@ -332,7 +332,18 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
         for (int32_t i = tid; i < processed; i += nthr) {
             const int32_t v = order[i];
             const int32_t o = om_poff[i] - doff[v];
-            for (int32_t k = doff[v]; k < doff[v + 1]; ++k) om_ps[o + k] = slot[dep[k]];
+            const int32_t k1 = doff[v + 1];
+            // four predecessors at a time: loads issued before the stores
+            for (int32_t k = doff[v]; k < k1; k += 4) {
+                int32_t d[4], sl[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) d[u] = k + u < k1 ? dep[k + u] : 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) sl[u] = k + u < k1 ? slot[d[u]] : 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (k + u < k1) om_ps[o + k + u] = sl[u];
+            }
         }
         // ---- calibration classes: dense ids of present (layer, type) pairs
         int32_t* mark = s.cls_mark + t0 * NT;   // [L * NT] <= n * NT
