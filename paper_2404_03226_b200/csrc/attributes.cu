@@ -257,11 +257,18 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
             if (tid == 0) lstart[L + 1] = end;
             for (int32_t i = head + tid; i < end; i += nthr) {
                 const int32_t u = order[i];
-                for (int32_t k = soff[u]; k < soff[u + 1]; ++k) {
-                    const int32_t v = succ[k];
-                    if (atomicSub(&indeg[v], 1) == 1) {
-                        level[v] = L + 1;
-                        order[atomicAdd(&s_tail, 1)] = v;
+                const int32_t k1 = soff[u + 1];
+                for (int32_t k = soff[u]; k < k1; k += 4) {  // successor ids loaded four at a time
+                    int32_t vv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) vv[q] = k + q < k1 ? succ[k + q] : -1;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int32_t v = vv[q];
+                        if (v >= 0 && atomicSub(&indeg[v], 1) == 1) {
+                            level[v] = L + 1;
+                            order[atomicAdd(&s_tail, 1)] = v;
+                        }
                     }
                 }
             }
@@ -275,11 +282,24 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
                 const int32_t u = order[i];
                 int32_t h = 0, lu = lv;
                 double best = 0.0;
-                for (int32_t k = soff[u]; k < soff[u + 1]; ++k) {
-                    const int32_t v = succ[k];
-                    h = max(h, height[v] + 1);
-                    best = fmax(best, rank[v]);
-                    lu = max(lu, level[v]);
+                const int32_t k1 = soff[u + 1];
+                for (int32_t k = soff[u]; k < k1; k += 4) {  // four successors' records in flight
+                    int32_t vv[4], hv[4], lvv[4];
+                    double rv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) vv[q] = k + q < k1 ? succ[k + q] : -1;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        hv[q] = vv[q] >= 0 ? height[vv[q]] : -1;
+                        rv[q] = vv[q] >= 0 ? rank[vv[q]] : 0.0;
+                        lvv[q] = vv[q] >= 0 ? level[vv[q]] : lv;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        h = max(h, hv[q] + 1);
+                        best = fmax(best, rv[q]);
+                        lu = max(lu, lvv[q]);
+                    }
                 }
                 height[u] = h;
                 lastuse[u] = lu;
