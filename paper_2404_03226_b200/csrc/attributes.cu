@@ -1494,7 +1494,11 @@ __global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int
                                                  const double* unit_time_in, AttrOutDev o,
                                                  int64_t* cls_scratch, int64_t cls_stride, int32_t write_ability) {
     __shared__ int32_t s_score[kWindows];
-    int64_t* sums = cls_scratch + blockIdx.x * cls_stride;  // [C][kWindows] then cnt[C]
+    // class sums, counts and reduced fractions: in shared memory for graphs
+    // of <= kSmemClasses calibration classes, else in the CTA's HBM scratch
+    constexpr int kSmemClasses = 64;
+    __shared__ int64_t s_cls[kSmemClasses * (3 * kWindows + 1)];
+    int64_t* const g_sums = cls_scratch + blockIdx.x * cls_stride;  // [C][kWindows] then cnt[C]
     for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) {
         const int64_t t0 = b.task_base[g];
         const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
@@ -1504,6 +1508,7 @@ __global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int
         int best = 0;
         if (sweep_mode == SWEEP_CALIBRATE) {
             const int32_t C = gi.n_classes;
+            int64_t* sums = C <= kSmemClasses ? s_cls : g_sums;
             int64_t* cnt = sums + static_cast<int64_t>(C) * kWindows;
             for (int64_t i = threadIdx.x; i < static_cast<int64_t>(C) * (kWindows + 1); i += blockDim.x) sums[i] = 0;
             if (threadIdx.x < kWindows) s_score[threadIdx.x] = 0;
