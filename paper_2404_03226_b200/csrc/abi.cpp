@@ -808,8 +808,9 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         // CTAs that each walk ~G/grid graphs would double the tail); small
         // graphs use small CTAs -- a level of a 1k-task DAG has ~100 nodes
         const int st_threads = d.max_n <= 4096 ? 128 : 512;
-        // in-degrees in shared memory for graphs of <= 2048 tasks (8 KB)
-        const int32_t st_ints = d.max_n < 2048 ? ((d.max_n + 1 + 31) & ~31) : 0;
+        // in-degrees and allocator cursors in shared memory for graphs of
+        // < 2048 tasks (<= 16 KB)
+        const int32_t st_ints = d.max_n < 2048 ? 2 * ((d.max_n + 1 + 31) & ~31) : 0;
         int per_sm = 0;
         cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_structure, st_threads, st_ints * 4),
                    "occupancy");

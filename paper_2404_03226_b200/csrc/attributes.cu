@@ -198,7 +198,9 @@ __device__ void load_costs(const DevCosts* costs_g, int32_t ci, DevCosts& sc, do
 __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* costs_g,
                                                   const int32_t* cost_idx, AttrScratch s,
                                                   int32_t want_rank, int32_t want_large, int32_t smem_ints) {
-    extern __shared__ int32_t s_indeg[];  // [smem_ints]: Kahn's in-degrees when n + 1 fit
+    // [smem_ints]: Kahn's in-degrees (later the slot allocator's counts) in
+    // the first half, the allocator's cursors in the second, when n + 1 fit
+    extern __shared__ int32_t s_indeg[];
     __shared__ DevCosts sc;
     __shared__ double s_mean[kMaxTypes];
     __shared__ int32_t s_tcount[kMaxTypes];
@@ -214,7 +216,9 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
         const int32_t* soff = b.succ_off + t0 + g;
         const int32_t* succ = b.succ + b.edge_base[g];
         const int32_t* type = b.type + t0;
-        int32_t* indeg = n + 1 <= smem_ints ? s_indeg : s.tmp + t0 + g;
+        const bool in_smem = n + 1 <= smem_ints / 2;
+        int32_t* indeg = in_smem ? s_indeg : s.tmp + t0 + g;
+        int32_t* cursors = in_smem ? s_indeg + smem_ints / 2 : s.tmp2 + t0 + g;
         int32_t* order = s.order + t0;
         int32_t* level = s.level + t0;
         int32_t* lstart = s.lstart + t0 + g;
@@ -309,7 +313,7 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
         }
         // ---- live-range slots for the forward sweep (released after the
         //      node's last consumer level)
-        const int32_t P = assign_slots(order, lstart, L, processed, lastuse, false, slot, indeg, s.tmp2 + t0 + g,
+        const int32_t P = assign_slots(order, lstart, L, processed, lastuse, false, slot, indeg, cursors,
                                        s.rel_order + t0, s.fstack + t0, warp_tot);
         // ---- large graphs: inverse order, edge level span, reverse slots for
         //      the bitset closure (released after the node's first consumer)
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
                 firstuse[v] = fu;
             }
             __syncthreads();
-            Pr = assign_slots(order, lstart, L, processed, firstuse, true, s.rslot + t0, indeg, s.tmp2 + t0 + g,
+            Pr = assign_slots(order, lstart, L, processed, firstuse, true, s.rslot + t0, indeg, cursors,
                               s.rel_order + t0, s.fstack + t0, warp_tot);
         }
         // ---- order-major node records for the sweep: slot, GPU time and

@@ -93,7 +93,8 @@ struct AttrOutDev {
 };
 
 __global__ void k_ingest(DevBatch b, int32_t* cursor_scratch, int32_t smem_ints);
-// smem_ints: dynamic shared ints for the in-degree counters (used when n+1 fit)
+// smem_ints: dynamic shared ints, two halves (in-degrees / allocator counts,
+// allocator cursors), used when n+1 fit in a half
 __global__ void k_structure(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
                             int32_t want_rank, int32_t want_large, int32_t smem_ints);
 __global__ void k_structure_large(DevBatch b, const DevCosts* costs, const int32_t* cost_idx, AttrScratch s,
