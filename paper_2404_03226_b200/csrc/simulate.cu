@@ -1020,18 +1020,27 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, SimTaskHdr* hdr, c
                                                    (static_cast<uint32_t>(nsucc) & 0xffffffu)));
             int64_t* inb = reinterpret_cast<int64_t*>(adj + x8);
             int32_t* inh = reinterpret_cast<int32_t*>(inb + nin);
+            int32_t* outl = inh + nin;
+            int32_t* succl = outl + nout;
             const int32_t* in = b.in + ib + i0;
-            for (int32_t k = tl; k < nin; k += TL) {
+            const int32_t* out = b.out + ob + o0;
+            const int32_t* succ = b.succ + eb + s0;
+            {  // first TL entries of every list: all loads issued before any store
+                const int32_t hd = tl < nin ? __ldg(&in[tl]) : 0;
+                const int32_t ov = tl < nout ? __ldg(&out[tl]) : 0;
+                const int32_t sv = tl < nsucc ? succ[tl] : 0;
+                const int64_t by = tl < nin ? __ldg(&b.handle_bytes[hb + hd]) : 0;
+                if (tl < nin) { inh[tl] = hd; inb[tl] = by; }
+                if (tl < nout) outl[tl] = ov;
+                if (tl < nsucc) succl[tl] = sv;
+            }
+            for (int32_t k = tl + TL; k < nin; k += TL) {
                 const int32_t hd = __ldg(&in[k]);
                 inh[k] = hd;
                 inb[k] = __ldg(&b.handle_bytes[hb + hd]);
             }
-            int32_t* outl = inh + nin;
-            const int32_t* out = b.out + ob + o0;
-            for (int32_t k = tl; k < nout; k += TL) outl[k] = __ldg(&out[k]);
-            int32_t* succl = outl + nout;
-            const int32_t* succ = b.succ + eb + s0;
-            for (int32_t k = tl; k < nsucc; k += TL) succl[k] = succ[k];
+            for (int32_t k = tl + TL; k < nout; k += TL) outl[k] = __ldg(&out[k]);
+            for (int32_t k = tl + TL; k < nsucc; k += TL) succl[k] = succ[k];
         }
     }
 }
