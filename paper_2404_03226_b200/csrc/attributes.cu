@@ -87,9 +87,17 @@ __global__ void __launch_bounds__(256) k_ingest(DevBatch b, int32_t* cursor_scra
             block_exclusive_scan_inplace(s_ctr, n + 1, warp_tot);
             for (int32_t i = threadIdx.x; i <= n; i += blockDim.x) soff[i] = s_ctr[i];
             __syncthreads();
-            for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
-                for (int32_t k = __ldg(&doff[v]); k < __ldg(&doff[v + 1]); ++k)
-                    succ[atomicAdd(&s_ctr[__ldg(&dep[k])], 1)] = v;
+            for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
+                const int32_t k1 = __ldg(&doff[v + 1]);
+                for (int32_t k = __ldg(&doff[v]); k < k1; k += 4) {  // four dep ids ahead of the stores
+                    int32_t d[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) d[q] = k + q < k1 ? __ldg(&dep[k + q]) : -1;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (d[q] >= 0) succ[atomicAdd(&s_ctr[d[q]], 1)] = v;
+                }
+            }
             __syncthreads();
             // s_ctr[u] is now the end of u's list
             for (int32_t u = threadIdx.x; u < n; u += blockDim.x) {
