@@ -40,6 +40,17 @@ namespace tbsim_dev {
 // ------------------------------------------------------------------ ingest
 
 __device__ void sort_small(int32_t* a, int32_t len) {
+    if (len <= 32) {  // in a thread-local copy (L1-resident) instead of in place in HBM
+        int32_t loc[32];
+        for (int32_t i = 0; i < len; ++i) {
+            const int32_t x = a[i];
+            int32_t j = i - 1;
+            while (j >= 0 && loc[j] > x) { loc[j + 1] = loc[j]; --j; }
+            loc[j + 1] = x;
+        }
+        for (int32_t i = 0; i < len; ++i) a[i] = loc[i];
+        return;
+    }
     if (len <= 48) {
         for (int32_t i = 1; i < len; ++i) {
             int32_t x = a[i], j = i - 1;
