@@ -1442,9 +1442,12 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
     __shared__ int32_t warp_tot[32];
     __shared__ int64_t carry;
     __shared__ int32_t all_fp32;
+    __shared__ int32_t n_wide;
+    __shared__ int64_t wide[1024];  // graphs of this chunk with > 64 tiles (written by warps)
     if (threadIdx.x == 0) {
         carry = 0;
         all_fp32 = 1;
+        n_wide = 0;
     }
     __syncthreads();
     for (int64_t base = 0; base < b.G; base += blockDim.x) {
@@ -1482,17 +1485,28 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
         const int32_t inc = block_inclusive_scan(tiles, warp_tot, &tot);
         const int64_t tb = carry + inc - tiles;
         if (g < b.G) s.tile_base[g] = tb;
+        // tile -> graph: a graph of <= 64 tiles by its own thread, wider
+        // ones by a warp each (listed here)
+        if (g < b.G) {
+            if (tiles <= 64) {
+                for (int32_t t = 0; t < tiles; ++t) s.tile_graph[tb + t] = static_cast<int32_t>(g);
+            } else {
+                wide[atomicAdd(&n_wide, 1)] = g;
+            }
+        }
         __syncthreads();
         if (threadIdx.x == 0) carry += tot;
-        __syncthreads();
-        // tile -> graph: a warp per graph of this chunk, lanes over its tiles
         const int lane = threadIdx.x & 31;
-        for (int64_t gg = base + (threadIdx.x >> 5); gg < b.G && gg < base + static_cast<int64_t>(blockDim.x); gg += blockDim.x >> 5) {
+        for (int32_t w = threadIdx.x >> 5; w < n_wide; w += blockDim.x >> 5) {
+            const int64_t gg = wide[w];
             const int64_t t_begin = s.tile_base[gg];
             const int32_t sw = s.tile_s[gg] & kTileWidthMask;
             const int32_t nt = (s.info[gg].processed + sw - 1) / sw;
             for (int32_t t = lane; t < nt; t += 32) s.tile_graph[t_begin + t] = static_cast<int32_t>(gg);
         }
+        __syncthreads();
+        if (threadIdx.x == 0) n_wide = 0;
+        __syncthreads();
     }
     if (threadIdx.x == 0) {
         s.tile_base[b.G] = carry;
