@@ -187,3 +187,77 @@ class BenchSet:
 
 def max_threads() -> int:
     return lib().ref_max_threads()
+
+
+# ---- C4 scale (oracle/ref_c4.cpp -> _ref/libtbsim_ref_c4.so) --------------
+
+C4_LIB_PATH = os.path.join(HERE, "_ref", "libtbsim_ref_c4.so")
+_lib_c4 = None
+
+
+def lib_c4():
+    global _lib_c4
+    if _lib_c4 is None:
+        if not os.path.exists(C4_LIB_PATH):
+            raise RuntimeError(f"reference library missing: {C4_LIB_PATH} (make -C oracle ref)")
+        L = C.CDLL(C4_LIB_PATH)
+        vp = C.c_void_p
+        L.ref_c4_last_error.restype = C.c_char_p
+        L.ref_c4_load.restype = vp
+        L.ref_c4_load.argtypes = [vp, vp, vp]
+        L.ref_c4_free.argtypes = [vp]
+        L.ref_c4_structure.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp, vp]
+        L.ref_c4_efficiency_sample.argtypes = [vp, vp, C.c_int64, vp, C.c_int, C.c_int, vp, vp]
+        _lib_c4 = L
+    return _lib_c4
+
+
+class C4Ref:
+    """One large graph (graph 0 of `batch`) held by the reference as a
+    TaskGraph: its public attribute API in full, and its internal per-source
+    efficiency_of (src/attributes.cpp:110-137) on sampled sources."""
+
+    def __init__(self, batch: GraphBatch, costs):
+        L = lib_c4()
+        c, self._keep = outbuf.costs_struct(costs, batch.type_names)
+        self._names = _names(batch)
+        self.n = batch.sizes(0)
+        self.h = L.ref_c4_load(C.addressof(batch.desc()), C.addressof(self._names), C.addressof(c))
+        if not self.h:
+            raise RefError(abi.TBSIM_E_RUNTIME, L.ref_c4_last_error().decode())
+
+    def _chk(self, status):
+        if status:
+            raise RefError(status, lib_c4().ref_c4_last_error().decode())
+
+    def structure(self, threads=0, ability=True, rank=True, depth=True, layers=True):
+        n = self.n
+        out = {"ability": np.zeros(n, np.int64) if ability else None,
+               "static_priority": np.zeros(n, np.int64) if rank else None,
+               "depth": np.zeros(n, np.int64) if depth else None,
+               "layer": np.zeros(n, np.int32) if layers else None}
+        w0 = C.c_double()
+        sec = np.zeros(4)
+        ptr = lambda a: None if a is None else a.ctypes.data
+        self._chk(lib_c4().ref_c4_structure(self.h, threads, ptr(out["ability"]), ptr(out["static_priority"]),
+                                            ptr(out["depth"]), ptr(out["layer"]), C.addressof(w0), sec.ctypes.data))
+        out["w0_ms"] = w0.value
+        out["seconds"] = dict(zip(("ability", "rank", "depth", "layers"), sec.tolist()))
+        return out
+
+    def efficiency_sample(self, sources, windows, threads=0):
+        """out[i, k] = efficiency_of(sources[i], windows[k]); (out, setup_s, calls_s)."""
+        src = np.ascontiguousarray(sources, np.int64)
+        w = np.ascontiguousarray(windows, np.float64)
+        out = np.zeros((len(src), len(w)), np.int64)
+        sec = np.zeros(2)
+        self._chk(lib_c4().ref_c4_efficiency_sample(self.h, src.ctypes.data, len(src), w.ctypes.data, len(w),
+                                                    threads, out.ctypes.data, sec.ctypes.data))
+        return out, float(sec[0]), float(sec[1])
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib_c4().ref_c4_free(C.c_void_p(self.h))
+        except Exception:
+            pass

@@ -748,13 +748,13 @@ AttrScratch alloc_attr_scratch(tbsim_ctx* ctx, const DevBatch& d) {
     s.om_poff = ctx->buf("a_ompoff").as<int32_t>(T + G);
     s.om_pslot = ctx->buf("a_ompslot").as<int32_t>(E);
     s.rank = ctx->buf("a_rank").as<double>(T);
-    s.hist = ctx->buf("a_hist").as<uint64_t>(4 * T);
+    s.hist = ctx->buf("a_hist").as<uint32_t>(static_cast<int64_t>(kBins) * T);
     s.info = ctx->buf("a_info").as<GraphInfo>(G);
     s.median = ctx->buf("a_median").as<double>(G);
     s.tile_base = ctx->buf("a_tilebase").as<int64_t>(G + 1);
     s.tile_s = ctx->buf("a_tiles").as<int32_t>(G);
     s.tile_graph = ctx->buf("a_tilegraph").as<int32_t>(T / 8 + G + 1);
-    s.plan_fp32 = ctx->buf("a_planfp32").as<int32_t>(1);
+    s.plan_fp32 = ctx->buf("a_planfp32").as<int32_t>(2);
     s.opos = ctx->buf("a_opos").as<int32_t>(T);
     s.firstuse = ctx->buf("a_firstuse").as<int32_t>(T);
     s.rslot = ctx->buf("a_rslot").as<int32_t>(T);
@@ -786,6 +786,14 @@ void launch_structure_large(tbsim_ctx* ctx, const DevBatch& d, const DevCosts* d
     cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_structure_large), grid, 512, args, 0, ctx->stream),
                "cudaLaunchCooperativeKernel(k_structure_large)");
     ctx->end("k_structure");
+}
+
+// CTAs of a sweep whose tiles use per-CTA global windows (stride doubles
+// each): one per SM while the windows total <= 8 GB, fewer for very wide
+// graphs (the tile queue is persistent, any grid is correct)
+int gwin_grid(const tbsim_ctx* ctx, int64_t stride) {
+    const int64_t budget = (8LL << 30) / 8;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->n_sms, budget / std::max<int64_t>(stride, 1))));
 }
 
 // Launch the whole attribute pipeline on a device batch.  Returns with the
@@ -825,9 +833,16 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         GraphInfo gi;
         cuda_check(cudaMemcpyAsync(&gi, run.s.info, sizeof gi, cudaMemcpyDeviceToHost, ctx->stream), "D2H info");
         ctx->sync();
-        if (gi.processed == d.max_n) {  // acyclic: otherwise the error path reports it
-            const int64_t nw = (static_cast<int64_t>(d.max_n) + 63) / 64;
-            uint64_t* sets = ctx->buf("a_sets").as<uint64_t>(static_cast<size_t>(std::max(gi.peak_rslots, 1)) * nw);
+        const int64_t nw = (static_cast<int64_t>(d.max_n) + 63) / 64;
+        const size_t need = static_cast<size_t>(std::max(gi.peak_rslots, 1)) * static_cast<size_t>(nw) * 8;
+        size_t free_b = 0, total_b = 0;
+        cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        // the closure keeps one full-width set per live slot: a graph with a
+        // very wide level cut (e.g. millions of sinks under one root) does
+        // not fit, and its ability comes from the unpruned sweep instead
+        const bool fits = need <= (free_b + ctx->buf("a_sets").bytes) / 2;
+        if (gi.processed == d.max_n && fits) {  // acyclic: otherwise the error path reports it
+            uint64_t* sets = ctx->buf("a_sets").as<uint64_t>(need / 8);
             cuda_check(cudaMemsetAsync(o.ability, 0, static_cast<size_t>(d.T) * 8, ctx->stream), "memset ability");
             int per_sm = 0;
             cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_closure<4>, 256, 0), "occupancy");
@@ -845,19 +860,28 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
             ability_done = true;
         }
     }
-    if (do_sweep && !(large && sweep_mode == SWEEP_ABILITY)) {
+    // the large-graph sweep prunes at the largest window unless it must
+    // count every descendant (ability requested and not from the closure)
+    const bool prune = large && (ability_done || !o.ability);
+    if (do_sweep && !(ability_done && sweep_mode == SWEEP_ABILITY)) {
         const int64_t smem = sweep_smem_bytes(ctx);
         ctx->begin("k_tile_plan");
         k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, run.s, smem, ctx->sweep_tile, d_costs, d_cost_idx, sweep_mode);
         ctx->end("k_tile_plan");
-        // graphs whose distance window exceeds shared memory use a global
-        // window; size it from the worst case (every node live)
+        // graphs whose distance window exceeds shared memory (P live slots x
+        // 32 FP64 columns per CTA in HBM): k_tile_plan reports the largest P
         int64_t gwin_stride = 0;
         double* gwin = nullptr;
-        const int sweep_grid = ctx->n_sms;  // one 512-thread CTA per SM (smem bound)
+        int sweep_grid = ctx->n_sms;  // one 512-thread CTA per SM (smem bound)
         if (static_cast<int64_t>(d.max_n) * 8 * 8 > smem) {
-            gwin_stride = static_cast<int64_t>(d.max_n) * 32;
-            gwin = ctx->buf("a_gwin").as<double>(gwin_stride * sweep_grid);
+            int32_t pmax = 0;
+            cuda_check(cudaMemcpyAsync(&pmax, run.s.plan_fp32 + 1, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H plan");
+            ctx->sync();
+            if (pmax > 0) {
+                gwin_stride = static_cast<int64_t>(pmax) * 32;
+                sweep_grid = gwin_grid(ctx, gwin_stride);
+                gwin = ctx->buf("a_gwin").as<double>(gwin_stride * sweep_grid);
+            }
         }
         unsigned long long* counter = ctx->buf("a_counter").as<unsigned long long>(1);
         cuda_check(cudaMemsetAsync(counter, 0, 8, ctx->stream), "memset");
@@ -886,13 +910,13 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         ctx->begin("k_sweep");
         k_sweep<<<sweep_grid, kSweepThreads, smem, ctx->stream>>>(d, d_costs, d_cost_idx, run.s, sweep_mode, d_unit_time,
                                                                   total_tiles, counter, smem, gwin, gwin_stride,
-                                                                  large ? 1 : 0, relax_ctr);
-        k_sweep_fp32<<<sweep_grid, 1024, smem, ctx->stream>>>(d, run.s, sweep_mode, d_unit_time, counter, large ? 1 : 0,
+                                                                  prune ? 1 : 0, relax_ctr);
+        k_sweep_fp32<<<sweep_grid, 1024, smem, ctx->stream>>>(d, run.s, sweep_mode, d_unit_time, counter, prune ? 1 : 0,
                                                                relax_ctr);
         ctx->end("k_sweep");
         const int64_t cls_stride = static_cast<int64_t>(d.max_n) * (3 * kWindows + 1) + 16;
         int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride * grid_g);
-        const int32_t write_ab = (large || ability_done) ? 0 : 1;
+        const int32_t write_ab = (prune || ability_done) ? 0 : 1;
         if (G == 1 && d.max_n >= ctx->large_threshold) {
             static int per_sm = 0;
             if (!per_sm)
@@ -1136,10 +1160,11 @@ extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbs
         // ---- efficiency sweep over this rank's share of the source tiles
         const int64_t smem = sweep_smem_bytes(ctx);
         k_tile_plan<<<1, 1024, 0, ctx->stream>>>(d, s, smem, ctx->sweep_tile, d_costs, nullptr, SWEEP_CALIBRATE);
-        int32_t S = 0;
+        int32_t S = 0, pmax = 0;
         int64_t tiles = 0;
         cuda_check(cudaMemcpyAsync(&S, s.tile_s, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H tile width");
         cuda_check(cudaMemcpyAsync(&tiles, s.tile_base + 1, 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H tiles");
+        cuda_check(cudaMemcpyAsync(&pmax, s.plan_fp32 + 1, 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H plan");
         ctx->sync();
         S &= kTileWidthMask;
         const int64_t t_lo = tiles * rank / world, t_hi = tiles * (rank + 1) / world;
@@ -1148,9 +1173,11 @@ extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbs
         if (t_hi > t_lo) {
             int64_t gwin_stride = 0;
             double* gwin = nullptr;
-            if (n * 8 * 8 > smem) {
-                gwin_stride = n * 32;
-                gwin = ctx->buf("a_gwin").as<double>(gwin_stride * ctx->n_sms);
+            int sweep_grid = ctx->n_sms;
+            if (pmax > 0) {  // global-window tiles (P x 32 FP64 per CTA)
+                gwin_stride = static_cast<int64_t>(pmax) * 32;
+                sweep_grid = gwin_grid(ctx, gwin_stride);
+                gwin = ctx->buf("a_gwin").as<double>(gwin_stride * sweep_grid);
             }
             unsigned long long* counter = ctx->buf("a_counter").as<unsigned long long>(1);
             const unsigned long long start = static_cast<unsigned long long>(t_lo);
@@ -1158,7 +1185,7 @@ extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbs
             cuda_check(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                        "cudaFuncSetAttribute(k_sweep)");
             ctx->begin("k_sweep");
-            k_sweep<<<ctx->n_sms, kSweepThreads, smem, ctx->stream>>>(d, d_costs, nullptr, s, SWEEP_CALIBRATE, nullptr,
+            k_sweep<<<sweep_grid, kSweepThreads, smem, ctx->stream>>>(d, d_costs, nullptr, s, SWEEP_CALIBRATE, nullptr,
                                                                       t_hi, counter, smem, gwin, gwin_stride, 1, nullptr);
             ctx->end("k_sweep");
         }

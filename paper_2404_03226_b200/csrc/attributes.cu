@@ -801,25 +801,6 @@ __device__ __forceinline__ int bin_of(double d, const Thresholds& th) {
     return k;
 }
 
-__device__ __forceinline__ void bump(uint64_t (&h)[4], int bin) {
-    // 12 counters of 21 bits, three per word
-    const int w = bin / 3;
-    const uint64_t inc = 1ull << (21 * (bin - 3 * w));
-    h[0] += w == 0 ? inc : 0ull;
-    h[1] += w == 1 ? inc : 0ull;
-    h[2] += w == 2 ? inc : 0ull;
-    h[3] += w == 3 ? inc : 0ull;
-}
-
-// 12 counters of 16 bits, four per word (per-tile counts < 2^16: n < 65536)
-__device__ __forceinline__ void bump16(uint64_t (&h)[3], int bin) {
-    const int w = bin >> 2;
-    const uint64_t inc = 1ull << (16 * (bin & 3));
-    h[0] += w == 0 ? inc : 0ull;
-    h[1] += w == 1 ? inc : 0ull;
-    h[2] += w == 2 ? inc : 0ull;
-}
-
 __device__ Thresholds make_thresholds(int32_t mode_req, double w0_or_unit) {
     Thresholds th;
     th.w0bits32 = 0;
@@ -895,6 +876,18 @@ __device__ __forceinline__ uint64_t shl64(uint64_t x, uint32_t sh) {
     uint64_t r;
     asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(sh));
     return r;
+}
+
+// a tile's per-source window-bin counts (s_hist[src * kBins + bin]) to the
+// task-indexed scratch read by k_finalize: 12 x uint32 per task, three
+// 16-byte stores per source (counts up to n - 1 < 2^24: no packing limit)
+__device__ __forceinline__ void store_bins(const AttrScratch& s, int64_t t0, const int32_t* order, int32_t nsrc,
+                                           const uint32_t* s_hist, int tid, int nthr) {
+    for (int i = tid; i < nsrc * (kBins / 4); i += nthr) {
+        const int32_t q = i / (kBins / 4), k = i - q * (kBins / 4);
+        reinterpret_cast<uint4*>(s.hist + (t0 + order[q]) * kBins)[k] =
+            reinterpret_cast<const uint4*>(s_hist + q * kBins)[k];
+    }
 }
 
 // Final flush of a tile's packed counters without shared atomics.  The
@@ -1104,13 +1097,7 @@ __device__ __forceinline__ void sweep_tile(const DevBatch& b, const AttrScratch&
     __syncthreads();
     if (relax_ctr && threadIdx.x == 0)  // [0]: FP64 windows, [1]: FP32
         atomicAdd(relax_ctr + (sizeof(T) == 4 ? 1 : 0), static_cast<unsigned long long>(nrel * S));
-    // per source: 12 bins as 21-bit fields in four words (k_finalize)
-    const int32_t* order = s.order + t0;
-    for (int i = threadIdx.x; i < nsrc * 4; i += blockDim.x) {
-        const uint32_t* c = s_hist + (i >> 2) * kBins + 3 * (i & 3);
-        s.hist[(t0 + order[first + (i >> 2)]) * 4 + (i & 3)] =
-            static_cast<uint64_t>(c[0]) | (static_cast<uint64_t>(c[1]) << 21) | (static_cast<uint64_t>(c[2]) << 42);
-    }
+    store_bins(s, t0, s.order + t0 + first, nsrc, s_hist, threadIdx.x, blockDim.x);
 }
 
 // FP32 windows run only in modes 0 and 2 (k_tile_plan never picks them for
@@ -1291,12 +1278,7 @@ __device__ __forceinline__ void sweep_tile_rows(const DevBatch& b, const AttrScr
     __syncthreads();
     if (relax_ctr && tid == 0)  // [0]: FP64 windows, [1]: FP32
         atomicAdd(relax_ctr + (sizeof(T) == 4 ? 1 : 0), static_cast<unsigned long long>(nrel * S));
-    const int32_t* order = s.order + t0;
-    for (int i = tid; i < nsrc * 4; i += nthr) {
-        const uint32_t* c = s_hist + (i >> 2) * kBins + 3 * (i & 3);
-        s.hist[(t0 + order[first + (i >> 2)]) * 4 + (i & 3)] =
-            static_cast<uint64_t>(c[0]) | (static_cast<uint64_t>(c[1]) << 21) | (static_cast<uint64_t>(c[2]) << 42);
-    }
+    store_bins(s, t0, s.order + t0 + first, nsrc, s_hist, tid, nthr);
 }
 
 template <int S, int GL, typename T = double>
@@ -1317,7 +1299,7 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_fp32(DevBatch b, AttrScratch 
                                                        const double* unit_time, unsigned long long* work_counter,
                                                        int32_t prune, unsigned long long* relax_ctr) {
     __shared__ int64_t s_item[2];
-    __shared__ uint32_t s_hist[kMaxTile * kBins];
+    __shared__ __align__(16) uint32_t s_hist[kMaxTile * kBins];
     if (!*s.plan_fp32) return;
     const int64_t total_tiles = s.tile_base[b.G];
     if (threadIdx.x == 0) s_item[0] = atomicAdd(work_counter, 1ull);
@@ -1352,7 +1334,7 @@ __global__ void __launch_bounds__(512) k_sweep(DevBatch b, const DevCosts* costs
                                               int64_t smem_bytes, double* gwin, int64_t gwin_stride,
                                               int32_t prune, unsigned long long* relax_ctr) {
     __shared__ int64_t s_item[2];
-    __shared__ uint32_t s_hist[kMaxTile * kBins];
+    __shared__ __align__(16) uint32_t s_hist[kMaxTile * kBins];
     (void)costs_g;
     (void)cost_idx;
     if (total_tiles < 0) {  // whole-batch launch: k_sweep_fp32 takes all-FP32 plans
@@ -1448,6 +1430,7 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
         carry = 0;
         all_fp32 = 1;
         n_wide = 0;
+        s.plan_fp32[1] = 0;
     }
     __syncthreads();
     for (int64_t base = 0; base < b.G; base += blockDim.x) {
@@ -1477,6 +1460,8 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
             else { S = 32; f32 = false; }  // global-memory window (FP64)
             if (S == 256 && !f32) S = 128;  // 256 columns only as FP32
             if (static_cast<int64_t>(P) * S * (f32 ? 4 : 8) > smem_bytes) { S = 32; f32 = false; }  // forced, too wide
+            // global-window graphs: the host sizes the per-CTA window (P x 32)
+            if (static_cast<int64_t>(P) * S * (f32 ? 4 : 8) > smem_bytes) atomicMax(s.plan_fp32 + 1, P);
             s.tile_s[g] = S | (f32 ? kTileF32 : 0);
             if (!f32 || S < 32) atomicAnd(&all_fp32, 0);
             tiles = (gi.processed + S - 1) / S;
@@ -1516,8 +1501,14 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
 
 // ---------------------------------------------------------------- finalize
 
-__device__ __forceinline__ int64_t field(const uint64_t* h, int bin) {
-    return static_cast<int64_t>((h[bin / 3] >> (21 * (bin % 3))) & ((1ull << 21) - 1));
+// a source's 12 window-bin counts (kBins uint32, 48 B, 16-B aligned)
+__device__ __forceinline__ void load_bins(const uint32_t* h, uint32_t (&c)[kBins]) {
+    const uint4* h4 = reinterpret_cast<const uint4*>(h);
+#pragma unroll
+    for (int q = 0; q < kBins / 4; ++q) {
+        const uint4 w = h4[q];
+        c[4 * q] = w.x; c[4 * q + 1] = w.y; c[4 * q + 2] = w.z; c[4 * q + 3] = w.w;
+    }
 }
 
 __device__ int64_t gcd64(int64_t a, int64_t b) {
@@ -1541,7 +1532,7 @@ __global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int
         const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
         const GraphInfo gi = s.info[g];
         if (gi.processed != n) continue;
-        const uint64_t* hist = s.hist + t0 * 4;
+        const uint32_t* hist = s.hist + t0 * kBins;
         int best = 0;
         if (sweep_mode == SWEEP_CALIBRATE) {
             const int32_t C = gi.n_classes;
@@ -1552,10 +1543,12 @@ __global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int
             __syncthreads();
             for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
                 const int32_t c = s.cls[t0 + v];
-                const uint64_t* h = hist + static_cast<int64_t>(v) * 4;
+                uint32_t f[kBins];
+                load_bins(hist + static_cast<int64_t>(v) * kBins, f);
                 int64_t acc = 0;
+#pragma unroll
                 for (int k = 0; k < kWindows; ++k) {
-                    acc += field(h, k);
+                    acc += f[k];
                     if (acc) atomicAdd(reinterpret_cast<unsigned long long*>(&sums[static_cast<int64_t>(c) * kWindows + k]),
                                        static_cast<unsigned long long>(acc));
                 }
@@ -1598,12 +1591,13 @@ __global__ void __launch_bounds__(256) k_finalize(DevBatch b, AttrScratch s, int
             }
         }
         for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
-            const uint64_t* h = hist + static_cast<int64_t>(v) * 4;
+            uint32_t f[kBins];
+            load_bins(hist + static_cast<int64_t>(v) * kBins, f);
             int64_t eff = 0, abil = 0;
+#pragma unroll
             for (int k = 0; k < kBins; ++k) {
-                const int64_t f = field(h, k);
-                if (k <= best) eff += f;
-                abil += f;
+                if (k <= best) eff += f[k];
+                abil += f[k];
             }
             if (o.efficiency && sweep_mode != SWEEP_ABILITY) o.efficiency[t0 + v] = eff;
             if (o.ability && write_ability) o.ability[t0 + v] = abil;
@@ -1635,7 +1629,7 @@ __global__ void __launch_bounds__(512) k_finalize_large(DevBatch b, AttrScratch 
     const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
     const GraphInfo gi = s.info[g];
     if (gi.processed != n) return;  // uniform: cyclic graphs are reported by the host
-    const uint64_t* hist = s.hist + t0 * 4;
+    const uint32_t* hist = s.hist + t0 * kBins;
     int best = 0;
     if (sweep_mode == SWEEP_CALIBRATE) {
         const int64_t C = gi.n_classes;
@@ -1654,10 +1648,12 @@ __global__ void __launch_bounds__(512) k_finalize_large(DevBatch b, AttrScratch 
             for (int64_t i = pos_lo + gtid; i < pos_hi; i += gthreads) {
                 const int64_t v = s.order[t0 + i];
                 const int32_t c = s.cls[t0 + v];
-                const uint64_t* h = hist + v * 4;
+                uint32_t f[kBins];
+                load_bins(hist + v * kBins, f);
                 int64_t acc = 0;
+#pragma unroll
                 for (int k = 0; k < kWindows; ++k) {
-                    acc += field(h, k);
+                    acc += f[k];
                     if (acc)
                         atomicAdd(reinterpret_cast<unsigned long long*>(&sums[static_cast<int64_t>(c) * kWindows + k]),
                                   static_cast<unsigned long long>(acc));
@@ -1709,12 +1705,13 @@ __global__ void __launch_bounds__(512) k_finalize_large(DevBatch b, AttrScratch 
     }
     for (int64_t i = pos_lo + gtid; i < pos_hi; i += gthreads) {
         const int64_t v = s.order[t0 + i];
-        const uint64_t* h = hist + v * 4;
+        uint32_t f[kBins];
+        load_bins(hist + v * kBins, f);
         int64_t eff = 0, abil = 0;
+#pragma unroll
         for (int k = 0; k < kBins; ++k) {
-            const int64_t f = field(h, k);
-            if (k <= best) eff += f;
-            abil += f;
+            if (k <= best) eff += f[k];
+            abil += f[k];
         }
         if (o.efficiency && sweep_mode != SWEEP_ABILITY) o.efficiency[t0 + v] = eff;
         if (o.ability && write_ability) o.ability[t0 + v] = abil;

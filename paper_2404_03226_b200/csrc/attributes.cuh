@@ -55,13 +55,13 @@ struct AttrScratch {
     int32_t* om_poff;    // [T+G] order-major CSR offsets of predecessor slots
     int32_t* om_pslot;   // [E]   order-major predecessor slots
     double* rank;        // [T]
-    uint64_t* hist;      // [4T] packed 12 x 21-bit window bins per source
+    uint32_t* hist;      // [12T] window-bin counts per source (kBins x uint32, 16-B aligned rows)
     GraphInfo* info;     // [G]
     double* median;      // [G] lower-median GPU time (regulator defaults)
     int64_t* tile_base;  // [G+1]
     int32_t* tile_s;     // [G]
     int32_t* tile_graph; // [tiles] graph of each sweep tile (<= T/8 + G)
-    int32_t* plan_fp32;  // [1] every tile is an FP32-exact shape k_sweep_fp32 runs
+    int32_t* plan_fp32;  // [2] every tile is an FP32-exact shape k_sweep_fp32 runs; max P of global-window graphs
 };
 
 // Grid-wide counters of k_structure_large (zeroed before the launch),

@@ -34,3 +34,60 @@ def all_gather_results(dist, makespans, workers):
         dist.all_gather(list(ms_out.chunk(world)), makespans)
         dist.all_gather(list(w_out.chunk(world)), workers)
     return ms_out, w_out
+
+
+RESULT_KEYS = ("makespan_ms", "worker", "start_ms", "end_ms")
+
+
+def init_process_group(local: int):
+    """One process per GPU over NCCL.  TBSIM_DIST_BACKEND=gloo selects gloo
+    (the single-GPU multi-process test runs two ranks on one device, which
+    NCCL refuses); returns torch.distributed."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+    backend = os.environ.get("TBSIM_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    return dist
+
+
+def allreduce_max(dist, x: float, device) -> float:
+    """Max over ranks of a host float (CUDA tensor under NCCL, CPU under gloo)."""
+    import torch
+    dev = device if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class AssignmentGather:
+    """The north star's final all-gather: every rank's makespans [G] and
+    per-task assignments (worker int32, start/end FP64 [T]) onto every GPU,
+    in rank order.  Under NCCL the collectives run on the
+    device with no host round trip (async_op=True lets a copy stream wait for
+    them while the compute stream moves on); under gloo (tests) the tensors
+    go through host memory."""
+
+    def __init__(self, dist, local: dict):
+        import torch
+        self.dist = dist
+        self.world = dist.get_world_size()
+        self.nccl = dist.get_backend() == "nccl"
+        self.out = {k: torch.empty(self.world * local[k].numel(), dtype=local[k].dtype, device=local[k].device)
+                    for k in RESULT_KEYS if k in local}
+
+    def __call__(self, local: dict, async_op: bool = False):
+        import torch
+        if self.nccl:
+            works = [self.dist.all_gather_into_tensor(self.out[k], local[k], async_op=async_op) for k in self.out]
+            return [w for w in works if w is not None]
+        for k in self.out:
+            src = local[k].cpu()
+            parts = [torch.empty_like(src) for _ in range(self.world)]
+            self.dist.all_gather(parts, src)
+            self.out[k].copy_(torch.cat(parts))
+        return []

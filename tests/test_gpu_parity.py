@@ -569,3 +569,42 @@ def test_c5_one_percent_sample_matches_the_reference(ctx):
         eq(r["attr_" + k], ra[k], k)
     for k in ("worker", "start_ms", "end_ms", "makespan_ms"):
         eq(r[k], rs[k], k)
+
+
+def _star_batch(m):
+    """Root (LAYERK3) -> m UNIT leaves, built as CSR directly."""
+    n = m + 1
+    z = lambda k: np.zeros(k, np.int64)
+    dep_off = np.concatenate([[0], np.arange(0, m + 1)]).astype(np.int32)
+    type_ = np.full(n, P.TYPE_ID["UNIT"], np.int32)
+    type_[0] = P.TYPE_ID["LAYERK3"]
+    return GraphBatch([0, n], [0, m], [0, 0], [0, 0], [0, 0], dep_off, np.zeros(m, np.int32),
+                      np.zeros(n + 1, np.int32), np.zeros(0, np.int32), np.zeros(n + 1, np.int32),
+                      np.zeros(0, np.int32), type_, z(0), P.TYPE_NAMES)
+
+
+@pytest.mark.parametrize("path", ["large", "batched"])
+def test_window_bins_hold_more_than_2_21_descendants(ctx, path):
+    """A source with more than 2^21 descendants in ONE calibration window bin
+    (a 2^21+1000-leaf star: every leaf at distance 1.0 = W_3).  The bins were
+    21-bit fields in round 1 (ADVICE: silent carry into the next bin); they
+    are 32-bit counters now.  Expected values are analytic: w0 = 2 (lower
+    median 1), windows 2^(k-3); the root counts m leaves from W = 1 on, so
+    the score is 1 below k = 3 and 2 from k = 3 (strict > keeps W = 1)."""
+    m = (1 << 21) + 1000
+    b = _star_batch(m)
+    db = ctx.upload(b)
+    costs = P.default_cost_table()
+    ctx.set_large_graph_threshold(65536 if path == "large" else 1 << 30)
+    try:
+        a = ctx.attributes(db, costs, abi.ATTR_ALL)
+        c = ctx.attributes(db, costs, abi.ATTR_CALIBRATE)
+        e = ctx.attributes(db, costs, abi.ATTR_EFFICIENCY, unit_time=[64.0])
+    finally:
+        ctx.set_large_graph_threshold(65536)
+    assert a["ability"][0] == m and not a["ability"][1:].any()
+    assert a["efficiency"][0] == m and not a["efficiency"][1:].any()
+    assert a["unit_time_ms"][0] == 1.0
+    assert (c["w0_ms"][0], c["best_score"][0], c["w0_score"][0], c["evaluations"][0]) == (2.0, 2, 2, 11)
+    assert e["efficiency"][0] == m
+    assert a["static_priority"][0] == 15000 and (a["static_priority"][1:] == 1000).all()
