@@ -35,6 +35,7 @@ CXX_SRCS = ["hostbatch.cpp"]
 API_SRCS = ["api/taskgraph.cpp", "api/platform.cpp", "api/device.cpp", "api/attributes.cpp",
             "api/policies.cpp", "api/engine.cpp", "api/bench.cpp", "api/text.cpp"]
 API_OUT = os.path.join(HERE, "libtbsim_cpp.so")
+CLI_OUT = os.path.join(HERE, "tbsim")
 
 
 def _host_cxx():
@@ -111,6 +112,14 @@ def build(verbose: bool = False) -> str:
         # generators (tbsim_host::gen_*) and the C-ABI come from libtbsim_b200.so
         cmd = [cxx, "-shared", "-o", API_OUT] + api_objs + ["-L" + HERE, "-ltbsim_b200", "-Wl,-rpath,$ORIGIN",
                                                             "-lpthread"]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.check_call(cmd)
+    # the command-line front end (tools/main.cpp's twin) over the C++ API
+    cli_src = os.path.join(CSRC, "cli", "main.cpp")
+    if _stale(CLI_OUT, [cli_src, API_OUT] + api_hdrs):
+        cmd = [cxx, "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), cli_src, "-o", CLI_OUT,
+               "-L" + HERE, "-ltbsim_cpp", "-ltbsim_b200", "-Wl,-rpath,$ORIGIN", "-lpthread"]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

@@ -134,8 +134,13 @@ struct tbsim_ctx {
         int32_t rank = -1, world = 0;
         int32_t pos_lo = 0, pos_hi = 0;
         int64_t n_words = 0;
+        uint64_t gen = 0;  // scratch generation of the partial call
         AttrScratch s{};
     } shard;
+    // bumped by every attribute-scratch allocation: a shard finish must
+    // directly follow its partial call (no other attribute pass in between
+    // reusing or regrowing the scratch it reads)
+    uint64_t scratch_gen = 0;
     unsigned long long* relax_ctr = nullptr;  // device counter of the last timed sweep
     int64_t last_relax[2] = {0, 0};  // FP64-window, FP32-window relaxations
 
@@ -222,7 +227,8 @@ struct tbsim_batch {
     void* mem3 = nullptr;
     size_t mem3_bytes = 0;
     tbsim_dev::SimTaskHdr* hdr = nullptr;
-    char* adj = nullptr;
+    int64_t* dict = nullptr;  // [kByteClasses] handle-size dictionary (k_bytes_dict)
+    int32_t* adj = nullptr;
 };
 
 namespace {
@@ -241,16 +247,29 @@ void ensure_packed(tbsim_ctx* ctx, tbsim_batch* b) {
     const DevBatch& d = b->d;
     if (b->hdr || d.T == 0) return;
     const int64_t adj_bytes = sim_adj_bytes(d.T, d.I, d.O, d.E);
-    if (adj_bytes >= (int64_t(1) << 35)) raise(TBSIM_E_INVALID_ARGUMENT, "batch too large for the packed simulation graph");
+    if (adj_bytes >= (int64_t(1) << 34)) raise(TBSIM_E_INVALID_ARGUMENT, "batch too large for the packed simulation graph");
+    if (d.max_h > kHandleMask) raise(TBSIM_E_INVALID_ARGUMENT, "graph exceeds 2^28 handles for the simulator");
     const size_t hdr_bytes = static_cast<size_t>(d.T) * sizeof(SimTaskHdr);
-    b->mem3 = ctx->batch_alloc(hdr_bytes + static_cast<size_t>(adj_bytes) + 256, &b->mem3_bytes);
+    const size_t dict_at = (hdr_bytes + 255) & ~size_t(255), adj_at = dict_at + 256;
+    b->mem3 = ctx->batch_alloc(adj_at + static_cast<size_t>(adj_bytes) + 256, &b->mem3_bytes);
     b->hdr = static_cast<SimTaskHdr*>(b->mem3);
-    b->adj = static_cast<char*>(b->mem3) + ((hdr_bytes + 255) & ~size_t(255));
+    b->dict = reinterpret_cast<int64_t*>(static_cast<char*>(b->mem3) + dict_at);
+    b->adj = reinterpret_cast<int32_t*>(static_cast<char*>(b->mem3) + adj_at);
+    static const int64_t empty[kByteClasses] = {kDictEmpty, kDictEmpty, kDictEmpty, kDictEmpty, kDictEmpty, kDictEmpty,
+                                                kDictEmpty, kDictEmpty, kDictEmpty, kDictEmpty, kDictEmpty, kDictEmpty,
+                                                kDictEmpty, kDictEmpty, kDictEmpty, kDictEmpty};
+    cuda_check(cudaMemcpyAsync(b->dict, empty, sizeof empty, cudaMemcpyHostToDevice, ctx->stream), "H2D dict");
+    if (d.H > 0) {
+        const int grid_h = static_cast<int>(std::min<int64_t>((d.H + 255) / 256, 4LL * ctx->n_sms));
+        ctx->begin("k_bytes_dict");
+        k_bytes_dict<<<grid_h, 256, 0, ctx->stream>>>(d, reinterpret_cast<unsigned long long*>(b->dict));
+        ctx->end("k_bytes_dict");
+    }
     const int grid = static_cast<int>(std::min<int64_t>((d.T + 255) / 256, 16LL * ctx->n_sms));
     // 8 lanes per task (measured 1/2/4/8: C2 0.90/0.68/0.58/0.55 ms,
     // 2048 C5 DAGs 6.5/4.7/3.2/2.5 ms)
     ctx->begin("k_sim_pack");
-    k_sim_pack<8><<<grid, 256, 0, ctx->stream>>>(d, b->hdr, b->adj);
+    k_sim_pack<8><<<grid, 256, 0, ctx->stream>>>(d, b->dict, b->hdr, b->adj);
     ctx->end("k_sim_pack");
 }
 
@@ -729,6 +748,7 @@ struct AttrRun {
 };
 
 AttrScratch alloc_attr_scratch(tbsim_ctx* ctx, const DevBatch& d) {
+    ctx->scratch_gen += 1;
     AttrScratch s{};
     const int64_t T = d.T, G = d.G, E = d.E, NT = d.n_types;
     s.tmp = ctx->buf("a_tmp").as<int32_t>(T + G);
@@ -1228,6 +1248,7 @@ extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbs
         ctx->shard.pos_hi = pos_hi;
         ctx->shard.n_words = *n_words;
         ctx->shard.s = s;
+        ctx->shard.gen = ctx->scratch_gen;
     });
 }
 
@@ -1236,7 +1257,7 @@ extern "C" tbsim_status tbsim_attributes_shard_finish(tbsim_ctx* ctx, const tbsi
     return guarded([&] {
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
         const tbsim_ctx::Shard& sh = ctx->shard;
-        if (sh.b != b || n_words != sh.n_words)
+        if (sh.b != b || n_words != sh.n_words || sh.gen != ctx->scratch_gen)
             raise(TBSIM_E_INVALID_ARGUMENT, "shard finish must follow this rank's partial call on the same batch");
         if (out->on_device) raise(TBSIM_E_INVALID_ARGUMENT, "sharded attributes return host arrays");
         const DevBatch& d = b->d;
@@ -1425,6 +1446,17 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
     ensure_packed(ctx, const_cast<tbsim_batch*>(b));
     p.hdr = b->hdr;
     p.adj = b->adj;
+    p.class_bytes = b->dict;
+    {  // this call's transfer times per (platform, byte class, from, to)
+        const int32_t np = hp ? static_cast<int32_t>(hp->size()) : 1;
+        const int64_t nx = static_cast<int64_t>(np) * kByteClasses * p.max_nodes * p.max_nodes;
+        double* xtab = ctx->buf("s_xtab").as<double>(nx);
+        ctx->begin("k_xfer_table");
+        k_xfer_table<<<static_cast<int>(std::min<int64_t>((nx + 255) / 256, 64)), 256, 0, ctx->stream>>>(
+            p.platforms, np, b->dict, p.max_nodes, xtab);
+        ctx->end("k_xfer_table");
+        p.xtab = xtab;
+    }
     p.log = ctx->buf("s_log").as<SimLog>(std::max<int64_t>(d.T, 1));
     p.n_disp = ctx->buf("s_ndisp").as<int32_t>(G);
     if (d.T > 0) {

@@ -29,7 +29,7 @@ public:
 private:
     int id_;
     std::string name_;
-    const TaskAttributes* attrs_;  // dmdap / inspirit keep a reference, like the reference
+    const TaskAttributes* attrs_;  // dmdap / inspirit keep a reference, like the reference; null otherwise
     RegulatorConfig cfg_;
     RegulatorState state_;
     std::array<std::int64_t, 3> counts_{};

@@ -127,17 +127,25 @@ struct Sim {
                                     static_cast<uint32_t>(p.x));
     }
 
-    // first half of a packed record: (adj8, nin, nout, nsucc | type << 24)
+    // first half of a packed record: (adj4, nin, nout, nsucc | type << 24)
     __device__ __forceinline__ int4 head(int32_t task) const {
         return __ldg(reinterpret_cast<const int4*>(hdr + task));
     }
-    __device__ __forceinline__ const char* lists(const int4& h) const {
-        return P->adj + 8ull * static_cast<uint32_t>(h.x);
+    __device__ __forceinline__ const int32_t* lists(const int4& h) const {
+        return P->adj + static_cast<uint32_t>(h.x);
+    }
+
+    // size of an input's handle: its byte class, or handle_bytes (escape)
+    __device__ __forceinline__ int64_t bytes_of(int32_t word) const {
+        const int32_t cls = static_cast<int32_t>(static_cast<uint32_t>(word) >> kHandleBits);
+        if (cls != kEscapeClass) return __ldg(&P->class_bytes[cls]);
+        return __ldg(&P->b.handle_bytes[cold().hb + (word & kHandleMask)]);
     }
 
     // transfer_one_ms (engine.cpp:86-103): fastest resident copy, ties to the
-    // lowest node; Platform::transfer_time_ms (platform.cpp:56-63).
-    __device__ __forceinline__ double transfer_one(uint32_t m, int64_t bytes, int32_t to) const {
+    // lowest node; Platform::transfer_time_ms (platform.cpp:56-63) looked up
+    // per byte class (k_xfer_table), computed for escaped sizes.
+    __device__ __forceinline__ double transfer_one(uint32_t m, int32_t word, int32_t to) const {
         if ((m >> to) & 1u) return 0.0;
         const int32_t nn = cold().nn;
         int32_t best = 0;
@@ -147,7 +155,12 @@ struct Sim {
             const double b = bw(nd * nn + to);
             if (b > bbw) { bbw = b; best = nd; }
         }
-        return cold().lat + static_cast<double>(bytes) / bw(best * nn + to);
+        const int32_t cls = static_cast<int32_t>(static_cast<uint32_t>(word) >> kHandleBits);
+        if (cls != kEscapeClass) {
+            const int32_t mn = P->max_nodes;
+            return __ldg(&cold().xt[(cls * mn + best) * mn + to]);
+        }
+        return cold().lat + static_cast<double>(bytes_of(word)) / bw(best * nn + to);
     }
 
     // transfer_total_ms (engine.cpp:105-110) for node `want` (may differ per
@@ -158,8 +171,7 @@ struct Sim {
     // Over several rounds, zero terms are skipped: a resident input
     // contributes exactly +0.0 and the sum starts at +0.0 (it can never
     // become -0.0), so the in-order chain runs over non-resident inputs only.
-    __device__ __forceinline__ double transfer_total_lanes(const int64_t* inb, const int32_t* inh, int32_t nin,
-                                                           int32_t want) const {
+    __device__ __forceinline__ double transfer_total_lanes(const int32_t* inw, int32_t nin, int32_t want) const {
         if (nin == 0) return 0.0;
         const unsigned want_nodes = __reduce_or_sync(kFull, 1u << want);
         const int32_t nw = __popc(want_nodes);
@@ -174,7 +186,8 @@ struct Sim {
                     unsigned m = want_nodes;  // r-th set bit (few nodes; __fns is emulated)
                     for (int32_t i = 0; i < r; ++i) m &= m - 1;
                     const int32_t to = __ffs(m) - 1;
-                    t = transfer_one(rs[__ldg(&inh[k])], __ldg(&inb[k]), to);
+                    const int32_t wd = __ldg(&inw[k]);
+                    t = transfer_one(rs[wd & kHandleMask], wd, to);
                 }
                 const int32_t b0 = (r < nw ? r : 0) * nin;
                 // in-order sum; the shuffles are independent and issued ahead
@@ -202,7 +215,10 @@ struct Sim {
                 for (int32_t b0 = 0; b0 < nin; b0 += 32) {
                     const int32_t cnt = min(32, nin - b0);
                     double t = 0.0;
-                    if (lane < cnt) t = transfer_one(rs[__ldg(&inh[b0 + lane])], __ldg(&inb[b0 + lane]), to);
+                    if (lane < cnt) {
+                        const int32_t wd = __ldg(&inw[b0 + lane]);
+                        t = transfer_one(rs[wd & kHandleMask], wd, to);
+                    }
 #pragma unroll 1
                     for (int32_t j = 0; j < cnt; ++j) acc += __shfl_sync(kFull, t, j);
                 }
@@ -221,16 +237,14 @@ struct Sim {
             const int32_t to = act ? __ffs(m) - 1 : 0;
             const unsigned gmask = (c == 32 ? kFull : ((1u << c) - 1u)) << (act ? r * c : 0);
             double acc = 0.0;
-            int32_t h = 0;
-            int64_t by = 0;
-            if (act && k < nin) { h = __ldg(&inh[k]); by = __ldg(&inb[k]); }
+            int32_t wd = 0;
+            if (act && k < nin) wd = __ldg(&inw[k]);
 #pragma unroll 1
             for (int32_t b0 = 0; b0 < nin; b0 += c) {
                 const bool mine = act && b0 + k < nin;
-                const int32_t hc = h;
-                const int64_t bc = by;
-                if (act && b0 + c + k < nin) { h = __ldg(&inh[b0 + c + k]); by = __ldg(&inb[b0 + c + k]); }  // next round
-                const double t = mine ? transfer_one(rs[hc], bc, to) : 0.0;
+                const int32_t wc = wd;
+                if (act && b0 + c + k < nin) wd = __ldg(&inw[b0 + c + k]);  // next round
+                const double t = mine ? transfer_one(rs[wc & kHandleMask], wc, to) : 0.0;
                 unsigned nz = __ballot_sync(kFull, t != 0.0) & gmask;
                 const int32_t steps = __reduce_max_sync(kFull, static_cast<unsigned>(__popc(nz)));
                 // four shuffles in flight, then four in-order adds (an exhausted
@@ -258,14 +272,14 @@ struct Sim {
         const int4 hd = head(task);
         const int32_t nin = hd.y;
         if (nin == 0) return 1.0;
-        const int64_t* inb = reinterpret_cast<const int64_t*>(lists(hd));
-        const int32_t* inh = reinterpret_cast<const int32_t*>(inb + nin);
+        const int32_t* inw = lists(hd);
         const ResidT* rs = resid();
         int64_t total = 0, local = 0;
         for (int32_t k = 0; k < nin; ++k) {
-            const int64_t by = __ldg(&inb[k]);
+            const int32_t wd = __ldg(&inw[k]);
+            const int64_t by = bytes_of(wd);
             total += by;
-            if ((static_cast<uint32_t>(rs[__ldg(&inh[k])]) >> nd) & 1u) local += by;
+            if ((static_cast<uint32_t>(rs[wd & kHandleMask]) >> nd) & 1u) local += by;
         }
         return static_cast<double>(local) / static_cast<double>(total);
     }
@@ -388,14 +402,14 @@ struct Sim {
 
     // push_fifo / push_dm / push_dmda (policies.cpp:37-72): argmin over
     // capable workers, strict < so ties keep the lowest id.
-    __device__ __forceinline__ int32_t select_worker(const int64_t* inb, const int32_t* inh, int32_t nin, int32_t ty) {
+    __device__ __forceinline__ int32_t select_worker(const int32_t* inw, int32_t nin, int32_t ty) {
         if (pol() != TBSIM_POLICY_FIFO) refresh_free();
         double xfer[WPL];
 #pragma unroll
         for (int j = 0; j < WPL; ++j) xfer[j] = 0.0;
         if (pol() >= TBSIM_POLICY_DMDA) {
 #pragma unroll
-            for (int j = 0; j < WPL; ++j) xfer[j] = transfer_total_lanes(inb, inh, nin, node_of(j));
+            for (int j = 0; j < WPL; ++j) xfer[j] = transfer_total_lanes(inw, nin, node_of(j));
         }
         uint64_t bk = ~0ull;
         int32_t bwk = INT_MAX;
@@ -542,8 +556,7 @@ struct Sim {
         }
         const int32_t task = static_cast<int32_t>(e & 0xffffffu);
         const int32_t ty = static_cast<int32_t>(e >> 24);
-        const int64_t* inb = reinterpret_cast<const int64_t*>(lists(hd));
-        const double xfer = transfer_total_lanes(inb, reinterpret_cast<const int32_t*>(inb + hd.y), hd.y, nd);
+        const double xfer = transfer_total_lanes(lists(hd), hd.y, nd);
         const double exec = cost(ty, kd);
         const double start = now + xfer;
         const double end = start + exec;
@@ -583,8 +596,7 @@ struct Sim {
         const int64_t kp = static_cast<int64_t>((static_cast<uint64_t>(static_cast<uint32_t>(kk.w)) << 32) |
                                                 static_cast<uint32_t>(kk.z));
         const bool too_large = ka < 0;  // pop keys beyond int32 or > 2^24 successor entries
-        const int64_t* inb = reinterpret_cast<const int64_t*>(lists(hd));
-        const int32_t w = select_worker(inb, reinterpret_cast<const int32_t*>(inb + hd.y), hd.y, ty);
+        const int32_t w = select_worker(lists(hd), hd.y, ty);
         if (w < 0) { fail(GS_NO_WORKER, task); return -1; }
         if (too_large) { fail(GS_TOO_LARGE, task); return -1; }
         // compact keys: ability/efficiency < n < 2^15 always fit; the
@@ -730,10 +742,10 @@ struct Sim {
                 const uint32_t bit = 1u << nd;
                 const int4 hd = head(task);
                 const int32_t nin = hd.y, nout = hd.z;
-                const int32_t* inh = reinterpret_cast<const int32_t*>(lists(hd) + 8ull * nin);
+                const int32_t* inh = lists(hd);
                 if (!is_done) {  // TransferDone: inputs resident (engine.cpp:168-172)
                     for (int32_t k = lane; k < nin; k += 32) {
-                        const int32_t h = __ldg(&inh[k]);
+                        const int32_t h = __ldg(&inh[k]) & kHandleMask;
                         rs[h] = static_cast<ResidT>(rs[h] | bit);
                     }
                     __syncwarp();
@@ -848,6 +860,8 @@ __device__ void simulate_impl(const SimParams& p) {
             c.t0 = t0;
             c.nn = nn;
             c.lat = pf->latency_ms;
+            c.xt = p.xtab + static_cast<int64_t>(pfi) * kByteClasses * p.max_nodes * p.max_nodes;
+            c.hb = b.handle_base[g];
             c.n_push = c.n_samp = 0;
             c.n_pop = 0;
             c.pop0 = c.pop1 = c.pop2 = 0;
@@ -963,7 +977,18 @@ __device__ __forceinline__ int64_t graph_of(const DevBatch& b, int64_t t) {
 // lists); depends only on the batch, so it is built once per batch, at
 // upload (k_ingest's stream) or on first use.
 template <int TL>
-__global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, SimTaskHdr* hdr, char* adj) {
+__global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* dict, SimTaskHdr* hdr, int32_t* adj) {
+    __shared__ int64_t s_dict[kByteClasses];
+    if (threadIdx.x < kByteClasses) s_dict[threadIdx.x] = dict[threadIdx.x];
+    __syncthreads();
+    // input list word: handle | byte class << 28 (escape: not in the dictionary)
+    auto word = [&](int32_t h, int64_t by) {
+        int32_t c = kEscapeClass;
+#pragma unroll
+        for (int k = kEscapeClass - 1; k >= 0; --k)
+            if (s_dict[k] == by) c = k;
+        return static_cast<int32_t>(static_cast<uint32_t>(h) | (static_cast<uint32_t>(c) << kHandleBits));
+    };
     // teams of TL lanes, each over a contiguous range of tasks: the team
     // loads the offsets of its next TL tasks at once (lane j: task j, one
     // coalesced load) and hands them out by shuffles, copies each task's
@@ -1008,18 +1033,15 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, SimTaskHdr* hdr, c
             const int32_t o0 = __shfl_sync(tmask, lo0, j, TL), o1 = __shfl_sync(tmask, lo1, j, TL);
             const int32_t s0 = __shfl_sync(tmask, ls0, j, TL), s1 = __shfl_sync(tmask, ls1, j, TL);
             const int32_t ty = __shfl_sync(tmask, lty, j, TL);
-            // closed-form list offset: 4 bytes of slack per task absorb the
-            // 8-byte alignment of the input-bytes section
-            const int64_t x = 4 * t + 12 * (ib + i0) + 4 * (ob + o0) + 4 * (eb + s0);
-            const int64_t x8 = (x + 7) & ~int64_t(7);
+            // closed-form list offset (4-byte entries, task order)
+            const int64_t x = (ib + i0) + (ob + o0) + (eb + s0);
             const int32_t nin = i1 - i0, nout = o1 - o0, nsucc = s1 - s0;
             if (tl == 0)
                 reinterpret_cast<int4*>(hdr + t)[0] =
-                    make_int4(static_cast<int32_t>(x8 >> 3), nin, nout,
+                    make_int4(static_cast<int32_t>(static_cast<uint32_t>(x)), nin, nout,
                               static_cast<int32_t>((static_cast<uint32_t>(ty) << 24) |
                                                    (static_cast<uint32_t>(nsucc) & 0xffffffu)));
-            int64_t* inb = reinterpret_cast<int64_t*>(adj + x8);
-            int32_t* inh = reinterpret_cast<int32_t*>(inb + nin);
+            int32_t* inh = adj + x;
             int32_t* outl = inh + nin;
             int32_t* succl = outl + nout;
             const int32_t* in = b.in + ib + i0;
@@ -1030,14 +1052,13 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, SimTaskHdr* hdr, c
                 const int32_t ov = tl < nout ? __ldg(&out[tl]) : 0;
                 const int32_t sv = tl < nsucc ? succ[tl] : 0;
                 const int64_t by = tl < nin ? __ldg(&b.handle_bytes[hb + hd]) : 0;
-                if (tl < nin) { inh[tl] = hd; inb[tl] = by; }
+                if (tl < nin) inh[tl] = word(hd, by);
                 if (tl < nout) outl[tl] = ov;
                 if (tl < nsucc) succl[tl] = sv;
             }
             for (int32_t k = tl + TL; k < nin; k += TL) {
                 const int32_t hd = __ldg(&in[k]);
-                inh[k] = hd;
-                inb[k] = __ldg(&b.handle_bytes[hb + hd]);
+                inh[k] = word(hd, __ldg(&b.handle_bytes[hb + hd]));
             }
             for (int32_t k = tl + TL; k < nout; k += TL) outl[k] = __ldg(&out[k]);
             for (int32_t k = tl + TL; k < nsucc; k += TL) succl[k] = succ[k];
@@ -1045,7 +1066,45 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, SimTaskHdr* hdr, c
     }
 }
 
-template __global__ void k_sim_pack<8>(DevBatch, SimTaskHdr*, char*);
+template __global__ void k_sim_pack<8>(DevBatch, const int64_t*, SimTaskHdr*, int32_t*);
+
+__global__ void __launch_bounds__(256) k_bytes_dict(DevBatch b, unsigned long long* dict) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x; i0 < b.H; i0 += stride) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool act = i < b.H;
+        const unsigned long long v = act ? static_cast<unsigned long long>(__ldg(&b.handle_bytes[i])) : 0ull;
+        // one insertion per distinct value in the warp
+        const unsigned am = __ballot_sync(0xffffffffu, act);
+        if (!act) continue;
+        const unsigned peers = __match_any_sync(am, v);
+        if ((__ffs(peers) - 1) != (threadIdx.x & 31)) continue;
+        for (int c = 0; c < kEscapeClass; ++c) {
+            const unsigned long long cur = __ldcg(&dict[c]);
+            if (cur == v) break;
+            if (cur == static_cast<unsigned long long>(kDictEmpty)) {
+                const unsigned long long old = atomicCAS(&dict[c], static_cast<unsigned long long>(kDictEmpty), v);
+                if (old == static_cast<unsigned long long>(kDictEmpty) || old == v) break;
+            }
+        }
+    }
+}
+
+__global__ void k_xfer_table(const DevPlatform* pf, int32_t n_platforms, const int64_t* dict, int32_t mn,
+                             double* xtab) {
+    const int64_t total = static_cast<int64_t>(n_platforms) * kByteClasses * mn * mn;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t to = static_cast<int32_t>(i % mn), from = static_cast<int32_t>((i / mn) % mn);
+        const int32_t cls = static_cast<int32_t>((i / (mn * mn)) % kByteClasses);
+        const DevPlatform& P = pf[i / (static_cast<int64_t>(kByteClasses) * mn * mn)];
+        double t = 0.0;
+        const int64_t by = dict[cls];
+        if (from != to && from < P.n_nodes && to < P.n_nodes && by != kDictEmpty)
+            t = P.latency_ms + static_cast<double>(by) / P.bw[from * kMaxNodes + to];
+        xtab[i] = t;
+    }
+}
 
 // Pop keys of one simulation call (record words 4-7): ability, efficiency
 // and static priority; ab = -1 flags keys beyond the queue's int32 keys or a

@@ -19,6 +19,8 @@ struct SimCold {
     int64_t g, t0;
     int32_t phase, r_head, r_count, aux;
     int32_t nn;          // platform memory nodes
+    const double* xt;    // this platform's transfer table (SimParams::xtab)
+    int64_t hb;          // the graph's handle base (escaped handle sizes)
     int32_t n_pop;       // dispatches so far (log slot)
     int32_t rtail;       // last task of the ready list
 };
@@ -63,14 +65,27 @@ __host__ __device__ inline SimLayout sim_layout(int64_t max_n, int64_t max_h, in
     return L;
 }
 
+// Handle byte classes.  The batch's distinct handle sizes (up to 15, one
+// dictionary per batch, k_bytes_dict) are numbered; an input list entry is
+// handle | class << 28 (class 15: the size is not in the dictionary, read
+// handle_bytes).  The transfer estimate lat + bytes / bw(src, dst) of a class
+// is then one lookup in a per-call table (k_xfer_table, the same FP64
+// operations the reference performs, computed once) instead of an 8-byte
+// load and an FP64 divide per input.
+constexpr int kHandleBits = 28;
+constexpr int32_t kHandleMask = (1 << kHandleBits) - 1;
+constexpr int kByteClasses = 16;      // table rows; class 15 is the escape
+constexpr int kEscapeClass = kByteClasses - 1;
+constexpr int64_t kDictEmpty = INT64_MIN;
+
 // Per-task record of the packed simulation graph (k_sim_pack): everything a
 // push, dispatch or completion reads about one task in one 32-byte sector,
-// plus a byte offset (in 8-byte units) to the task's contiguous lists
-//   [input bytes: int64 x nin][input handles: int32 x nin][outputs: int32 x nout][successors: int32 x nsucc]
+// plus an offset (in 4-byte units) to the task's contiguous lists
+//   [inputs: int32 handle | class << 28 x nin][outputs: int32 x nout][successors: int32 x nsucc]
 // The CSR sections of the batch are scattered over ten arrays; packed, a task
-// touches ~3 consecutive sectors instead of ~25 scattered ones.
+// touches ~2 consecutive sectors instead of ~25 scattered ones.
 struct alignas(16) SimTaskHdr {
-    uint32_t adj8;      // list offset / 8 from the adjacency base
+    uint32_t adj4;      // list offset / 4 from the adjacency base
     uint32_t nin;
     uint32_t nout;
     uint32_t nsucc_ty;  // successors (24 bits) | type << 24
@@ -88,9 +103,10 @@ struct SimLog {
 };
 
 // Byte size of the adjacency region for a batch (closed-form per-task
-// offsets: 4 bytes of alignment slack per task).
+// offsets: every list entry is 4 bytes).
 __host__ __device__ inline int64_t sim_adj_bytes(int64_t T, int64_t I, int64_t O, int64_t E) {
-    return 4 * T + 12 * I + 4 * O + 4 * E + 16;
+    (void)T;
+    return 4 * I + 4 * O + 4 * E + 16;
 }
 
 struct SimParams {
@@ -102,7 +118,9 @@ struct SimParams {
     const double* median;             // [G] lower-median GPU time (default cfg)
     int32_t median_stride;            // elements between consecutive graphs' medians
     const SimTaskHdr* hdr;            // [T] packed task records (k_sim_pack)
-    const char* adj;                  // packed per-task lists
+    const int32_t* adj;               // packed per-task lists
+    const int64_t* class_bytes;       // [kByteClasses] the batch's handle-size dictionary
+    const double* xtab;               // [platform][class][max_nodes][max_nodes] transfer times
     SimLog* log;                      // [T] dispatch log
     int32_t* n_disp;                  // [G] log length, -1: outputs written directly
     // outputs
@@ -136,7 +154,15 @@ struct SimParams {
 // Builds the packed records' structural words and lists (once per batch);
 // k_sim_keys fills the pop keys of one call.  One thread per task.
 template <int TL>  // lanes per task (8 instantiated)
-__global__ void k_sim_pack(DevBatch b, SimTaskHdr* hdr, char* adj);
+__global__ void k_sim_pack(DevBatch b, const int64_t* dict, SimTaskHdr* hdr, int32_t* adj);
+// The batch's distinct handle sizes (first come, first numbered; at most
+// kEscapeClass of them, the rest read handle_bytes).  dict: kByteClasses
+// entries preset to kDictEmpty.
+__global__ void k_bytes_dict(DevBatch b, unsigned long long* dict);
+// Transfer time of every (platform, class, source node, destination node):
+// Platform::transfer_time_ms (platform.cpp:56-63), 0 on the same node.
+__global__ void k_xfer_table(const DevPlatform* pf, int32_t n_platforms, const int64_t* dict, int32_t mn,
+                             double* xtab);
 __global__ void k_sim_keys(DevBatch b, const int64_t* ability, const int64_t* efficiency, const int64_t* prio,
                            int32_t policy, SimTaskHdr* hdr);
 // Moves the dispatch logs into worker/start/end; one thread per log slot.

@@ -608,3 +608,18 @@ def test_window_bins_hold_more_than_2_21_descendants(ctx, path):
     assert (c["w0_ms"][0], c["best_score"][0], c["w0_score"][0], c["evaluations"][0]) == (2.0, 2, 2, 11)
     assert e["efficiency"][0] == m
     assert a["static_priority"][0] == 15000 and (a["static_priority"][1:] == 1000).all()
+
+
+def test_shard_finish_rejects_scratch_reused_in_between(ctx):
+    """a shard finish after another attribute pass on the same
+    context (which reuses/regrows the scratch the partial left) is rejected
+    instead of reading overwritten data."""
+    costs = P.default_cost_table()
+    b = _long_edge_graph(3, 6000, 60, 0.3)
+    c = api.Context(0)
+    c.set_large_graph_threshold(1000)
+    db = c.upload(b)
+    ab, sums = c.attributes_shard_partial(db, costs, 0, 2)
+    c.attributes(db, costs, abi.ATTR_ALL)
+    with pytest.raises(api.TbsimError):
+        c.attributes_shard_finish(db, sums)
