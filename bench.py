@@ -404,6 +404,68 @@ def run_c5(args):
     return 0
 
 
+# ncu kernel-name regexes of the kernels bench lines name (variants included)
+KERNEL_REGEX = {"k_simulate": "k_simulate_w", "k_sweep": "k_sweep", "k_closure": "k_closure"}
+
+
+def ncu_traffic(kernel_regex, probe_args, timeout=600):
+    """dram__bytes_read.sum + dram__bytes_write.sum of ONE launch of the
+    kernel, measured live on this build: a child `bench.py --traffic-probe`
+    (upload + one pass of the workload) under ncu, which flushes the caches
+    before the captured launch as the timed steps flush L2.  Returns a dict
+    with `bytes` (None when ncu is unavailable or this already runs under a
+    profiler)."""
+    import shutil
+    import subprocess
+    import tempfile
+    if any(k.startswith("NV_NSIGHT") or k.startswith("NSYS") for k in os.environ):
+        return {"bytes": None, "error": "running under a profiler"}
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return {"bytes": None, "error": "ncu not found"}
+    with tempfile.TemporaryDirectory() as td:
+        log = os.path.join(td, "t.csv")
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+               "--print-units", "base", "--clock-control", "none", "-k", "regex:" + kernel_regex, "-c", "1", "--csv",
+               "--log-file", log, sys.executable, os.path.abspath(__file__), "--traffic-probe"] + probe_args
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+            import csv
+            vals, name = {}, None
+            with open(log) as f:
+                rows = [row for row in csv.reader(f) if len(row) > 5]
+            hdr = rows[0]
+            for row in rows[1:]:
+                d = dict(zip(hdr, row))
+                name = d.get("Kernel Name", name)
+                vals[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
+            b = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+            return {"bytes": int(b), "read": int(vals["dram__bytes_read.sum"]),
+                    "write": int(vals["dram__bytes_write.sum"]), "kernel": name,
+                    "ncu_ms": vals.get("gpu__time_duration.sum", 0.0) / 1e6,
+                    "method": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -c 1, live child run of this "
+                              "build (cold caches; duration under ncu is not a timing)"}
+        except Exception as e:
+            return {"bytes": None, "error": f"ncu probe failed: {e!r}"[:300]}
+
+
+def traffic_probe(args):
+    """--traffic-probe: one pass of the workload for ncu_traffic's capture."""
+    from paper_2404_03226_b200 import abi, api
+    from paper_2404_03226_b200 import platform as P
+    ctx = api.Context(0)
+    if args.workload == "c4":
+        hb = api.HostBatch().add_layered(1 << 20, 1024, 1.0 / 256, [1])
+        ctx.attributes(ctx.upload(hb), P.default_cost_table(), abi.ATTR_ALL)
+    else:
+        w = WORKLOAD
+        hb = api.HostBatch().add_layered(w["n_tasks"], w["n_layers"], w["edge_prob"], np.arange(args.n_dags))
+        ctx.schedule(ctx.upload(hb), [P.assemble("8c2g", w["n_cpus"], w["n_gpus"])], w["policy"], want_attrs=False,
+                     want_states=False)
+    ctx.synchronize()
+    return 0
+
+
 def sweep_roofline(ctx, relaxations, sweep_ms):
     """The efficiency sweep's roofline: it is bound by shared-memory reads of
     predecessor rows + max, not HBM, so its denominator is the same inner
@@ -565,6 +627,10 @@ def run_c4(args):
                        "l2": "graph + descendant sets (>= 34 MB CSR, 344 GB of set traffic) far exceed L2"},
             "kernel_ms": m["kernel_ms"], "roofline": m["roofline"], "sweep_roofline": m["sweep_roofline"],
             "properties": m["properties"], "unit_time_ms": m["unit_time_ms"]}
+    if not args.no_traffic:
+        t = ncu_traffic(KERNEL_REGEX["k_closure"], ["--workload", "c4"])
+        line["roofline"]["traffic"] = t.get("bytes")
+        line["roofline"]["traffic_source"] = t
     if not args.no_cpu_baseline:
         line["cpu_baseline"], line["parity"] = c4_reference(keep)
     print(json.dumps(line), flush=True)
@@ -610,7 +676,11 @@ def main():
     ap.add_argument("--no-c4", action="store_true", help="skip the 1M-task attribute roofline probe")
     ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--dump-gathered", default=None, help="rank 0 saves the all-gathered results (npz)")
+    ap.add_argument("--no-traffic", action="store_true", help="skip the live ncu DRAM-traffic probe")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.traffic_probe:
+        return traffic_probe(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.workload == "c4":
@@ -703,14 +773,10 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg / (kms[dominant] / 1e3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        try:
-            with open(tp) as f:
-                traffic = json.load(f).get(dominant)
-        except Exception:
-            traffic = None
+    # DRAM bytes of one launch of the dominant kernel, measured live on this
+    # build by ncu in a child process (never a timing: ncu only counts bytes)
+    traffic = ncu_traffic(KERNEL_REGEX[dominant], ["--workload", "c2", "--n-dags", str(G)]) \
+        if rank == 0 and not args.no_traffic else {"skipped": "--no-traffic or rank > 0"}
 
     # ---------------- e2e: host buffers through the public API
     pinned = {"worker": torch.empty(T, dtype=torch.int32, pin_memory=True).numpy(),
@@ -871,7 +937,8 @@ def main():
             "simulator": dict(sim_shape, dags_in_flight=sim_shape["warps_per_sm"] * torch.cuda.get_device_properties(dev).multi_processor_count,
                               note="latency-bound: one warp per DAG, 2n dependent decisions"),
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic.get("bytes"),
+                         "traffic_source": traffic,
                          "algorithmic_bytes": alg, "kernel_ms": kms[dominant],
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650 GB/s",
                          "note": "latency/issue-bound event simulation and FP64 sweep; see DESIGN.md §4"},

@@ -360,6 +360,16 @@ tbsim_status tbsim_hostbatch_add_csr(tbsim_hostbatch* hb, int32_t n_tasks,
                                      const int64_t* handle_bytes,
                                      const int64_t* task_id);
 tbsim_status tbsim_hostbatch_desc(const tbsim_hostbatch* hb, tbsim_batch_desc* out);
+/* Binary CSR cache (replaces re-parsing NDJSON DAG files,
+ * src/dagio.cpp:86-138): save writes the packed batch (sections + type-name
+ * table) to one file; load creates a batch from such a file, reading each
+ * section straight into pinned memory, ready for tbsim_batch_upload.  A
+ * malformed file fails with TBSIM_E_INVALID_ARGUMENT. */
+tbsim_status tbsim_hostbatch_save(tbsim_hostbatch* hb, const char* path);
+tbsim_status tbsim_hostbatch_load(const char* path, tbsim_hostbatch** out);
+/* The same cache file from any host batch description (e.g. graphs parsed
+ * once from NDJSON by the C++ API, tbsim/csr_cache.hpp). */
+tbsim_status tbsim_batch_desc_save(const tbsim_batch_desc* desc, const char* path);
 /* Type-name table shared by all generated graphs (ids index it). */
 int32_t tbsim_type_count(void);
 const char* tbsim_type_name(int32_t type_id);

@@ -91,6 +91,21 @@ class HostBatch:
                 _p(one.handle_bytes, C.c_int64), _p(one.task_id, C.c_int64)))
         return self
 
+    def save(self, path: str) -> "HostBatch":
+        """Binary CSR cache of this batch (tbsim_hostbatch_save)."""
+        _check(load().tbsim_hostbatch_save(self._h, str(path).encode()))
+        return self
+
+    @classmethod
+    def load(cls, path: str) -> "HostBatch":
+        """A batch from a binary CSR cache (tbsim_hostbatch_load): sections
+        read straight into pinned memory, ready for Context.upload."""
+        hb = cls.__new__(cls)
+        hb._h = C.c_void_p()
+        hb._desc = None
+        _check(load().tbsim_hostbatch_load(str(path).encode(), C.byref(hb._h)))
+        return hb
+
     def desc(self) -> abi.BatchDesc:
         if self._desc is None:
             d = abi.BatchDesc()
@@ -111,7 +126,8 @@ class HostBatch:
         gb = GraphBatch(tb, eb, hb, ib, ob, arr(d.dep_off, T + G, np.int32), arr(d.dep, int(eb[-1]), np.int32),
                         arr(d.in_off, T + G, np.int32), arr(d.in_, int(ib[-1]), np.int32),
                         arr(d.out_off, T + G, np.int32), arr(d.out, int(ob[-1]), np.int32),
-                        arr(d.type, T, np.int32), arr(d.handle_bytes, int(hb[-1]), np.int64), TYPE_NAMES,
+                        arr(d.type, T, np.int32), arr(d.handle_bytes, int(hb[-1]), np.int64),
+                        [d.type_names[i].decode() for i in range(d.n_type_names)] if d.type_names else TYPE_NAMES,
                         None if not d.task_id else arr(d.task_id, T, np.int64))
         gb._owner = self
         return gb

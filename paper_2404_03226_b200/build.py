@@ -33,7 +33,7 @@ CU_EXTRA = {"simulate.cu": ["-Xcicc", "-O2"]}
 CXX_SRCS = ["hostbatch.cpp"]
 # the drop-in C++ API (namespace tbsim, include/tbsim/*.hpp) over the C-ABI
 API_SRCS = ["api/taskgraph.cpp", "api/platform.cpp", "api/device.cpp", "api/attributes.cpp",
-            "api/policies.cpp", "api/engine.cpp", "api/bench.cpp", "api/text.cpp"]
+            "api/policies.cpp", "api/engine.cpp", "api/bench.cpp", "api/text.cpp", "api/csr_cache.cpp"]
 API_OUT = os.path.join(HERE, "libtbsim_cpp.so")
 CLI_OUT = os.path.join(HERE, "tbsim")
 

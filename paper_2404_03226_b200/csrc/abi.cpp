@@ -1889,6 +1889,22 @@ tbsim_status tbsim_hostbatch_desc(const tbsim_hostbatch* hb, tbsim_batch_desc* o
     return guarded([&] { *out = const_cast<tbsim_hostbatch*>(hb)->hb.desc(); });
 }
 
+tbsim_status tbsim_hostbatch_save(tbsim_hostbatch* hb, const char* path) {
+    return guarded([&] { hb->hb.save(path); });
+}
+
+tbsim_status tbsim_batch_desc_save(const tbsim_batch_desc* desc, const char* path) {
+    return guarded([&] { tbsim_host::save_csr_cache(*desc, path); });
+}
+
+tbsim_status tbsim_hostbatch_load(const char* path, tbsim_hostbatch** out) {
+    return guarded([&] {
+        auto h = std::make_unique<tbsim_hostbatch>();
+        h->hb.load(path);
+        *out = h.release();
+    });
+}
+
 int32_t tbsim_type_count(void) { return tbsim_host::T_COUNT; }
 const char* tbsim_type_name(int32_t id) {
     return id >= 0 && id < tbsim_host::T_COUNT ? tbsim_host::kTypeNames[id] : nullptr;

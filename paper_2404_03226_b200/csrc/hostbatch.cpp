@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -260,13 +261,7 @@ void HostBatch::pack() {
         {handle_bytes_.data(), handle_bytes_.size() * 8}, {task_id_.data(), task_id_.size() * 8}};
     size_t total = 0;
     for (const auto& s : secs) total += align16(s.bytes);
-    if (cudaHostAlloc(&pinned_, std::max<size_t>(total, 16), cudaHostAllocDefault) == cudaSuccess) {
-        pinned_is_cuda_ = true;
-    } else {
-        cudaGetLastError();
-        pinned_ = std::malloc(std::max<size_t>(total, 16));
-        pinned_is_cuda_ = false;
-    }
+    alloc_pinned(total);
     char* p = static_cast<char*>(pinned_);
     std::vector<void*> dst;
     for (const auto& s : secs) {
@@ -301,6 +296,155 @@ void HostBatch::pack() {
 const tbsim_batch_desc& HostBatch::desc() {
     if (!packed_) pack();
     return desc_;
+}
+
+void HostBatch::alloc_pinned(size_t total) {
+    if (cudaHostAlloc(&pinned_, std::max<size_t>(total, 16), cudaHostAllocDefault) == cudaSuccess) {
+        pinned_is_cuda_ = true;
+    } else {
+        cudaGetLastError();
+        pinned_ = std::malloc(std::max<size_t>(total, 16));
+        pinned_is_cuda_ = false;
+    }
+}
+
+// ------------------------------------------------------- binary CSR cache
+//
+// Layout (little-endian): "TBSIMCSR" | u32 version (1) | u32 flags (bit 0:
+// task ids) | i64 G, T, E, H, I, O | u32 n_names, then per name u32 length +
+// bytes | the 14 sections of tbsim_batch_desc in order, each padded to 16
+// bytes (bases [G+1] x i64, offsets [T+G] x i32, entries, types [T] x i32,
+// handle bytes [H] x i64, task ids [T] x i64 when flagged).
+
+namespace {
+
+constexpr char kMagic[8] = {'T', 'B', 'S', 'I', 'M', 'C', 'S', 'R'};
+
+struct CacheDims {
+    int64_t G, T, E, H, I, O;
+};
+
+std::vector<size_t> section_bytes(const CacheDims& d, bool ids) {
+    return {static_cast<size_t>(d.G + 1) * 8, static_cast<size_t>(d.G + 1) * 8, static_cast<size_t>(d.G + 1) * 8,
+            static_cast<size_t>(d.G + 1) * 8, static_cast<size_t>(d.G + 1) * 8, static_cast<size_t>(d.T + d.G) * 4,
+            static_cast<size_t>(d.E) * 4,     static_cast<size_t>(d.T + d.G) * 4, static_cast<size_t>(d.I) * 4,
+            static_cast<size_t>(d.T + d.G) * 4, static_cast<size_t>(d.O) * 4,   static_cast<size_t>(d.T) * 4,
+            static_cast<size_t>(d.H) * 8,     ids ? static_cast<size_t>(d.T) * 8 : 0};
+}
+
+void put(std::FILE* f, const void* p, size_t n) {
+    if (n && std::fwrite(p, 1, n, f) != n) throw std::runtime_error("csr cache: write failed");
+}
+void get(std::FILE* f, void* p, size_t n) {
+    if (n && std::fread(p, 1, n, f) != n) throw std::invalid_argument("csr cache: truncated file");
+}
+
+}  // namespace
+
+void HostBatch::save(const std::string& path) { save_csr_cache(desc(), path); }
+
+void save_csr_cache(const tbsim_batch_desc& d, const std::string& path) {
+    const int64_t G = d.n_graphs;
+    const CacheDims dims{G, d.task_base[G], d.edge_base[G], d.handle_base[G], d.in_base[G], d.out_base[G]};
+    const bool ids = d.task_id != nullptr;
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw std::runtime_error("cannot write " + path);
+    try {
+        put(f, kMagic, 8);
+        const uint32_t version = 1, flags = ids ? 1u : 0u;
+        const uint32_t nn = d.type_names ? static_cast<uint32_t>(d.n_type_names) : 0u;
+        put(f, &version, 4);
+        put(f, &flags, 4);
+        put(f, &dims, sizeof dims);
+        put(f, &nn, 4);
+        for (uint32_t i = 0; i < nn; ++i) {
+            const uint32_t len = static_cast<uint32_t>(std::strlen(d.type_names[i]));
+            put(f, &len, 4);
+            put(f, d.type_names[i], len);
+        }
+        const void* src[14] = {d.task_base, d.edge_base, d.handle_base, d.in_base, d.out_base, d.dep_off, d.dep,
+                               d.in_off,    d.in,        d.out_off,     d.out,     d.type,    d.handle_bytes, d.task_id};
+        const auto sz = section_bytes(dims, ids);
+        static const char zeros[16] = {};
+        for (int i = 0; i < 14; ++i) {
+            put(f, src[i], sz[i]);
+            put(f, zeros, align16(sz[i]) - sz[i]);
+        }
+    } catch (...) {
+        std::fclose(f);
+        throw;
+    }
+    if (std::fclose(f) != 0) throw std::runtime_error("csr cache: write failed");
+}
+
+void HostBatch::load(const std::string& path) {
+    if (packed_ || n_graphs() != 0) throw std::logic_error("csr cache: load needs an empty batch");
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw std::runtime_error("cannot open " + path);
+    try {
+        char magic[8];
+        uint32_t version = 0, flags = 0, nn = 0;
+        CacheDims dims{};
+        get(f, magic, 8);
+        if (std::memcmp(magic, kMagic, 8) != 0) throw std::invalid_argument("csr cache: bad magic in " + path);
+        get(f, &version, 4);
+        if (version != 1) throw std::invalid_argument("csr cache: unsupported version");
+        get(f, &flags, 4);
+        get(f, &dims, sizeof dims);
+        if (dims.G < 0 || dims.T < 0 || dims.E < 0 || dims.H < 0 || dims.I < 0 || dims.O < 0)
+            throw std::invalid_argument("csr cache: negative section size");
+        get(f, &nn, 4);
+        if (nn > 4096) throw std::invalid_argument("csr cache: too many type names");
+        names_.resize(nn);
+        for (uint32_t i = 0; i < nn; ++i) {
+            uint32_t len = 0;
+            get(f, &len, 4);
+            if (len > 4096) throw std::invalid_argument("csr cache: type name too long");
+            names_[i].resize(len);
+            get(f, names_[i].data(), len);
+        }
+        const bool ids = flags & 1u;
+        const auto sz = section_bytes(dims, ids);
+        size_t total = 0;
+        for (size_t b : sz) total += align16(b);
+        alloc_pinned(total);
+        char* p = static_cast<char*>(pinned_);
+        std::vector<void*> dst;
+        for (size_t b : sz) {
+            get(f, p, align16(b));  // the file pads like the pinned block
+            dst.push_back(p);
+            p += align16(b);
+        }
+        desc_ = tbsim_batch_desc{};
+        desc_.n_graphs = dims.G;
+        desc_.task_base = static_cast<const int64_t*>(dst[0]);
+        desc_.edge_base = static_cast<const int64_t*>(dst[1]);
+        desc_.handle_base = static_cast<const int64_t*>(dst[2]);
+        desc_.in_base = static_cast<const int64_t*>(dst[3]);
+        desc_.out_base = static_cast<const int64_t*>(dst[4]);
+        desc_.dep_off = static_cast<const int32_t*>(dst[5]);
+        desc_.dep = static_cast<const int32_t*>(dst[6]);
+        desc_.in_off = static_cast<const int32_t*>(dst[7]);
+        desc_.in = static_cast<const int32_t*>(dst[8]);
+        desc_.out_off = static_cast<const int32_t*>(dst[9]);
+        desc_.out = static_cast<const int32_t*>(dst[10]);
+        desc_.type = static_cast<const int32_t*>(dst[11]);
+        desc_.handle_bytes = static_cast<const int64_t*>(dst[12]);
+        desc_.task_id = ids ? static_cast<const int64_t*>(dst[13]) : nullptr;
+        if (desc_.task_base[dims.G] != dims.T || desc_.edge_base[dims.G] != dims.E ||
+            desc_.handle_base[dims.G] != dims.H || desc_.in_base[dims.G] != dims.I || desc_.out_base[dims.G] != dims.O)
+            throw std::invalid_argument("csr cache: bases disagree with the header");
+        name_ptrs_.clear();
+        for (const auto& n : names_) name_ptrs_.push_back(n.c_str());
+        desc_.n_type_names = static_cast<int32_t>(nn);
+        desc_.type_names = name_ptrs_.data();
+        task_base_.assign(desc_.task_base, desc_.task_base + dims.G + 1);
+        packed_ = true;
+    } catch (...) {
+        std::fclose(f);
+        throw;
+    }
+    std::fclose(f);
 }
 
 }  // namespace tbsim_host

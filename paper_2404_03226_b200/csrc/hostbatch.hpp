@@ -34,6 +34,9 @@ GraphCSR gen_cholesky(int32_t nblocks, int64_t block_bytes);  // generators.cpp:
 GraphCSR gen_lu(int32_t nblocks, int64_t block_bytes);        // generators.cpp:89-142
 GraphCSR gen_qr(int32_t nblocks, int64_t block_bytes);        // builder's own tiled QR
 
+// Binary CSR cache of any host batch description (HostBatch::save's format).
+void save_csr_cache(const tbsim_batch_desc& d, const std::string& path);
+
 // Packed batch: sections in pinned memory when a CUDA runtime is present.
 class HostBatch {
 public:
@@ -43,8 +46,18 @@ public:
     const tbsim_batch_desc& desc();  // packs (once) and returns the view
     int64_t n_graphs() const { return static_cast<int64_t>(task_base_.size()) - 1; }
 
+    // Binary CSR cache (the packed sections as one file): save writes the
+    // batch (packing it), load replaces an empty batch's contents with a
+    // file's -- one read per section straight into pinned memory, no
+    // NDJSON parsing.  The file carries the type-name table.
+    void save(const std::string& path);
+    void load(const std::string& path);
+
 private:
     void pack();
+    void alloc_pinned(size_t total);
+    std::vector<std::string> names_;     // type names of a loaded cache (else kTypeNames)
+    std::vector<const char*> name_ptrs_;
     std::vector<int64_t> task_base_{0}, edge_base_{0}, handle_base_{0}, in_base_{0}, out_base_{0};
     std::vector<int32_t> dep_off_, dep_, in_off_, in_, out_off_, out_, type_;
     std::vector<int64_t> handle_bytes_, task_id_;

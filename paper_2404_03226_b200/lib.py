@@ -33,7 +33,9 @@ EXPORTS = [
     "tbsim_attributes", "tbsim_simulate", "tbsim_schedule", "tbsim_default_regulator_config",
     "tbsim_hostbatch_new", "tbsim_hostbatch_free", "tbsim_hostbatch_add_layered",
     "tbsim_hostbatch_add_cholesky", "tbsim_hostbatch_add_lu", "tbsim_hostbatch_add_qr",
-    "tbsim_hostbatch_add_csr", "tbsim_hostbatch_desc", "tbsim_type_count", "tbsim_type_name",
+    "tbsim_hostbatch_add_csr", "tbsim_hostbatch_desc", "tbsim_hostbatch_save", "tbsim_hostbatch_load",
+    "tbsim_batch_desc_save",
+    "tbsim_type_count", "tbsim_type_name",
     "tbsim_default_costs",
 ]
 
@@ -95,6 +97,9 @@ def load():
     L.tbsim_hostbatch_add_csr.argtypes = [vp, i32, P(i32), P(i32), P(i32), P(i32), P(i32), P(i32),
                                           P(i32), i32, P(i64), P(i64)]
     L.tbsim_hostbatch_desc.argtypes = [vp, P(abi.BatchDesc)]
+    L.tbsim_hostbatch_save.argtypes = [vp, C.c_char_p]
+    L.tbsim_hostbatch_load.argtypes = [C.c_char_p, P(vp)]
+    L.tbsim_batch_desc_save.argtypes = [P(abi.BatchDesc), C.c_char_p]
     L.tbsim_type_name.restype = C.c_char_p
     L.tbsim_default_costs.argtypes = [P(dbl), P(dbl)]
     _lib = L

@@ -15,11 +15,13 @@
 #include "mini_test.hpp"
 #include "tbsim/attributes.hpp"
 #include "tbsim/bench.hpp"
+#include "tbsim/csr_cache.hpp"
 #include "tbsim/engine.hpp"
 #include "tbsim/platform.hpp"
 #include "tbsim/policies.hpp"
 #include "tbsim/taskgraph.hpp"
 #include "tbsim/text.hpp"
+#include "tbsim_b200.h"
 
 using namespace tbsim;
 
@@ -317,6 +319,32 @@ TEST_CASE("dag files round-trip and the loader names the offending line") {
     save_dag_file(layered, (dir / "g.dag").string());
     CHECK(load_dag_file((dir / "g.dag").string()) == layered);
     CHECK_THROWS_WITH_AS(load_dag_file((dir / "absent.dag").string()), "cannot open", std::runtime_error);
+}
+
+TEST_CASE("dag files compile into a binary CSR cache") {
+    auto dir = std::filesystem::temp_directory_path() / "tbsim_cpp_test";
+    std::filesystem::create_directories(dir);
+    auto a = build_lu_dag(4, 640), b = generate_layered_dag(60, 6, 0.1, 9);
+    save_dag_file(a, (dir / "a.dag").string());
+    save_dag_file(b, (dir / "b.dag").string());
+    const std::string cache = (dir / "ab.csr").string();
+    compile_dag_cache({(dir / "a.dag").string(), (dir / "b.dag").string()}, cache);
+    tbsim_hostbatch* hb = nullptr;
+    CHECK(tbsim_hostbatch_load(cache.c_str(), &hb) == TBSIM_OK);
+    tbsim_batch_desc d{};
+    CHECK(tbsim_hostbatch_desc(hb, &d) == TBSIM_OK);
+    CHECK(d.n_graphs == 2);
+    CHECK(d.task_base[1] == static_cast<int64_t>(a.tasks.size()));
+    CHECK(d.task_base[2] == static_cast<int64_t>(a.tasks.size() + b.tasks.size()));
+    CHECK(d.edge_base[2] == static_cast<int64_t>(edge_count(a) + edge_count(b)));
+    // the second graph's first task with deps: positions of its ids
+    int64_t deps = 0;
+    for (int64_t t = d.task_base[1]; t < d.task_base[2]; ++t) deps += d.dep_off[t + 2] - d.dep_off[t + 1];
+    CHECK(deps == static_cast<int64_t>(edge_count(b)));
+    CHECK(std::string(d.type_names[d.type[0]]) == a.tasks[0].type);
+    tbsim_hostbatch_free(hb);
+    CHECK_THROWS_WITH_AS(compile_dag_cache({(dir / "absent.dag").string()}, cache), "cannot open",
+                         std::runtime_error);
 }
 
 // ---------------------------------------------------------------- platform

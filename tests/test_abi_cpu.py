@@ -116,3 +116,23 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(api.TbsimError) as e:
         api.Context(0)
     assert e.value.status == abi.TBSIM_E_CUDA
+
+
+def test_csr_cache_round_trip_and_errors(tmp_path):
+    """Binary CSR cache (tbsim_hostbatch_save / _load):
+    every section and the type-name table survive; a malformed file raises
+    invalid_argument."""
+    from paper_2404_03226_b200 import api
+    hb = api.HostBatch().add_layered(300, 7, 0.1, [1, 2, 3]).add_cholesky(5, 1000).add_qr(4, 640)
+    p = str(tmp_path / "b.csr")
+    hb.save(p)
+    a, b = hb.view(), api.HostBatch.load(p).view()
+    for k in ("task_base", "edge_base", "handle_base", "in_base", "out_base", "dep_off", "dep", "in_off", "in_",
+              "out_off", "out", "type", "handle_bytes"):
+        np.testing.assert_array_equal(getattr(a, k), getattr(b, k), err_msg=k)
+    assert b.type_names == a.type_names
+    (tmp_path / "bad.csr").write_bytes(b"TBSIMCSR" + b"\x02\x00\x00\x00" + bytes(64))
+    with pytest.raises(api.TbsimInvalidArgument):
+        api.HostBatch.load(str(tmp_path / "bad.csr"))
+    with pytest.raises(api.TbsimError):
+        api.HostBatch.load(str(tmp_path / "absent.csr"))

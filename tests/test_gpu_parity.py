@@ -623,3 +623,16 @@ def test_shard_finish_rejects_scratch_reused_in_between(ctx):
     c.attributes(db, costs, abi.ATTR_ALL)
     with pytest.raises(api.TbsimError):
         c.attributes_shard_finish(db, sums)
+
+
+def test_csr_cache_feeds_upload_with_identical_schedules(ctx, tmp_path):
+    """A batch saved to the binary CSR cache and loaded back uploads and
+    schedules exactly like the generated one."""
+    hb = api.HostBatch().add_layered(800, 8, 0.05, np.arange(40)).add_lu(6, 640)
+    p = str(tmp_path / "b.csr")
+    hb.save(p)
+    pl = [P.assemble("8c2g", 8, 2)]
+    a = ctx.schedule(ctx.upload(hb), pl, "inspirit")
+    b = ctx.schedule(ctx.upload(api.HostBatch.load(p)), pl, "inspirit")
+    for k in ("worker", "start_ms", "end_ms", "makespan_ms", "attr_ability", "attr_efficiency"):
+        eq(a[k], b[k], k)
