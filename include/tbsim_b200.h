@@ -181,6 +181,16 @@ int64_t tbsim_batch_h2d_bytes(const tbsim_batch* b);
 tbsim_status tbsim_batch_generate_layered(tbsim_ctx* ctx, int32_t n_tasks, int32_t n_layers,
                                           double edge_prob, const uint64_t* seeds,
                                           int64_t n_seeds, tbsim_batch** out);
+
+/* The tiled factorization DAGs built directly in HBM: `count` copies of
+ * build_cholesky_dag / build_lu_dag (src/generators.cpp:30-142) or the tiled
+ * QR, bit-identical to tbsim_hostbatch_add_cholesky / _lu / _qr (a thread
+ * per task decodes its role and last writers in closed form). */
+#define TBSIM_TILED_CHOLESKY 0
+#define TBSIM_TILED_LU 1
+#define TBSIM_TILED_QR 2
+tbsim_status tbsim_batch_generate_tiled(tbsim_ctx* ctx, int32_t kind, int32_t nblocks,
+                                        int64_t block_bytes, int64_t count, tbsim_batch** out);
 /* Totals of a device batch: [G, T, E, H, I, O]. */
 tbsim_status tbsim_batch_sizes(const tbsim_batch* b, int64_t* sizes6);
 /* Copy a device batch back into caller buffers laid out like

@@ -261,6 +261,15 @@ class Context:
                                                    _p(seeds, C.c_uint64), len(seeds), C.byref(h)))
         return DeviceBatch(self, h, n_tasks * len(seeds), len(seeds), TYPE_NAMES)
 
+    def generate_tiled(self, kind: str, nblocks: int, block_bytes: int, count: int = 1) -> DeviceBatch:
+        """`count` copies of a tiled Cholesky / LU / QR DAG built directly in
+        HBM (bit-identical to HostBatch.add_cholesky / add_lu / add_qr)."""
+        k = {"cholesky": 0, "lu": 1, "qr": 2}[kind]
+        h = C.c_void_p()
+        _check(load().tbsim_batch_generate_tiled(self.h, k, nblocks, block_bytes, count, C.byref(h)))
+        n = api_tiled_tasks(kind, nblocks)
+        return DeviceBatch(self, h, n * count, count, TYPE_NAMES)
+
     # ---------------------------------------------------------- attributes
     def attributes(self, db: DeviceBatch, costs: CostTable, request: int,
                    prio: int = abi.PRIO_UPWARD_RANK, unit_time=None) -> dict:
@@ -356,6 +365,15 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def api_tiled_tasks(kind: str, nb: int) -> int:
+    """Tasks of a tiled DAG: sum over steps of its roles (generators.cpp)."""
+    total = 0
+    for k in range(nb):
+        m = nb - k - 1
+        total += 1 + 2 * m + (m * (m - 1) // 2 if kind == "cholesky" else m * m)
+    return total
 
 
 def default_regulator_config(n_workers: int, median_gpu_ms: float) -> abi.RegulatorCfg:

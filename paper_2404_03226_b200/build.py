@@ -25,7 +25,7 @@ CU_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPI
 CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off",
              "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I/usr/local/cuda/include"]
 
-CU_SRCS = ["attributes.cu", "simulate.cu", "generate.cu", "probe.cu", "abi.cpp"]  # abi.cpp launches kernels: nvcc -x cu
+CU_SRCS = ["attributes.cu", "simulate.cu", "generate.cu", "generate_tiled.cu", "probe.cu", "abi.cpp"]  # abi.cpp launches kernels: nvcc -x cu
 # NVVM at -O2 for the simulator: cicc -O3 segfaults on most edits of this
 # translation unit (deterministically once ASLR is off), -O2 compiles it and
 # the kernels run as fast

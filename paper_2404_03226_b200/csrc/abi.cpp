@@ -736,6 +736,88 @@ tbsim_status tbsim_batch_generate_layered(tbsim_ctx* ctx, int32_t n, int32_t L, 
     });
 }
 
+tbsim_status tbsim_batch_generate_tiled(tbsim_ctx* ctx, int32_t kind, int32_t nb, int64_t bytes, int64_t count,
+                                        tbsim_batch** out) {
+    return guarded([&] {
+        static const char* names[3] = {"cholesky", "lu", "qr"};
+        if (kind < TBSIM_TILED_CHOLESKY || kind > TBSIM_TILED_QR) raise(TBSIM_E_INVALID_ARGUMENT, "unknown tiled DAG kind");
+        if (nb < 1) raise(TBSIM_E_INVALID_ARGUMENT, std::string(names[kind]) + ": nblocks must be >= 1");
+        if (bytes <= 0) raise(TBSIM_E_INVALID_ARGUMENT, std::string(names[kind]) + ": block_bytes must be > 0");
+        if (count < 0) raise(TBSIM_E_INVALID_ARGUMENT, "negative graph count");
+        const int64_t n64 = tiled_task_count(kind, nb);
+        if (n64 >= (1 << 24)) raise(TBSIM_E_INVALID_ARGUMENT, "graph exceeds 2^24 tasks");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int32_t n = static_cast<int32_t>(n64);
+        const int32_t nh = kind == TBSIM_TILED_CHOLESKY ? nb * (nb + 1) / 2 : nb * nb;
+        const int64_t G = count, T = G * n, H = G * nh;
+        // one graph's list lengths -> local offsets (identical in every copy)
+        int32_t* off = ctx->buf("g_tiled_off").as<int32_t>(3 * (static_cast<int64_t>(n) + 1));
+        int64_t* d_tot = ctx->buf("g_tiled_tot").as<int64_t>(3);
+        const int gridc = static_cast<int>(std::min<int64_t>((n + 256) / 256, 16LL * ctx->n_sms));
+        ctx->begin("k_gen_tiled_count");
+        k_gen_tiled_count<<<gridc, 256, 0, ctx->stream>>>(kind, nb, n, off);
+        k_gen_tiled_scan<<<1, 1024, 0, ctx->stream>>>(n, off, d_tot);
+        ctx->end("k_gen_tiled_count");
+        int64_t tot[3];
+        cuda_check(cudaMemcpyAsync(tot, d_tot, sizeof tot, cudaMemcpyDeviceToHost, ctx->stream), "D2H totals");
+        ctx->sync();
+        const int64_t E = G * tot[0], I = G * tot[1], O = G * tot[2];
+        auto b = std::make_unique<tbsim_batch>();
+        DevBatch& d = b->d;
+        const size_t bytes_all = 5 * al16((G + 1) * 8) + 3 * al16((T + G) * 4) + 2 * al16(E * 4) + al16(I * 4) +
+                                 al16(O * 4) + al16(T * 4) + al16(H * 8) + al16((T + G) * 4);
+        b->mem = ctx->batch_alloc(bytes_all + 16, &b->mem_bytes);
+        char* c = static_cast<char*>(b->mem);
+        auto take = [&](size_t sz) { char* r = c; c += al16(sz); return r; };
+        int64_t* task_base = reinterpret_cast<int64_t*>(take((G + 1) * 8));
+        int64_t* edge_base = reinterpret_cast<int64_t*>(take((G + 1) * 8));
+        int64_t* handle_base = reinterpret_cast<int64_t*>(take((G + 1) * 8));
+        int64_t* in_base = reinterpret_cast<int64_t*>(take((G + 1) * 8));
+        int64_t* out_base = reinterpret_cast<int64_t*>(take((G + 1) * 8));
+        d.dep_off = reinterpret_cast<int32_t*>(take((T + G) * 4));
+        d.in_off = reinterpret_cast<int32_t*>(take((T + G) * 4));
+        d.out_off = reinterpret_cast<int32_t*>(take((T + G) * 4));
+        d.dep = reinterpret_cast<int32_t*>(take(E * 4));
+        d.in = reinterpret_cast<int32_t*>(take(I * 4));
+        d.out = reinterpret_cast<int32_t*>(take(O * 4));
+        d.type = reinterpret_cast<int32_t*>(take(T * 4));
+        d.handle_bytes = reinterpret_cast<int64_t*>(take(H * 8));
+        d.succ_off = reinterpret_cast<int32_t*>(take((T + G) * 4));
+        d.succ = reinterpret_cast<int32_t*>(take(E * 4));
+        std::vector<int64_t> tb(G + 1), eb(G + 1), hb(G + 1), ib(G + 1), ob(G + 1);
+        for (int64_t g = 0; g <= G; ++g) {
+            tb[g] = g * n; eb[g] = g * tot[0]; hb[g] = g * nh; ib[g] = g * tot[1]; ob[g] = g * tot[2];
+        }
+        const std::pair<int64_t*, const std::vector<int64_t>*> bases[5] = {
+            {task_base, &tb}, {edge_base, &eb}, {handle_base, &hb}, {in_base, &ib}, {out_base, &ob}};
+        for (const auto& pb : bases)
+            cuda_check(cudaMemcpyAsync(pb.first, pb.second->data(), (G + 1) * 8, cudaMemcpyHostToDevice, ctx->stream),
+                       "H2D bases");
+        b->h2d_bytes = 5 * (G + 1) * 8;
+        d.task_base = task_base; d.edge_base = edge_base; d.handle_base = handle_base;
+        d.in_base = in_base; d.out_base = out_base;
+        d.G = G; d.T = T; d.E = E; d.H = H; d.I = I; d.O = O;
+        d.max_n = n;
+        d.max_h = nh;
+        d.max_e = static_cast<int32_t>(tot[0]);
+        d.n_types = tbsim_host::T_COUNT;
+        if (G > 0) {
+            const int gridf = static_cast<int>(std::min<int64_t>((G * (n + 1) + 255) / 256, 16LL * ctx->n_sms));
+            ctx->begin("k_gen_tiled_fill");
+            k_gen_tiled_fill<<<gridf, 256, 0, ctx->stream>>>(kind, nb, n, nh, bytes, off, d);
+            ctx->end("k_gen_tiled_fill");
+            int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(T + G);
+            const int grid = static_cast<int>(std::min<int64_t>(G, 8LL * ctx->n_sms));
+            ctx->begin("k_ingest");
+            launch_ingest(ctx, d, grid, cursor);
+            ctx->end("k_ingest");
+        }
+        b->task_base = tb;
+        for (int i = 0; i < tbsim_host::T_COUNT; ++i) b->type_names.push_back(tbsim_host::kTypeNames[i]);
+        *out = b.release();
+    });
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------- attributes
@@ -1797,7 +1879,10 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
             cuda_check(cudaEventRecord(ctx->set_free[set], ctx->download), "cudaEventRecord");
             ctx->set_pending[set] = true;
         }
-        ctx->sync();
+        // asynchronous results: the statuses were checked after the
+        // simulation; what is left on the compute stream (the dispatch-log
+        // scatter) overlaps the caller's next call instead of a host wait
+        if (!async || ctx->timing) ctx->sync();
         ctx->collect_timing();
     });
 }

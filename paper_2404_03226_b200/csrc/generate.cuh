@@ -23,6 +23,12 @@ struct GenParams {
 };
 
 __global__ void k_gen_layered_count(GenParams q);
+// tiled factorizations (generate_tiled.cu): kind = TBSIM_TILED_*
+int64_t tiled_task_count(int kind, int32_t nb);
+__global__ void k_gen_tiled_count(int kind, int32_t nb, int32_t n, int32_t* off);
+__global__ void k_gen_tiled_scan(int32_t n, int32_t* off, int64_t* tot);
+__global__ void k_gen_tiled_fill(int kind, int32_t nb, int32_t n, int32_t n_handles, int64_t block_bytes,
+                                 const int32_t* off, DevBatch b);
 __global__ void k_gen_layered_fill(GenParams q, DevBatch b);
 
 }  // namespace tbsim_dev

@@ -114,6 +114,11 @@ struct Sim {
     uint32_t seq;
     int32_t status;
     int32_t mode;
+    // the last push's transfer estimate for the worker it chose (DMDA and
+    // up): an immediate dispatch of that task (the worker idle, the queue
+    // holding only it, no event in between) reuses it -- same inputs, same
+    // residency, the same FP64 sum
+    double pxfer;
 
     __device__ __forceinline__ void fail(int32_t st, int32_t task) {
         status = st;
@@ -433,6 +438,13 @@ struct Sim {
         }
         const uint64_t mk = warp_min_u64(bk);
         const int32_t w = __reduce_min_sync(kFull, bk == mk ? bwk : INT_MAX);
+        if (pol() >= TBSIM_POLICY_DMDA && mk != ~0ull) {
+            double xw = 0.0;
+#pragma unroll
+            for (int j = 0; j < WPL; ++j)
+                if (j == (w >> 5)) xw = xfer[j];
+            pxfer = __shfl_sync(kFull, xw, w & 31);
+        }
         return mk == ~0ull ? -1 : w;
     }
 
@@ -452,6 +464,7 @@ struct Sim {
                 else c.pop2 += 1;
             }
         }
+        if (ql == 1) return 0;  // a single entry is its own argmax
         const int32_t* q = queue(w);
         const KeyT* ka = qab(w);
         const KeyT* ke = qef(w);
@@ -556,7 +569,9 @@ struct Sim {
         }
         const int32_t task = static_cast<int32_t>(e & 0xffffffu);
         const int32_t ty = static_cast<int32_t>(e >> 24);
-        const double xfer = transfer_total_lanes(lists(hd), hd.y, nd);
+        // pushed to an idle worker with an empty queue: the push's estimate
+        const bool reuse = pushed && ql == 1 && pol() >= TBSIM_POLICY_DMDA;
+        const double xfer = reuse ? pxfer : transfer_total_lanes(lists(hd), hd.y, nd);
         const double exec = cost(ty, kd);
         const double start = now + xfer;
         const double end = start + exec;

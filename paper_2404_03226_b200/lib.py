@@ -29,6 +29,7 @@ EXPORTS = [
     "tbsim_ctx_last_sim_shape",
     "tbsim_probe_sweep_peak",
     "tbsim_batch_upload", "tbsim_batch_free", "tbsim_batch_h2d_bytes", "tbsim_batch_generate_layered",
+    "tbsim_batch_generate_tiled",
     "tbsim_batch_sizes", "tbsim_batch_download",
     "tbsim_attributes", "tbsim_simulate", "tbsim_schedule", "tbsim_default_regulator_config",
     "tbsim_hostbatch_new", "tbsim_hostbatch_free", "tbsim_hostbatch_add_layered",
@@ -80,6 +81,7 @@ def load():
     L.tbsim_batch_h2d_bytes.argtypes = [vp]
     L.tbsim_batch_h2d_bytes.restype = i64
     L.tbsim_batch_generate_layered.argtypes = [vp, i32, i32, dbl, P(C.c_uint64), i64, P(vp)]
+    L.tbsim_batch_generate_tiled.argtypes = [vp, i32, i32, i64, i64, P(vp)]
     L.tbsim_batch_sizes.argtypes = [vp, P(i64)]
     L.tbsim_batch_download.argtypes = [vp, vp, P(abi.BatchDesc)]
     L.tbsim_attributes.argtypes = [vp, vp, P(abi.Costs), i32, i32, P(abi.AttrOut)]

@@ -636,3 +636,19 @@ def test_csr_cache_feeds_upload_with_identical_schedules(ctx, tmp_path):
     b = ctx.schedule(ctx.upload(api.HostBatch.load(p)), pl, "inspirit")
     for k in ("worker", "start_ms", "end_ms", "makespan_ms", "attr_ability", "attr_efficiency"):
         eq(a[k], b[k], k)
+
+
+@pytest.mark.parametrize("kind", ["cholesky", "lu", "qr"])
+@pytest.mark.parametrize("nb", [1, 2, 3, 10, 40])
+def test_device_tiled_generators_are_bit_identical_to_host(ctx, kind, nb):
+    """tiled Cholesky / LU / QR built on the device equal the
+    host builders (which replay generators.cpp:30-142) section by section."""
+    bytes_ = 160 * 160 * 4
+    dev = ctx.generate_tiled(kind, nb, bytes_, count=3).download()
+    hb = api.HostBatch()
+    for _ in range(3):
+        getattr(hb, "add_" + kind)(nb, bytes_)
+    host = hb.view()
+    for k in ("task_base", "edge_base", "handle_base", "in_base", "out_base", "dep_off", "dep", "in_off", "in_",
+              "out_off", "out", "type", "handle_bytes"):
+        eq(getattr(dev, k), getattr(host, k), f"{kind}{nb}:{k}")
