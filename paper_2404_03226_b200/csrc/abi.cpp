@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -141,6 +143,46 @@ struct tbsim_ctx {
     // directly follow its partial call (no other attribute pass in between
     // reusing or regrowing the scratch it reads)
     uint64_t scratch_gen = 0;
+    // uploads on the upload stream leave k_ingest / k_sim_pack to the
+    // compute stream (TBSIM_INGEST_ON_UPLOAD=1: run them on the upload stream)
+    bool defer_ingest = true;
+    // pinned host staging (grow-only, by name)
+    struct PinnedBuf {
+        void* p = nullptr;
+        size_t bytes = 0;
+    };
+    std::map<std::string, PinnedBuf> pbufs;
+    template <typename T>
+    T* pin(const std::string& name, size_t count) {
+        PinnedBuf& b = pbufs[name];
+        const size_t need = std::max<size_t>(count * sizeof(T), 16);
+        if (need > b.bytes) {
+            if (b.p) cudaFreeHost(b.p);
+            b.p = nullptr;
+            b.bytes = 0;
+            cuda_check(cudaMallocHost(&b.p, need), "cudaMallocHost");
+            b.bytes = need;
+        }
+        return static_cast<T*>(b.p);
+    }
+    // Deferred error checks of asynchronous schedule calls (one per result
+    // set): the statuses / attribute infos are copied to pinned staging and
+    // decoded at tbsim_ctx_synchronize, or when the set is reused -- no
+    // host round trip inside the call.
+    struct Pending {
+        bool active = false;
+        cudaEvent_t done = nullptr;
+        int64_t G = 0;
+        const GraphInfo* info = nullptr;  // compute_attributes infos (checked first)
+        const int32_t* status = nullptr;
+        const int32_t* aux = nullptr;
+        const int64_t* completed = nullptr;
+        std::vector<int64_t> task_base, task_id;
+        std::vector<std::string> type_names;
+        const int32_t* worker_out = nullptr;  // caller's worker array (stuck-task listing)
+        bool worker_on_device = false;
+        cudaEvent_t copies_done = nullptr;    // the host arrays' D2H (download stream)
+    } pend[2];
     unsigned long long* relax_ctr = nullptr;  // device counter of the last timed sweep
     int64_t last_relax[2] = {0, 0};  // FP64-window, FP32-window relaxations
 
@@ -227,6 +269,7 @@ struct tbsim_batch {
     void* mem3 = nullptr;
     size_t mem3_bytes = 0;
     tbsim_dev::SimTaskHdr* hdr = nullptr;
+    bool needs_ingest = false;  // copied on the upload stream, derived sections not built yet
     int64_t* dict = nullptr;  // [kByteClasses] handle-size dictionary (k_bytes_dict)
     int32_t* adj = nullptr;
 };
@@ -317,6 +360,8 @@ DevPlatform to_dev_platform(const tbsim_platform_desc& p, int32_t n_types_batch)
     return d;
 }
 
+void check_pending(tbsim_ctx* ctx, int set);  // deferred checks of asynchronous calls (below)
+
 // Routes a batch upload onto ctx->upload for its duration.
 struct UploadStream {
     tbsim_ctx* ctx;
@@ -328,9 +373,26 @@ struct UploadStream {
     bool active() const { return ctx->stream != saved; }
 };
 
-// Compute on a batch uploaded on another stream waits for its copies.
+// Compute on a batch uploaded on another stream waits for its copies, then
+// (first use) builds its derived sections -- successor CSR (k_ingest) and
+// the simulator's packed view (k_bytes_dict, k_sim_pack) -- on the compute
+// stream.  Measured on C2: overlapping those kernels with the previous
+// step's attribute/simulation kernels cost that step 1.56 ms (they take
+// SMs the full-GPU kernels wait for); in order they cost ~0.6 ms.
 void wait_batch(tbsim_ctx* ctx, const tbsim_batch* b) {
-    if (b && b->ready) cuda_check(cudaStreamWaitEvent(ctx->stream, b->ready, 0), "cudaStreamWaitEvent(batch)");
+    if (!b) return;
+    if (b->ready) cuda_check(cudaStreamWaitEvent(ctx->stream, b->ready, 0), "cudaStreamWaitEvent(batch)");
+    if (b->needs_ingest) {
+        auto* m = const_cast<tbsim_batch*>(b);
+        m->needs_ingest = false;
+        const DevBatch& d = m->d;
+        int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(d.T + d.G);
+        const int grid = static_cast<int>(std::min<int64_t>(d.G, 8LL * ctx->n_sms));
+        ctx->begin("k_ingest");
+        launch_ingest(ctx, d, grid, cursor);
+        ctx->end("k_ingest");
+        ensure_packed(ctx, m);
+    }
 }
 
 }  // namespace
@@ -356,6 +418,7 @@ tbsim_status tbsim_ctx_create(int device, tbsim_ctx** out) {
         if (prop.major < 10)
             raise(TBSIM_E_CUDA, std::string("device ") + prop.name + " is not sm_100 (built for sm_100a)");
         c->n_sms = prop.multiProcessorCount;
+        if (const char* e = std::getenv("TBSIM_INGEST_ON_UPLOAD")) c->defer_ingest = std::string(e) != "1";
         c->smem_optin = prop.sharedMemPerBlockOptin;
         cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
         c->stream = c->own;
@@ -385,6 +448,10 @@ tbsim_status tbsim_ctx_destroy(tbsim_ctx* ctx) {
         for (auto& e : ctx->set_free)
             if (e) cudaEventDestroy(e);
         if (ctx->pinned) cudaFreeHost(ctx->pinned);
+        for (auto& [k, b] : ctx->pbufs)
+            if (b.p) cudaFreeHost(b.p);
+        for (auto& pd : ctx->pend)
+            if (pd.done) cudaEventDestroy(pd.done);
         if (ctx->own) cudaStreamDestroy(ctx->own);
         delete ctx;
     });
@@ -402,6 +469,18 @@ tbsim_status tbsim_ctx_synchronize(tbsim_ctx* ctx) {
     return guarded([&] {
         ctx->sync();
         if (ctx->download) cuda_check(cudaStreamSynchronize(ctx->download), "cudaStreamSynchronize(download)");
+        // deferred checks of asynchronous calls, oldest first; both are
+        // cleared, the first failure is raised
+        const int first = ctx->parity;  // the set the next call would use = the older one
+        std::exception_ptr err;
+        for (int k = 0; k < 2; ++k) {
+            try {
+                check_pending(ctx, (first + k) & 1);
+            } catch (...) {
+                if (!err) err = std::current_exception();
+            }
+        }
+        if (err) std::rethrow_exception(err);
     });
 }
 
@@ -559,8 +638,11 @@ tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim
         if (h->task_id) b->task_id.assign(h->task_id, h->task_id + T);
         for (int i = 0; i < h->n_type_names; ++i)
             b->type_names.push_back(h->type_names && h->type_names[i] ? h->type_names[i] : "type" + std::to_string(i));
-        // derived successor CSR (sorted, multi-edges kept)
-        if (G > 0) {
+        // derived successor CSR (sorted, multi-edges kept); deferred to the
+        // compute stream when the copies ran on the upload stream
+        if (G > 0 && us.active() && ctx->defer_ingest) {
+            b->needs_ingest = true;
+        } else if (G > 0) {
             int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(T + G);
             const int grid = static_cast<int>(std::min<int64_t>(G, 8LL * ctx->n_sms));
             ctx->begin("k_ingest");
@@ -826,7 +908,10 @@ namespace {
 
 struct AttrRun {
     AttrScratch s{};
-    std::vector<GraphInfo> info;  // host copy after sync
+    std::string pin_sfx;              // pinned staging name suffix (async result set)
+    const GraphInfo* pinned = nullptr;  // D2H target of the per-graph infos
+    std::vector<GraphInfo> info;      // host copy: fetch() after the stream reached the copy
+    void fetch(int64_t G) { info.assign(pinned, pinned + G); }
 };
 
 AttrScratch alloc_attr_scratch(tbsim_ctx* ctx, const DevBatch& d) {
@@ -1052,23 +1137,29 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
             ctx->end("k_structure_out");
         }
     }
-    run.info.resize(G);
-    cuda_check(cudaMemcpyAsync(run.info.data(), run.s.info, G * sizeof(GraphInfo), cudaMemcpyDeviceToHost, ctx->stream),
+    GraphInfo* pinned_info = ctx->pin<GraphInfo>("p_info" + run.pin_sfx, static_cast<size_t>(G));
+    run.pinned = pinned_info;
+    cuda_check(cudaMemcpyAsync(pinned_info, run.s.info, G * sizeof(GraphInfo), cudaMemcpyDeviceToHost, ctx->stream),
                "D2H info");
 }
 
 // Compose the reference's exception for the first failing graph, in the
 // order each reference function checks its preconditions.
-void attr_errors(const tbsim_batch* b, const std::vector<GraphInfo>& info, int32_t request, const double* unit_time) {
-    for (int64_t g = 0; g < static_cast<int64_t>(info.size()); ++g) {
+std::string type_name_of(const std::vector<std::string>& names, int32_t ty) {
+    if (ty >= 0 && ty < static_cast<int32_t>(names.size())) return names[ty];
+    return "type" + std::to_string(ty);
+}
+
+void attr_errors(const GraphInfo* info, int64_t G, const std::vector<int64_t>& task_base,
+                 const std::vector<std::string>& type_names, int32_t request, const double* unit_time) {
+    for (int64_t g = 0; g < G; ++g) {
         const GraphInfo& gi = info[g];
-        const int64_t n = b->task_base[g + 1] - b->task_base[g];
+        const int64_t n = task_base[g + 1] - task_base[g];
         const bool cyc = gi.processed != n;
+        // the failing tasks' types were recorded by the structure pass
         auto ty_of = [&](int32_t pos) -> std::string {
-            // type id is on the device; fetch lazily
-            int32_t ty = 0;
-            cudaMemcpy(&ty, b->d.type + b->task_base[g] + pos, 4, cudaMemcpyDeviceToHost);
-            return type_name(b, ty);
+            const int32_t ty = pos == gi.miss_gpu ? (gi.miss_types & 0xffff) : (gi.miss_types >> 16) & 0xffff;
+            return type_name_of(type_names, ty);
         };
         if (request & (TBSIM_ATTR_ALL | TBSIM_ATTR_CALIBRATE)) {
             // calibrate_unit_time: topological_layers, then median_gpu_time_ms
@@ -1090,6 +1181,10 @@ void attr_errors(const tbsim_batch* b, const std::vector<GraphInfo>& info, int32
         if (request & (TBSIM_ATTR_DEPTH | TBSIM_ATTR_LAYERS))
             if (cyc) raise(TBSIM_E_RUNTIME, "graph has a dependency cycle");
     }
+}
+
+void attr_errors(const tbsim_batch* b, const std::vector<GraphInfo>& info, int32_t request, const double* unit_time) {
+    attr_errors(info.data(), static_cast<int64_t>(info.size()), b->task_base, b->type_names, request, unit_time);
 }
 
 // Device output staging for host-pointer outputs.
@@ -1171,6 +1266,7 @@ extern "C" tbsim_status tbsim_attributes(tbsim_ctx* ctx, const tbsim_batch* b, c
             cuda_check(cudaMemcpyAsync(c.first, c.second.first, c.second.second, cudaMemcpyDeviceToHost, ctx->stream), "D2H out");
         ctx->sync();
         ctx->collect_timing();
+        run.fetch(G);
         std::vector<double> unit_host;
         if (eff_only && dev) {
             unit_host.resize(G);
@@ -1518,9 +1614,71 @@ struct SimKeys {
 // A batch mixing worker counts is dispatched longest-first: graphs on the
 // fewest workers (longest queues, slowest simulations) start first, so they
 // do not pile up at the tail of the atomic DAG queue.
+// The first failing graph's exception (engine / policy texts), from the
+// simulator's statuses; aux = task position | type id << 24.  worker_of(g)
+// returns the graph's per-task workers (stuck-task listing).
+void sim_errors(int64_t G, const int32_t* status, const int32_t* aux, const int64_t* completed,
+                const std::vector<int64_t>& task_base, const std::vector<int64_t>& task_id,
+                const std::vector<std::string>& type_names,
+                const std::function<std::vector<int32_t>(int64_t)>& worker_of) {
+    for (int64_t g = 0; g < G; ++g) {
+        if (status[g] == GS_OK) continue;
+        const int64_t t0 = task_base[g], n = task_base[g + 1] - t0;
+        const int32_t pos = aux[g] >= 0 ? (aux[g] & 0xffffff) : aux[g];
+        const int32_t ty = aux[g] >= 0 ? (aux[g] >> 24) : 0;
+        auto ident = [&](int64_t q) { return task_id.empty() ? q : task_id[t0 + q]; };
+        switch (status[g]) {
+            case GS_NO_WORKER: raise(TBSIM_E_RUNTIME, "no worker can run task type " + type_name_of(type_names, ty));
+            case GS_TOO_LARGE:
+                raise(TBSIM_E_INVALID_ARGUMENT, "task " + std::to_string(ident(pos)) +
+                                                    " exceeds the device simulator's limits (ability/efficiency "
+                                                    "beyond its int32 queue keys, or 2^24 successor entries)");
+            case GS_DEGENERATE_TIME:
+                raise(TBSIM_E_RUNTIME, "event of task " + std::to_string(ident(pos)) +
+                                           " would fire at the current time (transfer/exec below FP64 resolution)");
+            case GS_STUCK: {
+                const std::vector<int32_t> w = worker_of(g);
+                const int64_t done = completed[g];
+                std::string msg = "simulation stuck with " + std::to_string(n - done) + " tasks unfinished:";
+                int64_t listed = 0;
+                for (int64_t i = 0; i < n && i < static_cast<int64_t>(w.size()) && listed < 20; ++i)
+                    if (w[i] < 0) { msg += " " + std::to_string(ident(i)); ++listed; }
+                if (listed < n - done) msg += " ...";
+                raise(TBSIM_E_RUNTIME, msg);
+            }
+            default: raise(TBSIM_E_RUNTIME, "device simulator failed with status " + std::to_string(status[g]));
+        }
+    }
+}
+
+// Decodes and clears a deferred check (its copies are complete once its
+// event is): compute_attributes errors first, then the simulation's.
+void check_pending(tbsim_ctx* ctx, int set) {
+    tbsim_ctx::Pending& pd = ctx->pend[set];
+    if (!pd.active) return;
+    cuda_check(cudaEventSynchronize(pd.done), "cudaEventSynchronize(pending)");
+    if (pd.copies_done) cuda_check(cudaEventSynchronize(pd.copies_done), "cudaEventSynchronize(copies)");
+    pd.active = false;
+    if (pd.info) attr_errors(pd.info, pd.G, pd.task_base, pd.type_names, TBSIM_ATTR_ALL, nullptr);
+    sim_errors(pd.G, pd.status, pd.aux, pd.completed, pd.task_base, pd.task_id, pd.type_names, [&](int64_t g) {
+        const int64_t t0 = pd.task_base[g], n = pd.task_base[g + 1] - t0;
+        std::vector<int32_t> w(static_cast<size_t>(n));
+        if (n && pd.worker_out) {
+            if (pd.worker_on_device) cudaMemcpy(w.data(), pd.worker_out + t0, n * 4, cudaMemcpyDeviceToHost);
+            else std::copy(pd.worker_out + t0, pd.worker_out + t0 + n, w.begin());
+        }
+        return w;
+    });
+}
+
+// deferred = -1: statuses are checked here (one host round trip after the
+// simulation); 0/1: the result set of an asynchronous call -- queue
+// overflows are re-run on the device (list built on the device) and the
+// statuses are checked later (check_pending).
 void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t max_workers, const SimKeys& keys,
                     const int32_t* pof_host = nullptr, const std::vector<DevPlatform>* hp = nullptr,
-                    const AttrRun* attrs_first = nullptr) {
+                    AttrRun* attrs_first = nullptr, int deferred = -1, const int32_t* worker_out = nullptr,
+                    bool worker_on_device = false) {
     const DevBatch& d = b->d;
     const int64_t G = d.G;
     if (G == 0) return;
@@ -1585,11 +1743,53 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
         launch_sim(ctx, p, max_workers, G);
     }
     p.graph_list = nullptr;
+    if (deferred >= 0) {
+        int32_t* list = ctx->buf("s_rerun").as<int32_t>(G);
+        int64_t* count = ctx->buf("s_rerun_n").as<int64_t>(1);
+        k_sim_collect_reruns<<<1, 1024, 0, ctx->stream>>>(G, p.status, list, count);
+        SimParams q = p;
+        q.graph_list = list;
+        q.qcap = std::max<int32_t>(b->d.max_n, 1);
+        q.n_items_dev = count;
+        // sized for a few reruns; the launch reads the real count on the device
+        launch_sim(ctx, q, max_workers, std::min<int64_t>(G, 4LL * ctx->n_sms), "k_simulate_rerun");
+        if (d.T > 0) {
+            const int grid = static_cast<int>(std::min<int64_t>((d.T + 255) / 256, 16LL * ctx->n_sms));
+            ctx->begin("k_sim_scatter");
+            k_sim_scatter<<<grid, 256, 0, ctx->stream>>>(d, p.log, p.n_disp, p.worker, p.start_ms, p.end_ms);
+            ctx->end("k_sim_scatter");
+        }
+        const std::string sfx = deferred ? "_a1" : "_a0";
+        tbsim_ctx::Pending& pd = ctx->pend[deferred];
+        int32_t* st = ctx->pin<int32_t>("p_status" + sfx, static_cast<size_t>(2 * G));
+        int64_t* done = ctx->pin<int64_t>("p_done" + sfx, static_cast<size_t>(G));
+        cuda_check(cudaMemcpyAsync(st, p.status, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
+        cuda_check(cudaMemcpyAsync(st + G, p.status_aux, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H aux");
+        cuda_check(cudaMemcpyAsync(done, p.completed, G * 8, cudaMemcpyDeviceToHost, ctx->stream), "D2H completed");
+        if (!pd.done) cuda_check(cudaEventCreateWithFlags(&pd.done, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventRecord(pd.done, ctx->stream), "cudaEventRecord(pending)");
+        pd.active = true;
+        pd.G = G;
+        pd.info = attrs_first ? attrs_first->pinned : nullptr;
+        pd.status = st;
+        pd.aux = st + G;
+        pd.completed = done;
+        pd.task_base = b->task_base;
+        pd.task_id = b->task_id;
+        pd.type_names = b->type_names;
+        pd.worker_out = worker_out;
+        pd.worker_on_device = worker_on_device;
+        pd.copies_done = worker_on_device ? nullptr : ctx->set_free[deferred];
+        return;
+    }
     std::vector<int32_t> status(G), aux(G);
     cuda_check(cudaMemcpyAsync(status.data(), p.status, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
     cuda_check(cudaMemcpyAsync(aux.data(), p.status_aux, G * 4, cudaMemcpyDeviceToHost, ctx->stream), "D2H aux");
     ctx->sync();
-    if (attrs_first) attr_errors(b, attrs_first->info, TBSIM_ATTR_ALL, nullptr);
+    if (attrs_first) {
+        attrs_first->fetch(G);
+        attr_errors(b, attrs_first->info, TBSIM_ATTR_ALL, nullptr);
+    }
     std::vector<int32_t> rerun;
     for (int64_t g = 0; g < G; ++g)
         if (status[g] == GS_QUEUE_OVERFLOW) rerun.push_back(static_cast<int32_t>(g));
@@ -1612,38 +1812,15 @@ void run_simulation(tbsim_ctx* ctx, const tbsim_batch* b, SimParams p, int32_t m
         k_sim_scatter<<<grid, 256, 0, ctx->stream>>>(d, p.log, p.n_disp, p.worker, p.start_ms, p.end_ms);
         ctx->end("k_sim_scatter");
     }
-    for (int64_t g = 0; g < G; ++g) {
-        if (status[g] == GS_OK) continue;
+    std::vector<int64_t> completed(G);
+    if (std::any_of(status.begin(), status.end(), [](int32_t x) { return x != GS_OK; }))
+        cuda_check(cudaMemcpy(completed.data(), p.completed, G * 8, cudaMemcpyDeviceToHost), "D2H completed");
+    sim_errors(G, status.data(), aux.data(), completed.data(), b->task_base, b->task_id, b->type_names, [&](int64_t g) {
         const int64_t t0 = b->task_base[g], n = b->task_base[g + 1] - t0;
-        auto ty_at = [&](int32_t pos) {
-            int32_t ty = 0;
-            cudaMemcpy(&ty, b->d.type + t0 + pos, 4, cudaMemcpyDeviceToHost);
-            return type_name(b, ty);
-        };
-        switch (status[g]) {
-            case GS_NO_WORKER: raise(TBSIM_E_RUNTIME, "no worker can run task type " + ty_at(aux[g]));
-            case GS_TOO_LARGE:
-                raise(TBSIM_E_INVALID_ARGUMENT, "task " + std::to_string(task_ident(b, g, aux[g])) +
-                                                    " exceeds the device simulator's limits (ability/efficiency "
-                                                    "beyond its int32 queue keys, or 2^24 successor entries)");
-            case GS_DEGENERATE_TIME:
-                raise(TBSIM_E_RUNTIME, "event of task " + std::to_string(task_ident(b, g, aux[g])) +
-                                           " would fire at the current time (transfer/exec below FP64 resolution)");
-            case GS_STUCK: {
-                std::vector<int32_t> w(n);
-                int64_t done = 0;
-                cudaMemcpy(&done, p.completed + g, 8, cudaMemcpyDeviceToHost);
-                if (n) cudaMemcpy(w.data(), p.worker + t0, n * 4, cudaMemcpyDeviceToHost);
-                std::string msg = "simulation stuck with " + std::to_string(n - done) + " tasks unfinished:";
-                int64_t listed = 0;
-                for (int64_t i = 0; i < n && listed < 20; ++i)
-                    if (w[i] < 0) { msg += " " + std::to_string(task_ident(b, g, i)); ++listed; }
-                if (listed < n - done) msg += " ...";
-                raise(TBSIM_E_RUNTIME, msg);
-            }
-            default: raise(TBSIM_E_RUNTIME, "device simulator failed with status " + std::to_string(status[g]));
-        }
-    }
+        std::vector<int32_t> w(static_cast<size_t>(n));
+        if (n) cudaMemcpy(w.data(), p.worker + t0, n * 4, cudaMemcpyDeviceToHost);
+        return w;
+    });
 }
 
 struct SimStage {
@@ -1790,6 +1967,9 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         const int set = async ? ctx->parity : 0;
         if (async) {
             ctx->parity ^= 1;
+            // this set's previous call: its deferred checks (raised here if
+            // it failed), and its copies before the staging is rewritten
+            check_pending(ctx, set);
             if (ctx->set_pending[set])
                 cuda_check(cudaStreamWaitEvent(ctx->stream, ctx->set_free[set], 0), "cudaStreamWaitEvent");
         }
@@ -1826,6 +2006,7 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         o.w0_score = stage_out(ctx, ast, nm("f_ws").c_str(), ao->w0_score, G, adev);
         o.evaluations = stage_out(ctx, ast, nm("f_ev").c_str(), ao->evaluations, G, adev);
         AttrRun run;
+        if (async) run.pin_sfx = set ? "_a1" : "_a0";
         run_attributes(ctx, b, d_costs, d_pof, SWEEP_CALIBRATE, nullptr, priority_kind == TBSIM_PRIO_UPWARD_RANK, true,
                        o, priority_kind, true, run);
         // no host round trip here: compute_attributes' errors are raised
@@ -1863,7 +2044,8 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
         p.reg_state = sim_out_ptr(ctx, st, nm("s_rstate").c_str(), out->reg_state, G, dev, true);
         p.status = ctx->buf("s_status").as<int32_t>(G);
         p.status_aux = ctx->buf("s_aux").as<int32_t>(G);
-        run_simulation(ctx, b, p, maxw, keys, platform_of, &hp, &run);
+        // asynchronous results: no host round trip in the call (deferred checks)
+        run_simulation(ctx, b, p, maxw, keys, platform_of, &hp, &run, async ? set : -1, out->worker, dev);
         cudaStream_t dl = ctx->stream;
         if (async) {  // the copies wait for this call's kernels, not the next call's
             cudaEvent_t done = ctx->set_free[set];

@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
             gi.miss_gpu = s_miss_gpu == INT32_MAX ? -1 : s_miss_gpu;
             gi.miss_any = s_miss_any == INT32_MAX ? -1 : s_miss_any;
             gi.order_det = 0;
-            gi.pad_ = 0;
+            gi.miss_types = (gi.miss_gpu >= 0 ? type[gi.miss_gpu] : 0) | ((gi.miss_any >= 0 ? type[gi.miss_any] : 0) << 16);
             gi.gpu_types = 0;
             for (int t = 0; t < kMaxTypes; ++t)
                 if (s_tcount[t] > 0) gi.gpu_types |= 1ull << t;
@@ -750,8 +750,8 @@ __global__ void __launch_bounds__(512) k_structure_large(DevBatch b, const DevCo
         gi.n_classes = n_cls;
         gi.miss_gpu = mg > 0 ? n - mg : -1;
         gi.miss_any = ma > 0 ? n - ma : -1;
+        gi.miss_types = (gi.miss_gpu >= 0 ? type[gi.miss_gpu] : 0) | ((gi.miss_any >= 0 ? type[gi.miss_any] : 0) << 16);
         gi.order_det = sort_levels && !__ldcg(&ctl->unsorted) ? 1 : 0;
-        gi.pad_ = 0;
         gi.gpu_types = 0;
         for (int t = 0; t < kMaxTypes; ++t)
             if (tc[t] > 0) gi.gpu_types |= 1ull << t;

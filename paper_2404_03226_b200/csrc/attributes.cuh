@@ -27,7 +27,7 @@ struct GraphInfo {
     int32_t miss_gpu;    // first task position without a GPU cost, -1 if none
     int32_t miss_any;    // first task position without any cost, -1 if none
     int32_t order_det;   // level order sorted by position inside each level (large-graph path)
-    int32_t pad_;
+    int32_t miss_types;  // type ids of the miss_gpu / miss_any tasks (bits 0-15 / 16-31), for error texts
     uint64_t gpu_types;  // task types present (with a GPU time): bit t
     double median;       // lower-median GPU time (valid when miss_gpu < 0 and n > 0)
 };

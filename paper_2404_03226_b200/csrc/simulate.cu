@@ -25,6 +25,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "blockscan.cuh"
 #include "common.cuh"
 #include "simulate.cuh"
 
@@ -834,7 +835,7 @@ __device__ void simulate_impl(const SimParams& p) {
         unsigned long long item = 0;
         if (lane == 0) item = atomicAdd(p.work_counter, 1ull);
         item = __shfl_sync(kFull, item, 0);
-        if (item >= static_cast<unsigned long long>(p.n_items)) break;
+        if (item >= static_cast<unsigned long long>(p.n_items_dev ? *p.n_items_dev : p.n_items)) break;
         const int64_t g = p.graph_list ? p.graph_list[item] : static_cast<int64_t>(item);
         const int64_t t0 = b.task_base[g];
         s.n = static_cast<int32_t>(b.task_base[g + 1] - t0);
@@ -944,7 +945,9 @@ __device__ void simulate_impl(const SimParams& p) {
             int32_t st = s.status;
             if (st == GS_OK && done != s.n) st = GS_STUCK;
             p.status[g] = st;
-            p.status_aux[g] = c.aux;
+            // aux: the failing task's position, its type id in bits 24..30
+            // (error texts name the type without reading the batch back)
+            p.status_aux[g] = c.aux >= 0 ? (c.aux | (__ldg(&b.type[t0 + c.aux]) << 24)) : c.aux;
             // makespan: the last completion (times only grow; a completed
             // graph's last event is a TaskDone)
             p.makespan[g] = done > 0 ? s.now : 0.0;
@@ -1159,6 +1162,24 @@ __global__ void __launch_bounds__(256) k_sim_scatter(DevBatch b, const SimLog* l
         start_ms[t0 + e.task] = e.start;
         end_ms[t0 + e.task] = e.end;
     }
+}
+
+// Graphs whose simulation overflowed a shared-memory queue, compacted into
+// the rerun list (count in *n): the rerun launch reads its item count from
+// the device, so no host round trip decides whether it has work.
+__global__ void __launch_bounds__(1024) k_sim_collect_reruns(int64_t G, const int32_t* status, int32_t* list,
+                                                            int64_t* n) {
+    __shared__ int32_t warp_tot[32];
+    int32_t carry = 0;
+    for (int64_t base = 0; base < G; base += blockDim.x) {
+        const int64_t g = base + threadIdx.x;
+        const int32_t x = g < G && status[g] == GS_QUEUE_OVERFLOW ? 1 : 0;
+        int32_t tot;
+        const int32_t inc = block_inclusive_scan(x, warp_tot, &tot);
+        if (x) list[carry + inc - 1] = static_cast<int32_t>(g);
+        carry += tot;
+    }
+    if (threadIdx.x == 0) *n = carry;
 }
 
 #define TBSIM_SIM_KERNEL(NAME, WPL, COMPACT, POL, MANYIN, THREADS, MINB)                             \

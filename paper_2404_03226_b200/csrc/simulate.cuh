@@ -148,6 +148,7 @@ struct SimParams {
     SimLayout layout;                 // per-warp state sections (set by launch_sim)
     const int32_t* graph_list;        // subset of graphs (rerun) or null
     int64_t n_items;                  // graphs to process (list length or G)
+    const int64_t* n_items_dev;       // or read on the device (rerun lists), when set
     unsigned long long* work_counter;
 };
 
@@ -166,6 +167,7 @@ __global__ void k_xfer_table(const DevPlatform* pf, int32_t n_platforms, const i
 __global__ void k_sim_keys(DevBatch b, const int64_t* ability, const int64_t* efficiency, const int64_t* prio,
                            int32_t policy, SimTaskHdr* hdr);
 // Moves the dispatch logs into worker/start/end; one thread per log slot.
+__global__ void k_sim_collect_reruns(int64_t G, const int32_t* status, int32_t* list, int64_t* n);
 __global__ void k_sim_scatter(DevBatch b, const SimLog* log, const int32_t* n_disp, int32_t* worker, double* start_ms,
                               double* end_ms);
 

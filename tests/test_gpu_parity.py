@@ -652,3 +652,53 @@ def test_device_tiled_generators_are_bit_identical_to_host(ctx, kind, nb):
     for k in ("task_base", "edge_base", "handle_base", "in_base", "out_base", "dep_off", "dep", "in_off", "in_",
               "out_off", "out", "type", "handle_bytes"):
         eq(getattr(dev, k), getattr(host, k), f"{kind}{nb}:{k}")
+
+
+def test_async_schedule_defers_errors_to_synchronize(ctx):
+    """Asynchronous results: schedule() makes no host round trip, so its
+    errors (the reference's texts) surface at synchronize() -- a missing GPU
+    cost (compute_attributes), a cycle, a task no worker can run -- and a
+    good call on the same context is unaffected."""
+    gonly_pl = P.make_preset("homog2")
+    gonly_pl.costs = P.CostTable()
+    gonly_pl.costs.set("GONLY_TYPE", P.GPU, 1.0)
+    gonly = GraphBatch.from_taskgraphs([TaskGraph("g", [TaskNode(0, "GONLY_TYPE")])])
+    cyc = _tg([TaskNode(0, "UNIT", [1]), TaskNode(1, "UNIT", [0])])
+    good = api.HostBatch().add_layered(200, 5, 0.1, np.arange(8))
+    want = ctx.schedule(ctx.upload(good), [P.assemble("8c2g", 8, 2)], "inspirit", want_attrs=False)
+    ctx.set_async_results(True)
+    try:
+        for batch, pl, msg in ((gonly, gonly_pl, "no worker can run task type GONLY_TYPE"),
+                               (cyc, P.assemble("8c2g", 8, 2), "graph has a dependency cycle")):
+            ctx.schedule(ctx.upload(batch), [pl], "dmda", want_attrs=False, want_states=False)
+            with pytest.raises(api.TbsimRuntimeError, match=msg):
+                ctx.synchronize()
+        got = ctx.schedule(ctx.upload(good), [P.assemble("8c2g", 8, 2)], "inspirit", want_attrs=False,
+                           want_states=False)
+        ctx.synchronize()
+        for k in ("worker", "start_ms", "end_ms", "makespan_ms"):
+            eq(got[k], want[k], k)
+    finally:
+        ctx.set_async_results(False)
+
+
+def test_async_schedule_reruns_queue_overflows_on_the_device(ctx):
+    """The overflow rerun list is built on the device in asynchronous mode:
+    the same schedules as the synchronous call."""
+    G = 2 * 148 * 4
+    hb = api.HostBatch().add_layered(120, 6, 0.1, np.arange(G)).add_layered(1500, 2, 0.01, [5, 6])
+    pl = [P.assemble("8c2g", 8, 2)]
+    db = ctx.upload(hb)
+    want = ctx.schedule(db, pl, "inspirit", want_attrs=False)
+    ctx.set_async_results(True)
+    ctx.set_timing(True)
+    try:
+        got = ctx.schedule(db, pl, "inspirit", want_attrs=False, want_states=False)
+        ctx.synchronize()
+        rerun_ms = ctx.last_kernel_ms("k_simulate_rerun")
+    finally:
+        ctx.set_timing(False)
+        ctx.set_async_results(False)
+    for k in ("worker", "start_ms", "end_ms", "makespan_ms", "completed"):
+        eq(got[k], want[k], k)
+    assert rerun_ms > 0.0
