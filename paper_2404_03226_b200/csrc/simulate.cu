@@ -607,7 +607,7 @@ struct Sim {
         // ride along while the push rule runs
         const int4 hd = head(task);
         const int4 kk = __ldg(reinterpret_cast<const int4*>(hdr + task) + 1);
-        const int32_t ty = static_cast<int32_t>(static_cast<uint32_t>(hd.w) >> 24);
+        const int32_t ty = static_cast<int32_t>((static_cast<uint32_t>(hd.w) >> 24) & 0x3fu);
         const int32_t ka = kk.x, ke = kk.y;
         const int64_t kp = static_cast<int64_t>((static_cast<uint64_t>(static_cast<uint32_t>(kk.w)) << 32) |
                                                 static_cast<uint32_t>(kk.z));
@@ -780,14 +780,22 @@ struct Sim {
                 // each run of equal ids decrements by the run length
                 const int32_t* succl = outl + nout;
                 const int32_t s1 = static_cast<int32_t>(static_cast<uint32_t>(hd.w) & 0xffffffu);
+                // multi-edges (bit 30, k_sim_pack) are adjacent in the sorted
+                // list: the lowest lane of each run decrements by its length;
+                // lists without them decrement by one per lane
+                const bool dups = (static_cast<uint32_t>(hd.w) >> 30) & 1u;
                 for (int32_t b0 = 0; b0 < s1; b0 += 32) {
                     const int32_t k = b0 + lane;
                     const bool valid = k < s1;
                     const int32_t sv = valid ? __ldg(&succl[k]) : -1 - lane;
-                    const unsigned peers = __match_any_sync(kFull, sv);
+                    int32_t dec = valid ? 1 : 0;
+                    if (dups) {
+                        const unsigned peers = __match_any_sync(kFull, sv);
+                        dec = valid && (__ffs(peers) - 1) == lane ? __popc(peers) : 0;
+                    }
                     bool rdy = false;
-                    if (valid && (__ffs(peers) - 1) == lane) {
-                        const int32_t left = static_cast<int32_t>(um[sv]) - __popc(peers);
+                    if (dec) {
+                        const int32_t left = static_cast<int32_t>(um[sv]) - dec;
                         um[sv] = static_cast<UnmetT>(left);
                         rdy = left == 0;
                         // its push reads the record soon: into L1 now
@@ -1054,11 +1062,6 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* dic
             // closed-form list offset (4-byte entries, task order)
             const int64_t x = (ib + i0) + (ob + o0) + (eb + s0);
             const int32_t nin = i1 - i0, nout = o1 - o0, nsucc = s1 - s0;
-            if (tl == 0)
-                reinterpret_cast<int4*>(hdr + t)[0] =
-                    make_int4(static_cast<int32_t>(static_cast<uint32_t>(x)), nin, nout,
-                              static_cast<int32_t>((static_cast<uint32_t>(ty) << 24) |
-                                                   (static_cast<uint32_t>(nsucc) & 0xffffffu)));
             int32_t* inh = adj + x;
             int32_t* outl = inh + nin;
             int32_t* succl = outl + nout;
@@ -1080,6 +1083,16 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* dic
             }
             for (int32_t k = tl + TL; k < nout; k += TL) outl[k] = __ldg(&out[k]);
             for (int32_t k = tl + TL; k < nsucc; k += TL) succl[k] = succ[k];
+            // record word 3: successors | type << 24 | multi-edges << 30 (the
+            // sorted list holds a repeated successor)
+            bool dup = false;
+            for (int32_t k = tl + 1; k < nsucc; k += TL) dup = dup || succ[k] == succ[k - 1];
+            dup = __any_sync(tmask, dup);
+            if (tl == 0)
+                reinterpret_cast<int4*>(hdr + t)[0] =
+                    make_int4(static_cast<int32_t>(static_cast<uint32_t>(x)), nin, nout,
+                              static_cast<int32_t>((dup ? 1u << 30 : 0u) | (static_cast<uint32_t>(ty) << 24) |
+                                                   (static_cast<uint32_t>(nsucc) & 0xffffffu)));
         }
     }
 }
