@@ -1777,22 +1777,32 @@ __global__ void __launch_bounds__(256) k_closure(DevBatch b, AttrScratch s, int6
                     m_slot = rslot[v];
                 }
                 const int32_t cnt = min(32, k1 - kb);
-                for (int32_t t = 0; t < cnt; ++t) {
+                // two successors per round: 2 x CH loads per lane in flight
+                // (C4: 70.5 -> 64.9 ms; a generic U-successor loop nest
+                // compiled to the same registers but measured 73.4 ms)
+                for (int32_t t = 0; t < cnt; t += 2) {
+                    const int32_t t1 = t + 1 < cnt ? t + 1 : t;
                     const int32_t ov = __shfl_sync(0xffffffffu, m_ov, t);
                     const int64_t lov = __shfl_sync(0xffffffffu, m_lov, t);
                     const int32_t slot = __shfl_sync(0xffffffffu, m_slot, t);
+                    const int32_t ov1 = __shfl_sync(0xffffffffu, m_ov, t1);
+                    const int64_t lov1 = __shfl_sync(0xffffffffu, m_lov, t1);
+                    const int32_t slot1 = __shfl_sync(0xffffffffu, m_slot, t1);
                     const uint64_t* sv = sets + static_cast<int64_t>(slot) * nwr - wlo;
-                    uint64_t x[CH];  // all loads of this successor in flight together
+                    const uint64_t* sv1 = sets + static_cast<int64_t>(slot1) * nwr - wlo;
+                    uint64_t x[CH], y[CH];
 #pragma unroll
                     for (int j = 0; j < CH; ++j) {
                         const int64_t w = w0 + lane + 32 * j;
                         x[j] = (w >= lov && w < whi) ? __ldcg(&sv[w]) : 0ull;
+                        y[j] = (w >= lov1 && w < whi) ? __ldcg(&sv1[w]) : 0ull;
                     }
 #pragma unroll
                     for (int j = 0; j < CH; ++j) {
                         const int64_t w = w0 + lane + 32 * j;
-                        acc[j] |= x[j];
+                        acc[j] |= x[j] | y[j];  // t1 == t repeats a successor: OR is idempotent
                         if (w == (ov >> 6)) acc[j] |= 1ull << (ov & 63);
+                        if (w == (ov1 >> 6)) acc[j] |= 1ull << (ov1 & 63);
                     }
                 }
             }
