@@ -787,10 +787,6 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg / (kms[dominant] / 1e3) / 1e9
-    # DRAM bytes of one launch of the dominant kernel, measured live on this
-    # build by ncu in a child process (never a timing: ncu only counts bytes)
-    traffic = ncu_traffic(KERNEL_REGEX[dominant], ["--workload", "c2", "--n-dags", str(G)]) \
-        if rank == 0 and not args.no_traffic else {"skipped": "--no-traffic or rank > 0"}
 
     # ---------------- e2e: host buffers through the public API
     pinned = {"worker": torch.empty(T, dtype=torch.int32, pin_memory=True).numpy(),
@@ -935,6 +931,11 @@ def main():
         except Exception as e:  # pragma: no cover
             c4 = {"error": str(e)}
 
+    # DRAM bytes of one launch of the dominant kernel, measured live on this
+    # build by ncu in a child process after every timed region (never a
+    # timing: ncu only counts bytes)
+    traffic = ncu_traffic(KERNEL_REGEX[dominant], ["--workload", "c2", "--n-dags", str(G)]) \
+        if rank == 0 and not args.no_traffic else {"bytes": None, "skipped": "--no-traffic or rank > 0"}
     if rank == 0:
         line = {
             "metric": "DAGs scheduled/sec", "value": value, "unit": "DAGs/s", "n_gpus": world,

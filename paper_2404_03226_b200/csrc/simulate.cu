@@ -1099,26 +1099,37 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* dic
 
 template __global__ void k_sim_pack<8>(DevBatch, const int64_t*, SimTaskHdr*, int32_t*);
 
-__global__ void __launch_bounds__(256) k_bytes_dict(DevBatch b, unsigned long long* dict) {
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x; i0 < b.H; i0 += stride) {
-        const int64_t i = i0 + threadIdx.x;
-        const bool act = i < b.H;
-        const unsigned long long v = act ? static_cast<unsigned long long>(__ldg(&b.handle_bytes[i])) : 0ull;
-        // one insertion per distinct value in the warp
-        const unsigned am = __ballot_sync(0xffffffffu, act);
-        if (!act) continue;
-        const unsigned peers = __match_any_sync(am, v);
-        if ((__ffs(peers) - 1) != (threadIdx.x & 31)) continue;
-        for (int c = 0; c < kEscapeClass; ++c) {
-            const unsigned long long cur = __ldcg(&dict[c]);
-            if (cur == v) break;
-            if (cur == static_cast<unsigned long long>(kDictEmpty)) {
-                const unsigned long long old = atomicCAS(&dict[c], static_cast<unsigned long long>(kDictEmpty), v);
-                if (old == static_cast<unsigned long long>(kDictEmpty) || old == v) break;
-            }
+// A value into a dictionary of kEscapeClass slots (first come, first
+// numbered); false when it is full of other values.
+__device__ __forceinline__ bool dict_insert(unsigned long long* d, unsigned long long v) {
+    for (int c = 0; c < kEscapeClass; ++c) {
+        const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(&d[c]);
+        if (cur == v) return true;
+        if (cur == static_cast<unsigned long long>(kDictEmpty)) {
+            const unsigned long long old = atomicCAS(&d[c], static_cast<unsigned long long>(kDictEmpty), v);
+            if (old == static_cast<unsigned long long>(kDictEmpty) || old == v) return true;
         }
     }
+    return false;
+}
+
+// Each CTA collects its handles' distinct sizes in shared memory (a few
+// shared-memory compares per handle), then merges them into the batch's
+// dictionary -- a handful of global CAS per CTA instead of per warp.
+__global__ void __launch_bounds__(256) k_bytes_dict(DevBatch b, unsigned long long* dict) {
+    __shared__ unsigned long long sd[kEscapeClass];
+    if (threadIdx.x < kEscapeClass) sd[threadIdx.x] = static_cast<unsigned long long>(kDictEmpty);
+    __syncthreads();
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < b.H; i += stride) {
+        const unsigned long long v = static_cast<unsigned long long>(__ldg(&b.handle_bytes[i]));
+        // this CTA's dictionary full of other values: straight to the
+        // batch's (where it may still get a class)
+        if (!dict_insert(sd, v)) dict_insert(dict, v);
+    }
+    __syncthreads();
+    if (threadIdx.x < kEscapeClass && sd[threadIdx.x] != static_cast<unsigned long long>(kDictEmpty))
+        dict_insert(dict, sd[threadIdx.x]);
 }
 
 __global__ void k_xfer_table(const DevPlatform* pf, int32_t n_platforms, const int64_t* dict, int32_t mn,
