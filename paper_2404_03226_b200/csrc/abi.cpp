@@ -614,7 +614,18 @@ tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim
         b->mem = ctx->batch_alloc(total + derived + 16, &b->mem_bytes);
         char* p = static_cast<char*>(b->mem);
         int64_t moved = 0;
-        for (const auto& s : secs) {
+        for (size_t k = 0; k < secs.size(); ++k) {
+            const Sec& s = secs[k];
+            // a section that aliases an earlier one in the host descriptor
+            // (e.g. inputs == dependencies, HostBatch packs them once) is
+            // copied once and aliased on the device (read-only sections)
+            bool aliased = false;
+            for (size_t j = 0; j < k && !aliased; ++j)
+                if (s.bytes && secs[j].src == s.src && secs[j].bytes == s.bytes) {
+                    *s.dst = *secs[j].dst;
+                    aliased = true;
+                }
+            if (aliased) continue;
             *s.dst = p;
             if (s.bytes) {
                 cuda_check(cudaMemcpyAsync(p, s.src, s.bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D batch");
