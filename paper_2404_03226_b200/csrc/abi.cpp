@@ -1042,8 +1042,15 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         if (gi.processed == d.max_n && fits) {  // acyclic: otherwise the error path reports it
             uint64_t* sets = ctx->buf("a_sets").as<uint64_t>(need / 8);
             cuda_check(cudaMemsetAsync(o.ability, 0, static_cast<size_t>(d.T) * 8, ctx->stream), "memset ability");
+            // TMA bulk copies need 16-byte aligned set rows (an even word count)
+            // TMA bulk copies of 4-KB successor chunks (k_closure_tma) need
+            // 16-byte aligned set rows: an even word count
+            const bool tma = nw % 2 == 0;
+            const void* kern = tma ? reinterpret_cast<const void*>(k_closure_tma<3, 16, 2>)
+                                   : reinterpret_cast<const void*>(k_closure<4>);
+            const int threads = tma ? 64 : 256;
             int per_sm = 0;
-            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_closure<4>, 256, 0), "occupancy");
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0), "occupancy");
             const int grid = std::max(1, per_sm) * ctx->n_sms;
             int64_t g0 = 0;
             int64_t wlo = 0, whi = nw;
@@ -1052,7 +1059,7 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
             unsigned long long* ab = reinterpret_cast<unsigned long long*>(o.ability);
             void* args[] = {&dv, &sv, &g0, &sets, &wlo, &whi, &ab};
             ctx->begin("k_closure");
-            cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_closure<4>), grid, 256, args, 0, ctx->stream),
+            cuda_check(cudaLaunchCooperativeKernel(kern, grid, threads, args, 0, ctx->stream),
                        "cudaLaunchCooperativeKernel(k_closure)");
             ctx->end("k_closure");
             ability_done = true;
@@ -1353,8 +1360,13 @@ extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbs
         cuda_check(cudaMemsetAsync(d_ab, 0, static_cast<size_t>(n) * 8, ctx->stream), "memset ability");
         if (whi > wlo) {
             uint64_t* sets = ctx->buf("a_sets").as<uint64_t>(static_cast<size_t>(std::max(gi.peak_rslots, 1)) * (whi - wlo));
+            // TMA bulk copies when this rank's rows start 16-byte aligned
+            const bool tma = wlo % 2 == 0 && (whi - wlo) % 2 == 0;
+            const void* kern = tma ? reinterpret_cast<const void*>(k_closure_tma<3, 16, 2>)
+                                   : reinterpret_cast<const void*>(k_closure<4>);
+            const int threads = tma ? 64 : 256;
             int per_sm = 0;
-            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_closure<4>, 256, 0), "occupancy");
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0), "occupancy");
             const int grid = std::max(1, per_sm) * ctx->n_sms;
             int64_t g0 = 0, lo_ = wlo, hi_ = whi;
             DevBatch dv = d;
@@ -1362,7 +1374,7 @@ extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbs
             unsigned long long* ab = reinterpret_cast<unsigned long long*>(d_ab);
             void* args[] = {&dv, &sv, &g0, &sets, &lo_, &hi_, &ab};
             ctx->begin("k_closure");
-            cuda_check(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_closure<4>), grid, 256, args, 0, ctx->stream),
+            cuda_check(cudaLaunchCooperativeKernel(kern, grid, threads, args, 0, ctx->stream),
                        "cudaLaunchCooperativeKernel(k_closure)");
             ctx->end("k_closure");
         }

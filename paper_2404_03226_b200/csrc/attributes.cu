@@ -1825,6 +1825,166 @@ __global__ void __launch_bounds__(256) k_closure(DevBatch b, AttrScratch s, int6
 
 template __global__ void k_closure<4>(DevBatch, AttrScratch, int64_t, uint64_t*, int64_t, int64_t, unsigned long long*);
 
+// ---- the same closure with the successor chunks moved by TMA bulk copies
+//
+// Each warp keeps a ring of kStages 1-KB shared-memory stages with one
+// mbarrier each: lane 0 issues `cp.async.bulk` global->shared copies for up
+// to kStages successors' chunks of the current item (the asynchronous proxy
+// moves them; no registers hold in-flight data), the warp ORs each stage as
+// its barrier completes.  A successor's chunk is copied from its lower word
+// bound rounded down to 16 bytes; words below the bound (stale memory of a
+// reused slot) and beyond whi are masked at the OR, as in k_closure.
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+}  // namespace
+
+template <int kStages, int CH, int kWarps>
+__global__ void __launch_bounds__(32 * kWarps) k_closure_tma(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets,
+                                                             int64_t wlo, int64_t whi, unsigned long long* ability) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    constexpr int64_t kChunk = 32 * CH;  // words per item (CH x 256 B)
+    // stage rows of kChunk + 2 words: a chunk starting at an odd word lands
+    // one word in (16-byte alignment of both ends of the copy)
+    __shared__ __align__(128) uint64_t s_stage[kWarps][kStages][kChunk + 2];
+    __shared__ __align__(8) uint64_t s_bar[kWarps][kStages];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint64_t* bars = s_bar[wib];
+    if (lane < kStages) mbar_init(&bars[lane], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    uint32_t issued = 0, consumed = 0;  // copies through this warp's ring (stage = n % kStages)
+
+    const int64_t t0 = b.task_base[g];
+    const GraphInfo gi = s.info[g];
+    const int32_t* lstart = s.lstart + t0 + g;
+    const int32_t* order = s.order + t0;
+    const int32_t* opos = s.opos + t0;
+    const int32_t* rslot = s.rslot + t0;
+    const int32_t* level = s.level + t0;
+    const int32_t* soff = b.succ_off + t0 + g;
+    const int32_t* succ = b.succ + b.edge_base[g];
+    const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int64_t nwr = whi - wlo;
+    for (int32_t lv = gi.n_levels - 1; lv >= 0; --lv) {
+        // the previous level's sets (generic-proxy stores, grid barrier)
+        // are read by the asynchronous proxy from here on
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        const int32_t a0 = lstart[lv], cnt = lstart[lv + 1] - a0;
+        const int64_t lo = max(static_cast<int64_t>(lstart[lv + 1] >> 6), wlo);
+        const int64_t chunks = whi > lo ? (whi - lo + kChunk - 1) / kChunk : 0;
+        const int64_t items = static_cast<int64_t>(cnt) * chunks;
+        for (int64_t item = gwarp; item < items; item += nwarps) {
+            const int32_t i = a0 + static_cast<int32_t>(item / chunks);
+            const int64_t w0 = lo + (item % chunks) * kChunk;
+            const int32_t u = order[i];
+            const int32_t shift = static_cast<int32_t>(w0 & 1);  // word w at stage index w - w0 + shift
+            uint64_t acc[CH];
+#pragma unroll
+            for (int j = 0; j < CH; ++j) acc[j] = 0;
+            const int32_t k0 = __ldg(&soff[u]), k1 = __ldg(&soff[u + 1]);
+            for (int32_t kb = k0; kb < k1; kb += 32) {
+                int32_t m_ov = 0, m_slot = 0, m_lov = 0;
+                if (kb + lane < k1) {
+                    const int32_t v = __ldg(&succ[kb + lane]);
+                    m_ov = opos[v];
+                    m_lov = lstart[level[v] + 1] >> 6;
+                    m_slot = rslot[v];
+                }
+                const int32_t cnt_s = min(32, k1 - kb);
+                // copy of successor t into stage `issued % kStages`
+                auto issue = [&](int32_t t) {
+                    const int64_t lov = __shfl_sync(0xffffffffu, m_lov, t);
+                    const int32_t slot = __shfl_sync(0xffffffffu, m_slot, t);
+                    if (lane == 0) {
+                        const uint32_t st = issued % kStages;
+                        const int64_t a = max(lov, w0) & ~int64_t(1);  // 16-byte aligned start
+                        int64_t e = min(w0 + kChunk, whi);
+                        e = (e + 1) & ~int64_t(1);
+                        if (e > a) {
+                            const uint64_t* src = sets + static_cast<int64_t>(slot) * nwr + (a - wlo);
+                            const uint32_t bytes = static_cast<uint32_t>((e - a) * 8);
+                            mbar_expect_tx(&bars[st], bytes);
+                            bulk_g2s(&s_stage[wib][st][a - w0 + shift], src, bytes, &bars[st]);
+                        } else {
+                            mbar_arrive(&bars[st]);
+                        }
+                    }
+                    ++issued;
+                };
+                int32_t next = 0;
+                for (; next < cnt_s && next < kStages; ++next) issue(next);
+                for (int32_t t = 0; t < cnt_s; ++t) {
+                    const uint32_t st = consumed % kStages;
+                    mbar_wait(&bars[st], (consumed / kStages) & 1u);
+                    const int32_t ov = __shfl_sync(0xffffffffu, m_ov, t);
+                    const int64_t lov = __shfl_sync(0xffffffffu, m_lov, t);
+#pragma unroll
+                    for (int j = 0; j < CH; ++j) {
+                        const int64_t w = w0 + lane + 32 * j;
+                        if (w >= lov && w < whi) acc[j] |= s_stage[wib][st][lane + 32 * j + shift];
+                        if (w == (ov >> 6)) acc[j] |= 1ull << (ov & 63);
+                    }
+                    ++consumed;
+                    __syncwarp();  // every lane is done with the stage before it is refilled
+                    if (next < cnt_s) {
+                        if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        issue(next++);
+                    }
+                }
+            }
+            uint64_t* su = sets + static_cast<int64_t>(rslot[u]) * nwr - wlo;
+            int pc = 0;
+#pragma unroll
+            for (int j = 0; j < CH; ++j) {
+                const int64_t w = w0 + lane + 32 * j;
+                if (w < whi) {
+                    __stcg(&su[w], acc[j]);
+                    pc += __popcll(acc[j]);
+                }
+            }
+            pc = __reduce_add_sync(0xffffffffu, pc);
+            if (lane == 0 && pc) atomicAdd(&ability[t0 + u], static_cast<unsigned long long>(pc));
+        }
+        grid.sync();
+    }
+}
+
+// measured on C4 (stages, words per lane, warps per CTA): <4,4,8> 85.5 ms,
+// <4,8,4> 64.4, <4,16,2> 63.0, <2,16,2> 59.6, <3,16,2> 59.1, <1,16,2> 65.8,
+// <4,32,1> 88.0; the register-staged k_closure<4> 64.9
+template __global__ void k_closure_tma<3, 16, 2>(DevBatch, AttrScratch, int64_t, uint64_t*, int64_t, int64_t,
+                                                 unsigned long long*);
+
 // Per-task outputs of the structure pass (layers, depth, static priority).
 __global__ void k_structure_out(DevBatch b, AttrScratch s, AttrOutDev o, int32_t prio_kind, int32_t want_prio) {
     const int64_t T = b.T;

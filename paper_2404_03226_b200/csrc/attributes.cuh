@@ -114,6 +114,9 @@ enum FinPhase : int32_t { FIN_ALL = 0, FIN_PARTIAL = 1, FIN_FINISH = 2 };
 __global__ void k_finalize_large(DevBatch b, AttrScratch s, int32_t sweep_mode, AttrOutDev o, int64_t* scratch,
                                  int32_t* tab, int64_t tab_cap, int32_t* score, int32_t write_ability, int32_t phase,
                                  int32_t pos_lo, int32_t pos_hi, const int64_t* sums_in);
+template <int kStages, int CH, int kWarps>  // stages of CH x 256 B per warp (TMA bulk copies)
+__global__ void k_closure_tma(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets, int64_t wlo, int64_t whi,
+                              unsigned long long* ability);
 template <int CH>  // words per lane
 __global__ void k_closure(DevBatch b, AttrScratch s, int64_t g, uint64_t* sets, int64_t wlo, int64_t whi,
                           unsigned long long* ability);
