@@ -972,7 +972,11 @@ void launch_structure_large(tbsim_ctx* ctx, const DevBatch& d, const DevCosts* d
                             const AttrScratch& s, bool want_rank, bool sort_levels = false) {
     static int per_sm = 0;
     if (!per_sm) cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_structure_large, 512, 0), "occupancy");
-    const int grid = std::max(1, std::min(per_sm, 2)) * ctx->n_sms;
+    // one CTA per SM: the per-level grid barriers cost less with fewer
+    // participants (C4, 2 x 1024 barriers: 296 CTAs 9.3 ms, 148 8.0 ms,
+    // 64 7.6 ms, 32 11.2 ms -- below ~one warp per frontier node the
+    // levels' dependent memory chains dominate)
+    const int grid = std::max(1, std::min(per_sm, 1)) * ctx->n_sms;
     const size_t ctl_bytes = sizeof(LargeCtl) + 4 * static_cast<size_t>(grid);
     LargeCtl* ctl = static_cast<LargeCtl*>(ctx->buf("a_large_ctl").get(ctl_bytes));
     cuda_check(cudaMemsetAsync(ctl, 0, ctl_bytes, ctx->stream), "memset");
