@@ -1037,12 +1037,18 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         ctx->sync();
         const int64_t nw = (static_cast<int64_t>(d.max_n) + 63) / 64;
         const size_t need = static_cast<size_t>(std::max(gi.peak_rslots, 1)) * static_cast<size_t>(nw) * 8;
-        size_t free_b = 0, total_b = 0;
-        cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
         // the closure keeps one full-width set per live slot: a graph with a
         // very wide level cut (e.g. millions of sinks under one root) does
         // not fit, and its ability comes from the unpruned sweep instead
-        const bool fits = need <= (free_b + ctx->buf("a_sets").bytes) / 2;
+        // (free memory is queried only when the set buffer must grow:
+        // cudaMemGetInfo costs milliseconds)
+        const size_t have = ctx->buf("a_sets").bytes;
+        bool fits = need <= have;
+        if (!fits) {
+            size_t free_b = 0, total_b = 0;
+            cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+            fits = need <= (free_b + have) / 2;
+        }
         if (gi.processed == d.max_n && fits) {  // acyclic: otherwise the error path reports it
             uint64_t* sets = ctx->buf("a_sets").as<uint64_t>(need / 8);
             cuda_check(cudaMemsetAsync(o.ability, 0, static_cast<size_t>(d.T) * 8, ctx->stream), "memset ability");
