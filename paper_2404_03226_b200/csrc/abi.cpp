@@ -294,7 +294,9 @@ void ensure_packed(tbsim_ctx* ctx, tbsim_batch* b) {
     if (d.max_h > kHandleMask) raise(TBSIM_E_INVALID_ARGUMENT, "graph exceeds 2^28 handles for the simulator");
     const size_t hdr_bytes = static_cast<size_t>(d.T) * sizeof(SimTaskHdr);
     const size_t dict_at = (hdr_bytes + 255) & ~size_t(255), adj_at = dict_at + 256;
-    b->mem3 = ctx->batch_alloc(adj_at + static_cast<size_t>(adj_bytes) + 256, &b->mem3_bytes);
+    const size_t cls_at = (adj_at + static_cast<size_t>(adj_bytes) + 255) & ~size_t(255);
+    b->mem3 = ctx->batch_alloc(cls_at + static_cast<size_t>(d.H) + 256, &b->mem3_bytes);
+    uint8_t* hcls = static_cast<uint8_t*>(b->mem3) + cls_at;
     b->hdr = static_cast<SimTaskHdr*>(b->mem3);
     b->dict = reinterpret_cast<int64_t*>(static_cast<char*>(b->mem3) + dict_at);
     b->adj = reinterpret_cast<int32_t*>(static_cast<char*>(b->mem3) + adj_at);
@@ -306,13 +308,14 @@ void ensure_packed(tbsim_ctx* ctx, tbsim_batch* b) {
         const int grid_h = static_cast<int>(std::min<int64_t>((d.H + 255) / 256, 4LL * ctx->n_sms));
         ctx->begin("k_bytes_dict");
         k_bytes_dict<<<grid_h, 256, 0, ctx->stream>>>(d, reinterpret_cast<unsigned long long*>(b->dict));
+        k_bytes_class<<<grid_h, 256, 0, ctx->stream>>>(d, b->dict, hcls);
         ctx->end("k_bytes_dict");
     }
     const int grid = static_cast<int>(std::min<int64_t>((d.T + 255) / 256, 16LL * ctx->n_sms));
     // 8 lanes per task (measured 1/2/4/8: C2 0.90/0.68/0.58/0.55 ms,
     // 2048 C5 DAGs 6.5/4.7/3.2/2.5 ms)
     ctx->begin("k_sim_pack");
-    k_sim_pack<8><<<grid, 256, 0, ctx->stream>>>(d, b->dict, b->hdr, b->adj);
+    k_sim_pack<8><<<grid, 256, 0, ctx->stream>>>(d, hcls, b->hdr, b->adj);
     ctx->end("k_sim_pack");
 }
 

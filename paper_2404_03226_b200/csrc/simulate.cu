@@ -1003,16 +1003,9 @@ __device__ __forceinline__ int64_t graph_of(const DevBatch& b, int64_t t) {
 // lists); depends only on the batch, so it is built once per batch, at
 // upload (k_ingest's stream) or on first use.
 template <int TL>
-__global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* dict, SimTaskHdr* hdr, int32_t* adj) {
-    __shared__ int64_t s_dict[kByteClasses];
-    if (threadIdx.x < kByteClasses) s_dict[threadIdx.x] = dict[threadIdx.x];
-    __syncthreads();
-    // input list word: handle | byte class << 28 (escape: not in the dictionary)
-    auto word = [&](int32_t h, int64_t by) {
-        int32_t c = kEscapeClass;
-#pragma unroll
-        for (int k = kEscapeClass - 1; k >= 0; --k)
-            if (s_dict[k] == by) c = k;
+__global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const uint8_t* hcls, SimTaskHdr* hdr, int32_t* adj) {
+    // input list word: handle | size class << 28 (k_bytes_class)
+    auto word = [&](int32_t h, uint8_t c) {
         return static_cast<int32_t>(static_cast<uint32_t>(h) | (static_cast<uint32_t>(c) << kHandleBits));
     };
     // teams of TL lanes, each over a contiguous range of tasks: the team
@@ -1072,14 +1065,14 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* dic
                 const int32_t hd = tl < nin ? __ldg(&in[tl]) : 0;
                 const int32_t ov = tl < nout ? __ldg(&out[tl]) : 0;
                 const int32_t sv = tl < nsucc ? succ[tl] : 0;
-                const int64_t by = tl < nin ? __ldg(&b.handle_bytes[hb + hd]) : 0;
-                if (tl < nin) inh[tl] = word(hd, by);
+                const uint8_t cl = tl < nin ? __ldg(&hcls[hb + hd]) : 0;
+                if (tl < nin) inh[tl] = word(hd, cl);
                 if (tl < nout) outl[tl] = ov;
                 if (tl < nsucc) succl[tl] = sv;
             }
             for (int32_t k = tl + TL; k < nin; k += TL) {
                 const int32_t hd = __ldg(&in[k]);
-                inh[k] = word(hd, __ldg(&b.handle_bytes[hb + hd]));
+                inh[k] = word(hd, __ldg(&hcls[hb + hd]));
             }
             for (int32_t k = tl + TL; k < nout; k += TL) outl[k] = __ldg(&out[k]);
             for (int32_t k = tl + TL; k < nsucc; k += TL) succl[k] = succ[k];
@@ -1097,7 +1090,25 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const int64_t* dic
     }
 }
 
-template __global__ void k_sim_pack<8>(DevBatch, const int64_t*, SimTaskHdr*, int32_t*);
+template __global__ void k_sim_pack<8>(DevBatch, const uint8_t*, SimTaskHdr*, int32_t*);
+
+// Every handle's size class in the batch's (final) dictionary, once per
+// handle -- the pack then reads one byte per input instead of the 8-byte
+// size and a dictionary search per input entry.
+__global__ void __launch_bounds__(256) k_bytes_class(DevBatch b, const int64_t* dict, uint8_t* hcls) {
+    __shared__ int64_t s_dict[kByteClasses];
+    if (threadIdx.x < kByteClasses) s_dict[threadIdx.x] = dict[threadIdx.x];
+    __syncthreads();
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < b.H; i += stride) {
+        const int64_t by = __ldg(&b.handle_bytes[i]);
+        uint8_t c = kEscapeClass;
+#pragma unroll
+        for (int k = kEscapeClass - 1; k >= 0; --k)
+            if (s_dict[k] == by) c = static_cast<uint8_t>(k);
+        hcls[i] = c;
+    }
+}
 
 // A value into a dictionary of kEscapeClass slots (first come, first
 // numbered); false when it is full of other values.

@@ -155,7 +155,8 @@ struct SimParams {
 // Builds the packed records' structural words and lists (once per batch);
 // k_sim_keys fills the pop keys of one call.  One thread per task.
 template <int TL>  // lanes per task (8 instantiated)
-__global__ void k_sim_pack(DevBatch b, const int64_t* dict, SimTaskHdr* hdr, int32_t* adj);
+__global__ void k_sim_pack(DevBatch b, const uint8_t* hcls, SimTaskHdr* hdr, int32_t* adj);
+__global__ void k_bytes_class(DevBatch b, const int64_t* dict, uint8_t* hcls);
 // The batch's distinct handle sizes (first come, first numbered; at most
 // kEscapeClass of them, the rest read handle_bytes).  dict: kByteClasses
 // entries preset to kDictEmpty.
