@@ -758,6 +758,22 @@ tbsim_status tbsim_batch_generate_layered(tbsim_ctx* ctx, int32_t n, int32_t L, 
         q.hist = ctx->buf("g_hist").as<int32_t>(G * (q.max_degree + 1));
         q.edges = ctx->buf("g_edges").as<int64_t>(G);
         q.type_base = tbsim_host::T_LAYERK0;
+        // pass 1 records the draws' outcome (member bits, forced picks) so
+        // pass 2 expands them without a second replay of the generator
+        std::vector<int32_t> wl(static_cast<size_t>(L) + 1, 0);
+        for (int32_t l = 0; l < L; ++l) {
+            const int64_t members = l == 0 ? 0 : (static_cast<int64_t>(n) - 1 - (l - 1)) / L + 1;
+            wl[l + 1] = wl[l] + static_cast<int32_t>((members + 31) / 32);
+        }
+        const int64_t per_dag = static_cast<int64_t>(n / L) * wl[L] + wl[n % L];
+        int32_t* d_wl = ctx->buf("g_wl").as<int32_t>(wl.size());
+        cuda_check(cudaMemcpyAsync(d_wl, wl.data(), wl.size() * 4, cudaMemcpyHostToDevice, ctx->stream), "H2D wl");
+        q.wl_prefix = d_wl;
+        q.mask_per_dag = std::max<int64_t>(per_dag, 1);
+        q.mask = ctx->buf("g_mask").as<uint32_t>(static_cast<size_t>(G * q.mask_per_dag));
+        q.forced = ctx->buf("g_forced").as<int32_t>(std::max<int64_t>(T, 1));
+        cuda_check(cudaMemsetAsync(q.mask, 0, static_cast<size_t>(G * q.mask_per_dag) * 4, ctx->stream), "memset mask");
+        cuda_check(cudaMemsetAsync(q.forced, 0xff, static_cast<size_t>(T) * 4, ctx->stream), "memset forced");
         // fixed-size sections: bases, offsets, out, type, handle_bytes
         DevBatch& d = b->d;
         const size_t fixed = 5 * al16((G + 1) * 8) + 3 * al16((T + G) * 4) + al16(T * 4) + al16(T * 4) + al16(T * 8);
@@ -803,11 +819,12 @@ tbsim_status tbsim_batch_generate_layered(tbsim_ctx* ctx, int32_t n, int32_t L, 
         for (int64_t* dst : {edge_base, in_base})
             cuda_check(cudaMemcpyAsync(dst, ebase.data(), (G + 1) * 8, cudaMemcpyHostToDevice, ctx->stream), "H2D bases");
         b->h2d_bytes += 5 * (G + 1) * 8;
-        const size_t edge_sec = 2 * al16(E * 4) + al16((T + G) * 4) + al16(E * 4);
+        const size_t edge_sec = al16(E * 4) + al16((T + G) * 4) + al16(E * 4);
         b->mem2 = ctx->batch_alloc(edge_sec + 16, &b->mem2_bytes);
         c = static_cast<char*>(b->mem2);
         d.dep = reinterpret_cast<int32_t*>(take(E * 4));
-        d.in = reinterpret_cast<int32_t*>(take(E * 4));
+        d.in = d.dep;  // inputs are the dependencies' handles (generators.cpp:239-243)
+        d.in_off = d.dep_off;
         d.succ_off = reinterpret_cast<int32_t*>(take((T + G) * 4));
         d.succ = reinterpret_cast<int32_t*>(take(E * 4));
         d.G = G; d.T = T; d.E = E; d.H = T; d.I = E; d.O = T;
@@ -818,7 +835,7 @@ tbsim_status tbsim_batch_generate_layered(tbsim_ctx* ctx, int32_t n, int32_t L, 
         d.n_types = tbsim_host::T_COUNT;
         if (G > 0) {
             ctx->begin("k_gen_layered_fill");
-            k_gen_layered_fill<<<static_cast<unsigned>((G + 3) / 4), 128, 0, ctx->stream>>>(q, d);
+            k_gen_layered_expand<<<static_cast<unsigned>(std::min<int64_t>(G, 8LL * ctx->n_sms)), 256, 0, ctx->stream>>>(q, d);
             ctx->end("k_gen_layered_fill");
             int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(T + G);
             const int grid = static_cast<int>(std::min<int64_t>(G, 8LL * ctx->n_sms));

@@ -11,6 +11,7 @@
 // CSR entries.
 #include <cstdint>
 
+#include "blockscan.cuh"
 #include "common.cuh"
 #include "generate.cuh"
 
@@ -137,14 +138,22 @@ __global__ void __launch_bounds__(128) k_gen_layered_count(GenParams q) {
     for (int i = lane; i < n; i += 32) deg[i] = 0;
     __syncwarp();
     int64_t edges = 0;
+    uint32_t* mask = q.mask + g * q.mask_per_dag;
+    const int64_t period = q.wl_prefix[L];
     for (int i = 0; i < n; ++i) {
+        uint32_t* mi = mask + static_cast<int64_t>(i / L) * period + q.wl_prefix[i % L];
         const int c = deps_of(r, i, n, L, q.p, [&](unsigned bal, int m0, int prev) {
             if (m0 < 0) {
-                if (lane == 0) atomicAdd(&deg[prev + (-1 - m0) * L], 1);
+                if (lane == 0) {
+                    atomicAdd(&deg[prev + (-1 - m0) * L], 1);
+                    q.forced[g * n + i] = -1 - m0;
+                }
             } else if ((bal >> lane) & 1u) {
                 atomicAdd(&deg[prev + (m0 + lane) * L], 1);
+                atomicOr(&mi[(m0 + lane) >> 5], 1u << ((m0 + lane) & 31));
             }
         });
+
         if (lane == 0) {
             ndep[i] = c;
             atomicAdd(&deg[i], c);
@@ -186,50 +195,45 @@ __global__ void __launch_bounds__(128) k_gen_layered_count(GenParams q) {
     if (lane == 0) q.edges[g] = edges;
 }
 
-// Pass 2: replay the dependency draws and write the CSR entries (deps and,
-// identically, inputs; outputs are the task's own handle).
-__global__ void __launch_bounds__(128) k_gen_layered_fill(GenParams q, DevBatch b) {
-    __shared__ uint64_t mt_s[4][kNN];
-    __shared__ int32_t s_pos[4];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t g = static_cast<int64_t>(blockIdx.x) * 4 + w;
-    if (g >= q.G) return;
+// Pass 2: the CSR entries from pass 1's record -- a CTA per DAG scans the
+// dependency counts into the local offsets, then a thread per task expands
+// its member bits in ascending order (the draw order: members are drawn in
+// ascending order, so the reference appends them in that order) or writes
+// its forced pick.  Inputs alias the dependencies (same handles); output
+// t is handle t.
+__global__ void __launch_bounds__(256) k_gen_layered_expand(GenParams q, DevBatch b) {
+    __shared__ int32_t warp_tot[32];
     const int n = q.n, L = q.L;
-    WarpMT r{mt_s[w], kNN, lane};
-    r.seed(q.seeds[g]);
-    int32_t* dep = const_cast<int32_t*>(b.dep) + b.edge_base[g];
-    int32_t* in = const_cast<int32_t*>(b.in) + b.in_base[g];
-    int32_t* doff = const_cast<int32_t*>(b.dep_off) + b.task_base[g] + g;
-    int32_t* ioff = const_cast<int32_t*>(b.in_off) + b.task_base[g] + g;
-    int32_t* ooff = const_cast<int32_t*>(b.out_off) + b.task_base[g] + g;
-    int32_t* out = const_cast<int32_t*>(b.out) + b.out_base[g];
-    if (lane == 0) s_pos[w] = 0;
-    __syncwarp();
-    for (int i = 0; i < n; ++i) {
-        if (lane == 0) doff[i] = s_pos[w];
-        __syncwarp();
-        deps_of(r, i, n, L, q.p, [&](unsigned bal, int m0, int prev) {
-            const int base = s_pos[w];
-            if (m0 < 0) {
-                if (lane == 0) {
-                    dep[base] = prev + (-1 - m0) * L;
-                    in[base] = dep[base];
-                }
-            } else if ((bal >> lane) & 1u) {
-                const int k = base + __popc(bal & ((1u << lane) - 1u));
-                dep[k] = prev + (m0 + lane) * L;
-                in[k] = dep[k];
+    const int64_t period = q.wl_prefix[L];
+    for (int64_t g = blockIdx.x; g < q.G; g += gridDim.x) {
+        int32_t* doff = const_cast<int32_t*>(b.dep_off) + b.task_base[g] + g;
+        int32_t* ooff = const_cast<int32_t*>(b.out_off) + b.task_base[g] + g;
+        int32_t* out = const_cast<int32_t*>(b.out) + b.out_base[g];
+        int32_t* dep = const_cast<int32_t*>(b.dep) + b.edge_base[g];
+        for (int i = threadIdx.x; i <= n; i += blockDim.x) {
+            doff[i] = i < n ? q.ndep[g * n + i] : 0;
+            ooff[i] = i;
+            if (i < n) out[i] = i;
+        }
+        __syncthreads();
+        block_exclusive_scan_inplace(doff, n + 1, warp_tot);
+        const uint32_t* mask = q.mask + g * q.mask_per_dag;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int layer = i % L;
+            if (layer == 0) continue;
+            const int prev = layer - 1;
+            int32_t at = doff[i];
+            const int32_t f = q.forced[g * n + i];
+            if (f >= 0) {
+                dep[at] = prev + f * L;
+                continue;
             }
-            __syncwarp();
-            if (lane == 0) s_pos[w] = base + (m0 < 0 ? 1 : __popc(bal));
-            __syncwarp();
-        });
-    }
-    for (int i = lane; i <= n; i += 32) {
-        if (i == n) doff[n] = s_pos[w];
-        ioff[i] = i == n ? s_pos[w] : doff[i];
-        ooff[i] = i;
-        if (i < n) out[i] = i;
+            const int members = (n - 1 - prev) / L + 1;
+            const uint32_t* mi = mask + static_cast<int64_t>(i / L) * period + q.wl_prefix[layer];
+            for (int w = 0; w * 32 < members; ++w)
+                for (uint32_t bits = mi[w]; bits; bits &= bits - 1) dep[at++] = prev + (32 * w + __ffs(bits) - 1) * L;
+        }
+        __syncthreads();
     }
 }
 
