@@ -370,6 +370,9 @@ tbsim_status tbsim_hostbatch_add_csr(tbsim_hostbatch* hb, int32_t n_tasks,
                                      const int64_t* handle_bytes,
                                      const int64_t* task_id);
 tbsim_status tbsim_hostbatch_desc(const tbsim_hostbatch* hb, tbsim_batch_desc* out);
+/* The type-name table the batch's type ids index (default: the generators'
+ * table, tbsim_type_name); set before the first tbsim_hostbatch_desc. */
+tbsim_status tbsim_hostbatch_set_type_names(tbsim_hostbatch* hb, int32_t n, const char* const* names);
 /* Binary CSR cache (replaces re-parsing NDJSON DAG files,
  * src/dagio.cpp:86-138): save writes the packed batch (sections + type-name
  * table) to one file; load creates a batch from such a file, reading each

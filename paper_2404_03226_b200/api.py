@@ -81,6 +81,9 @@ class HostBatch:
         return self
 
     def add_batch(self, gb: GraphBatch):
+        if list(gb.type_names) != list(TYPE_NAMES):
+            names = (C.c_char_p * len(gb.type_names))(*[t.encode() for t in gb.type_names])
+            _check(load().tbsim_hostbatch_set_type_names(self._h, len(gb.type_names), names))
         for g in range(gb.n_graphs):
             one = gb._one(g)
             n = one.n_tasks

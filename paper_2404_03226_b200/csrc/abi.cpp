@@ -2209,6 +2209,15 @@ tbsim_status tbsim_hostbatch_desc(const tbsim_hostbatch* hb, tbsim_batch_desc* o
     return guarded([&] { *out = const_cast<tbsim_hostbatch*>(hb)->hb.desc(); });
 }
 
+tbsim_status tbsim_hostbatch_set_type_names(tbsim_hostbatch* hb, int32_t n, const char* const* names) {
+    return guarded([&] {
+        if (n < 0 || n > kMaxTypes) raise(TBSIM_E_INVALID_ARGUMENT, "more than 64 task types");
+        std::vector<std::string> v;
+        for (int32_t i = 0; i < n; ++i) v.push_back(names[i] ? names[i] : "type" + std::to_string(i));
+        hb->hb.set_type_names(v);
+    });
+}
+
 tbsim_status tbsim_hostbatch_save(tbsim_hostbatch* hb, const char* path) {
     return guarded([&] { hb->hb.save(path); });
 }

@@ -294,8 +294,15 @@ void HostBatch::pack() {
     desc_.type = static_cast<const int32_t*>(dst[11]);
     desc_.handle_bytes = static_cast<const int64_t*>(dst[12]);
     desc_.task_id = has_ids_ ? static_cast<const int64_t*>(dst[13]) : nullptr;
-    desc_.n_type_names = T_COUNT;
-    desc_.type_names = kTypeNames;
+    if (names_.empty()) {
+        desc_.n_type_names = T_COUNT;
+        desc_.type_names = kTypeNames;
+    } else {
+        name_ptrs_.clear();
+        for (const auto& nm : names_) name_ptrs_.push_back(nm.c_str());
+        desc_.n_type_names = static_cast<int32_t>(names_.size());
+        desc_.type_names = name_ptrs_.data();
+    }
     // the vectors are no longer needed
     std::vector<int32_t>().swap(dep_); std::vector<int32_t>().swap(in_); std::vector<int32_t>().swap(out_);
     std::vector<int32_t>().swap(dep_off_); std::vector<int32_t>().swap(in_off_); std::vector<int32_t>().swap(out_off_);
@@ -306,6 +313,11 @@ void HostBatch::pack() {
 const tbsim_batch_desc& HostBatch::desc() {
     if (!packed_) pack();
     return desc_;
+}
+
+void HostBatch::set_type_names(const std::vector<std::string>& names) {
+    if (packed_) throw std::logic_error("batch already packed");
+    names_ = names;
 }
 
 void HostBatch::alloc_pinned(size_t total) {

@@ -52,6 +52,8 @@ public:
     // NDJSON parsing.  The file carries the type-name table.
     void save(const std::string& path);
     void load(const std::string& path);
+    // the type-name table the ids index (default: the generators' table)
+    void set_type_names(const std::vector<std::string>& names);
 
 private:
     void pack();

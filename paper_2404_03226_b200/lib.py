@@ -34,7 +34,7 @@ EXPORTS = [
     "tbsim_attributes", "tbsim_simulate", "tbsim_schedule", "tbsim_default_regulator_config",
     "tbsim_hostbatch_new", "tbsim_hostbatch_free", "tbsim_hostbatch_add_layered",
     "tbsim_hostbatch_add_cholesky", "tbsim_hostbatch_add_lu", "tbsim_hostbatch_add_qr",
-    "tbsim_hostbatch_add_csr", "tbsim_hostbatch_desc", "tbsim_hostbatch_save", "tbsim_hostbatch_load",
+    "tbsim_hostbatch_add_csr", "tbsim_hostbatch_desc", "tbsim_hostbatch_save", "tbsim_hostbatch_load", "tbsim_hostbatch_set_type_names",
     "tbsim_batch_desc_save",
     "tbsim_type_count", "tbsim_type_name",
     "tbsim_default_costs",
@@ -100,6 +100,7 @@ def load():
                                           P(i32), i32, P(i64), P(i64)]
     L.tbsim_hostbatch_desc.argtypes = [vp, P(abi.BatchDesc)]
     L.tbsim_hostbatch_save.argtypes = [vp, C.c_char_p]
+    L.tbsim_hostbatch_set_type_names.argtypes = [vp, i32, P(C.c_char_p)]
     L.tbsim_hostbatch_load.argtypes = [C.c_char_p, P(vp)]
     L.tbsim_batch_desc_save.argtypes = [P(abi.BatchDesc), C.c_char_p]
     L.tbsim_type_name.restype = C.c_char_p

@@ -136,3 +136,22 @@ def test_csr_cache_round_trip_and_errors(tmp_path):
         api.HostBatch.load(str(tmp_path / "bad.csr"))
     with pytest.raises(api.TbsimError):
         api.HostBatch.load(str(tmp_path / "absent.csr"))
+
+
+def test_csr_cache_keeps_task_ids_and_custom_type_names(tmp_path):
+    """A batch built from TaskGraphs with arbitrary ids and type names (the
+    NDJSON case) round-trips through the binary cache with its id and name
+    tables."""
+    from paper_2404_03226_b200 import api
+    from paper_2404_03226_b200.batch import GraphBatch, TaskGraph, TaskNode
+    g = TaskGraph("x", [TaskNode(17, "ALPHA"), TaskNode(5, "BETA", [17], [100], [101]),
+                        TaskNode(9, "ALPHA", [17, 5], [101], [])], [(100, 64), (101, 4096)])
+    gb = GraphBatch.from_taskgraphs([g])
+    hb = api.HostBatch().add_batch(gb)
+    p = str(tmp_path / "x.csr")
+    hb.save(p)
+    back = api.HostBatch.load(p).view()
+    np.testing.assert_array_equal(back.task_id, [17, 5, 9])
+    np.testing.assert_array_equal(back.dep, gb.dep)
+    np.testing.assert_array_equal(back.handle_bytes, [64, 4096])
+    assert [back.type_names[t] for t in back.type] == [gb.type_names[t] for t in gb.type]
