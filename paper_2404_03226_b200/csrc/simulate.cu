@@ -177,9 +177,17 @@ struct Sim {
     // Over several rounds, zero terms are skipped: a resident input
     // contributes exactly +0.0 and the sum starts at +0.0 (it can never
     // become -0.0), so the in-order chain runs over non-resident inputs only.
-    __device__ __forceinline__ double transfer_total_lanes(const int32_t* inw, int32_t nin, int32_t want) const {
-        if (nin == 0) return 0.0;
-        const unsigned want_nodes = __reduce_or_sync(kFull, 1u << want);
+    // TWO: the totals for this lane's two workers' nodes (want, want2) in one
+    // pass -- two workers per lane push once instead of twice (the second
+    // total is returned through x2)
+    template <bool TWO = false>
+    __device__ __forceinline__ double transfer_total_lanes(const int32_t* inw, int32_t nin, int32_t want,
+                                                           int32_t want2 = 0, double* x2 = nullptr) const {
+        if (nin == 0) {
+            if constexpr (TWO) *x2 = 0.0;
+            return 0.0;
+        }
+        const unsigned want_nodes = __reduce_or_sync(kFull, TWO ? (1u << want) | (1u << want2) : 1u << want);
         const int32_t nw = __popc(want_nodes);
         const ResidT* rs = resid();
         if constexpr (!MANYIN) {
@@ -211,10 +219,11 @@ struct Sim {
 #pragma unroll 1
                 for (; j < nin; ++j) acc += __shfl_sync(kFull, t, b0 + j);
                 const int32_t rw = __popc(want_nodes & ((1u << want) - 1u));
+                if constexpr (TWO) *x2 = __shfl_sync(kFull, acc, __popc(want_nodes & ((1u << want2) - 1u)) * nin);
                 return __shfl_sync(kFull, acc, rw * nin);
             }
             // one pass per node, 32 inputs per round
-            double mine = 0.0;
+            double mine = 0.0, mine2 = 0.0;
             for (unsigned wn = want_nodes; wn; wn &= wn - 1) {
                 const int32_t to = __ffs(wn) - 1;
                 double acc = 0.0;
@@ -229,7 +238,9 @@ struct Sim {
                     for (int32_t j = 0; j < cnt; ++j) acc += __shfl_sync(kFull, t, j);
                 }
                 if (want == to) mine = acc;
+                if (TWO && want2 == to) mine2 = acc;
             }
+            if constexpr (TWO) *x2 = mine2;
             return mine;
         } else {
             // rounds of c inputs per node, all nodes at once
@@ -269,6 +280,7 @@ struct Sim {
                 }
             }
             const int32_t rw = __popc(want_nodes & ((1u << want) - 1u));
+            if constexpr (TWO) *x2 = __shfl_sync(kFull, acc, __popc(want_nodes & ((1u << want2) - 1u)) * c);
             return __shfl_sync(kFull, acc, rw * c);
         }
     }
@@ -414,8 +426,12 @@ struct Sim {
 #pragma unroll
         for (int j = 0; j < WPL; ++j) xfer[j] = 0.0;
         if (pol() >= TBSIM_POLICY_DMDA) {
+            if constexpr (WPL == 2) {
+                xfer[0] = transfer_total_lanes<true>(inw, nin, node_of(0), node_of(1), &xfer[1]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < WPL; ++j) xfer[j] = transfer_total_lanes(inw, nin, node_of(j));
+                for (int j = 0; j < WPL; ++j) xfer[j] = transfer_total_lanes(inw, nin, node_of(j));
+            }
         }
         uint64_t bk = ~0ull;
         int32_t bwk = INT_MAX;
