@@ -451,7 +451,8 @@ def ncu_traffic(kernel_regex, probe_args, timeout=600):
         return {"bytes": None, "error": "ncu not found"}
     with tempfile.TemporaryDirectory() as td:
         log = os.path.join(td, "t.csv")
-        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
+               "smsp__inst_executed.sum",
                "--print-units", "base", "--clock-control", "none", "-k", "regex:" + kernel_regex, "-c", "1", "--csv",
                "--log-file", log, sys.executable, os.path.abspath(__file__), "--traffic-probe"] + probe_args
         try:
@@ -469,6 +470,8 @@ def ncu_traffic(kernel_regex, probe_args, timeout=600):
             return {"bytes": int(b), "read": int(vals["dram__bytes_read.sum"]),
                     "write": int(vals["dram__bytes_write.sum"]), "kernel": name,
                     "ncu_ms": vals.get("gpu__time_duration.sum", 0.0) / 1e6,
+                    "warp_instructions": int(vals["smsp__inst_executed.sum"]) if "smsp__inst_executed.sum" in vals
+                    else None,
                     "method": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum -c 1, live child run of this "
                               "build (cold caches; duration under ncu is not a timing)"}
         except Exception as e:
@@ -952,6 +955,21 @@ def main():
     # timing: ncu only counts bytes)
     traffic = ncu_traffic(KERNEL_REGEX[dominant], ["--workload", "c2", "--n-dags", str(G)]) \
         if rank == 0 and not args.no_traffic else {"bytes": None, "skipped": "--no-traffic or rank > 0"}
+    # the simulator's actual limit: warp-instruction issue (one per cycle
+    # per SM sub-partition), from the same live ncu run's instruction count
+    # and this run's event-timed kernel at the sampled SM clock
+    issue_roof = None
+    if traffic.get("warp_instructions"):
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        mhz = clk.summary().get("sm_mhz") or 1965.0
+        ipk = traffic["warp_instructions"]
+        ach = ipk / (kms[dominant] * 1e-3)
+        pk = 4.0 * sms * mhz * 1e6
+        issue_roof = {"bound": "issue", "kernel": dominant, "warp_instructions": ipk,
+                      "per_decision": ipk / (2.0 * G * w["n_tasks"]) if dominant == "k_simulate" else None, "achieved": ach, "peak": pk,
+                      "unit": "warp-instructions/s", "frac": ach / pk,
+                      "peak_source": f"4 SMSPs x {sms} SMs x 1 issue/cycle at the sampled {mhz:.0f} MHz",
+                      "note": "28 DAG warps per SM share the issue slots; time ~ instructions per decision"}
     if rank == 0:
         line = {
             "metric": "DAGs scheduled/sec", "value": value, "unit": "DAGs/s", "n_gpus": world,
@@ -974,6 +992,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback 6650 GB/s",
                          "note": "latency/issue-bound event simulation and FP64 sweep; see DESIGN.md §4"},
             "kernel_ms": kms,
+            "issue_roofline": issue_roof,
             "sweep_roofline": sweep_roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "DAGs/s", "h2d_bytes_per_step": int(h2d),
