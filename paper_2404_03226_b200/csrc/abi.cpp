@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "generate.cuh"
 #include "hostbatch.hpp"
+#include "rules.cuh"
 #include "simulate.cuh"
 
 using namespace tbsim_dev;
@@ -317,16 +318,6 @@ void ensure_packed(tbsim_ctx* ctx, tbsim_batch* b) {
     ctx->begin("k_sim_pack");
     k_sim_pack<8><<<grid, 256, 0, ctx->stream>>>(d, hcls, b->hdr, b->adj);
     ctx->end("k_sim_pack");
-}
-
-std::string type_name(const tbsim_batch* b, int32_t ty) {
-    if (ty >= 0 && ty < static_cast<int32_t>(b->type_names.size())) return b->type_names[ty];
-    return "type" + std::to_string(ty);
-}
-
-int64_t task_ident(const tbsim_batch* b, int64_t g, int64_t pos) {
-    const int64_t t = b->task_base[g] + pos;
-    return b->task_id.empty() ? pos : b->task_id[t];
 }
 
 DevCosts to_dev_costs(const tbsim_costs& c, int32_t n_types_batch) {
@@ -2124,17 +2115,9 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
 
 extern "C" tbsim_status tbsim_default_regulator_config(int32_t n_workers, double median, tbsim_regulator_cfg* out) {
     return guarded([&] {
-        // default_regulator_config, src/policies.cpp:139-151
-        const int64_t n = n_workers;
-        const int64_t tw = std::max<int64_t>(2, (n + 3) / 4);
-        *out = tbsim_regulator_cfg{};
-        out->task_window = tw;
-        out->s_inc = n;
-        out->k_inc = static_cast<double>(n) / median;
-        out->s_dec = tw;
-        out->c = (tw + 1) / 2;
-        out->dec_step = tw;
-        out->slope_samples = 8;
+        // default_regulator_config, src/policies.cpp:139-151 (shared with the
+        // device's default in simulate.cu)
+        *out = tbsim_rules::default_config(n_workers, median);
     });
 }
 

@@ -27,6 +27,7 @@
 
 #include "blockscan.cuh"
 #include "common.cuh"
+#include "rules.cuh"
 #include "simulate.cuh"
 
 namespace tbsim_dev {
@@ -299,34 +300,17 @@ struct Sim {
             total += by;
             if ((static_cast<uint32_t>(rs[wd & kHandleMask]) >> nd) & 1u) local += by;
         }
-        return static_cast<double>(local) / static_cast<double>(total);
+        return tbsim_rules::resident_fraction(local, total);
     }
 
     // ---------------------------------------------------------- regulator
     __device__ __forceinline__ double calculate_k(const SimCold& c) const {  // policies.cpp:153-169
-        if (c.r_count < 2) return 0.0;
-        const int ring_mask = P->ring - 1;
+        const int ring_mask = P->ring - 1, head = c.r_head;
         const double* st = samp_t();
         const int64_t* sn = samp_n();
-        double sx = 0.0, sy = 0.0;
-#pragma unroll 1
-        for (int i = 0; i < c.r_count; ++i) {
-            const int idx = (c.r_head + i) & ring_mask;
-            sx += st[idx];
-            sy += static_cast<double>(sn[idx]);
-        }
-        const double dn = static_cast<double>(c.r_count);
-        const double mx = sx / dn, my = sy / dn;
-        double sxx = 0.0, sxy = 0.0;
-#pragma unroll 1
-        for (int i = 0; i < c.r_count; ++i) {
-            const int idx = (c.r_head + i) & ring_mask;
-            const double dx = st[idx] - mx;
-            sxx += dx * dx;
-            sxy += dx * (static_cast<double>(sn[idx]) - my);
-        }
-        if (sxx == 0.0) return 0.0;
-        return sxy / sxx;
+        return tbsim_rules::slope(
+            c.r_count, [&](int32_t i) { return st[(head + i) & ring_mask]; },
+            [&](int32_t i) { return sn[(head + i) & ring_mask]; });
     }
 
     // regulator_step (policies.cpp:171-203).  Every lane computes the same
@@ -343,8 +327,7 @@ struct Sim {
             r_head = (r_head + 1) & ring_mask;
             --r_count;
         }
-        const int64_t last = c.last_trigger;
-        const int64_t d = cur - last;
+        const bool fires = tbsim_rules::regulator_fires(cur, c.last_trigger, c.cfg);
         __syncwarp();
         if (lane == 0) {
             samp_t()[idx] = now;
@@ -352,37 +335,24 @@ struct Sim {
             c.r_head = r_head;
             c.r_count = r_count;
         }
-        if ((d < 0 ? -d : d) < c.cfg.task_window) {
+        if (!fires) {
             __syncwarp();
             return;
         }
-        int64_t peak = c.peak, s_dec_count = c.s_dec_count;
-        peak = cur > peak ? cur : peak;
-        const int32_t phase = cur >= peak - c.cfg.dec_step ? TBSIM_PHASE_INC : TBSIM_PHASE_DEC;
-        double cur_k = c.cur_k;
-        if (phase == TBSIM_PHASE_INC) {
-            if (cur - c.prev_nready >= c.cfg.s_inc) {
-                __syncwarp();  // the sample just written
-                cur_k = calculate_k(c);
-                if (cur_k < c.cfg.k_inc) mode = TBSIM_MODE_EFFICIENCY;
-                else if (cur_k > c.cfg.k_inc) mode = TBSIM_MODE_ABILITY;
-            }
-        } else {
-            if (cur > peak - c.cfg.s_dec * s_dec_count) {
-                mode = TBSIM_MODE_ABILITY;
-            } else if (cur <= peak - c.cfg.s_dec * (s_dec_count + 1) + c.cfg.c) {
-                mode = TBSIM_MODE_LOCALITY;
-                if (cur <= peak - c.cfg.s_dec * (s_dec_count + 1)) s_dec_count += 1;
-            }
-        }
+        tbsim_rules::RegScalars rs{mode, c.phase, c.peak, c.prev_nready, c.last_trigger, c.s_dec_count, c.cur_k};
+        tbsim_rules::regulator_update(rs, c.cfg, cur, [&] {
+            __syncwarp();  // the sample just written
+            return calculate_k(c);
+        });
+        mode = rs.mode;
         __syncwarp();
         if (lane == 0) {
-            c.last_trigger = cur;
-            c.peak = peak;
-            c.phase = phase;
-            c.cur_k = cur_k;
-            c.s_dec_count = s_dec_count;
-            c.prev_nready = cur;
+            c.last_trigger = rs.last_trigger;
+            c.peak = rs.peak;
+            c.phase = rs.phase;
+            c.cur_k = rs.cur_k;
+            c.s_dec_count = rs.s_dec_count;
+            c.prev_nready = rs.prev_nready;
         }
         __syncwarp();
     }
@@ -443,12 +413,11 @@ struct Sim {
             if (!(ce > 0.0)) continue;
             double key;
             if (pol() == TBSIM_POLICY_FIFO) {
-                key = static_cast<double>(qlen[j]) + (busy_of(j) ? 1.0 : 0.0);
+                key = tbsim_rules::fifo_key(qlen[j], busy_of(j));
             } else {
                 const double fa = busy_of(j) ? fsum[j] : now;
-                const double st = now < fa ? fa : now;  // std::max(now, free_at)
-                if (pol() == TBSIM_POLICY_DM) key = st + ce;
-                else key = (st + xfer[j]) + ce;
+                if (pol() == TBSIM_POLICY_DM) key = tbsim_rules::dm_key(now, fa, ce);
+                else key = tbsim_rules::dmda_key(now, fa, xfer[j], ce);
             }
             const uint64_t kb = ord_f64(key);
             if (kb < bk) { bk = kb; bwk = w; }
@@ -492,15 +461,12 @@ struct Sim {
             uint64_t k0, k1;
             if (pol() == TBSIM_POLICY_DMDAP) {
                 k0 = k1 = 1;
-            } else if (m == TBSIM_MODE_ABILITY) {
-                k0 = ord_f64(static_cast<double>(ka[i]));
-                k1 = ord_f64(0.0);
-            } else if (m == TBSIM_MODE_EFFICIENCY) {
-                k0 = ord_f64(static_cast<double>(ke[i]));
-                k1 = ord_f64(0.0);
             } else {
-                k0 = ord_f64(resident_fraction(q[i] & 0xffffff, nd));
-                k1 = ord_f64(static_cast<double>(ke[i]));
+                double d0, d1;
+                tbsim_rules::adaptive_key(m, static_cast<double>(ka[i]), static_cast<double>(ke[i]),
+                                          [&] { return resident_fraction(q[i] & 0xffffff, nd); }, d0, d1);
+                k0 = ord_f64(d0);
+                k1 = ord_f64(d1);
             }
             const uint64_t k2 = ord_i64(COMPACT ? prio_of(q[i] & 0xffffff) : static_cast<int64_t>(kp[i]));
             const bool better = bpos == INT_MAX || k0 > b0 ||
@@ -911,15 +877,7 @@ __device__ void simulate_impl(const SimParams& p) {
             if (p.reg) {
                 c.cfg = p.reg[g];
             } else {
-                const int64_t nw = W;
-                const int64_t tw = (nw + 3) / 4 > 2 ? (nw + 3) / 4 : 2;
-                c.cfg.task_window = tw;
-                c.cfg.s_inc = nw;
-                c.cfg.k_inc = static_cast<double>(nw) / p.median[g * p.median_stride];
-                c.cfg.s_dec = tw;
-                c.cfg.c = (tw + 1) / 2;
-                c.cfg.dec_step = tw;
-                c.cfg.slope_samples = 8;
+                c.cfg = tbsim_rules::default_config(W, p.median[g * p.median_stride]);
             }
         }
         // regulator state: caller-provided (in/out) or RegulatorState{}
