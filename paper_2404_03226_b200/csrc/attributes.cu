@@ -34,6 +34,7 @@
 #include "attributes.cuh"
 #include "blockscan.cuh"
 #include "common.cuh"
+#include "rules.cuh"
 
 namespace tbsim_dev {
 
@@ -205,11 +206,9 @@ __device__ void load_costs(const DevCosts* costs_g, int32_t ci, DevCosts& sc, do
         reinterpret_cast<double*>(&sc)[i] = reinterpret_cast<const double*>(costs_g + ci)[i];
     __syncthreads();
     if (tid < kMaxTypes) {
-        double sum = 0.0;
-        int cnt = 0;
-        if (tid < sc.n_types && sc.cpu[tid] > 0.0) { sum += sc.cpu[tid]; ++cnt; }
-        if (tid < sc.n_types && sc.gpu[tid] > 0.0) { sum += sc.gpu[tid]; ++cnt; }
-        s_mean[tid] = cnt ? sum / cnt : 0.0;
+        const bool in = tid < sc.n_types;
+        s_mean[tid] = tbsim_rules::mean_cost_ms(in && sc.cpu[tid] > 0.0, sc.cpu[tid], in && sc.gpu[tid] > 0.0,
+                                                sc.gpu[tid]);
     }
     __syncthreads();
 }
@@ -1999,7 +1998,7 @@ __global__ void k_structure_out(DevBatch b, AttrScratch s, AttrOutDev o, int32_t
         if (o.depth) o.depth[i] = s.height[i];
         if (want_prio && o.static_priority) {
             int64_t p = 0;
-            if (prio_kind == TBSIM_PRIO_UPWARD_RANK) p = static_cast<int64_t>(s.rank[i] * 1000.0);
+            if (prio_kind == TBSIM_PRIO_UPWARD_RANK) p = tbsim_rules::rank_priority(s.rank[i]);
             else if (prio_kind == TBSIM_PRIO_DEPTH) p = s.height[i];
             o.static_priority[i] = p;
         }

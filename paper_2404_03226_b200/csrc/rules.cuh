@@ -71,6 +71,26 @@ TBSIM_HD double resident_fraction(int64_t local_bytes, int64_t total_bytes) {
     return static_cast<double>(local_bytes) / static_cast<double>(total_bytes);
 }
 
+// ---------------------------------------------------------- cost model
+// Platform::transfer_time_ms between distinct nodes (src/platform.cpp:56-63)
+TBSIM_HD double transfer_ms(double latency_ms, int64_t bytes, double bandwidth) {
+    return latency_ms + static_cast<double>(bytes) / bandwidth;
+}
+
+// CostTable::mean_ms (src/platform.cpp:39-50): the mean over the kinds that
+// have an entry, CPU first; 0 when neither has one (the host API throws)
+TBSIM_HD double mean_cost_ms(bool has_cpu, double cpu_ms, bool has_gpu, double gpu_ms) {
+    double sum = 0.0;
+    int n = 0;
+    if (has_cpu) { sum += cpu_ms; ++n; }
+    if (has_gpu) { sum += gpu_ms; ++n; }
+    return n ? sum / n : 0.0;
+}
+
+// upward_rank_priority (src/attributes.cpp:234-253): rank ms -> int64 by
+// truncation of rank * 1000
+TBSIM_HD int64_t rank_priority(double rank_ms) { return static_cast<int64_t>(rank_ms * 1000.0); }
+
 // ------------------------------------------------------------- regulator
 // default_regulator_config (src/policies.cpp:139-151)
 TBSIM_HD tbsim_regulator_cfg default_config(int64_t n_workers, double median_gpu_ms) {

@@ -167,7 +167,7 @@ struct Sim {
             const int32_t mn = P->max_nodes;
             return __ldg(&cold().xt[(cls * mn + best) * mn + to]);
         }
-        return cold().lat + static_cast<double>(bytes_of(word)) / bw(best * nn + to);
+        return tbsim_rules::transfer_ms(cold().lat, bytes_of(word), bw(best * nn + to));
     }
 
     // transfer_total_ms (engine.cpp:105-110) for node `want` (may differ per
@@ -1128,7 +1128,7 @@ __global__ void k_xfer_table(const DevPlatform* pf, int32_t n_platforms, const i
         double t = 0.0;
         const int64_t by = dict[cls];
         if (from != to && from < P.n_nodes && to < P.n_nodes && by != kDictEmpty)
-            t = P.latency_ms + static_cast<double>(by) / P.bw[from * kMaxNodes + to];
+            t = tbsim_rules::transfer_ms(P.latency_ms, by, P.bw[from * kMaxNodes + to]);
         xtab[i] = t;
     }
 }
