@@ -702,3 +702,76 @@ def test_async_schedule_reruns_queue_overflows_on_the_device(ctx):
     for k in ("worker", "start_ms", "end_ms", "makespan_ms", "completed"):
         eq(got[k], want[k], k)
     assert rerun_ms > 0.0
+
+
+def _edge_shapes():
+    """Degenerate shapes the reference accepts: an empty graph, one task,
+    no edges, a chain, a star (one source, 49 sinks) and a join (50 sources
+    into one task)."""
+    return [TaskGraph("empty", []),
+            TaskGraph("one", [TaskNode(0, "UNIT")]),
+            TaskGraph("flat", [TaskNode(i, "LAYERK1") for i in range(40)]),
+            TaskGraph("chain", [TaskNode(i, "LAYERK2", [i - 1] if i else []) for i in range(60)]),
+            TaskGraph("star", [TaskNode(0, "LAYERK3")] + [TaskNode(i, "LAYERK0", [0]) for i in range(1, 50)]),
+            TaskGraph("join", [TaskNode(i, "LAYERK0") for i in range(50)] + [TaskNode(50, "LAYERK3", list(range(50)))])]
+
+
+def test_degenerate_shapes_match_oracle(ctx):
+    b = GraphBatch.from_taskgraphs(_edge_shapes(), P.TYPE_NAMES)
+    costs = P.default_cost_table()
+    db = ctx.upload(b)
+    for req, keys in ((abi.ATTR_ABILITY, ("ability",)), (abi.ATTR_LAYERS, ("layer",)), (abi.ATTR_DEPTH, ("depth",))):
+        g, o = ctx.attributes(db, costs, req), po.attributes(b, costs, req)
+        for k in keys:
+            eq(g[k], o[k], k)
+    pls = [P.make_preset("26cpu_2gpu"), P.make_preset("homog2")]
+    pof = np.arange(b.n_graphs) % 2
+    reg = [abi.RegulatorCfg(task_window=2, s_inc=4, k_inc=1.0, s_dec=2, c=1, dec_step=2, slope_samples=8)] * b.n_graphs
+    for pol in abi.POLICIES:
+        g = ctx.simulate(db, pls, pol, reg, platform_of=pof, record=True)
+        o = po.simulate(b, pls, pol, platform_of=pof, reg=reg, record=True)
+        for k in SIM_KEYS:
+            eq(g[k], o[k], f"{pol}/{k}")
+    # the full pipeline on the non-empty shapes (an empty graph has no median)
+    nb = GraphBatch.from_taskgraphs(_edge_shapes()[1:], P.TYPE_NAMES)
+    ndb = ctx.upload(nb)
+    oa = po.attributes(nb, costs, abi.ATTR_ALL)
+    ga = ctx.attributes(ndb, costs, abi.ATTR_ALL)
+    for k in ("ability", "efficiency", "static_priority", "unit_time_ms"):
+        eq(ga[k], oa[k], k)
+    r = ctx.schedule(ndb, [pls[0]], "inspirit")
+    nreg = [po.default_regulator_config(nb, i, pls[0]) for i in range(nb.n_graphs)]
+    o = po.simulate(nb, [pls[0]], "inspirit", reg=nreg, attrs=oa, record=False)
+    for k in ("worker", "start_ms", "end_ms", "makespan_ms"):
+        eq(r[k], o[k], k)
+
+
+def test_wide_state_simulators_match_oracle(ctx):
+    """The non-compact simulator kernels (32-bit unmet counters, 64-bit
+    event slots): graphs of >= 32768 tasks, and platforms of more than 8
+    memory nodes, each with one and with two workers per lane."""
+    costs = P.default_cost_table()
+    # more than 8 memory nodes: random graphs on 4c9g (13 workers) and 32c9g (41)
+    b = random_graphs(11, 24)
+    pls = [P.assemble("4c9g", 4, 9), P.assemble("32c9g", 32, 9)]
+    db = ctx.upload(b)
+    oa = po.attributes(b, costs, abi.ATTR_ALL)
+    for pl in pls:
+        reg = [po.default_regulator_config(b, g, pl) for g in range(b.n_graphs)]
+        for pol in abi.POLICIES:
+            g = ctx.simulate(db, [pl], pol, reg, attrs=oa, record=True)
+            o = po.simulate(b, [pl], pol, reg=reg, attrs=oa, record=True)
+            for k in SIM_KEYS:
+                eq(g[k], o[k], f"{pl.name}/{pol}/{k}")
+    # >= 32768 tasks (the attributes are the device's, pinned elsewhere)
+    hb = api.HostBatch().add_layered(40000, 40, 0.002, 3)
+    lb = hb.view()
+    ldb = ctx.upload(hb)
+    ga = ctx.attributes(ldb, costs, abi.ATTR_ALL)
+    for pl in (P.assemble("4c1g", 4, 1), P.assemble("32c4g", 32, 4)):
+        reg = [po.default_regulator_config(lb, 0, pl)]
+        for pol in ("dmda", "inspirit"):
+            g = ctx.simulate(ldb, [pl], pol, reg, attrs=ga, record=True)
+            o = po.simulate(lb, [pl], pol, reg=reg, attrs=ga, record=True)
+            for k in SIM_KEYS:
+                eq(g[k], o[k], f"40k/{pl.name}/{pol}/{k}")
