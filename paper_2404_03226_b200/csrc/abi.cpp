@@ -1641,6 +1641,12 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
                         : (w2 ? k_simulate_w2 : k_simulate_w1);
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "cudaFuncSetAttribute(k_simulate)");
+    // HBM (L2-resident) state: every byte of the SM's unified L1/shared
+    // array as L1, which caches the warps' state lines; shared-memory state:
+    // the runtime's choice for the requested size
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    p.use_smem ? -1 : static_cast<int>(cudaSharedmemCarveoutMaxL1)),
+               "cudaFuncSetAttribute(k_simulate carveout)");
     ctx->begin(name);
     kern<<<grid, kThreads, smem, ctx->stream>>>(p);
     ctx->end(name);
