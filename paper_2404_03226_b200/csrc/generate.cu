@@ -96,8 +96,18 @@ struct WarpMT {
 // Draws for task i's dependencies: one uniform01 per member of layer-1,
 // chosen when < p; a forced member when none is chosen.  emit(lane_mask of
 // chosen members in this chunk, member base) is called per chunk.
+// uniform01(x) < p (generators.cpp:20-22: (x >> 11) * 2^-53 < p) as one
+// integer compare: k = x >> 11 < 2^53 is exact in a double and the scaling
+// by 2^-53 is exact, so k * 2^-53 < p  <=>  k < p * 2^53  <=>  k < ceil(p * 2^53)
+__device__ __forceinline__ uint64_t uniform01_threshold(double p) {
+    const double s = p * 0x1.0p53;                  // exact (power-of-two scale)
+    if (!(s > 0.0)) return 0;                       // p <= 0 or NaN: never taken
+    if (s >= 0x1.0p53) return uint64_t(1) << 53;    // p >= 1: always taken
+    return static_cast<uint64_t>(ceil(s));
+}
+
 template <typename Emit>
-__device__ int deps_of(WarpMT& r, int i, int n, int L, double p, Emit emit) {
+__device__ int deps_of(WarpMT& r, int i, int n, int L, uint64_t pt, Emit emit) {
     const int layer = i % L;
     if (layer == 0) return 0;
     const int prev = layer - 1;
@@ -106,7 +116,7 @@ __device__ int deps_of(WarpMT& r, int i, int n, int L, double p, Emit emit) {
     for (int m0 = 0; m0 < members;) {
         uint64_t x = 0;
         const int got = r.take(members - m0, &x);
-        const bool hit = r.lane < got && static_cast<double>(x >> 11) * 0x1.0p-53 < p;
+        const bool hit = r.lane < got && (x >> 11) < pt;
         const unsigned bal = __ballot_sync(0xffffffffu, hit);
         emit(bal, m0, prev);
         taken += __popc(bal);
@@ -138,11 +148,12 @@ __global__ void __launch_bounds__(128) k_gen_layered_count(GenParams q) {
     for (int i = lane; i < n; i += 32) deg[i] = 0;
     __syncwarp();
     int64_t edges = 0;
+    const uint64_t pt = uniform01_threshold(q.p);
     uint32_t* mask = q.mask + g * q.mask_per_dag;
     const int64_t period = q.wl_prefix[L];
     for (int i = 0; i < n; ++i) {
         uint32_t* mi = mask + static_cast<int64_t>(i / L) * period + q.wl_prefix[i % L];
-        const int c = deps_of(r, i, n, L, q.p, [&](unsigned bal, int m0, int prev) {
+        const int c = deps_of(r, i, n, L, pt, [&](unsigned bal, int m0, int prev) {
             if (m0 < 0) {
                 if (lane == 0) {
                     atomicAdd(&deg[prev + (-1 - m0) * L], 1);
