@@ -46,6 +46,26 @@ void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) raise(TBSIM_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Makes the context's device current for one ABI call and restores the
+// caller's device afterwards (a host thread driving several GPUs, or a
+// framework with its own current device, keeps it across our calls).
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        int cur = -1;
+        if (cudaGetDevice(&cur) != cudaSuccess) cur = -1;
+        if (cur != dev) {
+            cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+            prev = cur;
+        }
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceScope(const DeviceScope&) = delete;
+    DeviceScope& operator=(const DeviceScope&) = delete;
+};
+
 template <typename F>
 tbsim_status guarded(F&& f) {
     try {
@@ -121,6 +141,10 @@ struct tbsim_ctx {
     int64_t large_threshold = 65536;  // single graphs at least this large take the closure path
     int32_t sweep_tile = 0;           // forced sources per sweep tile (0: widest that fits)
     int32_t sim_warps_per_sm = 0, sim_state_smem = 0, sim_qcap = 0;  // last k_simulate launch shape
+    // per-device launch facts (function attributes are per device, so they
+    // live with the context, not in process-wide statics)
+    bool sweep_attr = false, sweep32_attr = false;
+    int structure_large_per_sm = 0, finalize_large_per_sm = 0;
     // Asynchronous results (tbsim_ctx_set_async_results): host-bound outputs
     // of tbsim_schedule are staged in one of two device buffer sets and copied
     // on the download stream, so a call's D2H overlaps the next call's
@@ -406,7 +430,7 @@ tbsim_status tbsim_ctx_create(int device, tbsim_ctx** out) {
         if (device < 0 || device >= n) raise(TBSIM_E_INVALID_ARGUMENT, "bad device index");
         auto c = std::make_unique<tbsim_ctx>();
         c->device = device;
-        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        DeviceScope dev_scope(device);
         cudaDeviceProp prop;
         cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
         if (prop.major < 10)
@@ -423,7 +447,7 @@ tbsim_status tbsim_ctx_create(int device, tbsim_ctx** out) {
 tbsim_status tbsim_ctx_destroy(tbsim_ctx* ctx) {
     return guarded([&] {
         if (!ctx) return;
-        cudaSetDevice(ctx->device);
+        DeviceScope dev_scope(ctx->device);
         cudaStreamSynchronize(ctx->stream);
         for (auto& [k, b] : ctx->bufs) b.release();
         if (ctx->upload) cudaStreamSynchronize(ctx->upload);
@@ -461,6 +485,7 @@ tbsim_status tbsim_ctx_set_upload_stream(tbsim_ctx* ctx, void* s) {
 
 tbsim_status tbsim_ctx_synchronize(tbsim_ctx* ctx) {
     return guarded([&] {
+        DeviceScope dev_scope(ctx->device);
         ctx->sync();
         if (ctx->download) cuda_check(cudaStreamSynchronize(ctx->download), "cudaStreamSynchronize(download)");
         // deferred checks of asynchronous calls, oldest first; both are
@@ -480,7 +505,7 @@ tbsim_status tbsim_ctx_synchronize(tbsim_ctx* ctx) {
 
 tbsim_status tbsim_ctx_set_async_results(tbsim_ctx* ctx, int enable) {
     return guarded([&] {
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DeviceScope dev_scope(ctx->device);
         if (enable && !ctx->download) {
             cuda_check(cudaStreamCreateWithFlags(&ctx->download, cudaStreamNonBlocking), "cudaStreamCreate");
             for (auto& e : ctx->set_free)
@@ -512,7 +537,7 @@ tbsim_status tbsim_ctx_set_timing(tbsim_ctx* ctx, int enable) {
 
 tbsim_status tbsim_probe_sweep_peak(tbsim_ctx* ctx, int32_t repeats, double* fp64_per_s, double* fp32_per_s) {
     return guarded([&] {
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DeviceScope dev_scope(ctx->device);
         constexpr int32_t kRows = 128, kIters = 20000, kThreads = 512;
         double* out = ctx->buf("p_out").as<double>(ctx->n_sms);
         cudaEvent_t e0, e1;
@@ -570,7 +595,7 @@ tbsim_status tbsim_ctx_last_kernel_ms(const tbsim_ctx* ctx, const char* kernel, 
 
 tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim_batch** out) {
     return guarded([&] {
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DeviceScope dev_scope(ctx->device);
         // copies + ingest on the upload stream; compute calls wait on b->ready
         UploadStream us(ctx);
         const int64_t G = h->n_graphs;
@@ -666,6 +691,8 @@ tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim
 tbsim_status tbsim_batch_free(tbsim_ctx* ctx, tbsim_batch* b) {
     return guarded([&] {
         if (!b) return;
+        std::unique_ptr<DeviceScope> dev_scope;
+        if (ctx) dev_scope = std::make_unique<DeviceScope>(ctx->device);
         if (ctx) {
             // stream-ordered reuse: a later upload waits for every kernel
             // that reads this batch (all on the compute stream)
@@ -699,6 +726,7 @@ tbsim_status tbsim_batch_sizes(const tbsim_batch* b, int64_t* s) {
 
 tbsim_status tbsim_batch_download(tbsim_ctx* ctx, const tbsim_batch* b, tbsim_batch_desc* h) {
     return guarded([&] {
+        DeviceScope dev_scope(ctx->device);
         wait_batch(ctx, b);
         const DevBatch& d = b->d;
         const int64_t G = d.G, T = d.T;
@@ -731,7 +759,7 @@ tbsim_status tbsim_batch_generate_layered(tbsim_ctx* ctx, int32_t n, int32_t L, 
         if (n < L) raise(TBSIM_E_INVALID_ARGUMENT, "autogen: n_tasks must be >= n_layers");
         if (!(p >= 0.0 && p <= 1.0)) raise(TBSIM_E_INVALID_ARGUMENT, "autogen: edge_prob must be in [0,1]");
         if (n >= (1 << 24)) raise(TBSIM_E_INVALID_ARGUMENT, "graph exceeds 2^24 tasks");
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DeviceScope dev_scope(ctx->device);
         const int64_t G = n_seeds, T = G * n;
         auto b = std::make_unique<tbsim_batch>();
         GenParams q{};
@@ -850,7 +878,7 @@ tbsim_status tbsim_batch_generate_tiled(tbsim_ctx* ctx, int32_t kind, int32_t nb
         if (count < 0) raise(TBSIM_E_INVALID_ARGUMENT, "negative graph count");
         const int64_t n64 = tiled_task_count(kind, nb);
         if (n64 >= (1 << 24)) raise(TBSIM_E_INVALID_ARGUMENT, "graph exceeds 2^24 tasks");
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DeviceScope dev_scope(ctx->device);
         const int32_t n = static_cast<int32_t>(n64);
         const int32_t nh = kind == TBSIM_TILED_CHOLESKY ? nb * (nb + 1) / 2 : nb * nb;
         const int64_t G = count, T = G * n, H = G * nh;
@@ -981,7 +1009,7 @@ int64_t sweep_smem_bytes(tbsim_ctx* ctx) {
 // One large graph: the structure pass with the whole GPU (cooperative).
 void launch_structure_large(tbsim_ctx* ctx, const DevBatch& d, const DevCosts* d_costs, const int32_t* d_cost_idx,
                             const AttrScratch& s, bool want_rank, bool sort_levels = false) {
-    static int per_sm = 0;
+    int& per_sm = ctx->structure_large_per_sm;
     if (!per_sm) cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_structure_large, 512, 0), "occupancy");
     // one CTA per SM: the per-level grid barriers cost less with fewer
     // participants (C4, 2 x 1024 barriers: 296 CTAs 9.3 ms, 148 8.0 ms,
@@ -1112,11 +1140,10 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         unsigned long long* counter = ctx->buf("a_counter").as<unsigned long long>(1);
         cuda_check(cudaMemsetAsync(counter, 0, 8, ctx->stream), "memset");
         const int64_t total_tiles = -1;  // read on the device from tile_base[G]
-        static bool attr_set = false;
-        if (!attr_set) {
+        if (!ctx->sweep_attr) {
             cuda_check(cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                        "cudaFuncSetAttribute(k_sweep)");
-            attr_set = true;
+            ctx->sweep_attr = true;
         }
         // executed relaxations (rows x columns) when timing: the sweep's
         // achieved rate for bench.py's roofline
@@ -1126,11 +1153,10 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
             cuda_check(cudaMemsetAsync(relax_ctr, 0, 16, ctx->stream), "memset");
             ctx->relax_ctr = relax_ctr;
         }
-        static bool attr_set32 = false;
-        if (!attr_set32) {
+        if (!ctx->sweep32_attr) {
             cuda_check(cudaFuncSetAttribute(k_sweep_fp32, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                        "cudaFuncSetAttribute(k_sweep_fp32)");
-            attr_set32 = true;
+            ctx->sweep32_attr = true;
         }
         // both launched: the plan (device) selects one, the other returns
         ctx->begin("k_sweep");
@@ -1144,7 +1170,7 @@ void run_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const DevCosts* d_cost
         int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride * grid_g);
         const int32_t write_ab = (prune || ability_done) ? 0 : 1;
         if (G == 1 && d.max_n >= ctx->large_threshold) {
-            static int per_sm = 0;
+            int& per_sm = ctx->finalize_large_per_sm;
             if (!per_sm)
                 cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_finalize_large, 512, 0), "occupancy");
             const int grid = std::max(1, std::min(per_sm, 2)) * ctx->n_sms;
@@ -1246,7 +1272,7 @@ T* stage_out(tbsim_ctx* ctx, OutStage& st, const char* name, T* host, size_t cou
 extern "C" tbsim_status tbsim_attributes(tbsim_ctx* ctx, const tbsim_batch* b, const tbsim_costs* costs,
                                          int32_t request, int32_t priority_kind, tbsim_attr_out* out) {
     return guarded([&] {
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DeviceScope dev_scope(ctx->device);
         wait_batch(ctx, b);
         const DevBatch& d = b->d;
         const int64_t T = d.T, G = d.G;
@@ -1353,7 +1379,7 @@ extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbs
                                                        int32_t rank, int32_t world, int64_t* ability_partial,
                                                        int64_t* class_sums, int64_t cap, int64_t* n_words) {
     return guarded([&] {
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DeviceScope dev_scope(ctx->device);
         wait_batch(ctx, b);
         const DevBatch& d = b->d;
         if (d.G != 1) raise(TBSIM_E_INVALID_ARGUMENT, "sharded attributes take a batch of one graph");
@@ -1438,7 +1464,7 @@ extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbs
         const int64_t cls_stride = n * (3 * kWindows + 1) + 16;
         int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride);
         {
-            static int per_sm = 0;
+            int& per_sm = ctx->finalize_large_per_sm;
             if (!per_sm)
                 cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_finalize_large, 512, 0), "occupancy");
             const int grid = std::max(1, std::min(per_sm, 2)) * ctx->n_sms;
@@ -1477,7 +1503,7 @@ extern "C" tbsim_status tbsim_attributes_shard_partial(tbsim_ctx* ctx, const tbs
 extern "C" tbsim_status tbsim_attributes_shard_finish(tbsim_ctx* ctx, const tbsim_batch* b, const int64_t* class_sums,
                                                       int64_t n_words, int32_t priority_kind, tbsim_attr_out* out) {
     return guarded([&] {
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DeviceScope dev_scope(ctx->device);
         const tbsim_ctx::Shard& sh = ctx->shard;
         if (sh.b != b || n_words != sh.n_words || sh.gen != ctx->scratch_gen)
             raise(TBSIM_E_INVALID_ARGUMENT, "shard finish must follow this rank's partial call on the same batch");
@@ -1499,7 +1525,7 @@ extern "C" tbsim_status tbsim_attributes_shard_finish(tbsim_ctx* ctx, const tbsi
         o.evaluations = stage_out(ctx, st, "o_evals", out->evaluations, 1, false);
         const int64_t cls_stride = n * (3 * kWindows + 1) + 16;
         int64_t* cls_scratch = ctx->buf("a_cls_sums").as<int64_t>(cls_stride);
-        static int per_sm = 0;
+        int& per_sm = ctx->finalize_large_per_sm;
         if (!per_sm) cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_finalize_large, 512, 0), "occupancy");
         const int grid = std::max(1, std::min(per_sm, 2)) * ctx->n_sms;
         int64_t tab_cap = 1;
@@ -1921,7 +1947,7 @@ extern "C" tbsim_status tbsim_simulate(tbsim_ctx* ctx, const tbsim_batch* b, con
                                        int32_t n_platforms, const int32_t* platform_of, int32_t policy,
                                        const tbsim_regulator_cfg* reg, const tbsim_attr_in* attrs, tbsim_sim_out* out) {
     return guarded([&] {
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DeviceScope dev_scope(ctx->device);
         wait_batch(ctx, b);
         if (policy < 0 || policy > TBSIM_POLICY_INSPIRIT) raise(TBSIM_E_RUNTIME, "unknown policy id");
         const DevBatch& d = b->d;
@@ -2006,7 +2032,7 @@ extern "C" tbsim_status tbsim_schedule(tbsim_ctx* ctx, const tbsim_batch* b, con
                                        int32_t n_platforms, const int32_t* platform_of, int32_t policy,
                                        int32_t priority_kind, tbsim_attr_out* attr_out, tbsim_sim_out* out) {
     return guarded([&] {
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        DeviceScope dev_scope(ctx->device);
         wait_batch(ctx, b);
         if (policy < 0 || policy > TBSIM_POLICY_INSPIRIT) raise(TBSIM_E_RUNTIME, "unknown policy id");
         const DevBatch& d = b->d;

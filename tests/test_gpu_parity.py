@@ -775,3 +775,41 @@ def test_wide_state_simulators_match_oracle(ctx):
             o = po.simulate(lb, [pl], pol, reg=reg, attrs=ga, record=True)
             for k in SIM_KEYS:
                 eq(g[k], o[k], f"40k/{pl.name}/{pol}/{k}")
+
+
+def test_contexts_on_concurrent_host_threads_match_serial():
+    """one context (and stream) per calling thread.  Four host
+    threads schedule different batches at once on the same GPU (ctypes drops
+    the GIL in the calls); every result equals the same batch run alone."""
+    import threading
+    pl = [P.assemble("8c2g", 8, 2)]
+    seeds = [np.arange(64 * k, 64 * k + 64, dtype=np.uint64) for k in range(4)]
+    hbs = [api.HostBatch().add_layered(1000, 10, 0.05, s) for s in seeds]
+
+    def run(hb):
+        c = api.Context(0)
+        try:
+            r = c.schedule(c.upload(hb), pl, "inspirit")
+            return {k: np.array(r[k]) for k in ("worker", "start_ms", "end_ms", "makespan_ms")}
+        finally:
+            c.close()
+
+    serial = [run(hb) for hb in hbs]
+    out, errs = [None] * 4, []
+
+    def worker(i):
+        try:
+            for _ in range(3):
+                out[i] = run(hbs[i])
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for i in range(4):
+        for k, v in serial[i].items():
+            eq(out[i][k], v, f"thread {i}: {k}")
