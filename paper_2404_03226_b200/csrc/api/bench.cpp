@@ -107,6 +107,7 @@ bool run_group(const BenchSpec& spec, std::vector<Cell*>& cells, const std::vect
     try {
         device::Csr csr;
         for (Cell* c : cells) csr.add(c->g);
+        csr.require_known_handles();
         device::Uploaded up(csr);
         const Platform& pl = cells.front()->platform;
         const int64_t T = csr.task_base.back(), G = static_cast<int64_t>(cells.size());

@@ -63,8 +63,16 @@ void Csr::add(const TaskGraph& g) {
                                             std::to_string(d));
             dep.push_back(it->second);
         }
-        for (HandleId h : t.inputs) in.push_back(hpos.at(h));
-        for (HandleId h : t.outputs) out.push_back(hpos.at(h));
+        for (HandleId h : t.inputs) {
+            const auto it = hpos.find(h);
+            if (it == hpos.end()) unknown_handle = true;
+            else in.push_back(it->second);
+        }
+        for (HandleId h : t.outputs) {
+            const auto it = hpos.find(h);
+            if (it == hpos.end()) unknown_handle = true;
+            else out.push_back(it->second);
+        }
         dep_off.push_back(static_cast<int32_t>(dep.size() - e0));
         in_off.push_back(static_cast<int32_t>(in.size() - i0));
         out_off.push_back(static_cast<int32_t>(out.size() - o0));
@@ -82,6 +90,12 @@ void Csr::add(const TaskGraph& g) {
     handle_base.push_back(static_cast<int64_t>(handle_bytes.size()));
     in_base.push_back(static_cast<int64_t>(in.size()));
     out_base.push_back(static_cast<int64_t>(out.size()));
+}
+
+void Csr::require_known_handles() const {
+    // the text std::unordered_map::at throws in libstdc++, as the reference's
+    // engine would
+    if (unknown_handle) throw std::out_of_range("_Map_base::at");
 }
 
 const tbsim_batch_desc& Csr::finish() {

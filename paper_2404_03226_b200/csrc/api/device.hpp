@@ -32,7 +32,13 @@ struct Csr {
     std::vector<std::string> type_names;
     std::vector<const char*> name_ptrs;
     tbsim_batch_desc desc{};
+    // a task names a handle the graph does not declare: the reference's
+    // engine fails on it (std::out_of_range from handle_pos.at(),
+    // src/engine.cpp:68,108,171) while its attribute functions never look;
+    // such entries are left out here and simulate() throws
+    bool unknown_handle = false;
     void add(const TaskGraph& g);  // throws build_index's errors
+    void require_known_handles() const;
     const tbsim_batch_desc& finish();
 };
 

@@ -63,6 +63,7 @@ SimTrace simulate(const TaskGraph& g, const Platform& platform, Policy& policy, 
                                  "\" is not a built-in; the B200 engine runs fifo, dm, dmda, dmdap and inspirit");
     device::Csr csr;
     csr.add(g);
+    csr.require_known_handles();
     device::Uploaded up(csr);
     const size_t n = g.tasks.size();
     device::PlatformArrays pa = device::platform_arrays(platform, csr.type_names);

@@ -744,6 +744,15 @@ GPU_CASE("determinism, trace switch, policy ordering and failures") {
         size_t select_entry(int, const std::vector<QueueEntry>&, const EngineView&) override { return 0; }
     } custom;
     CHECK_THROWS_AS(simulate(chain3(), make_preset("homog2"), custom), std::runtime_error);
+    // a task reading an undeclared handle: the attribute functions never
+    // look at handles; the engine fails on it (handle_pos.at(),
+    // src/engine.cpp:68,108) with std::out_of_range
+    TaskGraph stray;
+    stray.handles = {{7, 4096}};
+    stray.tasks = {{0, "UNIT", {}, {7}, {7}}, {1, "UNIT", {0}, {99}, {}}};
+    TaskAttributes sa = compute_attributes(stray, make_preset("homog2").costs, PriorityKind::UpwardRank);
+    CHECK(sa.ability.size() == 2 && sa.ability[0] == 1);
+    CHECK_THROWS_AS(simulate(stray, make_preset("homog2"), *dmda), std::out_of_range);
 }
 
 GPU_CASE("README goldens through run_bench") {
