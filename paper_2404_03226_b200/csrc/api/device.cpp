@@ -93,9 +93,9 @@ void Csr::add(const TaskGraph& g) {
 }
 
 void Csr::require_known_handles() const {
-    // the text std::unordered_map::at throws in libstdc++, as the reference's
-    // engine would
-    if (unknown_handle) throw std::out_of_range("_Map_base::at");
+    // the exception (type and text) the reference's engine gets from
+    // handle_pos.at() -- raised by the same standard-library call
+    if (unknown_handle) (void)std::unordered_map<HandleId, size_t>{}.at(HandleId{});
 }
 
 const tbsim_batch_desc& Csr::finish() {

@@ -1126,7 +1126,7 @@ __global__ void k_xfer_table(const DevPlatform* pf, int32_t n_platforms, const i
         const int32_t cls = static_cast<int32_t>((i / (mn * mn)) % kByteClasses);
         const DevPlatform& P = pf[i / (static_cast<int64_t>(kByteClasses) * mn * mn)];
         double t = 0.0;
-        const int64_t by = dict[cls];
+        const int64_t by = dict ? dict[cls] : kDictEmpty;  // no dictionary: a batch without tasks
         if (from != to && from < P.n_nodes && to < P.n_nodes && by != kDictEmpty)
             t = tbsim_rules::transfer_ms(P.latency_ms, by, P.bw[from * kMaxNodes + to]);
         xtab[i] = t;
