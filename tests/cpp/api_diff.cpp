@@ -309,6 +309,76 @@ void graph_section(const std::string& name, const TaskGraph& g, const std::vecto
     });
 }
 
+// An EngineView of arbitrary state, for the push/pop free functions
+struct FakeView final : EngineView {
+    const TaskGraph* g = nullptr;
+    const Platform* p = nullptr;
+    double now_ms = 0.0;
+    std::vector<size_t> qlen;
+    std::vector<char> busy;
+    std::vector<double> free_at;
+    std::vector<std::vector<double>> transfer, fraction;
+    double now() const override { return now_ms; }
+    const TaskGraph& graph() const override { return *g; }
+    const Platform& platform() const override { return *p; }
+    size_t queue_length(int w) const override { return qlen[w]; }
+    bool worker_busy(int w) const override { return busy[w] != 0; }
+    double worker_free_at(int w) const override { return free_at[w]; }
+    double estimated_transfer_ms(size_t t, int w) const override { return transfer[t][w]; }
+    double resident_fraction(size_t t, int n) const override { return fraction[t][n]; }
+};
+
+// push_* / pop_* over random views and queues: ties are frequent (values
+// on a coarse grid), so the tie-breaks are exercised
+void rules_section(uint64_t seed, const Platform& p) {
+    out << "== rules " << seed << ' ' << p.name << '\n';
+    std::mt19937_64 rng(seed);
+    const TaskGraph g = random_dag(seed, 40, 0.1, true);
+    FakeView v;
+    v.g = &g;
+    v.p = &p;
+    const size_t W = p.workers.size();
+    auto grid = [&](int k) { return 0.25 * static_cast<double>(rng() % k); };
+    for (int round = 0; round < 6; ++round) {
+        v.now_ms = grid(40);
+        v.qlen.assign(W, 0);
+        v.busy.assign(W, 0);
+        v.free_at.assign(W, 0.0);
+        for (size_t w = 0; w < W; ++w) {
+            v.qlen[w] = rng() % 4;
+            v.busy[w] = static_cast<char>(rng() % 2);
+            v.free_at[w] = grid(60);
+        }
+        v.transfer.assign(g.tasks.size(), std::vector<double>(W, 0.0));
+        v.fraction.assign(g.tasks.size(), std::vector<double>(p.num_nodes, 1.0));
+        for (auto& r : v.transfer)
+            for (auto& x : r) x = grid(8);
+        for (auto& r : v.fraction)
+            for (auto& x : r) x = 0.125 * static_cast<double>(rng() % 9);
+        std::vector<int> pf, pd, pa;
+        for (size_t t = 0; t < g.tasks.size(); ++t) {
+            guard("push_fifo", [&] { pf.push_back(push_fifo(t, v)); });
+            guard("push_dm", [&] { pd.push_back(push_dm(t, v)); });
+            guard("push_dmda", [&] { pa.push_back(push_dmda(t, v)); });
+        }
+        vec("push_fifo", pf);
+        vec("push_dm", pd);
+        vec("push_dmda", pa);
+        TaskAttributes a;
+        for (size_t t = 0; t < g.tasks.size(); ++t) {
+            a.ability.push_back(static_cast<int64_t>(rng() % 4));
+            a.efficiency.push_back(static_cast<int64_t>(rng() % 3));
+            a.static_priority.push_back(static_cast<int64_t>(rng() % 3) * 1000);
+        }
+        std::vector<QueueEntry> q;
+        for (int k = 0; k < 12; ++k) q.push_back({static_cast<size_t>(rng() % g.tasks.size()), rng() % 50});
+        out << "pop_fifo " << pop_fifo(q) << " pop_priority " << pop_priority(q, a);
+        for (PopMode m : {PopMode::HighAbility, PopMode::HighEfficiency, PopMode::HighEfficiencyLocality})
+            out << ' ' << to_string(m) << '=' << pop_adaptive(m, static_cast<int>(rng() % W), q, a, v);
+        out << '\n';
+    }
+}
+
 }  // namespace
 
 int main() {
@@ -469,6 +539,23 @@ int main() {
         guard("platfile missing", [&] { load_platform_file("/nonexistent/api_diff.json"); });
         guard("resolve", [&] { out << "resolve " << resolve_platform("2gpu").workers.size() << '\n'; });
         for (const auto& n : preset_names()) out << "preset " << n << '\n';
+    }
+    // the push/pop free functions on views of arbitrary state
+    for (uint64_t r = 1; r <= 3; ++r) rules_section(r, mixed[r % mixed.size()]);
+    // stress shapes for the device paths: many inputs per task over many
+    // memory nodes, more than 32 workers, deep and dense graphs, >= 32768 tasks
+    {
+        TaskGraph wide = random_dag(101, 120, 0.05, true);
+        std::mt19937_64 rng(5);
+        for (auto& t : wide.tasks)
+            for (int k = 0; k < 40 + static_cast<int>(rng() % 30); ++k)
+                t.inputs.push_back(900 + 3 * static_cast<int64_t>(rng() % wide.handles.size()));
+        graph_section("wide_inputs", wide, {mixed_platform("m2c9g", 2, 9, 0.005), mixed_platform("m6c3g", 6, 3, 0.05)}, mc);
+        graph_section("many_workers", random_dag(102, 400, 0.02, true),
+                      {mixed_platform("m40c8g", 40, 8, 0.01), mixed_platform("m33c1g", 33, 1, 0.0)}, mc);
+        graph_section("deep", generate_layered_dag(3000, 300, 0.01, 11), {presets[0], mixed[1]}, dc);
+        graph_section("dense", random_dag(103, 150, 0.5, true), {mixed[0], mixed[2]}, mc);
+        graph_section("big", generate_layered_dag(40000, 100, 0.0005, 13), {presets[0]}, dc);
     }
     // formatting and the regulator's host functions
     for (double v : {0.0, 1.0, 1.5, 2.125, 1234.5678901, 1e-7, 3.0000001})
