@@ -556,6 +556,15 @@ int main() {
         graph_section("deep", generate_layered_dag(3000, 300, 0.01, 11), {presets[0], mixed[1]}, dc);
         graph_section("dense", random_dag(103, 150, 0.5, true), {mixed[0], mixed[2]}, mc);
         graph_section("big", generate_layered_dag(40000, 100, 0.0005, 13), {presets[0]}, dc);
+        // asymmetric links, GPUs sharing a memory node, a GPU on the host
+        // node (Platform objects built in code skip check_platform)
+        Platform odd = mixed_platform("m_odd", 3, 3, 0.03);
+        odd.workers[3].memory_node = 1;
+        odd.workers[4].memory_node = 1;
+        odd.workers[5].memory_node = 0;
+        odd.num_nodes = 3;
+        odd.bandwidth = {{0.0, 9e6, 1.7e7}, {2.1e7, 0.0, 4e7}, {6e6, 3.3e7, 0.0}};
+        graph_section("odd_platform", random_dag(104, 160, 0.06, true), {odd}, mc);
     }
     // formatting and the regulator's host functions
     for (double v : {0.0, 1.0, 1.5, 2.125, 1234.5678901, 1e-7, 3.0000001})
