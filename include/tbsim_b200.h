@@ -19,7 +19,9 @@
  *   - Host buffers are caller-owned.  Device buffers are owned by the context
  *     (tbsim_ctx) or by the caller when TBSIM_OUT_DEVICE is set.
  *   - A context is bound to one CUDA device and one stream; use one context
- *     per calling thread.  There is no CPU fallback: every compute entry point
+ *     per calling thread.  Every call makes the context's device current for
+ *     its duration and restores the caller's current device before it
+ *     returns, so one host thread may drive contexts on several GPUs.  There is no CPU fallback: every compute entry point
  *     runs on the GPU and fails with TBSIM_E_CUDA when no device is present.
  */
 #ifndef TBSIM_B200_H
