@@ -311,9 +311,10 @@ void launch_ingest(tbsim_ctx* ctx, const DevBatch& d, int grid, int32_t* cursor)
 // The simulator's packed view of a batch (one 32-byte record per task +
 // contiguous lists), built once on the stream the call runs on -- at upload,
 // after k_ingest, or on a generated batch's first simulation.
-void ensure_packed(tbsim_ctx* ctx, tbsim_batch* b) {
+// Allocation, size dictionary and per-handle size classes of the packed
+// view; returns the class table the pack reads.
+uint8_t* prepare_packed(tbsim_ctx* ctx, tbsim_batch* b) {
     const DevBatch& d = b->d;
-    if (b->hdr || d.T == 0) return;
     const int64_t adj_bytes = sim_adj_bytes(d.T, d.I, d.O, d.E);
     if (adj_bytes >= (int64_t(1) << 34)) raise(TBSIM_E_INVALID_ARGUMENT, "batch too large for the packed simulation graph");
     if (d.max_h > kHandleMask) raise(TBSIM_E_INVALID_ARGUMENT, "graph exceeds 2^28 handles for the simulator");
@@ -336,6 +337,13 @@ void ensure_packed(tbsim_ctx* ctx, tbsim_batch* b) {
         k_bytes_class<<<grid_h, 256, 0, ctx->stream>>>(d, b->dict, hcls);
         ctx->end("k_bytes_dict");
     }
+    return hcls;
+}
+
+void ensure_packed(tbsim_ctx* ctx, tbsim_batch* b) {
+    const DevBatch& d = b->d;
+    if (b->hdr || d.T == 0) return;
+    uint8_t* hcls = prepare_packed(ctx, b);
     const int grid = static_cast<int>(std::min<int64_t>((d.T + 255) / 256, 16LL * ctx->n_sms));
     // 8 lanes per task (measured 1/2/4/8: C2 0.90/0.68/0.58/0.55 ms,
     // 2048 C5 DAGs 6.5/4.7/3.2/2.5 ms)
@@ -391,6 +399,30 @@ struct UploadStream {
     bool active() const { return ctx->stream != saved; }
 };
 
+// Derived sections of an uploaded batch: the successor CSR and the
+// simulator's packed view, in one pass per graph (k_ingest_pack) unless
+// TBSIM_SPLIT_INGEST asks for the two-kernel form (k_ingest, k_sim_pack).
+void ingest_uploaded(tbsim_ctx* ctx, tbsim_batch* m) {
+    const DevBatch& d = m->d;
+    if (d.G == 0) return;
+    int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(d.T + d.G);
+    const int grid = static_cast<int>(std::min<int64_t>(d.G, 8LL * ctx->n_sms));
+    static const bool split = std::getenv("TBSIM_SPLIT_INGEST") != nullptr;
+    if (!m->hdr && d.T > 0 && !split) {
+        uint8_t* hcls = prepare_packed(ctx, m);
+        const int64_t want = static_cast<int64_t>(d.max_n) + 1;
+        const int32_t ints = want * 4 <= 48 * 1024 ? static_cast<int32_t>(want) : 0;
+        ctx->begin("k_ingest_pack");
+        k_ingest_pack<<<grid, 256, static_cast<size_t>(ints) * 4, ctx->stream>>>(d, cursor, ints, hcls, m->hdr, m->adj);
+        ctx->end("k_ingest_pack");
+        return;
+    }
+    ctx->begin("k_ingest");
+    launch_ingest(ctx, d, grid, cursor);
+    ctx->end("k_ingest");
+    ensure_packed(ctx, m);
+}
+
 // Compute on a batch uploaded on another stream waits for its copies, then
 // (first use) builds its derived sections -- successor CSR (k_ingest) and
 // the simulator's packed view (k_bytes_dict, k_sim_pack) -- on the compute
@@ -403,13 +435,7 @@ void wait_batch(tbsim_ctx* ctx, const tbsim_batch* b) {
     if (b->needs_ingest) {
         auto* m = const_cast<tbsim_batch*>(b);
         m->needs_ingest = false;
-        const DevBatch& d = m->d;
-        int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(d.T + d.G);
-        const int grid = static_cast<int>(std::min<int64_t>(d.G, 8LL * ctx->n_sms));
-        ctx->begin("k_ingest");
-        launch_ingest(ctx, d, grid, cursor);
-        ctx->end("k_ingest");
-        ensure_packed(ctx, m);
+        ingest_uploaded(ctx, m);
     }
 }
 
@@ -673,12 +699,7 @@ tbsim_status tbsim_batch_upload(tbsim_ctx* ctx, const tbsim_batch_desc* h, tbsim
         if (G > 0 && us.active() && ctx->defer_ingest) {
             b->needs_ingest = true;
         } else if (G > 0) {
-            int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(T + G);
-            const int grid = static_cast<int>(std::min<int64_t>(G, 8LL * ctx->n_sms));
-            ctx->begin("k_ingest");
-            launch_ingest(ctx, d, grid, cursor);
-            ctx->end("k_ingest");
-            ensure_packed(ctx, b.get());
+            ingest_uploaded(ctx, b.get());
         }
         if (us.active()) {
             cuda_check(cudaEventCreateWithFlags(&b->ready, cudaEventDisableTiming), "cudaEventCreate");

@@ -34,106 +34,18 @@
 #include "attributes.cuh"
 #include "blockscan.cuh"
 #include "common.cuh"
+#include "ingest.cuh"
 #include "rules.cuh"
 
 namespace tbsim_dev {
 
 // ------------------------------------------------------------------ ingest
 
-__device__ void sort_small(int32_t* a, int32_t len) {
-    if (len <= 32) {  // in a thread-local copy (L1-resident) instead of in place in HBM
-        int32_t loc[32];
-        for (int32_t i = 0; i < len; ++i) {
-            const int32_t x = a[i];
-            int32_t j = i - 1;
-            while (j >= 0 && loc[j] > x) { loc[j + 1] = loc[j]; --j; }
-            loc[j + 1] = x;
-        }
-        for (int32_t i = 0; i < len; ++i) a[i] = loc[i];
-        return;
-    }
-    if (len <= 48) {
-        for (int32_t i = 1; i < len; ++i) {
-            int32_t x = a[i], j = i - 1;
-            while (j >= 0 && a[j] > x) { a[j + 1] = a[j]; --j; }
-            a[j + 1] = x;
-        }
-        return;
-    }
-    // heapsort for long lists
-    auto sift = [&](int32_t root, int32_t end) {
-        while (2 * root + 1 < end) {
-            int32_t c = 2 * root + 1;
-            if (c + 1 < end && a[c] < a[c + 1]) ++c;
-            if (a[root] >= a[c]) return;
-            int32_t t = a[root]; a[root] = a[c]; a[c] = t;
-            root = c;
-        }
-    };
-    for (int32_t i = len / 2 - 1; i >= 0; --i) sift(i, len);
-    for (int32_t end = len - 1; end > 0; --end) {
-        int32_t t = a[0]; a[0] = a[end]; a[end] = t;
-        sift(0, end);
-    }
-}
-
-// Successor CSR of each graph (one CTA per graph): count, scan, scatter,
-// sort each list.  Counts and cursors live in shared memory when the graph
-// fits (smem_ints >= n + 1), else in global memory.
+// Successor CSR of each graph (one CTA per graph, ingest.cuh).
 __global__ void __launch_bounds__(256) k_ingest(DevBatch b, int32_t* cursor_scratch, int32_t smem_ints) {
     __shared__ int32_t warp_tot[32];
     extern __shared__ int32_t s_ctr[];
-    for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) {
-        const int64_t t0 = b.task_base[g];
-        const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
-        const int32_t* doff = b.dep_off + t0 + g;
-        const int32_t* dep = b.dep + b.edge_base[g];
-        int32_t* soff = b.succ_off + t0 + g;
-        int32_t* succ = b.succ + b.edge_base[g];
-        if (n + 1 <= smem_ints) {
-            for (int32_t i = threadIdx.x; i <= n; i += blockDim.x) s_ctr[i] = 0;
-            __syncthreads();
-            for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
-                for (int32_t k = __ldg(&doff[v]); k < __ldg(&doff[v + 1]); ++k) atomicAdd(&s_ctr[__ldg(&dep[k])], 1);
-            __syncthreads();
-            block_exclusive_scan_inplace(s_ctr, n + 1, warp_tot);
-            for (int32_t i = threadIdx.x; i <= n; i += blockDim.x) soff[i] = s_ctr[i];
-            __syncthreads();
-            for (int32_t v = threadIdx.x; v < n; v += blockDim.x) {
-                const int32_t k1 = __ldg(&doff[v + 1]);
-                for (int32_t k = __ldg(&doff[v]); k < k1; k += 4) {  // four dep ids ahead of the stores
-                    int32_t d[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) d[q] = k + q < k1 ? __ldg(&dep[k + q]) : -1;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (d[q] >= 0) succ[atomicAdd(&s_ctr[d[q]], 1)] = v;
-                }
-            }
-            __syncthreads();
-            // s_ctr[u] is now the end of u's list
-            for (int32_t u = threadIdx.x; u < n; u += blockDim.x) {
-                const int32_t e = s_ctr[u], s = u == 0 ? 0 : s_ctr[u - 1];
-                sort_small(succ + s, e - s);
-            }
-            __syncthreads();
-            continue;
-        }
-        int32_t* cur = cursor_scratch + t0 + g;
-        for (int32_t i = threadIdx.x; i <= n; i += blockDim.x) soff[i] = 0;
-        __syncthreads();
-        for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
-            for (int32_t k = doff[v]; k < doff[v + 1]; ++k) atomicAdd(&soff[dep[k]], 1);
-        __syncthreads();
-        block_exclusive_scan_inplace(soff, n + 1, warp_tot);
-        for (int32_t i = threadIdx.x; i <= n; i += blockDim.x) cur[i] = soff[i];
-        __syncthreads();
-        for (int32_t v = threadIdx.x; v < n; v += blockDim.x)
-            for (int32_t k = doff[v]; k < doff[v + 1]; ++k) succ[atomicAdd(&cur[dep[k]], 1)] = v;
-        __syncthreads();
-        for (int32_t u = threadIdx.x; u < n; u += blockDim.x) sort_small(succ + soff[u], soff[u + 1] - soff[u]);
-        __syncthreads();
-    }
+    for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) ingest_graph(b, g, cursor_scratch, smem_ints, s_ctr, warp_tot);
 }
 
 // --------------------------------------------------------------- structure

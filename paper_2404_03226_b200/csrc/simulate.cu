@@ -27,6 +27,7 @@
 
 #include "blockscan.cuh"
 #include "common.cuh"
+#include "ingest.cuh"
 #include "rules.cuh"
 #include "simulate.cuh"
 
@@ -1065,6 +1066,65 @@ __global__ void __launch_bounds__(256) k_sim_pack(DevBatch b, const uint8_t* hcl
 }
 
 template __global__ void k_sim_pack<8>(DevBatch, const uint8_t*, SimTaskHdr*, int32_t*);
+
+// Uploaded batches: the successor CSR and the packed simulation graph of a
+// graph in one pass of its CTA (ingest.cuh, then the k_sim_pack layout) --
+// the graph's offsets and freshly sorted successor lists are still in L1/L2
+// when they are packed, and one launch replaces two.  Teams of 8 lanes copy
+// a task's three lists; the record follows once the team knows whether the
+// successor list repeats an entry.  hcls (k_bytes_class) must be complete.
+__global__ void __launch_bounds__(256) k_ingest_pack(DevBatch b, int32_t* cursor_scratch, int32_t smem_ints,
+                                                     const uint8_t* hcls, SimTaskHdr* hdr, int32_t* adj) {
+    __shared__ int32_t warp_tot[32];
+    extern __shared__ int32_t s_ctr[];
+    constexpr int TL = 8;
+    const int tl = threadIdx.x & (TL - 1), team = threadIdx.x / TL, nteams = blockDim.x / TL;
+    const unsigned tmask = ((1u << TL) - 1u) << ((threadIdx.x & 31) & ~(TL - 1));
+    for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) {
+        ingest_graph(b, g, cursor_scratch, smem_ints, s_ctr, warp_tot);
+        const int64_t t0 = b.task_base[g];
+        const int32_t n = static_cast<int32_t>(b.task_base[g + 1] - t0);
+        const int64_t ib = b.in_base[g], ob = b.out_base[g], eb = b.edge_base[g], hb = b.handle_base[g];
+        const int32_t* ioff = b.in_off + t0 + g;
+        const int32_t* ooff = b.out_off + t0 + g;
+        const int32_t* soff = b.succ_off + t0 + g;  // written by this CTA: plain loads
+        const int32_t* in = b.in + ib;
+        const int32_t* out = b.out + ob;
+        const int32_t* succ = b.succ + eb;
+        for (int32_t v = team; v < n; v += nteams) {
+            const int32_t i0 = __ldg(&ioff[v]), i1 = __ldg(&ioff[v + 1]);
+            const int32_t o0 = __ldg(&ooff[v]), o1 = __ldg(&ooff[v + 1]);
+            const int32_t s0 = soff[v], s1 = soff[v + 1];
+            const int32_t ty = __ldg(&b.type[t0 + v]);
+            const int64_t x = (ib + i0) + (ob + o0) + (eb + s0);
+            const int32_t nin = i1 - i0, nout = o1 - o0, nsucc = s1 - s0;
+            int32_t* inh = adj + x;
+            int32_t* outl = inh + nin;
+            int32_t* succl = outl + nout;
+            for (int32_t k = tl; k < nin; k += TL) {
+                const int32_t h = __ldg(&in[i0 + k]);
+                inh[k] = static_cast<int32_t>(static_cast<uint32_t>(h) |
+                                              (static_cast<uint32_t>(__ldg(&hcls[hb + h])) << kHandleBits));
+            }
+            for (int32_t k = tl; k < nout; k += TL) outl[k] = __ldg(&out[o0 + k]);
+            bool dup = false;
+            for (int32_t k = tl; k < nsucc; k += TL) {
+                const int32_t sv = succ[s0 + k];
+                succl[k] = sv;
+                dup = dup || (k > 0 && succ[s0 + k - 1] == sv);
+            }
+            // record words 0-3: list offset, inputs, outputs, successors |
+            // type << 24 | multi-edges << 30 (as k_sim_pack)
+            dup = __any_sync(tmask, dup);
+            if (tl == 0)
+                reinterpret_cast<int4*>(hdr + t0 + v)[0] =
+                    make_int4(static_cast<int32_t>(static_cast<uint32_t>(x)), nin, nout,
+                              static_cast<int32_t>((dup ? 1u << 30 : 0u) | (static_cast<uint32_t>(ty) << 24) |
+                                                   (static_cast<uint32_t>(nsucc) & 0xffffffu)));
+        }
+        __syncthreads();  // s_ctr / cursors are reused by the next graph
+    }
+}
 
 // Every handle's size class in the batch's (final) dictionary, once per
 // handle -- the pack then reads one byte per input instead of the 8-byte

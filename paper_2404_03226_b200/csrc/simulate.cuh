@@ -157,6 +157,9 @@ struct SimParams {
 template <int TL>  // lanes per task (8 instantiated)
 __global__ void k_sim_pack(DevBatch b, const uint8_t* hcls, SimTaskHdr* hdr, int32_t* adj);
 __global__ void k_bytes_class(DevBatch b, const int64_t* dict, uint8_t* hcls);
+// k_ingest and k_sim_pack of an uploaded batch in one pass per graph
+__global__ void k_ingest_pack(DevBatch b, int32_t* cursor_scratch, int32_t smem_ints, const uint8_t* hcls,
+                              SimTaskHdr* hdr, int32_t* adj);
 // The batch's distinct handle sizes (first come, first numbered; at most
 // kEscapeClass of them, the rest read handle_bytes).  dict: kByteClasses
 // entries preset to kDictEmpty.

@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""Times the per-batch upload kernels (k_ingest, k_sim_pack) on C2's host
+"""Times the per-batch upload kernels (k_ingest_pack, or k_ingest + k_sim_pack
+with TBSIM_SPLIT_INGEST=1) on C2's host
 batch and on C5-shaped DAGs (diagnostic)."""
 import sys
 
@@ -20,4 +21,6 @@ for n, G in ((1000, 4096), (4096, 2048)):
         ctx.schedule(db, pl, "fifo", want_attrs=False)
     ctx.set_timing(False)
     print(f"layered({n}) x {G}: k_ingest {ctx.last_kernel_ms('k_ingest'):.3f} ms, "
-          f"k_sim_pack {ctx.last_kernel_ms('k_sim_pack'):.3f} ms", flush=True)
+          f"k_sim_pack {ctx.last_kernel_ms('k_sim_pack'):.3f} ms, "
+          f"k_ingest_pack {ctx.last_kernel_ms('k_ingest_pack'):.3f} ms, "
+          f"k_bytes_dict {ctx.last_kernel_ms('k_bytes_dict'):.3f} ms", flush=True)
