@@ -1091,36 +1091,63 @@ __global__ void __launch_bounds__(256) k_ingest_pack(DevBatch b, int32_t* cursor
         const int32_t* in = b.in + ib;
         const int32_t* out = b.out + ob;
         const int32_t* succ = b.succ + eb;
-        for (int32_t v = team; v < n; v += nteams) {
-            const int32_t i0 = __ldg(&ioff[v]), i1 = __ldg(&ioff[v + 1]);
-            const int32_t o0 = __ldg(&ooff[v]), o1 = __ldg(&ooff[v + 1]);
-            const int32_t s0 = soff[v], s1 = soff[v + 1];
-            const int32_t ty = __ldg(&b.type[t0 + v]);
-            const int64_t x = (ib + i0) + (ob + o0) + (eb + s0);
-            const int32_t nin = i1 - i0, nout = o1 - o0, nsucc = s1 - s0;
-            int32_t* inh = adj + x;
-            int32_t* outl = inh + nin;
-            int32_t* succl = outl + nout;
-            for (int32_t k = tl; k < nin; k += TL) {
-                const int32_t h = __ldg(&in[i0 + k]);
-                inh[k] = static_cast<int32_t>(static_cast<uint32_t>(h) |
-                                              (static_cast<uint32_t>(__ldg(&hcls[hb + h])) << kHandleBits));
+        // a team's next TL tasks: their offsets in one load per lane, handed
+        // out by shuffles; each task's first TL list entries loaded before
+        // any store
+        for (int32_t base = team; base < n; base += TL * nteams) {
+            const int32_t vt = base + tl * nteams;
+            int32_t li0 = 0, li1 = 0, lo0 = 0, lo1 = 0, ls0 = 0, ls1 = 0, lty = 0;
+            if (vt < n) {
+                li0 = __ldg(&ioff[vt]); li1 = __ldg(&ioff[vt + 1]);
+                lo0 = __ldg(&ooff[vt]); lo1 = __ldg(&ooff[vt + 1]);
+                ls0 = soff[vt]; ls1 = soff[vt + 1];
+                lty = __ldg(&b.type[t0 + vt]);
             }
-            for (int32_t k = tl; k < nout; k += TL) outl[k] = __ldg(&out[o0 + k]);
-            bool dup = false;
-            for (int32_t k = tl; k < nsucc; k += TL) {
-                const int32_t sv = succ[s0 + k];
-                succl[k] = sv;
-                dup = dup || (k > 0 && succ[s0 + k - 1] == sv);
+            for (int j = 0; j < TL; ++j) {
+                const int32_t v = base + j * nteams;
+                if (v >= n) break;  // uniform in the team
+                const int32_t i0 = __shfl_sync(tmask, li0, j, TL), i1 = __shfl_sync(tmask, li1, j, TL);
+                const int32_t o0 = __shfl_sync(tmask, lo0, j, TL), o1 = __shfl_sync(tmask, lo1, j, TL);
+                const int32_t s0 = __shfl_sync(tmask, ls0, j, TL), s1 = __shfl_sync(tmask, ls1, j, TL);
+                const int32_t ty = __shfl_sync(tmask, lty, j, TL);
+                const int64_t x = (ib + i0) + (ob + o0) + (eb + s0);
+                const int32_t nin = i1 - i0, nout = o1 - o0, nsucc = s1 - s0;
+                int32_t* inh = adj + x;
+                int32_t* outl = inh + nin;
+                int32_t* succl = outl + nout;
+                bool dup = false;
+                {
+                    const int32_t h = tl < nin ? __ldg(&in[i0 + tl]) : 0;
+                    const int32_t ov = tl < nout ? __ldg(&out[o0 + tl]) : 0;
+                    const int32_t sv = tl < nsucc ? succ[s0 + tl] : 0;
+                    const int32_t sp = __shfl_up_sync(tmask, sv, 1, TL);  // the previous entry (tl > 0)
+                    const uint8_t cl = tl < nin ? __ldg(&hcls[hb + h]) : 0;
+                    if (tl < nin)
+                        inh[tl] = static_cast<int32_t>(static_cast<uint32_t>(h) | (static_cast<uint32_t>(cl) << kHandleBits));
+                    if (tl < nout) outl[tl] = ov;
+                    if (tl < nsucc) succl[tl] = sv;
+                    dup = tl > 0 && tl < nsucc && sp == sv;
+                }
+                for (int32_t k = tl + TL; k < nin; k += TL) {
+                    const int32_t h = __ldg(&in[i0 + k]);
+                    inh[k] = static_cast<int32_t>(static_cast<uint32_t>(h) |
+                                                  (static_cast<uint32_t>(__ldg(&hcls[hb + h])) << kHandleBits));
+                }
+                for (int32_t k = tl + TL; k < nout; k += TL) outl[k] = __ldg(&out[o0 + k]);
+                for (int32_t k = tl + TL; k < nsucc; k += TL) {
+                    const int32_t sv = succ[s0 + k];
+                    succl[k] = sv;
+                    dup = dup || succ[s0 + k - 1] == sv;
+                }
+                // record words 0-3: list offset, inputs, outputs, successors |
+                // type << 24 | multi-edges << 30 (as k_sim_pack)
+                dup = __any_sync(tmask, dup);
+                if (tl == 0)
+                    reinterpret_cast<int4*>(hdr + t0 + v)[0] =
+                        make_int4(static_cast<int32_t>(static_cast<uint32_t>(x)), nin, nout,
+                                  static_cast<int32_t>((dup ? 1u << 30 : 0u) | (static_cast<uint32_t>(ty) << 24) |
+                                                       (static_cast<uint32_t>(nsucc) & 0xffffffu)));
             }
-            // record words 0-3: list offset, inputs, outputs, successors |
-            // type << 24 | multi-edges << 30 (as k_sim_pack)
-            dup = __any_sync(tmask, dup);
-            if (tl == 0)
-                reinterpret_cast<int4*>(hdr + t0 + v)[0] =
-                    make_int4(static_cast<int32_t>(static_cast<uint32_t>(x)), nin, nout,
-                              static_cast<int32_t>((dup ? 1u << 30 : 0u) | (static_cast<uint32_t>(ty) << 24) |
-                                                   (static_cast<uint32_t>(nsucc) & 0xffffffu)));
         }
         __syncthreads();  // s_ctr / cursors are reused by the next graph
     }
