@@ -399,7 +399,7 @@ struct UploadStream {
     bool active() const { return ctx->stream != saved; }
 };
 
-// Derived sections of an uploaded batch: the successor CSR and the
+// Derived sections of an uploaded or generated batch: the successor CSR and the
 // simulator's packed view, in one pass per graph (k_ingest_pack) unless
 // TBSIM_SPLIT_INGEST asks for the two-kernel form (k_ingest, k_sim_pack).
 void ingest_uploaded(tbsim_ctx* ctx, tbsim_batch* m) {
@@ -879,11 +879,7 @@ tbsim_status tbsim_batch_generate_layered(tbsim_ctx* ctx, int32_t n, int32_t L, 
             ctx->begin("k_gen_layered_fill");
             k_gen_layered_expand<<<static_cast<unsigned>(std::min<int64_t>(G, 8LL * ctx->n_sms)), 256, 0, ctx->stream>>>(q, d);
             ctx->end("k_gen_layered_fill");
-            int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(T + G);
-            const int grid = static_cast<int>(std::min<int64_t>(G, 8LL * ctx->n_sms));
-            ctx->begin("k_ingest");
-            launch_ingest(ctx, d, grid, cursor);
-            ctx->end("k_ingest");
+            ingest_uploaded(ctx, b.get());  // successor CSR + packed simulation view
         }
         b->task_base = tbase;
         for (int i = 0; i < tbsim_host::T_COUNT; ++i) b->type_names.push_back(tbsim_host::kTypeNames[i]);
@@ -961,11 +957,7 @@ tbsim_status tbsim_batch_generate_tiled(tbsim_ctx* ctx, int32_t kind, int32_t nb
             ctx->begin("k_gen_tiled_fill");
             k_gen_tiled_fill<<<gridf, 256, 0, ctx->stream>>>(kind, nb, n, nh, bytes, off, d);
             ctx->end("k_gen_tiled_fill");
-            int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(T + G);
-            const int grid = static_cast<int>(std::min<int64_t>(G, 8LL * ctx->n_sms));
-            ctx->begin("k_ingest");
-            launch_ingest(ctx, d, grid, cursor);
-            ctx->end("k_ingest");
+            ingest_uploaded(ctx, b.get());  // successor CSR + packed simulation view
         }
         b->task_base = tb;
         for (int i = 0; i < tbsim_host::T_COUNT; ++i) b->type_names.push_back(tbsim_host::kTypeNames[i]);
