@@ -400,15 +400,17 @@ struct UploadStream {
 };
 
 // Derived sections of an uploaded or generated batch: the successor CSR and the
-// simulator's packed view, in one pass per graph (k_ingest_pack) unless
-// TBSIM_SPLIT_INGEST asks for the two-kernel form (k_ingest, k_sim_pack).
+// simulator's packed view.  Batches of many graphs build both in one pass
+// per graph (k_ingest_pack); a few large graphs (C1, C3, C4) keep the
+// two-kernel form, whose pack spreads every graph over the whole GPU
+// (TBSIM_SPLIT_INGEST forces it).
 void ingest_uploaded(tbsim_ctx* ctx, tbsim_batch* m) {
     const DevBatch& d = m->d;
     if (d.G == 0) return;
     int32_t* cursor = ctx->buf("ingest_cursor").as<int32_t>(d.T + d.G);
     const int grid = static_cast<int>(std::min<int64_t>(d.G, 8LL * ctx->n_sms));
     static const bool split = std::getenv("TBSIM_SPLIT_INGEST") != nullptr;
-    if (!m->hdr && d.T > 0 && !split) {
+    if (!m->hdr && d.T > 0 && !split && d.G >= 4LL * ctx->n_sms) {
         uint8_t* hcls = prepare_packed(ctx, m);
         const int64_t want = static_cast<int64_t>(d.max_n) + 1;
         const int32_t ints = want * 4 <= 48 * 1024 ? static_cast<int32_t>(want) : 0;
