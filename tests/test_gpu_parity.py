@@ -56,13 +56,13 @@ def test_simulation_matches_reference_fixture(ctx, name):
                 eq([s.cur_k for s in r["reg_state"][:f.batch.n_graphs]], want["reg_cur_k"], "cur_k")
 
 
-def random_graphs(seed, count, with_handles=True):
+def random_graphs(seed, count, with_handles=True, max_n=120):
     """Random DAGs with non-contiguous ids, multi-edges, ids out of order and
     inputs that are not dependencies (a construction unlike both generators)."""
     rng = np.random.default_rng(seed)
     out = []
     for gi in range(count):
-        n = int(rng.integers(1, 120))
+        n = int(rng.integers(1, max_n))
         ids = rng.permutation(np.arange(n) * 7 + 1000)
         tasks = []
         handles = [(5000 + 3 * h, int(rng.integers(1, 5)) * 100_000) for h in range(n)]
@@ -85,6 +85,33 @@ def test_random_graphs_all_policies_platform_mix(ctx):
     pof = np.arange(b.n_graphs) % len(pls)
     db = ctx.upload(b)
     ga = ctx.attributes(db, costs, abi.ATTR_ALL)
+    oa = po.attributes(b, costs, abi.ATTR_ALL)
+    for k in ("ability", "efficiency", "static_priority", "unit_time_ms"):
+        eq(ga[k], oa[k], k)
+    reg = [po.default_regulator_config(b, g, pls[pof[g]]) for g in range(b.n_graphs)]
+    for pol in abi.POLICIES:
+        g = ctx.simulate(db, pls, pol, reg, platform_of=pof, attrs=oa, record=True)
+        o = po.simulate(b, pls, pol, platform_of=pof, reg=reg, attrs=oa, record=True)
+        for k in SIM_KEYS:
+            eq(g[k], o[k], f"{pol}/{k}")
+
+
+def test_fused_upload_kernel_on_many_random_graphs(ctx):
+    """Batches of >= 4 graphs per SM build their successor CSR and packed
+    simulation view in one pass (k_ingest_pack): multi-edges, shuffled ids,
+    inputs that are not dependencies, tasks without inputs, every policy and
+    the full push/pop/nready ledger against the oracle."""
+    b = random_graphs(11, 640, max_n=40)
+    costs = P.default_cost_table()
+    pls = [P.assemble("8c2g", 8, 2), P.make_preset("2gpu"), P.assemble("4c1g", 4, 1)]
+    pof = np.arange(b.n_graphs) % len(pls)
+    ctx.set_timing(True)
+    try:
+        db = ctx.upload(b)
+        ga = ctx.attributes(db, costs, abi.ATTR_ALL)
+        assert ctx.last_kernel_ms("k_ingest_pack") > 0.0, "the fused upload kernel did not run"
+    finally:
+        ctx.set_timing(False)
     oa = po.attributes(b, costs, abi.ATTR_ALL)
     for k in ("ability", "efficiency", "static_priority", "unit_time_ms"):
         eq(ga[k], oa[k], k)
