@@ -554,25 +554,39 @@ def test_queue_overflow_rerun_matches_oracle(ctx):
     assert rerun_ms > 0.0, "the wide graphs were expected to overflow into the HBM rerun"
 
 
-def test_c2_every_dag_matches_the_reference(ctx):
+_C2_REF = {}
+
+
+def _c2_reference():
+    """C2's host batch and the reference's attributes of all 4096 DAGs (once)."""
+    from oracle import pyref
+    if "b" not in _C2_REF:
+        hb = api.HostBatch().add_layered(1000, 10, 0.05, np.arange(4096))
+        _C2_REF["hb"] = hb
+        _C2_REF["b"] = hb.view()
+        _C2_REF["ra"] = pyref.attributes(_C2_REF["b"], P.default_cost_table(), abi.ATTR_ALL,
+                                         threads=pyref.max_threads())
+    return _C2_REF["hb"], _C2_REF["b"], _C2_REF["ra"]
+
+
+@pytest.mark.parametrize("policy", abi.POLICIES)
+def test_c2_every_dag_matches_the_reference(ctx, policy):
     """BASELINE configs[1] in full: all 4096 layered DAGs of C2 scheduled on
     the device equal the reference implementation (oracle/_ref, the reference
-    sources compiled unmodified, on all host threads) -- attributes, every
-    assignment, every start/end double and every makespan."""
+    sources compiled unmodified, on all host threads) under every policy --
+    attributes, every assignment, every start/end double and every
+    makespan."""
     from oracle import pyref
     if not pyref.available():
         pytest.skip("oracle/_ref not built")
-    hb = api.HostBatch().add_layered(1000, 10, 0.05, np.arange(4096))
-    b = hb.view()
+    hb, b, ra = _c2_reference()
     pl = [P.assemble("8c2g", 8, 2)]
-    r = ctx.schedule(ctx.upload(hb), pl, "inspirit")
-    costs = P.default_cost_table()
-    ra = pyref.attributes(b, costs, abi.ATTR_ALL, threads=pyref.max_threads())
-    rs = pyref.simulate(b, pl, "inspirit", attrs=ra, record=False, threads=pyref.max_threads())
+    r = ctx.schedule(ctx.upload(hb), pl, policy)
+    rs = pyref.simulate(b, pl, policy, attrs=ra, record=False, threads=pyref.max_threads())
     for k in ("ability", "efficiency", "static_priority"):
         eq(r["attr_" + k], ra[k], k)
     for k in ("worker", "start_ms", "end_ms", "makespan_ms"):
-        eq(r[k], rs[k], k)
+        eq(r[k], rs[k], f"{policy}/{k}")
 
 
 def test_c5_one_percent_sample_matches_the_reference(ctx):
