@@ -331,6 +331,27 @@ def test_c3_lu_and_qr_on_32c4g(ctx):
             eq(g[k], o[k], f"{pol}/{k}")
 
 
+@pytest.mark.parametrize("policy", abi.POLICIES)
+def test_c3_matches_the_reference_library(ctx, policy):
+    """BASELINE configs[2] against the reference library itself (oracle/_ref:
+    the reference sources compiled unmodified), every policy: the LU DAG is
+    the reference's own generator, the QR DAG this repo's (the reference has
+    none), both scheduled by the reference's compute_attributes + simulate."""
+    from oracle import pyref
+    if not pyref.available():
+        pytest.skip("oracle/_ref not built")
+    hb = api.HostBatch().add_lu(40, 160 * 160 * 4).add_qr(40, 160 * 160 * 4)
+    b = hb.view()
+    pl = [P.assemble("32c4g", 32, 4, True)]
+    r = ctx.schedule(ctx.upload(hb), pl, policy)
+    ra = pyref.attributes(b, pl[0].costs, abi.ATTR_ALL, threads=2)
+    rs = pyref.simulate(b, pl, policy, attrs=ra, record=False, threads=2)
+    for k in ("ability", "efficiency", "static_priority"):
+        eq(r["attr_" + k], ra[k], k)
+    for k in ("worker", "start_ms", "end_ms", "makespan_ms"):
+        eq(r[k], rs[k], f"{policy}/{k}")
+
+
 def _long_edge_graph(seed, n, levels, p_long):
     """Layered DAG plus random long edges (edge spans > 1 exercise the
     pruning history and the reverse live ranges)."""
@@ -589,10 +610,12 @@ def test_c2_every_dag_matches_the_reference(ctx, policy):
         eq(r[k], rs[k], f"{policy}/{k}")
 
 
-def test_c5_one_percent_sample_matches_the_reference(ctx):
+@pytest.mark.parametrize("policy", abi.POLICIES)
+def test_c5_one_percent_sample_matches_the_reference(ctx, policy):
     """BASELINE configs[4]: a 1% sample (every 100th seed of a GPU's 8192) of
     the 4096-task layered DAGs on the four worker mixes (seed mod 4),
-    generated on the device, equals the reference implementation."""
+    generated on the device, equals the reference implementation under every
+    policy."""
     from oracle import pyref
     if not pyref.available():
         pytest.skip("oracle/_ref not built")
@@ -601,15 +624,16 @@ def test_c5_one_percent_sample_matches_the_reference(ctx):
     pls = [P.assemble(f"{c}c{g}g", c, g) for c, g in mixes]
     pof = (seeds % 4).astype(np.int32)
     db = ctx.generate_layered(4096, 10, 0.05, seeds)
-    r = ctx.schedule(db, pls, "inspirit", platform_of=pof)
-    b = api.HostBatch().add_layered(4096, 10, 0.05, seeds).view()
-    costs = P.default_cost_table()
-    ra = pyref.attributes(b, costs, abi.ATTR_ALL, threads=pyref.max_threads())
-    rs = pyref.simulate(b, pls, "inspirit", platform_of=pof, attrs=ra, record=False, threads=pyref.max_threads())
+    r = ctx.schedule(db, pls, policy, platform_of=pof)
+    if "c5" not in _C2_REF:  # the reference's attributes of the sample, once
+        b5 = api.HostBatch().add_layered(4096, 10, 0.05, seeds).view()
+        _C2_REF["c5"] = (b5, pyref.attributes(b5, P.default_cost_table(), abi.ATTR_ALL, threads=pyref.max_threads()))
+    b, ra = _C2_REF["c5"]
+    rs = pyref.simulate(b, pls, policy, platform_of=pof, attrs=ra, record=False, threads=pyref.max_threads())
     for k in ("ability", "efficiency", "static_priority"):
         eq(r["attr_" + k], ra[k], k)
     for k in ("worker", "start_ms", "end_ms", "makespan_ms"):
-        eq(r[k], rs[k], k)
+        eq(r[k], rs[k], f"{policy}/{k}")
 
 
 def _star_batch(m):
