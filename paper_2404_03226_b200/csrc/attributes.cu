@@ -1235,7 +1235,8 @@ __global__ void __launch_bounds__(1024, 1) k_sweep_fp32(DevBatch b, AttrScratch 
                 case 256: sweep_tile_mode<256, true, float>(b, s, g, tile, nullptr, P, th, s_hist, prune_span, relax_ctr); break;
                 case 128: sweep_tile_mode<128, true, float>(b, s, g, tile, nullptr, P, th, s_hist, prune_span, relax_ctr); break;
                 case 64: sweep_tile_rows_mode<64, 8, float>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
-                default: sweep_tile_rows_mode<32, 4, float>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+                case 32: sweep_tile_rows_mode<32, 4, float>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
+                default: sweep_tile_rows_mode<16, 2, float>(b, s, g, tile, P, th, s_hist, prune_span, relax_ctr); break;
             }
         }
         __syncthreads();
@@ -1379,7 +1380,7 @@ __global__ void k_tile_plan(DevBatch b, AttrScratch s, int64_t smem_bytes, int32
             // global-window graphs: the host sizes the per-CTA window (P x 32)
             if (static_cast<int64_t>(P) * S * (f32 ? 4 : 8) > smem_bytes) atomicMax(s.plan_fp32 + 1, P);
             s.tile_s[g] = S | (f32 ? kTileF32 : 0);
-            if (!f32 || S < 32) atomicAnd(&all_fp32, 0);
+            if (!f32 || S < 16) atomicAnd(&all_fp32, 0);
             tiles = (gi.processed + S - 1) / S;
         }
         int32_t tot;
