@@ -520,20 +520,32 @@ __global__ void __launch_bounds__(512) k_structure_large(DevBatch b, const DevCo
         cnt = __ldcg(&ctl->ctr[L % 3]);
     }
     const int32_t processed = begin;
-    // ---- deterministic level order: each level's nodes sorted by position
-    // (bitonic sort of the level in shared memory, a CTA per level).  The
-    // atomic appends above leave an arbitrary order inside a level; every
-    // single-GPU consumer is order-free, but ranks sharing one graph's bit
-    // space (sharded closure) must agree on every node's bit index.
-    for (int32_t lv = sort_levels ? blockIdx.x : L; lv < L; lv += gridDim.x) {
+    // ---- level order: each level's nodes sorted in shared memory (bitonic,
+    // a CTA per level).  The atomic appends above leave an arbitrary order
+    // inside a level and every single-GPU consumer is order-free, so one GPU
+    // sorts by in-degree: the sweep's lane groups take consecutive nodes, so
+    // a warp's nodes then have equal predecessor counts and its relaxation
+    // loop runs without idle lanes.  Ranks sharing one graph's bit space
+    // (sharded closure) must agree on every node's bit index: they sort by
+    // position.
+    for (int32_t lv = blockIdx.x; lv < L; lv += gridDim.x) {
         const int32_t a0 = __ldcg(&lstart[lv]), m = __ldcg(&lstart[lv + 1]) - a0;
         if (m > kSortLevel) {
-            if (tid == 0) atomicMax(&ctl->unsorted, 1);
+            if (sort_levels && tid == 0) atomicMax(&ctl->unsorted, 1);
             continue;  // uniform per CTA
         }
+        if (m <= 1) continue;
         int32_t N = 1;
         while (N < m) N <<= 1;
-        for (int32_t i = tid; i < N; i += nthr) s_sort[i] = i < m ? __ldcg(&order[a0 + i]) : INT32_MAX;
+        // key: position (n < 2^24), or in-degree (clipped at 127) above it
+        for (int32_t i = tid; i < N; i += nthr) {
+            int32_t key = INT32_MAX;
+            if (i < m) {
+                const int32_t v = __ldcg(&order[a0 + i]);
+                key = sort_levels ? v : (min(doff[v + 1] - doff[v], 127) << 24) | v;
+            }
+            s_sort[i] = key;
+        }
         __syncthreads();
         for (int32_t k = 2; k <= N; k <<= 1) {
             for (int32_t j = k >> 1; j > 0; j >>= 1) {
@@ -547,7 +559,7 @@ __global__ void __launch_bounds__(512) k_structure_large(DevBatch b, const DevCo
                 __syncthreads();
             }
         }
-        for (int32_t i = tid; i < m; i += nthr) order[a0 + i] = s_sort[i];
+        for (int32_t i = tid; i < m; i += nthr) order[a0 + i] = s_sort[i] & 0xffffff;
         __syncthreads();
     }
     grid.sync();
