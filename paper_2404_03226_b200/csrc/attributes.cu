@@ -150,6 +150,8 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
     __shared__ int32_t s_tcount[kMaxTypes];
     __shared__ int32_t warp_tot[32];
     __shared__ int32_t s_tail, s_end, s_miss_gpu, s_miss_any, s_span;
+    constexpr int32_t kDegSortMin = 192, kDegSortMax = 1024;
+    __shared__ int32_t s_key[kDegSortMax];
     const int tid = threadIdx.x, nthr = blockDim.x;
     int32_t loaded = -1;
     for (int64_t g = blockIdx.x; g < b.G; g += gridDim.x) {
@@ -229,6 +231,40 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
             ++L;
         }
         const int32_t processed = head;
+        // ---- wide levels sorted by in-degree (bitonic, shared memory): the
+        // sweep's row tiles (8 or 4 lanes per node, chosen for graphs whose
+        // live window is wide) give a warp consecutive nodes, which then have
+        // equal predecessor counts; one-node-per-warp tiles of narrow graphs
+        // do not need it (as k_structure_large)
+        for (int32_t lv = 0; lv < L; ++lv) {
+            const int32_t a0 = lstart[lv], m = lstart[lv + 1] - a0;
+            if (m < kDegSortMin || m > kDegSortMax) continue;  // uniform
+            int32_t N = 1;
+            while (N < m) N <<= 1;
+            for (int32_t i = tid; i < N; i += nthr) {
+                int32_t key = INT32_MAX;
+                if (i < m) {
+                    const int32_t v = order[a0 + i];
+                    key = (min(doff[v + 1] - doff[v], 127) << 24) | v;  // n < 2^24
+                }
+                s_key[i] = key;
+            }
+            __syncthreads();
+            for (int32_t k = 2; k <= N; k <<= 1) {
+                for (int32_t j = k >> 1; j > 0; j >>= 1) {
+                    for (int32_t i = tid; i < N; i += nthr) {
+                        const int32_t ixj = i ^ j;
+                        if (ixj > i) {
+                            const int32_t x = s_key[i], y = s_key[ixj];
+                            if ((x > y) == ((i & k) == 0)) { s_key[i] = y; s_key[ixj] = x; }
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int32_t i = tid; i < m; i += nthr) order[a0 + i] = s_key[i] & 0xffffff;
+            __syncthreads();
+        }
         // ---- reverse level sweep: height (depth), upward rank, last use
         for (int32_t lv = L - 1; lv >= 0; --lv) {
             for (int32_t i = lstart[lv] + tid; i < lstart[lv + 1]; i += nthr) {
