@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
         // sweep's row tiles (8 or 4 lanes per node, chosen for graphs whose
         // live window is wide) give a warp consecutive nodes, which then have
         // equal predecessor counts; one-node-per-warp tiles of narrow graphs
-        // do not need it (as k_structure_large)
+        // do not need it (as k_structure_large).  Descending: C5 sweep 280 ->
+        // 270 ms against ascending; C2's 100-node levels sorted either way
+        // measured slower (4.32 -> 4.63 ms), hence the 192-node floor.
         for (int32_t lv = 0; lv < L; ++lv) {
             const int32_t a0 = lstart[lv], m = lstart[lv + 1] - a0;
             if (m < kDegSortMin || m > kDegSortMax) continue;  // uniform
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(512) k_structure(DevBatch b, const DevCosts* c
                 int32_t key = INT32_MAX;
                 if (i < m) {
                     const int32_t v = order[a0 + i];
-                    key = (min(doff[v + 1] - doff[v], 127) << 24) | v;  // n < 2^24
+                    key = ((127 - min(doff[v + 1] - doff[v], 127)) << 24) | v;  // n < 2^24, deg descending
                 }
                 s_key[i] = key;
             }
