@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(512) k_structure_large(DevBatch b, const DevCo
             int32_t key = INT32_MAX;
             if (i < m) {
                 const int32_t v = __ldcg(&order[a0 + i]);
-                key = sort_levels ? v : (min(doff[v + 1] - doff[v], 127) << 24) | v;
+                key = sort_levels ? v : ((127 - min(doff[v + 1] - doff[v], 127)) << 24) | v;
             }
             s_sort[i] = key;
         }
