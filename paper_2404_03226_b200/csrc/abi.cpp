@@ -1680,7 +1680,9 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
     const bool many_in = d.T > 0 && d.I * p.max_nodes > 32 * d.T && p.policy >= TBSIM_POLICY_DMDA;
     auto kern = compact ? (w2 ? (many_in ? k_simulate_w2c_mi : k_simulate_w2c)
                               : many_in ? k_simulate_w1c_mi
-                              : p.policy == TBSIM_POLICY_INSPIRIT ? k_simulate_w1c_ins : k_simulate_w1c)
+                              : p.policy == TBSIM_POLICY_INSPIRIT && !p.push_time && !p.pop_time && !p.sample_time
+                                  ? k_simulate_w1c_ins  // (compiled without trace recording)
+                                  : k_simulate_w1c)
                         : (w2 ? k_simulate_w2 : k_simulate_w1);
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "cudaFuncSetAttribute(k_simulate)");

@@ -59,6 +59,9 @@ struct Sim {
     using KeyT = typename std::conditional<COMPACT, int16_t, int32_t>::type;
     using PrioT = typename std::conditional<COMPACT, int32_t, int64_t>::type;
     const SimParams* P;
+    // the policy-specialised kernel is launched only without trace outputs
+    // (abi.cpp), so its push/pop/sample recording compiles away
+    static constexpr bool kTrace = POL < 0;
     char* base;  // this warp's state memory
     // ---- graph
     int32_t n;
@@ -360,7 +363,7 @@ struct Sim {
 
     __device__ __forceinline__ void queue_event() {
         SimCold& c = cold();
-        if (P->sample_time) {
+        if (kTrace && P->sample_time) {
             const int64_t ns = c.n_samp;
             __syncwarp();
             if (lane == 0) {
@@ -542,7 +545,7 @@ struct Sim {
                     SimCold& c = cold();
                     slot = c.t0 + c.n_pop;
                     c.n_pop += 1;
-                    if (P->pop_time) {
+                    if (kTrace && P->pop_time) {
                         P->pop_time[slot] = now;
                         P->pop_task[slot] = task;
                         P->pop_worker[slot] = w;
@@ -622,7 +625,7 @@ struct Sim {
         if (__shfl_sync(kFull, ovf, owner)) { fail(GS_QUEUE_OVERFLOW, task); return -1; }
         __syncwarp();
         nready += 1;
-        if (P->push_time) {
+        if (kTrace && P->push_time) {
             SimCold& c = cold();
             const int64_t np = c.n_push;
             __syncwarp();
