@@ -1678,11 +1678,13 @@ void launch_sim(tbsim_ctx* ctx, SimParams& p, int32_t max_workers, int64_t n_ite
     // skip resident inputs.  A separate kernel, because the extra code costs
     // the few-input kernel 10% (C2) even where it never runs.
     const bool many_in = d.T > 0 && d.I * p.max_nodes > 32 * d.T && p.policy >= TBSIM_POLICY_DMDA;
-    auto kern = compact ? (w2 ? (many_in ? k_simulate_w2c_mi : k_simulate_w2c)
-                              : many_in ? k_simulate_w1c_mi
-                              : p.policy == TBSIM_POLICY_INSPIRIT && !p.push_time && !p.pop_time && !p.sample_time
-                                  ? k_simulate_w1c_ins  // (compiled without trace recording)
-                                  : k_simulate_w1c)
+    // inspirit without trace outputs: the policy-specialised kernels (trace
+    // recording compiled away)
+    const bool ins = p.policy == TBSIM_POLICY_INSPIRIT && !p.push_time && !p.pop_time && !p.sample_time;
+    auto kern = compact ? (w2 ? (many_in ? (ins ? k_simulate_w2c_mi_ins : k_simulate_w2c_mi)
+                                         : (ins ? k_simulate_w2c_ins : k_simulate_w2c))
+                              : many_in ? (ins ? k_simulate_w1c_mi_ins : k_simulate_w1c_mi)
+                              : ins ? k_simulate_w1c_ins : k_simulate_w1c)
                         : (w2 ? k_simulate_w2 : k_simulate_w1);
     cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "cudaFuncSetAttribute(k_simulate)");

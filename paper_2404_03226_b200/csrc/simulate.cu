@@ -1295,6 +1295,11 @@ TBSIM_SIM_KERNEL(k_simulate_w1c_ins, 1, true, TBSIM_POLICY_INSPIRIT, false, 128,
 TBSIM_SIM_KERNEL(k_simulate_w1c_mi, 1, true, -1, true, 128, 7)
 TBSIM_SIM_KERNEL(k_simulate_w2c, 2, true, -1, false, 256, 2)
 TBSIM_SIM_KERNEL(k_simulate_w2c_mi, 2, true, -1, true, 256, 2)
+// inspirit-only, trace-free twins of the many-input and two-worker-per-lane
+// kernels (C5's mixes, C3's 36 workers)
+TBSIM_SIM_KERNEL(k_simulate_w1c_mi_ins, 1, true, TBSIM_POLICY_INSPIRIT, true, 128, 7)
+TBSIM_SIM_KERNEL(k_simulate_w2c_ins, 2, true, TBSIM_POLICY_INSPIRIT, false, 256, 2)
+TBSIM_SIM_KERNEL(k_simulate_w2c_mi_ins, 2, true, TBSIM_POLICY_INSPIRIT, true, 256, 2)
 TBSIM_SIM_KERNEL(k_simulate_w1, 1, false, -1, false, 256, 2)
 TBSIM_SIM_KERNEL(k_simulate_w2, 2, false, -1, false, 256, 2)
 #undef TBSIM_SIM_KERNEL

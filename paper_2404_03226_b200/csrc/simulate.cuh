@@ -177,6 +177,9 @@ __global__ void k_sim_scatter(DevBatch b, const SimLog* log, const int32_t* n_di
 
 __global__ void k_simulate_w1c(const __grid_constant__ SimParams p);  // <= 32 workers, compact state (128-thread CTAs)
 __global__ void k_simulate_w1c_ins(const __grid_constant__ SimParams p);  // the same, inspirit only
+__global__ void k_simulate_w1c_mi_ins(const __grid_constant__ SimParams p);
+__global__ void k_simulate_w2c_ins(const __grid_constant__ SimParams p);
+__global__ void k_simulate_w2c_mi_ins(const __grid_constant__ SimParams p);
 __global__ void k_simulate_w1c_mi(const __grid_constant__ SimParams p);   // the same, many inputs per task
 __global__ void k_simulate_w2c(const __grid_constant__ SimParams p);  // <= 64 workers, compact state
 __global__ void k_simulate_w2c_mi(const __grid_constant__ SimParams p);  // the same, many inputs per task
